@@ -1,0 +1,260 @@
+// TEST INFRASTRUCTURE ONLY — extern "C" entry points over the reference's OWN
+// headers (/root/reference/proj/include/randla/*.hpp, compiled read-only from
+// where they lie; nothing is copied), built into oracle/_ref/librandla_ref.so
+// by oracle/Makefile. Used to validate the plain-C restatement (oracle.c) and
+// as bench.py's cpu_baseline / --impl reference arm.
+//
+// The reference includes <Eigen/Dense>; oracle/ref_shim provides our own
+// minimal stand-in whose product routes to the same GEMM hook as oracle.c.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "oracle.h"
+#include "randla/circulant.hpp"
+#include "randla/fft.hpp"
+#include "randla/lu.hpp"
+#include "randla/multipliers.hpp"
+#include "randla/norms.hpp"
+#include "randla/parallel.hpp"
+#include "randla/preprocess.hpp"
+#include "randla/rng.hpp"
+#include "randla/stats.hpp"
+
+namespace Eigen::shim {
+void gemm_rowmajor(const double* a, const double* b, double* c, Index m, Index k, Index n) {
+    or_matmul(m, k, n, a, b, c);
+}
+void gemm_rowmajor(const std::complex<double>* a, const std::complex<double>* b, std::complex<double>* c,
+                   Index m, Index k, Index n) {
+    for (Index i = 0; i < m; ++i)
+        for (Index j = 0; j < n; ++j) {
+            std::complex<double> acc{};
+            for (Index t = 0; t < k; ++t) acc += a[i * k + t] * b[t * n + j];
+            c[i * n + j] = acc;
+        }
+}
+}  // namespace Eigen::shim
+
+using namespace randla;
+
+namespace {
+enum { RS_OK = 0, RS_DIM = 1, RS_ZERO_PIVOT = 2, RS_LOGIC = 5, RS_OTHER = 9 };
+
+RealMatrix wrap(int64_t m, int64_t n, const double* p) {
+    return RealMatrix(static_cast<std::size_t>(m), static_cast<std::size_t>(n), std::vector<double>(p, p + m * n));
+}
+
+template <typename F>
+int guarded(F&& f, int64_t* step = nullptr) {
+    try {
+        f();
+        return RS_OK;
+    } catch (const ZeroPivotError& e) {
+        if (step) *step = static_cast<int64_t>(e.step);
+        return RS_ZERO_PIVOT;
+    } catch (const DimensionError&) {
+        return RS_DIM;
+    } catch (const std::logic_error&) {
+        return RS_LOGIC;
+    } catch (...) {
+        return RS_OTHER;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+uint64_t ref_hash_label(const char* s) { return hash_label(s); }
+uint64_t ref_derive_seed(uint64_t seed, uint64_t k1, uint64_t k2) { return derive_seed(seed, k1, k2); }
+
+// golden driver (tests/test_testbed.cpp:187-204): trial t draws
+// RngStream(derive_seed(seed, hash_label(label), t)).next_double()
+// (testbed/experiment.hpp:32-35), then summarize (stats.hpp:19-34)
+void ref_golden_draws(const char* label, uint64_t seed, int64_t trials, double* draws, double* stats4) {
+    const uint64_t key = hash_label(label);
+    std::vector<double> v(static_cast<std::size_t>(trials));
+    for (int64_t t = 0; t < trials; ++t) {
+        RngStream rng(derive_seed(seed, key, static_cast<uint64_t>(t)));
+        v[t] = rng.next_double();
+        draws[t] = v[t];
+    }
+    const StatSummary s = summarize(v);
+    stats4[0] = s.mean;
+    stats4[1] = s.max;
+    stats4[2] = s.min;
+    stats4[3] = s.std;
+}
+
+void ref_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out) {
+    const RealMatrix g = gen_gaussian(static_cast<std::size_t>(m), static_cast<std::size_t>(n), seed);
+    std::memcpy(out, g.data(), sizeof(double) * m * n);
+}
+
+void ref_gen_real_circulant_column(int64_t n, uint64_t seed, double* out) {
+    const RealCirculant c = gen_real_circulant(static_cast<std::size_t>(n), seed);
+    std::memcpy(out, c.first_column().data(), sizeof(double) * n);
+}
+
+int ref_matmul(int64_t m, int64_t k, int64_t n, const double* a, const double* b, double* c) {
+    return guarded([&] {
+        const RealMatrix p = matmul(wrap(m, k, a), wrap(k, n, b));
+        std::memcpy(c, p.data(), sizeof(double) * m * n);
+    });
+}
+
+double ref_spectral_norm_estimate(int64_t m, int64_t n, const double* a) {
+    return spectral_norm_estimate(wrap(m, n, a));
+}
+
+// genp_factor (lu.hpp:40-58), L and U unpacked into one packed buffer
+int ref_genp_factor(int64_t n, const double* a, double* lu, int64_t* zero_step) {
+    *zero_step = 0;
+    return guarded(
+        [&] {
+            const LuFactors<double> f = genp_factor(wrap(n, n, a));
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t j = 0; j < n; ++j)
+                    lu[i * n + j] = (j < i) ? f.lower(static_cast<std::size_t>(i), static_cast<std::size_t>(j))
+                                            : f.upper(static_cast<std::size_t>(i), static_cast<std::size_t>(j));
+        },
+        zero_step);
+}
+
+// lu_solve (lu.hpp:100-123) on packed factors
+void ref_lu_solve(int64_t n, const double* lu, const double* b, double* x) {
+    LuFactors<double> f{RealMatrix::identity(static_cast<std::size_t>(n)),
+                        RealMatrix(static_cast<std::size_t>(n), static_cast<std::size_t>(n)), std::nullopt};
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            if (j < i)
+                f.lower(static_cast<std::size_t>(i), static_cast<std::size_t>(j)) = lu[i * n + j];
+            else
+                f.upper(static_cast<std::size_t>(i), static_cast<std::size_t>(j)) = lu[i * n + j];
+        }
+    const std::vector<double> y = lu_solve(f, std::vector<double>(b, b + n));
+    std::memcpy(x, y.data(), sizeof(double) * n);
+}
+
+int ref_fft(int64_t n, double* z, int inverse) {
+    return guarded([&] {
+        std::vector<Complex> v(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) v[i] = Complex(z[2 * i], z[2 * i + 1]);
+        const std::vector<Complex> w = inverse ? inverse_fft(std::move(v)) : fft(std::move(v));
+        for (int64_t i = 0; i < n; ++i) {
+            z[2 * i] = w[i].real();
+            z[2 * i + 1] = w[i].imag();
+        }
+    });
+}
+
+int ref_circulant_apply(int64_t n, const double* c, const double* x, double* y) {
+    return guarded([&] {
+        const RealCirculant circ(std::vector<double>(c, c + n));
+        const std::vector<double> out = circulant_apply(circ, std::vector<double>(x, x + n));
+        std::memcpy(y, out.data(), sizeof(double) * n);
+    });
+}
+
+int ref_matmul_by_circulant(int64_t m, int64_t n, const double* a, const double* c, double* out) {
+    return guarded([&] {
+        const RealCirculant circ(std::vector<double>(c, c + n));
+        const RealMatrix p = matmul_by_circulant(wrap(m, n, a), circ);
+        std::memcpy(out, p.data(), sizeof(double) * m * n);
+    });
+}
+
+int ref_matmul_by_toeplitz_block(int64_t m, int64_t k, const double* a, int64_t np, const double* c, int64_t l,
+                                 double* out) {
+    return guarded([&] {
+        const ToeplitzBlock<double> t(RealCirculant(std::vector<double>(c, c + np)), static_cast<std::size_t>(k),
+                                      static_cast<std::size_t>(l));
+        const RealMatrix p = matmul_by_toeplitz_block(wrap(m, k, a), t);
+        std::memcpy(out, p.data(), sizeof(double) * m * l);
+    });
+}
+
+// preprocess_solve(a, b, none, post, refine) (preprocess.hpp:156-180).
+// post_kind 0 none, 1 Gaussian with seed, 2 reference RealCirculant (uniform,
+// multipliers.hpp:67-73) with seed. history gets refine+1 entries (NaN-padded
+// when the loop stopped on divergence).
+int ref_preprocess_solve(int64_t n, const double* a, const double* b, int post_kind, uint64_t seed, int64_t refine,
+                         double* x, double* history, int* diverged, int64_t* zero_step) {
+    *zero_step = 0;
+    return guarded(
+        [&] {
+            MultiplierSpec post;
+            post.kind = post_kind == 1   ? MultiplierKind::Gaussian
+                        : post_kind == 2 ? MultiplierKind::RealCirculant
+                                         : MultiplierKind::None;
+            post.seed = seed;
+            const SolveOutcome<double> out = preprocess_solve(wrap(n, n, a), std::vector<double>(b, b + n),
+                                                              MultiplierSpec{}, post,
+                                                              static_cast<std::size_t>(refine));
+            std::memcpy(x, out.x.data(), sizeof(double) * n);
+            for (int64_t s = 0; s <= refine; ++s)
+                history[s] = s < static_cast<int64_t>(out.residual_history.size()) ? out.residual_history[s] : NAN;
+            *diverged = out.diverged ? 1 : 0;
+        },
+        zero_step);
+}
+
+// BASELINE config 2 with the reference's own trial pool
+// (parallel_for_index, parallel.hpp:14-35): system i uses ts = base + i0 + i
+// and the seed mapping of SURVEY §8(d). Returns the number of ZeroPivots.
+int64_t ref_batched_config2(int64_t dim, uint64_t base, int64_t i0, int64_t count, double* x_out,
+                            double* resid_out) {
+    std::vector<int> failed(static_cast<std::size_t>(count), 0);
+    const std::size_t d = static_cast<std::size_t>(dim);
+    parallel_for_index(static_cast<std::size_t>(count), [&](std::size_t k) {
+        const uint64_t ts = base + static_cast<uint64_t>(i0) + k;
+        const RealMatrix a = gen_gaussian(d, d, derive_seed(ts, 1));
+        RngStream rb(derive_seed(ts, 2));
+        std::vector<double> b(d);
+        for (double& v : b) v = rb.next_gaussian();
+        MultiplierSpec post{MultiplierKind::Gaussian};
+        post.seed = derive_seed(ts, 3);
+        try {
+            const SolveOutcome<double> out = preprocess_solve(a, b, MultiplierSpec{}, post, 0);
+            if (x_out) std::memcpy(x_out + k * d, out.x.data(), sizeof(double) * d);
+            if (resid_out) resid_out[k] = out.residual_history[0];
+        } catch (const ZeroPivotError&) {
+            failed[k] = 1;
+            if (resid_out) resid_out[k] = NAN;
+        }
+    });
+    int64_t nf = 0;
+    for (int f : failed) nf += f;
+    return nf;
+}
+
+// --impl reference arm: `trials` independent preprocess_solve(A_t, b_t, none,
+// {Gaussian, seeds[t]}, 0) calls (the multiplier G_t is generated inside, as
+// the reference does) run on the reference's own trial pool
+// (parallel_for_index). A_t, b_t are caller-provided so input generation
+// stays outside the timed call. Returns the number of ZeroPivots.
+int64_t ref_parallel_dense_trials(int64_t n, int64_t trials, const double* a_all, const double* b_all,
+                                  const uint64_t* seeds, double* resid_out) {
+    std::vector<int> failed(static_cast<std::size_t>(trials), 0);
+    const std::size_t nn = static_cast<std::size_t>(n);
+    parallel_for_index(static_cast<std::size_t>(trials), [&](std::size_t k) {
+        const RealMatrix a = wrap(n, n, a_all + k * nn * nn);
+        const std::vector<double> b(b_all + k * nn, b_all + (k + 1) * nn);
+        MultiplierSpec post{MultiplierKind::Gaussian};
+        post.seed = seeds[k];
+        try {
+            const SolveOutcome<double> out = preprocess_solve(a, b, MultiplierSpec{}, post, 0);
+            if (resid_out) resid_out[k] = out.residual_history[0];
+        } catch (const ZeroPivotError&) {
+            failed[k] = 1;
+            if (resid_out) resid_out[k] = NAN;
+        }
+    });
+    int64_t nf = 0;
+    for (int f : failed) nf += f;
+    return nf;
+}
+
+}  // extern "C"
