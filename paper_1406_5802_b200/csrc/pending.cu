@@ -1,0 +1,53 @@
+// Entry points declared in include/randla_capi.h whose kernels are not in
+// this build yet: they fail loudly with RL_ERR_UNSUPPORTED (never a CPU
+// fallback). Each moves to its own translation unit when implemented.
+#include "runtime.cuh"
+
+#define RL_PENDING(name)                                                          \
+    return rl::set_error(RL_ERR_UNSUPPORTED, "%s: not implemented in this build", name)
+
+extern "C" {
+
+RL_API rl_status rl_dgemm(rl_context*, rl_mem, int64_t, int64_t, int64_t, const double*, int64_t, const double*,
+                          int64_t, double*, int64_t) {
+    RL_PENDING("rl_dgemm");
+}
+
+RL_API rl_status rl_spectral_norm_estimate(rl_context*, rl_mem, int64_t, int64_t, const double*, double*) {
+    RL_PENDING("rl_spectral_norm_estimate");
+}
+
+RL_API rl_status rl_genp_factor(rl_context*, rl_mem, int64_t, const double*, double*, rl_solve_info*) {
+    RL_PENDING("rl_genp_factor");
+}
+
+RL_API rl_status rl_lu_solve(rl_context*, rl_mem, int64_t, const double*, const double*, double*) {
+    RL_PENDING("rl_lu_solve");
+}
+
+RL_API rl_status rl_preprocessed_genp_solve(rl_context*, rl_mem, int64_t, const double*, const double*,
+                                            const rl_multiplier*, int64_t, double*, double*, int32_t,
+                                            rl_solve_info*) {
+    RL_PENDING("rl_preprocessed_genp_solve");
+}
+
+RL_API rl_status rl_circulant_right_multiply(rl_context*, rl_mem, int64_t, int64_t, const double*, const double*,
+                                             double*) {
+    RL_PENDING("rl_circulant_right_multiply");
+}
+
+RL_API rl_status rl_toeplitz_right_multiply(rl_context*, rl_mem, int64_t, int64_t, const double*, int64_t,
+                                            const double*, int64_t, double*) {
+    RL_PENDING("rl_toeplitz_right_multiply");
+}
+
+RL_API rl_status rl_cholqr2(rl_context*, rl_mem, int64_t, int64_t, const double*, double*, double*, int64_t*) {
+    RL_PENDING("rl_cholqr2");
+}
+
+RL_API rl_status rl_range_find_residual(rl_context*, rl_mem, int64_t, int64_t, const double*, int64_t,
+                                        const rl_multiplier*, double*, rl_lowrank_info*) {
+    RL_PENDING("rl_range_find_residual");
+}
+
+}  // extern "C"

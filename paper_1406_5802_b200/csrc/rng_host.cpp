@@ -1,0 +1,190 @@
+// Exact seeded multiplier generation on the host, parallel across cores.
+//
+// The reference draws every multiplier from one sequential RngStream
+// (rng.hpp:16-85): splitmix64 counter steps, Marsaglia polar Gaussians
+// (rng.hpp:56-71), entry (i, j) of gen_gaussian = draw i*n + j
+// (multipliers.hpp:58-65). Device generation cannot be bit-exact because
+// glibc's log is not correctly rounded (SURVEY §0 finding 6), so the
+// multipliers are generated here, bit-identical to the reference, and
+// uploaded.
+//
+// Parallelisation without changing a single bit: draw t of a stream is
+// finalize(state0 + t * gamma), so polar attempt a (draws 2a+1, 2a+2) can be
+// evaluated at any index. Pass 1 counts accepted attempts per chunk (integer
+// ops and one exact compare, no log); a prefix sum gives every chunk its
+// output offset; pass 2 generates the chunks independently.
+//
+// Compiled with -ffp-contract=off and no -march flags: u*u + v*v and the
+// polar factor round exactly as in the reference's x86-64 build.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+#include "../../include/randla_capi.h"
+
+namespace {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+inline uint64_t finalize(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// rng.hpp:74-80
+inline uint64_t mix_key(uint64_t state, uint64_t key) {
+    state ^= key + kGamma + (state << 6) + (state >> 2);
+    return finalize(state + kGamma);
+}
+
+inline uint64_t stream_state(uint64_t seed) { return mix_key(kGamma, seed); }  // rng.hpp:18
+
+// rng.hpp:40-43: uniform on [-1, 1] from draw number t (1-based) of the stream
+inline double symmetric_at(uint64_t state0, uint64_t t) {
+    const double d = static_cast<double>(finalize(state0 + t * kGamma) >> 11) * 0x1.0p-53;
+    return 2.0 * d - 1.0;
+}
+
+// polar attempt a: accepted when 0 < s < 1 (rng.hpp:61-66)
+inline bool attempt(uint64_t state0, uint64_t a, double& u, double& v, double& s) {
+    u = symmetric_at(state0, 2 * a + 1);
+    v = symmetric_at(state0, 2 * a + 2);
+    s = u * u + v * v;
+    return !(s >= 1.0 || s == 0.0);
+}
+
+int g_threads = 0;
+
+int thread_count() {
+    int t = g_threads > 0 ? g_threads : static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, t);
+}
+
+template <typename F>
+void parallel_for(int64_t count, F&& fn) {
+    const int workers = static_cast<int>(std::min<int64_t>(thread_count(), count));
+    if (workers <= 1) {
+        for (int64_t i = 0; i < count; ++i) fn(i);
+        return;
+    }
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    pool.reserve(workers);
+    for (int w = 0; w < workers; ++w)
+        pool.emplace_back([&] {
+            for (int64_t i = next.fetch_add(1); i < count; i = next.fetch_add(1)) fn(i);
+        });
+    for (auto& t : pool) t.join();
+}
+
+// Sequential generator (small matrices): exactly RngStream::next_gaussian.
+void gaussian_sequential(uint64_t seed, int64_t count, double* out) {
+    const uint64_t s0 = stream_state(seed);
+    uint64_t a = 0;
+    int64_t k = 0;
+    while (k < count) {
+        double u, v, s;
+        if (!attempt(s0, a++, u, v, s)) continue;
+        const double f = std::sqrt(-2.0 * std::log(s) / s);
+        out[k++] = u * f;
+        if (k < count) out[k++] = v * f;
+    }
+}
+
+constexpr int64_t kChunk = 1 << 16;  // polar attempts per chunk
+
+void gaussian_parallel(uint64_t seed, int64_t count, double* out) {
+    const int64_t pairs_needed = (count + 1) / 2;
+    if (count <= 4 * kChunk || thread_count() == 1) {
+        gaussian_sequential(seed, count, out);
+        return;
+    }
+    const uint64_t s0 = stream_state(seed);
+    std::vector<int64_t> accepted;
+    int64_t have = 0;
+    while (have < pairs_needed) {
+        // enough chunks for the remaining pairs at acceptance pi/4, plus slack
+        const int64_t base = static_cast<int64_t>(accepted.size());
+        const int64_t more = static_cast<int64_t>((pairs_needed - have) / (kChunk * 0.78539816)) + 2;
+        accepted.resize(base + more);
+        parallel_for(more, [&](int64_t i) {
+            const uint64_t a0 = static_cast<uint64_t>(base + i) * kChunk;
+            int64_t c = 0;
+            for (int64_t j = 0; j < kChunk; ++j) {
+                double u, v, s;
+                c += attempt(s0, a0 + j, u, v, s) ? 1 : 0;
+            }
+            accepted[base + i] = c;
+        });
+        have = 0;
+        for (int64_t c : accepted) have += c;
+    }
+    std::vector<int64_t> offset(accepted.size() + 1, 0);
+    for (size_t i = 0; i < accepted.size(); ++i) offset[i + 1] = offset[i] + accepted[i];
+    int64_t chunks = 0;
+    while (offset[chunks] < pairs_needed) ++chunks;
+    parallel_for(chunks, [&](int64_t i) {
+        const uint64_t a0 = static_cast<uint64_t>(i) * kChunk;
+        int64_t k = 2 * offset[i];
+        for (int64_t j = 0; j < kChunk && k < count; ++j) {
+            double u, v, s;
+            if (!attempt(s0, a0 + j, u, v, s)) continue;
+            const double f = std::sqrt(-2.0 * std::log(s) / s);
+            out[k++] = u * f;
+            if (k < count) out[k++] = v * f;
+        }
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+RL_API void rl_set_host_threads(int threads) { g_threads = threads; }
+
+// multipliers.hpp:54-56: RngStream(seed).derived(k1, k2).next_u64()
+RL_API uint64_t rl_derive_seed(uint64_t seed, uint64_t k1, uint64_t k2) {
+    const uint64_t st = mix_key(mix_key(stream_state(seed), k1), k2);
+    return finalize(st + kGamma);
+}
+
+// rng.hpp:87-95
+RL_API uint64_t rl_hash_label(const char* s) {
+    uint64_t h = 1469598103934665603ull;
+    for (; *s; ++s) {
+        h ^= static_cast<uint64_t>(static_cast<unsigned char>(*s));
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+RL_API rl_status rl_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out) {
+    if (m <= 0 || n <= 0 || !out) return RL_ERR_DIMENSION;
+    gaussian_parallel(seed, m * n, out);
+    return RL_OK;
+}
+
+RL_API rl_status rl_gen_gaussian_batch(int64_t count, int64_t m, int64_t n, const uint64_t* seeds, double* out) {
+    if (count < 0 || m <= 0 || n <= 0 || (count > 0 && (!out || !seeds))) return RL_ERR_DIMENSION;
+    const int64_t per = m * n;
+    constexpr int64_t kGroup = 256;
+    parallel_for((count + kGroup - 1) / kGroup, [&](int64_t g) {
+        const int64_t hi = std::min(count, (g + 1) * kGroup);
+        for (int64_t i = g * kGroup; i < hi; ++i) gaussian_sequential(seeds[i], per, out + i * per);
+    });
+    return RL_OK;
+}
+
+// multipliers.hpp:67-73: next_symmetric draws 1..n
+RL_API rl_status rl_gen_real_circulant_column(int64_t n, uint64_t seed, double* out) {
+    if (n <= 0 || !out) return RL_ERR_DIMENSION;
+    const uint64_t s0 = stream_state(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = symmetric_at(s0, static_cast<uint64_t>(i) + 1);
+    return RL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,173 @@
+// Context management, errors and launch accounting for the C ABI
+// (include/randla_capi.h).
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "runtime.cuh"
+
+namespace rl {
+
+std::atomic<int64_t> g_launches{0};
+
+static thread_local std::string t_error;
+
+rl_status set_error(rl_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_error = buf;
+    return st;
+}
+
+rl_status cuda_error(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) return set_error(RL_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        return set_error(RL_ERR_NO_DEVICE, "%s: %s", what, cudaGetErrorString(e));
+    return set_error(RL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static rl_status init_context(rl_context* c, int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return set_error(RL_ERR_NO_DEVICE, "no CUDA device available (librandla_b200 has no CPU fallback)");
+    if (device < 0 || device >= count) return set_error(RL_ERR_INVALID_ARGUMENT, "device %d out of range", device);
+    RL_CUDA(cudaSetDevice(device));
+    c->device = device;
+    RL_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    RL_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    c->flags_bytes = 4096;
+    RL_CUDA(cudaMalloc(&c->flags, c->flags_bytes));
+    RL_CUDA(cudaMemset(c->flags, 0, c->flags_bytes));
+    return RL_OK;
+}
+
+static void destroy_context(rl_context* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->ws) cudaFree(c->ws);
+    if (c->flags) cudaFree(c->flags);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+// Per-thread default contexts come from a process-wide pool: a thread that
+// exits hands its context back (no CUDA calls at thread exit), so callers that
+// spawn fresh worker threads per call (parallel_for_index, parallel.hpp:14-35)
+// reuse streams and workspaces instead of leaking them.
+static std::mutex g_pool_mu;
+static std::vector<rl_context*>* g_pool = new std::vector<rl_context*>();  // intentionally leaked
+
+struct ThreadDefault {
+    rl_context* ctx = nullptr;
+    ~ThreadDefault() {
+        if (!ctx) return;
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        g_pool->push_back(ctx);
+    }
+};
+static thread_local ThreadDefault t_default;
+
+rl_context* resolve(rl_context* ctx, rl_status* st) {
+    *st = RL_OK;
+    if (ctx) {
+        cudaSetDevice(ctx->device);
+        return ctx;
+    }
+    if (!t_default.ctx) {
+        {
+            std::lock_guard<std::mutex> lk(g_pool_mu);
+            if (!g_pool->empty()) {
+                t_default.ctx = g_pool->back();
+                g_pool->pop_back();
+            }
+        }
+        if (!t_default.ctx) {
+            rl_context* c = new rl_context();
+            rl_status s = init_context(c, 0);
+            if (s != RL_OK) {
+                delete c;
+                *st = s;
+                return nullptr;
+            }
+            t_default.ctx = c;
+        }
+    }
+    cudaSetDevice(t_default.ctx->device);
+    return t_default.ctx;
+}
+
+void* workspace(rl_context* ctx, size_t bytes) {
+    if (bytes <= ctx->ws_bytes) return ctx->ws;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+    size_t want = align_up(bytes, size_t(1) << 20);
+    cudaError_t e = cudaMalloc(&ctx->ws, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->ws = nullptr;
+        cuda_error(e, "workspace allocation");
+        return nullptr;
+    }
+    ctx->ws_bytes = want;
+    return ctx->ws;
+}
+
+}  // namespace rl
+
+extern "C" {
+
+RL_API int rl_abi_version(void) { return RL_ABI_VERSION; }
+
+RL_API const char* rl_last_error(void) { return rl::t_error.c_str(); }
+
+RL_API rl_status rl_context_create(int device, rl_context** out) {
+    if (!out) return rl::set_error(RL_ERR_INVALID_ARGUMENT, "rl_context_create: null out");
+    rl_context* c = new rl_context();
+    rl_status st = rl::init_context(c, device);
+    if (st != RL_OK) {
+        delete c;
+        *out = nullptr;
+        return st;
+    }
+    *out = c;
+    return RL_OK;
+}
+
+RL_API rl_status rl_context_destroy(rl_context* ctx) {
+    rl::destroy_context(ctx);
+    return RL_OK;
+}
+
+RL_API rl_status rl_context_set_stream(rl_context* ctx, void* s) {
+    rl_status st;
+    ctx = rl::resolve(ctx, &st);
+    if (!ctx) return st;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    return RL_OK;
+}
+
+RL_API void* rl_context_get_stream(rl_context* ctx) {
+    rl_status st;
+    ctx = rl::resolve(ctx, &st);
+    return ctx ? static_cast<void*>(ctx->stream) : nullptr;
+}
+
+RL_API rl_status rl_synchronize(rl_context* ctx) {
+    rl_status st;
+    ctx = rl::resolve(ctx, &st);
+    if (!ctx) return st;
+    RL_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RL_OK;
+}
+
+RL_API int64_t rl_kernel_launches(void) { return rl::g_launches.load(); }
+
+}  // extern "C"

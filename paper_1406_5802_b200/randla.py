@@ -1,0 +1,231 @@
+"""Reference-shaped host API over the C ABI.
+
+Mirrors the `randla` header API for the hot path (namespace randla,
+/root/reference/proj/include/randla/*.hpp, double instantiation): the same
+function names, argument meaning and error behaviour (typed exceptions
+carrying the 1-based step / position). Arrays are numpy (host, the drop-in
+form: every call stages through the device) or torch CUDA tensors (device
+pointers, no host round trip); results come back in the same form.
+
+The computation always runs in librandla_b200.so on the GPU; there is no CPU
+path in this module.
+"""
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import capi
+
+
+# ---- error contract (types.hpp:44-78) ------------------------------------
+class RandlaError(RuntimeError):
+    pass
+
+
+class DimensionError(ValueError):
+    """randla::DimensionError (std::invalid_argument), types.hpp:44-46"""
+
+
+class SingularMatrixError(RandlaError):
+    """types.hpp:48-50"""
+
+
+class RankDeficiencyError(RandlaError):
+    """types.hpp:52-54"""
+
+    def __init__(self, msg, column=0):
+        super().__init__(msg)
+        self.column = column
+
+
+class ZeroPivotError(RandlaError):
+    """GENP met a pivot below tolerance at `step` (1-based), types.hpp:56-62"""
+
+    def __init__(self, step):
+        super().__init__(f"zero pivot at elimination step {step}")
+        self.step = step
+
+
+class SingularPivotBlockError(RandlaError):
+    """types.hpp:64-68"""
+
+    def __init__(self, position):
+        super().__init__(f"numerically singular pivot block at position {position}")
+        self.position = position
+
+
+class LogicError(RuntimeError):
+    """std::logic_error — real circulant product with non-negligible imaginary
+    part (circulant.hpp:63-64)"""
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def _raise(status, info_step=0, what=""):
+    if status == capi.RL_OK:
+        return
+    msg = capi.last_error() or what
+    if status == capi.RL_ERR_DIMENSION:
+        raise DimensionError(msg)
+    if status == capi.RL_ERR_ZERO_PIVOT:
+        raise ZeroPivotError(info_step)
+    if status == capi.RL_ERR_SINGULAR_PIVOT_BLOCK:
+        raise SingularPivotBlockError(info_step)
+    if status == capi.RL_ERR_RANK_DEFICIENCY:
+        raise RankDeficiencyError(msg, info_step)
+    if status == capi.RL_ERR_SINGULAR_MATRIX:
+        raise SingularMatrixError(msg)
+    if status == capi.RL_ERR_LOGIC:
+        raise LogicError(msg)
+    raise DeviceError(f"librandla_b200 status {status}: {msg}")
+
+
+# ---- multipliers (multipliers.hpp:20-56) ------------------------------------
+class MultiplierKind(enum.IntEnum):
+    NONE = capi.RL_MULT_NONE
+    GAUSSIAN = capi.RL_MULT_GAUSSIAN
+    REAL_CIRCULANT = capi.RL_MULT_REAL_CIRCULANT          # reference family: uniform[-1,1] column
+    GAUSSIAN_CIRCULANT = capi.RL_MULT_GAUSSIAN_CIRCULANT  # BASELINE configs 3/5: N(0,1) column
+
+
+@dataclass
+class MultiplierSpec:
+    kind: MultiplierKind = MultiplierKind.NONE
+    seed: int = 0
+    dense: Optional[object] = None   # explicit n x n multiplier (GAUSSIAN)
+    column: Optional[object] = None  # explicit first column (circulant kinds)
+
+
+def derive_seed(seed, k1, k2=0):
+    """multipliers.hpp:54-56"""
+    return int(capi.lib().rl_derive_seed(seed, k1, k2))
+
+
+def hash_label(label):
+    """rng.hpp:87-95"""
+    return int(capi.lib().rl_hash_label(label.encode()))
+
+
+def gen_gaussian(m, n, seed):
+    """multipliers.hpp:58-65 — bit-identical to the reference generator."""
+    out = np.empty((m, n))
+    _raise(capi.lib().rl_gen_gaussian(m, n, seed, out.ctypes.data))
+    return out
+
+
+def gen_gaussian_vector(n, seed):
+    """testbed/inputs.hpp:85-90"""
+    return gen_gaussian(n, 1, seed).reshape(n)
+
+
+def gen_gaussian_batch(count, m, n, seeds):
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = np.empty((count, m, n))
+    _raise(capi.lib().rl_gen_gaussian_batch(count, m, n, seeds.ctypes.data, out.ctypes.data))
+    return out
+
+
+def gen_real_circulant_column(n, seed):
+    """multipliers.hpp:67-73 (first column of gen_real_circulant)"""
+    out = np.empty(n)
+    _raise(capi.lib().rl_gen_real_circulant_column(n, seed, out.ctypes.data))
+    return out
+
+
+# ---- array plumbing ----------------------------------------------------------
+def _is_device(*arrays):
+    dev = None
+    for a in arrays:
+        if a is None:
+            continue
+        d = not isinstance(a, np.ndarray)
+        if dev is None:
+            dev = d
+        elif dev != d:
+            raise DimensionError("mixing host (numpy) and device (torch) arrays in one call")
+    return bool(dev)
+
+
+def _host(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _dev(a):
+    import torch
+    if a.dtype != torch.float64 or not a.is_cuda:
+        raise DimensionError("device arrays must be float64 CUDA tensors")
+    return a.contiguous()
+
+
+def _empty_like_kind(device, shape, ref=None):
+    if device:
+        import torch
+        return torch.empty(shape, dtype=torch.float64, device=ref.device if ref is not None else "cuda")
+    return np.empty(shape)
+
+
+def _ctx():
+    return None  # per-thread default context
+
+
+def _mem(device):
+    return capi.RL_DEVICE if device else capi.RL_HOST
+
+
+def _sync_stream_for(device):
+    """Device calls run on the context stream; make torch's current stream the
+    context stream so ordering with surrounding torch work is preserved."""
+    if device:
+        import torch
+        capi.lib().rl_context_set_stream(None, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+# ---- batched small GENP (BASELINE config 2) ----------------------------------
+@dataclass
+class BatchedSolve:
+    lu: object
+    x: object
+    residual: object
+    growth: object
+    status: object
+    summary: dict
+
+
+def batched_preprocess_solve_32(a, g, b, want_lu=True, want_summary=True):
+    """Many independent preprocess_solve(A_i, b_i, none, {Gaussian, G_i}, 0)
+    (preprocess.hpp:156-180) on 32x32 systems. a, g: (batch, 32, 32); b: (batch, 32).
+    Per-system ZeroPivot verdicts are returned in `status` (1-based step, 0 = ok)
+    instead of raising, as the reference's trial engine counts them
+    (testbed/experiment.hpp:36-40)."""
+    device = _is_device(a, g, b)
+    if a.shape[-2:] != (32, 32) or g.shape != a.shape or b.shape != a.shape[:-1]:
+        raise DimensionError("batched_preprocess_solve_32: shapes must be (B,32,32), (B,32,32), (B,32)")
+    batch = a.shape[0]
+    if device:
+        import torch
+        a, g, b = _dev(a), _dev(g), _dev(b)
+        lu = torch.empty_like(a) if want_lu else None
+        x = torch.empty_like(b)
+        r = torch.empty(batch, dtype=torch.float64, device=a.device)
+        gr = torch.empty_like(r)
+        st = torch.empty(batch, dtype=torch.int32, device=a.device)
+    else:
+        a, g, b = _host(a), _host(g), _host(b)
+        lu = np.empty_like(a) if want_lu else None
+        x = np.empty_like(b)
+        r = np.empty(batch)
+        gr = np.empty(batch)
+        st = np.empty(batch, np.int32)
+    _sync_stream_for(device)
+    summ = capi.rl_batch_summary()
+    rc = capi.lib().rl_batched_genp_solve_32(_ctx(), _mem(device), batch, capi.addr(a), capi.addr(g), capi.addr(b),
+                                             capi.addr(lu), capi.addr(x), capi.addr(r), capi.addr(gr),
+                                             capi.addr(st), ctypes.byref(summ) if want_summary else None)
+    _raise(rc)
+    s = {k: getattr(summ, k) for k, _ in summ._fields_} if want_summary else {}
+    return BatchedSolve(lu, x, r, gr, st, s)

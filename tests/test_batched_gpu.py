@@ -1,0 +1,133 @@
+"""GPU parity: batched 32x32 preprocessed GENP (BASELINE config 2) through the
+C ABI vs the CPU oracle on identical seeded inputs.
+
+Tolerances (BASELINE north_star): L, U and x within relative Frobenius error
+1e-10 * kappa; growth factors and ZeroPivot verdicts identical (growth to
+rounding, 1e-10 * kappa relative)."""
+import numpy as np
+import pytest
+
+import paper_1406_5802_b200 as rl
+
+pytestmark = pytest.mark.gpu
+
+
+def _config2_inputs(orc, count, i0=0):
+    r = orc.C.batched_config2(count, base=7, i0=i0, threads=8, want_lu=True)
+    return r
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_config2_parity_first_4096(cuda, orc):
+    ref = _config2_inputs(orc, 4096)
+    out = rl.batched_preprocess_solve_32(ref["a"], ref["g"], ref["b"])
+    assert (out.status == 0).all() and (ref["status"] == 0).all()
+    worst_lu = worst_x = worst_g = 0.0
+    for i in range(4096):
+        ag = ref["a"][i] @ ref["g"][i]
+        kap_ag = np.linalg.cond(ag)
+        kap_a = np.linalg.cond(ref["a"][i])
+        e_lu = _rel(out.lu[i], ref["lu"][i]) / kap_ag
+        e_x = _rel(out.x[i], ref["x"][i]) / kap_a
+        e_g = abs(out.growth[i] - ref["growth"][i]) / ref["growth"][i] / kap_ag
+        worst_lu, worst_x, worst_g = max(worst_lu, e_lu), max(worst_x, e_x), max(worst_g, e_g)
+    assert worst_lu <= 1e-10, worst_lu
+    assert worst_x <= 1e-10, worst_x
+    assert worst_g <= 1e-10, worst_g
+    # residual ||Ax-b||/||b|| of the GPU solution is at the oracle's level
+    np.testing.assert_allclose(np.median(out.residual), np.median(ref["resid"]), rtol=0.5)
+    assert out.summary["zero_pivots"] == 0
+    assert abs(out.summary["max_growth"] - out.growth.max()) == 0
+
+
+def test_config2_full_batch_device_pointers(cuda, orc):
+    """65536 systems, device-resident (torch) — spot-check 512 systems against
+    the oracle and the whole batch through size-independent properties."""
+    torch = cuda
+    n = 65536
+    seeds = np.array([[rl.derive_seed(7 + i, k) for k in (1, 2, 3)] for i in range(n)], dtype=np.uint64)
+    a = rl.gen_gaussian_batch(n, 32, 32, seeds[:, 0])
+    b = rl.gen_gaussian_batch(n, 32, 1, seeds[:, 1]).reshape(n, 32)
+    g = rl.gen_gaussian_batch(n, 32, 32, seeds[:, 2])
+    da, dg, db = (torch.from_numpy(t).cuda() for t in (a, g, b))
+    out = rl.batched_preprocess_solve_32(da, dg, db)
+    torch.cuda.synchronize()
+    st = out.status.cpu().numpy()
+    x = out.x.cpu().numpy()
+    res = out.residual.cpu().numpy()
+    assert (st == 0).all()
+    # residuals recomputed on the host from the GPU solutions
+    r_host = np.linalg.norm(np.einsum("bij,bj->bi", a, x) - b, axis=1) / np.linalg.norm(b, axis=1)
+    np.testing.assert_allclose(res, r_host, rtol=1e-6, atol=1e-15)
+    assert np.median(res) < 1e-12 and res.max() < 1e-4
+    idx = np.random.default_rng(3).choice(n, 512, replace=False)
+    for i in idx:
+        ref = orc.C.batched_config2(1, base=7, i0=int(i), threads=1, want_lu=True)
+        assert _rel(x[i], ref["x"][0]) <= 1e-10 * np.linalg.cond(a[i])
+    # host-pointer path == device-pointer path, bit for bit
+    host = rl.batched_preprocess_solve_32(a[:1024], g[:1024], b[:1024])
+    np.testing.assert_array_equal(host.x, x[:1024])
+    np.testing.assert_array_equal(host.lu, out.lu[:1024].cpu().numpy())
+
+
+def test_kats_identity_and_zero_pivot(cuda, orc):
+    """tests/test_elimination.cpp:29-50 & :244-253 analogues at 32x32."""
+    n = 6
+    a = np.stack([np.eye(32)] * n)
+    g = np.stack([np.eye(32)] * n)
+    b = np.stack([orc.C.gen_gaussian_vector(32, 60 + i) for i in range(n)])
+    a[1, 0, 0] = 0.0                          # ZeroPivot at step 1
+    a[2] = np.eye(32)[::-1]                   # anti-diagonal: step 1
+    a[3, 7, 7] = 0.0                          # step 8
+    a[4, :2, :2] = [[2.0, 1.0], [4.0, 5.0]]   # KAT block: L21 = 2, U = [[2,1],[0,3]]
+    out = rl.batched_preprocess_solve_32(a, g, b)
+    assert list(out.status) == [0, 1, 1, 8, 0, 0]
+    np.testing.assert_array_equal(out.lu[0], np.eye(32))
+    np.testing.assert_array_equal(out.x[0], b[0])  # identity solve is exact
+    assert out.residual[0] == 0.0
+    assert out.lu[4][1, 0] == 2.0 and out.lu[4][0, 0] == 2.0 and out.lu[4][0, 1] == 1.0 and out.lu[4][1, 1] == 3.0
+    assert np.isnan(out.x[1]).all() and np.isnan(out.residual[1])
+    for i in range(n):
+        lu, zs, _ = orc.C.genp_factor(a[i] @ g[i])
+        assert zs == out.status[i]
+
+
+def test_ambiguous_band_verdict_uses_exact_power_iteration(cuda, orc):
+    """Pivots between tol_pivot*floor and tol_pivot*||P||_F force the exact
+    power iteration; the verdict must equal the oracle's genp_factor."""
+    cases = []
+    for piv in (5e-12, 2e-12, 3.3e-12, 3.1e-12, 1.7e-11, 1e-13):
+        p = np.eye(32)
+        p[5, 5] = piv
+        cases.append(p)
+    rng = np.random.default_rng(5)
+    q, _ = np.linalg.qr(rng.standard_normal((32, 32)))
+    p = np.diag(np.linspace(1.0, 2.0, 32)) @ q  # generic matrix, scaled pivot later
+    lu, zs, tol = orc.C.genp_factor(p)
+    cases.append(p)
+    a = np.stack(cases)
+    g = np.stack([np.eye(32)] * len(cases))
+    b = np.ones((len(cases), 32))
+    out = rl.batched_preprocess_solve_32(a, g, b)
+    for i in range(len(cases)):
+        _, zs, _ = orc.C.genp_factor(cases[i])
+        assert out.status[i] == zs, (i, out.status[i], zs)
+    assert list(out.status[:6]) == [0, 6, 0, 6, 0, 6]
+
+
+def test_empty_and_ragged_batches(cuda, orc):
+    for count in (0, 1, 3, 5, 33, 1031):
+        r = orc.C.batched_config2(count, base=7, threads=4, want_lu=True) if count else None
+        if count == 0:
+            out = rl.batched_preprocess_solve_32(np.zeros((0, 32, 32)), np.zeros((0, 32, 32)), np.zeros((0, 32)))
+            assert out.x.shape == (0, 32)
+            continue
+        out = rl.batched_preprocess_solve_32(r["a"], r["g"], r["b"])
+        assert (out.status == 0).all()
+        for i in range(count):
+            assert _rel(out.x[i], r["x"][i]) <= 1e-10 * np.linalg.cond(r["a"][i])
+    with pytest.raises(rl.DimensionError):
+        rl.batched_preprocess_solve_32(np.zeros((2, 31, 31)), np.zeros((2, 31, 31)), np.zeros((2, 31)))
