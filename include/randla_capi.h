@@ -128,7 +128,8 @@ RL_API int rl_abi_version(void);
 RL_API const char* rl_last_error(void);
 RL_API rl_status rl_context_create(int device, rl_context** out);
 RL_API rl_status rl_context_destroy(rl_context* ctx);
-/* use an external cudaStream_t (e.g. torch.cuda.current_stream()); NULL restores the context's own */
+/* enqueue on an external cudaStream_t (e.g. torch.cuda.current_stream()); NULL selects the
+ * legacy default stream. A new context uses its own non-blocking stream. */
 RL_API rl_status rl_context_set_stream(rl_context* ctx, void* cuda_stream);
 RL_API void* rl_context_get_stream(rl_context* ctx);
 RL_API rl_status rl_synchronize(rl_context* ctx);

@@ -150,7 +150,7 @@ RL_API rl_status rl_context_set_stream(rl_context* ctx, void* s) {
     rl_status st;
     ctx = rl::resolve(ctx, &st);
     if (!ctx) return st;
-    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    ctx->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
     return RL_OK;
 }
 
