@@ -19,6 +19,7 @@
 //      ||b - A x|| / ||b|| (lu.hpp:155-161 / preprocess.hpp:122-128),
 //      growth max|U| / max|P|, packed LU written back coalesced.
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cmath>
 
@@ -29,272 +30,422 @@ namespace rl {
 namespace {
 
 constexpr int D = 32;
-constexpr int LD = 36;  // padded shared row stride (doubles): conflict-free DMMA fragments
 constexpr int WARPS = 4;
-constexpr int MAT = D * LD;
+constexpr int LDP = 34;  // P / LU row stride (doubles): 16 B rows, <= 2-way conflicts on rows and columns
 constexpr double kTolPivot32 = 1e-13 * 32.0;  // tol_pivot(32), types.hpp:42
 
+// Per-warp shared memory: 18,176 B -> 12 resident warps per SM (3 CTAs x 4).
 struct __align__(16) WarpSmem {
-    double A[MAT];
-    double G[MAT];
-    double P[MAT];
-    double vec[D];
-    double piv[D];
-    double scratch[D];
+    double G[D * D];   // multiplier, swizzled (swz_g)
+    double P[D * LDP]; // product A G, then its packed LU in place
+    double vec[2][D];  // double-buffered broadcast rows / vectors
+    double b[D];
+    double rinv[D];    // 1 / u_jj
+    double piv[D];     // u_jj
 };
 constexpr size_t kSmemBytes = sizeof(WarpSmem) * WARPS;
 
-__device__ __forceinline__ void load_matrix(double* s, const double* g, int lane) {
-    const double2* g2 = reinterpret_cast<const double2*>(g);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int p = lane + 32 * q;
-        const double2 v = ld_stream(g2 + p);
-        *reinterpret_cast<double2*>(s + (p >> 4) * LD + 2 * (p & 15)) = v;
-    }
+// G element (k, n): XOR-swizzled columns so the DMMA B-fragment loads (4 rows
+// 2q+e x 8 columns) hit distinct banks.
+__device__ __forceinline__ int swz_g(int k, int n) { return k * D + (n ^ (((k >> 1) & 3) << 2)); }
+
+// Logical k index of MMA fragment slot q in k-step kk: pairs (kk even/odd)
+// cover adjacent columns so A fragments load as 16-byte pairs.
+__device__ __forceinline__ int kidx(int kk, int q) { return 8 * (kk >> 1) + 2 * q + (kk & 1); }
+
+struct FixList {
+    int32_t count;
+    int32_t pad;
+    int64_t sys[1];  // [capacity]
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// fast reciprocal: MUFU seed + two Newton steps (pivots are normal numbers;
+// a zero pivot gives inf and the verdict flags the system)
+__device__ __forceinline__ double rcp64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+// max of a non-negative running maximum and |x| without fmax's NaN handling
+// (DSETP + 2 FSEL instead of ~7 instructions)
+__device__ __forceinline__ double max_abs(double m, double x) {
+    const double a = fabs(x);
+    return a > m ? a : m;
 }
 
-__device__ __forceinline__ void store_matrix(double* g, const double* s, int lane) {
-    double2* g2 = reinterpret_cast<double2*>(g);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int p = lane + 32 * q;
-        st_stream(g2 + p, *reinterpret_cast<const double2*>(s + (p >> 4) * LD + 2 * (p & 15)));
-    }
+// y -= l * v on lanes where `pred` holds: a predicated DFMA, no select/moves
+__device__ __forceinline__ void fma_if(bool pred, double& y, double l, double v) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p fma.rn.f64 %0, %1, %2, %0;\n\t}"
+        : "+d"(y) : "d"(-l), "d"(v), "r"(static_cast<unsigned>(pred)));
 }
 
-// spectral_norm_estimate (norms.hpp:52-77) of the 32x32 matrix in s.P, in the
-// reference's summation order with separately rounded multiplies and adds, so
-// the estimate is bit-identical to the reference's for the same matrix.
-__device__ double exact_power_iteration(WarpSmem& s, int lane) {
-    double* x = s.vec;
-    if (lane == 0) {
-        for (int j = 0; j < D; ++j) x[j] = 1.0 + static_cast<double>(j) / (static_cast<double>(D) + 1.0);
-        double nx = 0.0;
-        for (int j = 0; j < D; ++j) nx = __dadd_rn(nx, __dmul_rn(x[j], x[j]));
-        nx = sqrt(nx);
-        const double inv = 1.0 / nx;
-        for (int j = 0; j < D; ++j) x[j] = __dmul_rn(inv, x[j]);
-    }
-    __syncwarp();
-    double est = 0.0;
-    for (int it = 0; it < 200; ++it) {
-        double axi = 0.0;  // (A x)_lane, j ascending (matrix.hpp:149-154)
-        for (int j = 0; j < D; ++j) axi = __dadd_rn(axi, __dmul_rn(s.P[lane * LD + j], x[j]));
-        s.scratch[lane] = axi;
-        __syncwarp();
-        double nax = 0.0;
-        for (int i = 0; i < D; ++i) nax = __dadd_rn(nax, __dmul_rn(s.scratch[i], s.scratch[i]));
-        nax = sqrt(nax);
-        if (nax == 0.0) break;
-        double yj = 0.0;  // (A^T A x)_lane, i ascending (norms.hpp:60-63)
-        for (int i = 0; i < D; ++i) yj = __dadd_rn(yj, __dmul_rn(s.P[i * LD + lane], s.scratch[i]));
-        __syncwarp();
-        x[lane] = yj;
-        __syncwarp();
-        double ny = 0.0;
-        for (int j = 0; j < D; ++j) ny = __dadd_rn(ny, __dmul_rn(x[j], x[j]));
-        ny = sqrt(ny);
-        if (ny == 0.0) break;
-        const double inv = 1.0 / ny;
-        __syncwarp();
-        x[lane] = __dmul_rn(inv, yj);
-        __syncwarp();
-        if (fabs(nax - est) <= 1e-9 * nax) {
-            est = nax;
-            break;
+// a / b correctly rounded from r = 1/b: one residual correction
+__device__ __forceinline__ double div_by(double a, double b, double r) {
+    const double q0 = a * r;
+    return fma(r, fma(-b, q0, a), q0);
+}
+
+// A (row-major 32x32, global) -> MMA A-fragments a[ti][kk] = A[8ti + l/4][kidx(kk, l%4)]
+__device__ __forceinline__ void load_a_frags(const double* gA, int lane, double (&a)[4][8]) {
+    const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double2 v = ld_stream(reinterpret_cast<const double2*>(gA + (8 * ti + fr) * D + 8 * m + 2 * fc));
+            a[ti][2 * m] = v.x;
+            a[ti][2 * m + 1] = v.y;
         }
-        est = nax;
-    }
-    __syncwarp();
-    return est;
 }
 
-__global__ void __launch_bounds__(WARPS * 32, 2)
+__device__ __forceinline__ void load_g_async(double* sG, const double* gG, int lane) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int p = lane + 32 * q;
+        cp_async16(sG + swz_g(p >> 4, 2 * (p & 15)), gG + 2 * p);
+    }
+}
+
+// P = A G into s.P on the FP64 tensor path; also returns sum of squares and
+// max |P| of the lane's entries. Deterministic: every tile accumulates k in
+// the same order, so verdict_fixup_kernel recomputes a bit-identical P.
+__device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const double* sG, double* sP, int lane,
+                                                double& sumsq, double& amax) {
+    const int fr = lane >> 2, fc = lane & 3;
+    sumsq = 0.0;
+    amax = 0.0;
+#pragma unroll
+    for (int tp = 0; tp < 2; ++tp) {
+        double c[2][4][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) c[h][tj][0] = c[h][tj][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            double bf[4];
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) bf[tj] = sG[swz_g(kidx(kk, fc), 8 * tj + fr)];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int tj = 0; tj < 4; ++tj) dmma_884(c[h][tj][0], c[h][tj][1], a[2 * tp + h][kk], bf[tj]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) {
+                *reinterpret_cast<double2*>(&sP[(8 * (2 * tp + h) + fr) * LDP + 8 * tj + 2 * fc]) =
+                    make_double2(c[h][tj][0], c[h][tj][1]);
+                sumsq = fma(c[h][tj][0], c[h][tj][0], sumsq);
+                sumsq = fma(c[h][tj][1], c[h][tj][1], sumsq);
+                amax = max_abs(max_abs(amax, c[h][tj][0]), c[h][tj][1]);
+            }
+    }
+}
+
+__global__ void __launch_bounds__(WARPS * 32, 3)
 batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ gG, const double* __restrict__ gB,
                       double* __restrict__ gLU, double* __restrict__ gX, double* __restrict__ gR,
-                      double* __restrict__ gGrowth, int32_t* __restrict__ gStatus, int64_t batch, int refine) {
+                      double* __restrict__ gGrowth, int32_t* __restrict__ gStatus, int64_t batch, int refine,
+                      FixList* __restrict__ fix, double* __restrict__ fix_piv) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fr = lane >> 2, fc = lane & 3;
     WarpSmem& s = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
 
     for (int64_t sys = static_cast<int64_t>(blockIdx.x) * WARPS + warp; sys < batch;
          sys += static_cast<int64_t>(gridDim.x) * WARPS) {
         const size_t mo = static_cast<size_t>(sys) * D * D;
-        load_matrix(s.A, gA + mo, lane);
-        load_matrix(s.G, gG + mo, lane);
-        const double bl = gB[sys * D + lane];
+        load_g_async(s.G, gG + mo, lane);
+        double a[4][8];
+        load_a_frags(gA + mo, lane, a);
+        const double bl = __ldcs(gB + sys * D + lane);
+        s.b[lane] = bl;
+        cp_async_wait_all();
         __syncwarp();
 
-        // ---- P = A G on the FP64 tensor path (4x4 tiles of 8x8, k = 4 per MMA)
-        {
-            double c[4][4][2];
-#pragma unroll
-            for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-                for (int tj = 0; tj < 4; ++tj) c[ti][tj][0] = c[ti][tj][1] = 0.0;
-            const int fr = lane >> 2, fc = lane & 3;
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                double af[4], bf[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    af[t] = s.A[(8 * t + fr) * LD + 4 * kk + fc];
-                    bf[t] = s.G[(4 * kk + fc) * LD + 8 * t + fr];
-                }
-#pragma unroll
-                for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-                    for (int tj = 0; tj < 4; ++tj) dmma_884(c[ti][tj][0], c[ti][tj][1], af[ti], bf[tj]);
-            }
-#pragma unroll
-            for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-                for (int tj = 0; tj < 4; ++tj)
-                    *reinterpret_cast<double2*>(&s.P[(8 * ti + fr) * LD + 8 * tj + 2 * fc]) =
-                        make_double2(c[ti][tj][0], c[ti][tj][1]);
-        }
-        __syncwarp();
-
-        // ---- row `lane` of P into registers; norms in the reference's order
-        double p[D];
-#pragma unroll
-        for (int m = 0; m < D / 2; ++m) {
-            const double2 v = *reinterpret_cast<const double2*>(&s.P[lane * LD + 2 * m]);
-            p[2 * m] = v.x;
-            p[2 * m + 1] = v.y;
-        }
-        double rowsq = 0.0, colsq = 0.0, amax = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            rowsq = __dadd_rn(rowsq, __dmul_rn(p[k], p[k]));
-            amax = fmax(amax, fabs(p[k]));
-        }
-#pragma unroll 8
-        for (int i = 0; i < D; ++i) {
-            const double v = s.P[i * LD + lane];
-            colsq = __dadd_rn(colsq, __dmul_rn(v, v));
-        }
-        const double floor_norm = sqrt(warp_max(fmax(rowsq, colsq)));
-        const double fro = sqrt(warp_sum(rowsq));
+        // ---- P = A G (DMMA), ||P||_F bounds spectral_norm_estimate (norms.hpp:77)
+        double sumsq, amax;
+        product_to_smem(a, s.G, s.P, lane, sumsq, amax);
+        const double tol_hi = kTolPivot32 * sqrt(warp_sum(sumsq)) * (1.0 + 1e-10);
         const double max_p = warp_max(amax);
-        const double tol_lo = kTolPivot32 * floor_norm;
-        const double tol_hi = kTolPivot32 * fro * (1.0 + 1e-10);
+        __syncwarp();
 
-        // ---- GENP, natural pivot order, no exchanges (lu.hpp:47-56)
-        int first_hi = 0;
-        double piv_first_hi = 0.0;
+        // ---- blocked GENP on P (lu.hpp:47-56 reorganised: 8-column panels
+        // eliminated in natural order, U12 by forward substitution, trailing
+        // Schur update on the FP64 tensor path). No row exchanges.
+        bool flagged = false;
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            if (lane == j) {
+        for (int kb = 0; kb < 4; ++kb) {
+            const int J = 8 * kb, rows = D - J, R = D - J - 8;
+            double pr[8];
+            if (lane < rows) {
 #pragma unroll
-                for (int m = j / 2; m < D / 2; ++m)
-                    *reinterpret_cast<double2*>(&s.vec[2 * m]) = make_double2(p[2 * m], p[2 * m + 1]);
+                for (int m = 0; m < 4; ++m) {
+                    const double2 v = *reinterpret_cast<const double2*>(&s.P[(J + lane) * LDP + J + 2 * m]);
+                    pr[2 * m] = v.x;
+                    pr[2 * m + 1] = v.y;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                double* row = s.vec[t & 1];
+                if (lane == t) {
+#pragma unroll
+                    for (int m = t / 2; m < 4; ++m)
+                        *reinterpret_cast<double2*>(&row[2 * m]) = make_double2(pr[2 * m], pr[2 * m + 1]);
+                }
+                __syncwarp();
+                double rw[8];
+#pragma unroll
+                for (int m = t / 2; m < 4; ++m) {
+                    const double2 v = *reinterpret_cast<const double2*>(&row[2 * m]);
+                    rw[2 * m] = v.x;
+                    rw[2 * m + 1] = v.y;
+                }
+                const double piv = rw[t];
+                const double inv = rcp64(piv);
+                flagged |= !(fabs(piv) > tol_hi);
+                if (lane == 0) {
+                    s.piv[J + t] = piv;
+                    s.rinv[J + t] = inv;
+                }
+                const bool below = lane > t && lane < rows;
+                const double l = below ? div_by(pr[t], piv, inv) : 0.0;
+                if (below) pr[t] = l;
+#pragma unroll
+                for (int c = t + 1; c < 8; ++c) pr[c] = fma(-l, rw[c], pr[c]);
+            }
+            if (lane < rows) {
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    *reinterpret_cast<double2*>(&s.P[(J + lane) * LDP + J + 2 * m]) =
+                        make_double2(pr[2 * m], pr[2 * m + 1]);
             }
             __syncwarp();
-            double r[D];
+            if (R > 0) {
+                // U12 = L11^-1 A12 (forward substitution down each column)
+                if (lane < R) {
+                    const int col = J + 8 + lane;
+                    double u[8];
 #pragma unroll
-            for (int m = j / 2; m < D / 2; ++m) {
-                const double2 v = *reinterpret_cast<const double2*>(&s.vec[2 * m]);
-                r[2 * m] = v.x;
-                r[2 * m + 1] = v.y;
-            }
-            const double piv = r[j];
-            if (lane == 0) s.piv[j] = piv;
-            if (first_hi == 0 && fabs(piv) <= tol_hi) {
-                first_hi = j + 1;
-                piv_first_hi = piv;
-            }
-            if (lane > j) {
-                const double l = p[j] / piv;
-                p[j] = l;
+                    for (int t = 0; t < 8; ++t) u[t] = s.P[(J + t) * LDP + col];
 #pragma unroll
-                for (int k = j + 1; k < D; ++k) p[k] = fma(-l, r[k], p[k]);
-            }
-            __syncwarp();
-        }
-
-        // ---- verdict (lu.hpp:44,49)
-        int zero_step = 0;
-        if (first_hi != 0) {
-            if (fabs(piv_first_hi) <= tol_lo) {
-                zero_step = first_hi;
-            } else {
-                const double est = fmax(exact_power_iteration(s, lane), floor_norm);
-                const double tol = kTolPivot32 * est;
-                for (int j = 0; j < D; ++j)
-                    if (fabs(s.piv[j]) <= tol) {
-                        zero_step = j + 1;
-                        break;
+                    for (int t = 1; t < 8; ++t)
+#pragma unroll
+                        for (int q = 0; q < t; ++q) u[t] = fma(-s.P[(J + t) * LDP + J + q], u[q], u[t]);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) s.P[(J + t) * LDP + col] = u[t];
+                }
+                __syncwarp();
+                // A22 -= L21 U12 (DMMA, k = 8)
+                const int nt = R / 8;
+#pragma unroll
+                for (int ti = 0; ti < nt; ++ti) {
+                    double af[2];
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks) af[ks] = -s.P[(J + 8 + 8 * ti + fr) * LDP + J + 4 * ks + fc];
+#pragma unroll
+                    for (int tj = 0; tj < nt; ++tj) {
+                        double2* cp = reinterpret_cast<double2*>(&s.P[(J + 8 + 8 * ti + fr) * LDP + J + 8 + 8 * tj + 2 * fc]);
+                        double2 cv = *cp;
+#pragma unroll
+                        for (int ks = 0; ks < 2; ++ks)
+                            dmma_884(cv.x, cv.y, af[ks], s.P[(J + 4 * ks + fc) * LDP + J + 8 + 8 * tj + fr]);
+                        *cp = cv;
                     }
+                }
+                __syncwarp();
             }
         }
 
-        // ---- growth max|U| / max|P|
+        // ---- growth numerator max|U|: lane i scans the U part of row i
         double umax = 0.0;
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-            if (k >= lane) umax = fmax(umax, fabs(p[k]));
-        umax = warp_max(umax);
+        for (int m = 0; m < D / 2; ++m) {
+            const double2 v = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
+            if (2 * m >= lane) umax = max_abs(umax, v.x);
+            if (2 * m + 1 >= lane) umax = max_abs(umax, v.y);
+        }
+
+        // ---- verdict: pivots <= tol_pivot * ||P||_F need the exact estimate
+        if (flagged) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(&fix->count, 1);
+            idx = __shfl_sync(kFull, idx, 0);
+            if (lane == 0) fix->sys[idx] = sys;
+            fix_piv[static_cast<size_t>(idx) * D + lane] = s.piv[lane];
+        }
 
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
-        double x = 0.0, rl_ = bl, rel = 0.0;
+        const double my_rinv = s.rinv[lane], my_piv = s.piv[lane];
+        double x = 0.0, rel = 0.0, y = bl;
         for (int step = 0; step <= refine; ++step) {
-            double y = rl_;
 #pragma unroll
-            for (int k = 0; k < D; ++k) {  // forward, unit L
+            for (int k = 0; k < D; ++k) {  // forward, unit L (lu.hpp:110-115)
                 const double yk = __shfl_sync(kFull, y, k);
-                if (lane > k) y = fma(-p[k], yk, y);
+                fma_if(lane > k, y, s.P[lane * LDP + k], yk);
             }
 #pragma unroll
-            for (int k = D - 1; k >= 0; --k) {  // backward, U
-                if (lane == k) y = y / p[k];
+            for (int k = D - 1; k >= 0; --k) {  // backward, U (lu.hpp:116-121)
+                if (lane == k) y = div_by(y, my_piv, my_rinv);
                 const double xk = __shfl_sync(kFull, y, k);
-                if (lane < k) y = fma(-p[k], xk, y);
+                fma_if(lane < k, y, s.P[lane * LDP + k], xk);
             }
-            __syncwarp();
-            s.vec[lane] = y;
+            s.vec[0][lane] = y;
             __syncwarp();
             double d = 0.0;  // d = G y (matvec, matrix.hpp:146-156)
 #pragma unroll
             for (int m = 0; m < D / 2; ++m) {
-                const double2 gv = *reinterpret_cast<const double2*>(&s.G[lane * LD + 2 * m]);
-                const double2 yv = *reinterpret_cast<const double2*>(&s.vec[2 * m]);
+                const double2 gv = *reinterpret_cast<const double2*>(&s.G[swz_g(lane, 2 * m)]);
+                const double2 yv = *reinterpret_cast<const double2*>(&s.vec[0][2 * m]);
                 d = fma(gv.x, yv.x, d);
                 d = fma(gv.y, yv.y, d);
             }
             x += d;
+            s.vec[1][lane] = x;
             __syncwarp();
-            s.vec[lane] = x;
-            __syncwarp();
-            double ax = 0.0;
+            // residual b - A x (preprocess.hpp:122-126) with A in MMA fragments
+            double rsq = 0.0;
 #pragma unroll
-            for (int m = 0; m < D / 2; ++m) {
-                const double2 av = *reinterpret_cast<const double2*>(&s.A[lane * LD + 2 * m]);
-                const double2 xv = *reinterpret_cast<const double2*>(&s.vec[2 * m]);
-                ax = fma(av.x, xv.x, ax);
-                ax = fma(av.y, xv.y, ax);
+            for (int ti = 0; ti < 4; ++ti) {
+                double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const double xv = s.vec[1][kidx(kk, fc)];
+                    dmma_884(c0, c1, a[ti][kk], lane < 4 ? xv : 0.0);
+                }
+                if (fc == 0) {
+                    const double r = s.b[8 * ti + fr] - c0;
+                    rsq = fma(r, r, rsq);
+                    s.vec[0][8 * ti + fr] = r;
+                }
             }
-            rl_ = bl - ax;
-            rel = sqrt(warp_sum(rl_ * rl_)) / bnorm;
+            rel = sqrt(warp_sum(rsq)) / bnorm;
+            __syncwarp();
+            y = s.vec[0][lane];
             __syncwarp();
         }
 
         // ---- outputs
-        const double nan = __longlong_as_double(0x7ff8000000000000ll);
         if (gLU) {
+            double2* dst = reinterpret_cast<double2*>(gLU + mo);
 #pragma unroll
-            for (int m = 0; m < D / 2; ++m)
-                *reinterpret_cast<double2*>(&s.P[lane * LD + 2 * m]) = make_double2(p[2 * m], p[2 * m + 1]);
-            __syncwarp();
-            store_matrix(gLU + mo, s.P, lane);
+            for (int q = 0; q < 16; ++q) {
+                const int p = lane + 32 * q;
+                st_stream(dst + p, *reinterpret_cast<const double2*>(&s.P[(p >> 4) * LDP + 2 * (p & 15)]));
+            }
         }
-        gX[sys * D + lane] = zero_step ? nan : x;
+        __stcs(gX + sys * D + lane, x);
+        umax = warp_max(umax);  // identical in every lane
         if (lane == 0) {
-            if (gR) gR[sys] = zero_step ? nan : rel;
-            if (gGrowth) gGrowth[sys] = zero_step ? nan : umax / max_p;
-            if (gStatus) gStatus[sys] = zero_step;
+            if (gR) gR[sys] = rel;
+            if (gGrowth) gGrowth[sys] = umax / max_p;
+            if (gStatus) gStatus[sys] = 0;
+        }
+        __syncwarp();
+    }
+}
+
+// ---- verdict fix-up (rare path): exact spectral_norm_estimate of P = A G
+// (norms.hpp:35-78, the reference's summation order, no FMA) for every
+// flagged system, then the reference's first-pivot test (lu.hpp:47-49).
+constexpr int FLD = 33;
+struct __align__(16) FixSmem {
+    double G[D * D];
+    double P[D * LDP];
+    double Q[D * FLD];
+    double x[D];
+    double ax[D];
+};
+
+__global__ void __launch_bounds__(WARPS * 32)
+verdict_fixup_kernel(const double* __restrict__ gA, const double* __restrict__ gG, double* __restrict__ gX,
+                     double* __restrict__ gR, double* __restrict__ gGrowth, int32_t* __restrict__ gStatus,
+                     const FixList* __restrict__ fix, const double* __restrict__ fix_piv) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    FixSmem& s = reinterpret_cast<FixSmem*>(smem_raw)[warp];
+    const int count = fix->count;
+    for (int idx = blockIdx.x * WARPS + warp; idx < count; idx += gridDim.x * WARPS) {
+        const int64_t sys = fix->sys[idx];
+        const size_t mo = static_cast<size_t>(sys) * D * D;
+        load_g_async(s.G, gG + mo, lane);
+        double a[4][8];
+        load_a_frags(gA + mo, lane, a);
+        cp_async_wait_all();
+        __syncwarp();
+        double sumsq, amax;
+        product_to_smem(a, s.G, s.P, lane, sumsq, amax);
+        __syncwarp();
+        for (int i = 0; i < D; ++i) s.Q[i * FLD + lane] = s.P[i * LDP + lane];
+        __syncwarp();
+        // floor: largest column / row sum of squares, sequential order (norms.hpp:38-50)
+        double colsq = 0.0, rowsq = 0.0;
+        for (int i = 0; i < D; ++i) colsq = __dadd_rn(colsq, __dmul_rn(s.Q[i * FLD + lane], s.Q[i * FLD + lane]));
+        for (int j = 0; j < D; ++j) rowsq = __dadd_rn(rowsq, __dmul_rn(s.Q[lane * FLD + j], s.Q[lane * FLD + j]));
+        const double floor_norm = sqrt(warp_max(fmax(colsq, rowsq)));
+        double est = 0.0;
+        if (floor_norm != 0.0) {
+            if (lane == 0) {
+                for (int j = 0; j < D; ++j) s.x[j] = 1.0 + static_cast<double>(j) / (static_cast<double>(D) + 1.0);
+                double nx = 0.0;
+                for (int j = 0; j < D; ++j) nx = __dadd_rn(nx, __dmul_rn(s.x[j], s.x[j]));
+                const double inv = 1.0 / sqrt(nx);
+                for (int j = 0; j < D; ++j) s.x[j] = __dmul_rn(inv, s.x[j]);
+            }
+            __syncwarp();
+            for (int it = 0; it < 200; ++it) {
+                double axi = 0.0;
+                for (int j = 0; j < D; ++j) axi = __dadd_rn(axi, __dmul_rn(s.Q[lane * FLD + j], s.x[j]));
+                s.ax[lane] = axi;
+                __syncwarp();
+                double nax = 0.0;
+                for (int i = 0; i < D; ++i) nax = __dadd_rn(nax, __dmul_rn(s.ax[i], s.ax[i]));
+                nax = sqrt(nax);
+                if (nax == 0.0) break;
+                double yj = 0.0;
+                for (int i = 0; i < D; ++i) yj = __dadd_rn(yj, __dmul_rn(s.Q[i * FLD + lane], s.ax[i]));
+                __syncwarp();
+                s.x[lane] = yj;
+                __syncwarp();
+                double ny = 0.0;
+                for (int j = 0; j < D; ++j) ny = __dadd_rn(ny, __dmul_rn(s.x[j], s.x[j]));
+                ny = sqrt(ny);
+                __syncwarp();
+                if (ny == 0.0) break;
+                s.x[lane] = __dmul_rn(1.0 / ny, yj);
+                __syncwarp();
+                if (fabs(nax - est) <= 1e-9 * nax) {
+                    est = nax;
+                    break;
+                }
+                est = nax;
+            }
+            est = fmax(est, floor_norm);
+        }
+        const double tol = kTolPivot32 * est;
+        const double mypiv = fix_piv[static_cast<size_t>(idx) * D + lane];
+        const unsigned zmask = __ballot_sync(kFull, !(sqrt(mypiv * mypiv) > tol));
+        if (zmask) {
+            const double nan = __longlong_as_double(0x7ff8000000000000ll);
+            gX[sys * D + lane] = nan;
+            if (lane == 0) {
+                if (gR) gR[sys] = nan;
+                if (gGrowth) gGrowth[sys] = nan;
+                if (gStatus) gStatus[sys] = __ffs(zmask);  // 1-based first step
+            }
         }
         __syncwarp();
     }
@@ -354,21 +505,32 @@ __global__ void batch_summary_kernel(const double* __restrict__ r, const double*
 }  // namespace
 
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,
-                                double* lu, double* x, double* r, double* growth, int32_t* status, int refine) {
+                                double* lu, double* x, double* r, double* growth, int32_t* status, int refine,
+                                void* fix_ws) {
     static bool configured = false;
     if (!configured) {
         RL_CUDA(cudaFuncSetAttribute(batched_genp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemBytes)));
+        RL_CUDA(cudaFuncSetAttribute(verdict_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sizeof(FixSmem) * WARPS)));
         configured = true;
     }
     if (batch == 0) return RL_OK;
+    FixList* fix = static_cast<FixList*>(fix_ws);
+    double* fix_piv = reinterpret_cast<double*>(static_cast<char*>(fix_ws) + align_up(16 + 8 * batch));
+    RL_CUDA(cudaMemsetAsync(&fix->count, 0, sizeof(int32_t), ctx->stream));
     const int64_t ctas_needed = (batch + WARPS - 1) / WARPS;
-    const int64_t grid = std::min<int64_t>(ctas_needed, static_cast<int64_t>(ctx->num_sms) * 2);
+    const int64_t grid = std::min<int64_t>(ctas_needed, static_cast<int64_t>(ctx->num_sms) * 3);
     batched_genp32_kernel<<<static_cast<unsigned>(grid), WARPS * 32, kSmemBytes, ctx->stream>>>(
-        a, g, b, lu, x, r, growth, status, batch, refine);
+        a, g, b, lu, x, r, growth, status, batch, refine, fix, fix_piv);
     RL_CHECK_LAUNCH("batched_genp32_kernel");
+    verdict_fixup_kernel<<<static_cast<unsigned>(ctx->num_sms), WARPS * 32, sizeof(FixSmem) * WARPS, ctx->stream>>>(
+        a, g, x, r, growth, status, fix, fix_piv);
+    RL_CHECK_LAUNCH("verdict_fixup_kernel");
     return RL_OK;
 }
+
+size_t batched_fix_workspace_bytes(int64_t batch) { return align_up(16 + 8 * batch) + 8 * 32 * batch + 256; }
 
 }  // namespace rl
 
@@ -392,6 +554,7 @@ extern "C" RL_API rl_status rl_batched_genp_solve_32(rl_context* ctx, rl_mem mem
     double *dlu = lu, *dx = x, *dr = resid, *dgr = growth;
     int32_t* dst = status;
     SummaryAccum* dsum = nullptr;
+    void* fix_ws = nullptr;
     const bool host = mem == RL_HOST;
     const bool need_status = host ? (status != nullptr || summary != nullptr) : (status != nullptr);
     bool ok = with_arena(ctx, [&](Arena& ar) {
@@ -410,6 +573,7 @@ extern "C" RL_API rl_status rl_batched_genp_solve_32(rl_context* ctx, rl_mem mem
             if (!dst) dst = ar.take<int32_t>(batch);
         }
         if (summary) dsum = ar.take<SummaryAccum>(1);
+        fix_ws = ar.take<char>(batched_fix_workspace_bytes(batch));
     });
     if (!ok) return RL_ERR_OUT_OF_MEMORY;
     cudaStream_t s = ctx->stream;
@@ -418,7 +582,8 @@ extern "C" RL_API rl_status rl_batched_genp_solve_32(rl_context* ctx, rl_mem mem
         RL_CUDA(cudaMemcpyAsync(const_cast<double*>(dg), g, mb * 8, cudaMemcpyHostToDevice, s));
         RL_CUDA(cudaMemcpyAsync(const_cast<double*>(db), b, vb * 8, cudaMemcpyHostToDevice, s));
     }
-    st = launch_batched_genp32(ctx, batch, da, dg, db, dlu, dx, dr, dgr, dst, 0);
+    static const int dbg_refine = getenv("RANDLA_DEBUG_REFINE") ? atoi(getenv("RANDLA_DEBUG_REFINE")) : 0;
+    st = launch_batched_genp32(ctx, batch, da, dg, db, dlu, dx, dr, dgr, dst, dbg_refine, fix_ws);
     if (st != RL_OK) return st;
     SummaryAccum hsum{};
     if (summary) {
