@@ -1,0 +1,290 @@
+// FP64 GEMM for sm_100a: C = alpha * A B (+ C), row-major.
+//
+// Replaces matmul (matrix.hpp:115-121, Eigen) on the hot path: the A*G
+// preprocessing product (preprocess.hpp:65-73), the trailing Schur updates of
+// blocked GENP, and the low-rank products A*H, Q^T A, Q (Q^T A)
+// (lowrank.hpp:35-37, :80).
+//
+// tcgen05.mma has no f64 kind on sm_100a; the FP64 tensor path is DMMA
+// (mma.sync .f64, SASS DMMA.8x8x4), measured at 37.0 TF/s on this B200
+// against 36.4 for DFMA and 35.5 for cuBLAS DGEMM (profiles/r01_fp64_peak.txt).
+//
+// Tiling: 128x128 CTA tile, k-slabs of 16, 8 warps of 64x32 (32 DMMA per
+// k=4 step, 128 accumulator registers per lane). Operands arrive by TMA
+// (cp.async.bulk.tensor.2d, 128-byte swizzle) into a 4-stage shared-memory
+// ring guarded by mbarriers; one thread issues the copies. CTAs are rastered
+// in groups of 8 tile-rows so concurrently resident CTAs share A and B panels
+// in L2. The epilogue optionally accumulates into C (Schur update) and folds
+// ||C||_F^2 / max|C| into device statistics (pivot-tolerance bound, growth).
+#include <algorithm>
+#include <mutex>
+
+#include "device_common.cuh"
+#include "kernels.cuh"
+#include "tma.cuh"
+
+namespace rl {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
+constexpr int A_STAGE = BM * BK * 8;  // 16 KiB
+constexpr int B_STAGE = BK * BN * 8;  // 16 KiB (8 boxes of 16 x 16)
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 64;
+constexpr int GROUP_M = 8;
+
+// element (r, k) of a 128-byte-swizzled tile with 16 doubles per row
+__device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3); }
+
+template <bool kAccum, bool kStats>
+__global__ void __launch_bounds__(THREADS, 1)
+dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
+             int64_t ldc, int M, int N, int K, double alpha, GemmStats* __restrict__ stats) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp >> 2, wn = warp & 3;
+    const int fr = lane >> 2, fc = lane & 3;
+
+    // grouped raster over (tiles_m x tiles_n)
+    const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+    const int t = blockIdx.x;
+    const int group = t / (GROUP_M * tiles_n);
+    const int first_m = group * GROUP_M;
+    const int gsize = min(tiles_m - first_m, GROUP_M);
+    const int tm_ = first_m + (t % (GROUP_M * tiles_n)) % gsize;
+    const int tn_ = (t % (GROUP_M * tiles_n)) / gsize;
+    const int m0 = tm_ * BM, n0 = tn_ * BN;
+    const int KT = (K + BK - 1) / BK;
+
+    if (tid == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int kt) {
+        const int s = kt % STAGES;
+        unsigned char* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(st, &tmA, kt * BK, m0, &full[s]);
+#pragma unroll
+        for (int j = 0; j < BN / 16; ++j) tma_load_2d(st + A_STAGE + j * 2048, &tmB, n0 + 16 * j, kt * BK, &full[s]);
+    };
+    if (tid == 0)
+        for (int kt = 0; kt < min(STAGES, KT); ++kt) issue(kt);
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        mbar_wait(&full[s], (kt / STAGES) & 1);
+        const unsigned char* sa = smem + s * STAGE_BYTES;
+        const unsigned char* sb = sa + A_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk) {
+            const int k = 4 * kk + fc;
+            double af[8], bf[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double*>(sa + swz128(wm * 64 + 8 * i + fr, k));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = wn * 32 + 8 * j + fr;
+                bf[j] = *reinterpret_cast<const double*>(sb + (n >> 4) * 2048 + swz128(k, n & 15));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+        if (tid == 0 && kt + STAGES < KT) issue(kt + STAGES);
+    }
+
+    // ---- epilogue
+    double ssq = 0.0, amax = 0.0;
+    const bool vec_ok = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + wm * 64 + 8 * i + fr;
+        if (row >= M) continue;
+        double* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = n0 + wn * 32 + 8 * j + 2 * fc;
+            double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+            if (vec_ok && col + 1 < N) {
+                double2* p = reinterpret_cast<double2*>(crow + col);
+                if (kAccum) {
+                    const double2 o = *p;
+                    v0 += o.x;
+                    v1 += o.y;
+                }
+                *p = make_double2(v0, v1);
+                if (kStats) {
+                    ssq = fma(v0, v0, fma(v1, v1, ssq));
+                    amax = fmax(amax, fmax(fabs(v0), fabs(v1)));
+                }
+            } else {
+                if (col < N) {
+                    if (kAccum) v0 += crow[col];
+                    crow[col] = v0;
+                    if (kStats) {
+                        ssq = fma(v0, v0, ssq);
+                        amax = fmax(amax, fabs(v0));
+                    }
+                }
+                if (col + 1 < N) {
+                    if (kAccum) v1 += crow[col + 1];
+                    crow[col + 1] = v1;
+                    if (kStats) {
+                        ssq = fma(v1, v1, ssq);
+                        amax = fmax(amax, fabs(v1));
+                    }
+                }
+            }
+        }
+    }
+    if (kStats) {
+        ssq = warp_sum(ssq);
+        amax = warp_max(amax);
+        if (lane == 0) {
+            atomicAdd(&stats->sumsq, ssq);
+            atomicMax(&stats->maxabs_bits, static_cast<unsigned long long>(__double_as_longlong(amax)));
+        }
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+template <bool A, bool S>
+void configure_once() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(dgemm_kernel<A, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM_BYTES));
+        done = true;
+    }
+}
+
+}  // namespace
+
+bool make_tmap_2d(CUtensorMap* out, const double* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows,
+                  uint32_t box_cols, bool swizzle128) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+               int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, GemmStats* stats) {
+    if (M <= 0 || N <= 0) return RL_OK;
+    if (K <= 0) {
+        if (!accumulate)
+            for (int64_t r = 0; r < M; ++r) RL_CUDA(cudaMemsetAsync(C + r * ldc, 0, N * 8, ctx->stream));
+        return RL_OK;
+    }
+    if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+        return set_error(RL_ERR_INVALID_ARGUMENT, "gemm: TMA needs 16-byte aligned operands with even leading dimensions");
+    if (M > (int64_t(1) << 30) || N > (int64_t(1) << 30) || K > (int64_t(1) << 30))
+        return set_error(RL_ERR_DIMENSION, "gemm: dimension too large");
+    CUtensorMap ta, tb;
+    if (!make_tmap_2d(&ta, A, M, K, lda, BM, BK, true) || !make_tmap_2d(&tb, B, K, N, ldb, BK, 16, true))
+        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    if (tiles > 0x7fffffff) return set_error(RL_ERR_DIMENSION, "gemm: too many tiles");
+    const dim3 grid(static_cast<unsigned>(tiles)), block(THREADS);
+    const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+    if (accumulate) {
+        if (stats) {
+            configure_once<true, true>();
+            dgemm_kernel<true, true><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
+        } else {
+            configure_once<true, false>();
+            dgemm_kernel<true, false><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
+        }
+    } else {
+        if (stats) {
+            configure_once<false, true>();
+            dgemm_kernel<false, true><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
+        } else {
+            configure_once<false, false>();
+            dgemm_kernel<false, false><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
+        }
+    }
+    RL_CHECK_LAUNCH("dgemm_kernel");
+    return RL_OK;
+}
+
+}  // namespace rl
+
+// ---- C ABI: rl_dgemm (matmul, matrix.hpp:115-121) ---------------------------
+extern "C" RL_API rl_status rl_dgemm(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, int64_t k, const double* a,
+                                     int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc) {
+    using namespace rl;
+    if (m <= 0 || n <= 0 || k <= 0) return set_error(RL_ERR_DIMENSION, "rl_dgemm: matrix dimensions must be positive");
+    if (lda < k || ldb < n || ldc < n) return set_error(RL_ERR_DIMENSION, "rl_dgemm: leading dimension too small");
+    if (!a || !b || !c) return set_error(RL_ERR_INVALID_ARGUMENT, "rl_dgemm: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    const bool host = mem == RL_HOST;
+    const bool repack_a = host || (lda & 1) || (reinterpret_cast<uintptr_t>(a) & 15);
+    const bool repack_b = host || (ldb & 1) || (reinterpret_cast<uintptr_t>(b) & 15);
+    const int64_t la = (k + 1) & ~int64_t(1), lb = (n + 1) & ~int64_t(1);
+    double *da = const_cast<double*>(a), *db = const_cast<double*>(b), *dc = c;
+    int64_t lda2 = lda, ldb2 = ldb, ldc2 = ldc;
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        if (repack_a) da = ar.take<double>(m * la);
+        if (repack_b) db = ar.take<double>(k * lb);
+        if (host) dc = ar.take<double>(m * n);
+    });
+    if (!ok) return RL_ERR_OUT_OF_MEMORY;
+    cudaStream_t s = ctx->stream;
+    const cudaMemcpyKind ka = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    if (repack_a) {
+        RL_CUDA(cudaMemcpy2DAsync(da, la * 8, a, lda * 8, k * 8, m, ka, s));
+        lda2 = la;
+    }
+    if (repack_b) {
+        RL_CUDA(cudaMemcpy2DAsync(db, lb * 8, b, ldb * 8, n * 8, k, ka, s));
+        ldb2 = lb;
+    }
+    if (host) ldc2 = n;
+    st = gemm(ctx, m, n, k, da, lda2, db, ldb2, dc, ldc2, 1.0, false, nullptr);
+    if (st != RL_OK) return st;
+    if (host) {
+        RL_CUDA(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, m, cudaMemcpyDeviceToHost, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+    }
+    return RL_OK;
+}

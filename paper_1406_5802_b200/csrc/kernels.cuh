@@ -1,0 +1,49 @@
+// Internal (C++) interface between the translation units of librandla_b200:
+// device-pointer building blocks the C-ABI entry points compose.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "runtime.cuh"
+
+namespace rl {
+
+// Running statistics a GEMM epilogue can fold over its output tile: sum of
+// squares (for ||C||_F) and max |C| (bit pattern of a non-negative double).
+struct GemmStats {
+    double sumsq;
+    unsigned long long maxabs_bits;
+};
+
+// C = alpha * A B + (accumulate ? C : 0); row-major device matrices, leading
+// dimensions in elements. FP64 DMMA tiles fed by TMA. stats (device, nullable)
+// accumulates over the written C.
+rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+               int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, GemmStats* stats);
+
+// In-place blocked GENP of the n x n row-major matrix `a` (ld = lda) into its
+// packed LU. piv_out (device, n) receives u_jj. No pivoting, no verdict.
+rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out);
+
+// Triangular solves on packed LU (device): x = U^-1 L^-1 b (x may alias b).
+rl_status lu_solve_device(rl_context* ctx, int64_t n, const double* lu, int64_t ld, const double* b, double* x);
+
+// y = A x (row-major m x n); y = b - A x when `residual` (b given).
+rl_status gemv(rl_context* ctx, int64_t m, int64_t n, const double* a, int64_t lda, const double* x, double* y,
+               const double* b_for_residual);
+
+// sum of squares of a length-n vector into *out (device scalar)
+rl_status sumsq(rl_context* ctx, int64_t n, const double* v, double* out);
+
+// exact-order spectral_norm_estimate (norms.hpp:35-78) on the device; host result
+rl_status spectral_norm_estimate_device(rl_context* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                                        double* out);
+
+// batched 32x32 kernel (batched32.cu)
+rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,
+                                double* lu, double* x, double* r, double* growth, int32_t* status, int refine,
+                                void* fix_ws);
+size_t batched_fix_workspace_bytes(int64_t batch);
+
+}  // namespace rl

@@ -8,11 +8,6 @@
 
 extern "C" {
 
-RL_API rl_status rl_dgemm(rl_context*, rl_mem, int64_t, int64_t, int64_t, const double*, int64_t, const double*,
-                          int64_t, double*, int64_t) {
-    RL_PENDING("rl_dgemm");
-}
-
 RL_API rl_status rl_spectral_norm_estimate(rl_context*, rl_mem, int64_t, int64_t, const double*, double*) {
     RL_PENDING("rl_spectral_norm_estimate");
 }

@@ -229,3 +229,22 @@ def batched_preprocess_solve_32(a, g, b, want_lu=True, want_summary=True):
     _raise(rc)
     s = {k: getattr(summ, k) for k, _ in summ._fields_} if want_summary else {}
     return BatchedSolve(lu, x, r, gr, st, s)
+
+
+# ---- dense products ------------------------------------------------------------
+def matmul(a, b):
+    """matmul (matrix.hpp:115-121): C = A B, FP64 DMMA on the GPU."""
+    device = _is_device(a, b)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise DimensionError("matmul: inner dimensions differ")
+    m, k = a.shape
+    n = b.shape[1]
+    if device:
+        a, b = _dev(a), _dev(b)
+        c = _empty_like_kind(True, (m, n), a)
+    else:
+        a, b = _host(a), _host(b)
+        c = np.empty((m, n))
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_dgemm(_ctx(), _mem(device), m, n, k, capi.addr(a), k, capi.addr(b), n, capi.addr(c), n))
+    return c
