@@ -1,0 +1,217 @@
+// Blocked GENP of a dense n x n matrix, in place (packed LU), for sm_100a.
+//
+// Mathematically genp_factor (lu.hpp:40-58): natural pivot order, no row
+// exchanges. Any recursive block factorization with unpivoted leaves "turns
+// into GENP up to the order", so the L and U here are the
+// reference's up to rounding. Structure (recursive, right-looking):
+//
+//   rec(c0, w):  factor columns [c0, c0+w) of the trailing rows [c0, n)
+//     w <= kBase:  panel_diag_kernel   — w x w diagonal block, one CTA in smem
+//                  panel_rows_kernel   — L21 = A21 U11^-1, one row per thread
+//     else:        rec(c0, w1); U12 = L11^-1 A12 (trsm); A22 -= L21 U12 (DMMA
+//                  GEMM, kernels.cuh); rec(c0+w1, w-w1)
+//
+// so nearly all 2n^3/3 flops run in large GEMMs (K = n/2, n/4, ...). The
+// unit-lower TRSM is recursive the same way down to a 64-row base kernel.
+#include <algorithm>
+#include <cmath>
+
+#include "device_common.cuh"
+#include "kernels.cuh"
+
+namespace rl {
+namespace {
+
+constexpr int kBase = 64;  // base panel width / base TRSM size
+
+// ---- w x w diagonal block (w <= 64): GENP in shared memory --------------
+__global__ void __launch_bounds__(256)
+panel_diag_kernel(double* __restrict__ a, int64_t lda, int w, double* __restrict__ piv_out,
+                  double* __restrict__ rinv_out) {
+    __shared__ double s[kBase][kBase + 1];
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < w * w; idx += 256) s[idx / w][idx % w] = a[(idx / w) * lda + idx % w];
+    __syncthreads();
+    const int tx = tid & 15, ty = tid >> 4;
+    for (int j = 0; j < w; ++j) {
+        const double piv = s[j][j];
+        if (tid > j && tid < w) s[tid][j] = s[tid][j] / piv;  // multiplier (lu.hpp:51)
+        __syncthreads();
+        for (int i = j + 1 + ty; i < w; i += 16) {
+            const double l = s[i][j];
+            for (int k = j + 1 + tx; k < w; k += 16) s[i][k] = fma(-l, s[j][k], s[i][k]);
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < w * w; idx += 256) a[(idx / w) * lda + idx % w] = s[idx / w][idx % w];
+    if (tid < w) {
+        piv_out[tid] = s[tid][tid];
+        rinv_out[tid] = 1.0 / s[tid][tid];
+    }
+}
+
+// a / b correctly rounded from r = 1/b (one residual correction)
+__device__ __forceinline__ double div_by(double a, double b, double r) {
+    const double q0 = a * r;
+    return fma(r, fma(-b, q0, a), q0);
+}
+
+// ---- rows below the diagonal block: L21 = A21 U11^-1 (row-wise) ---------
+// x U11 = a  ->  x_j = (a_j - sum_{i<j} x_i u_ij) / u_jj, one row per thread.
+template <int W>
+__global__ void __launch_bounds__(128)
+panel_rows_kernel(double* __restrict__ rows, int64_t lda, int64_t nrows, const double* __restrict__ u11,
+                  const double* __restrict__ piv, const double* __restrict__ rinv) {
+    __shared__ double su[W][W];
+    __shared__ double sp[W], sr[W];
+    for (int idx = threadIdx.x; idx < W * W; idx += 128) su[idx / W][idx % W] = u11[(idx / W) * lda + idx % W];
+    if (threadIdx.x < W) {
+        sp[threadIdx.x] = piv[threadIdx.x];
+        sr[threadIdx.x] = rinv[threadIdx.x];
+    }
+    __syncthreads();
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+    if (r >= nrows) return;
+    double2* row = reinterpret_cast<double2*>(rows + r * lda);
+    double x[W];
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+        const double2 v = row[j];
+        x[2 * j] = v.x;
+        x[2 * j + 1] = v.y;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        double acc = x[j];
+#pragma unroll
+        for (int i = 0; i < j; ++i) acc = fma(-x[i], su[i][j], acc);
+        x[j] = div_by(acc, sp[j], sr[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) row[j] = make_double2(x[2 * j], x[2 * j + 1]);
+}
+
+// ---- base TRSM: X = L^-1 B, L unit lower (w x w, w <= 64), column-parallel
+template <int W>
+__global__ void __launch_bounds__(128)
+trsm_lower_unit_kernel(const double* __restrict__ l, int64_t ldl, double* __restrict__ b, int64_t ldb, int64_t ncols) {
+    __shared__ double sl[W][W];
+    for (int idx = threadIdx.x; idx < W * W; idx += 128) sl[idx / W][idx % W] = l[(idx / W) * ldl + idx % W];
+    __syncthreads();
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+    if (c >= ncols) return;
+    double x[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) x[i] = b[i * ldb + c];
+#pragma unroll
+    for (int i = 1; i < W; ++i) {
+        double acc = x[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc = fma(-sl[i][k], x[k], acc);
+        x[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) b[i * ldb + c] = x[i];
+}
+
+// generic (w < 64, e.g. the ragged last block) versions: runtime width
+__global__ void __launch_bounds__(128)
+panel_rows_kernel_dyn(double* __restrict__ rows, int64_t lda, int64_t nrows, int w, const double* __restrict__ u11,
+                      const double* __restrict__ piv, const double* __restrict__ rinv) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+    if (r >= nrows) return;
+    double* x = rows + r * lda;
+    for (int j = 0; j < w; ++j) {
+        double acc = x[j];
+        for (int i = 0; i < j; ++i) acc = fma(-x[i], u11[i * lda + j], acc);
+        x[j] = div_by(acc, piv[j], rinv[j]);
+    }
+}
+
+__global__ void __launch_bounds__(128)
+trsm_lower_unit_kernel_dyn(const double* __restrict__ l, int64_t ldl, int w, double* __restrict__ b, int64_t ldb,
+                           int64_t ncols) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+    if (c >= ncols) return;
+    for (int i = 1; i < w; ++i) {
+        double acc = b[i * ldb + c];
+        for (int k = 0; k < i; ++k) acc = fma(-l[i * ldl + k], b[k * ldb + c], acc);
+        b[i * ldb + c] = acc;
+    }
+}
+
+struct Ctx {
+    rl_context* ctx;
+    double* a;
+    int64_t n, lda;
+    double* piv;
+    double* rinv;
+};
+
+// X = L^-1 B for the unit-lower diagonal block L = a[r0:r0+w, r0:r0+w],
+// B = a[r0:r0+w, c0:c0+ncols]
+rl_status trsm(const Ctx& g, int64_t r0, int64_t w, int64_t c0, int64_t ncols) {
+    if (ncols <= 0 || w <= 1) return RL_OK;
+    double* L = g.a + r0 * g.lda + r0;
+    double* B = g.a + r0 * g.lda + c0;
+    if (w <= kBase) {
+        const unsigned blocks = static_cast<unsigned>((ncols + 127) / 128);
+        if (w == kBase)
+            trsm_lower_unit_kernel<kBase><<<blocks, 128, 0, g.ctx->stream>>>(L, g.lda, B, g.lda, ncols);
+        else
+            trsm_lower_unit_kernel_dyn<<<blocks, 128, 0, g.ctx->stream>>>(L, g.lda, static_cast<int>(w), B, g.lda, ncols);
+        RL_CHECK_LAUNCH("trsm_lower_unit_kernel");
+        return RL_OK;
+    }
+    const int64_t w1 = std::max<int64_t>(kBase, (w / 2) / kBase * kBase);
+    rl_status st = trsm(g, r0, w1, c0, ncols);
+    if (st != RL_OK) return st;
+    // B2 -= L21 B1
+    st = gemm(g.ctx, w - w1, ncols, w1, g.a + (r0 + w1) * g.lda + r0, g.lda, g.a + r0 * g.lda + c0, g.lda,
+              g.a + (r0 + w1) * g.lda + c0, g.lda, -1.0, true, nullptr);
+    if (st != RL_OK) return st;
+    return trsm(g, r0 + w1, w - w1, c0, ncols);
+}
+
+rl_status panel(const Ctx& g, int64_t c0, int64_t w) {
+    const int64_t m = g.n - c0;
+    double* d = g.a + c0 * g.lda + c0;
+    panel_diag_kernel<<<1, 256, 0, g.ctx->stream>>>(d, g.lda, static_cast<int>(w), g.piv + c0, g.rinv + c0);
+    RL_CHECK_LAUNCH("panel_diag_kernel");
+    const int64_t rows = m - w;
+    if (rows > 0) {
+        const unsigned blocks = static_cast<unsigned>((rows + 127) / 128);
+        double* r = g.a + (c0 + w) * g.lda + c0;
+        if (w == kBase)
+            panel_rows_kernel<kBase><<<blocks, 128, 0, g.ctx->stream>>>(r, g.lda, rows, d, g.piv + c0, g.rinv + c0);
+        else
+            panel_rows_kernel_dyn<<<blocks, 128, 0, g.ctx->stream>>>(r, g.lda, rows, static_cast<int>(w), d,
+                                                                     g.piv + c0, g.rinv + c0);
+        RL_CHECK_LAUNCH("panel_rows_kernel");
+    }
+    return RL_OK;
+}
+
+rl_status rec(const Ctx& g, int64_t c0, int64_t w) {
+    if (w <= kBase) return panel(g, c0, w);
+    const int64_t w1 = std::max<int64_t>(kBase, (w / 2) / kBase * kBase);
+    rl_status st = rec(g, c0, w1);
+    if (st != RL_OK) return st;
+    st = trsm(g, c0, w1, c0 + w1, w - w1);
+    if (st != RL_OK) return st;
+    // A22 -= L21 U12   (rows c0+w1 .. n, cols c0+w1 .. c0+w)
+    st = gemm(g.ctx, g.n - c0 - w1, w - w1, w1, g.a + (c0 + w1) * g.lda + c0, g.lda, g.a + c0 * g.lda + c0 + w1,
+              g.lda, g.a + (c0 + w1) * g.lda + c0 + w1, g.lda, -1.0, true, nullptr);
+    if (st != RL_OK) return st;
+    return rec(g, c0 + w1, w - w1);
+}
+
+}  // namespace
+
+rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out) {
+    if (n <= 0) return RL_OK;
+    Ctx g{ctx, a, n, lda, piv_out, rinv_out};
+    return rec(g, 0, n);
+}
+
+}  // namespace rl

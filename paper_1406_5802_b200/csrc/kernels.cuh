@@ -22,12 +22,16 @@ struct GemmStats {
 rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, GemmStats* stats);
 
-// In-place blocked GENP of the n x n row-major matrix `a` (ld = lda) into its
-// packed LU. piv_out (device, n) receives u_jj. No pivoting, no verdict.
-rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out);
+// In-place blocked GENP of the n x n row-major matrix `a` (ld = lda, even,
+// 16-byte aligned) into its packed LU. piv_out / rinv_out (device, n) receive
+// u_jj and 1/u_jj. No pivoting, no verdict (the caller decides it).
+rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out);
 
 // Triangular solves on packed LU (device): x = U^-1 L^-1 b (x may alias b).
-rl_status lu_solve_device(rl_context* ctx, int64_t n, const double* lu, int64_t ld, const double* b, double* x);
+// `rinv` (nullable) = 1/u_jj from genp_inplace; `work` >= lu_solve_work_bytes(n).
+rl_status lu_solve_device(rl_context* ctx, int64_t n, const double* lu, int64_t ld, const double* rinv,
+                          const double* b, double* x, void* work);
+size_t lu_solve_work_bytes(int64_t n);
 
 // y = A x (row-major m x n); y = b - A x when `residual` (b given).
 rl_status gemv(rl_context* ctx, int64_t m, int64_t n, const double* a, int64_t lda, const double* x, double* y,

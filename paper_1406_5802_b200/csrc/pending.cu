@@ -8,24 +8,6 @@
 
 extern "C" {
 
-RL_API rl_status rl_spectral_norm_estimate(rl_context*, rl_mem, int64_t, int64_t, const double*, double*) {
-    RL_PENDING("rl_spectral_norm_estimate");
-}
-
-RL_API rl_status rl_genp_factor(rl_context*, rl_mem, int64_t, const double*, double*, rl_solve_info*) {
-    RL_PENDING("rl_genp_factor");
-}
-
-RL_API rl_status rl_lu_solve(rl_context*, rl_mem, int64_t, const double*, const double*, double*) {
-    RL_PENDING("rl_lu_solve");
-}
-
-RL_API rl_status rl_preprocessed_genp_solve(rl_context*, rl_mem, int64_t, const double*, const double*,
-                                            const rl_multiplier*, int64_t, double*, double*, int32_t,
-                                            rl_solve_info*) {
-    RL_PENDING("rl_preprocessed_genp_solve");
-}
-
 RL_API rl_status rl_circulant_right_multiply(rl_context*, rl_mem, int64_t, int64_t, const double*, const double*,
                                              double*) {
     RL_PENDING("rl_circulant_right_multiply");

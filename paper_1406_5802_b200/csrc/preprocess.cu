@@ -1,0 +1,413 @@
+// C-ABI entry points of the dense path:
+//   rl_preprocessed_genp_solve  preprocess_solve (preprocess.hpp:156-180)
+//   rl_genp_factor              genp_factor      (lu.hpp:40-58)
+//   rl_lu_solve                 lu_solve         (lu.hpp:100-123)
+//   rl_spectral_norm_estimate   spectral_norm_estimate (norms.hpp:35-78)
+//
+// The pivot verdict (lu.hpp:44,49: first j with |u_jj| <= tol_pivot(n) *
+// spectral_norm_estimate(product)) is decided without the power iteration in
+// the common case: floor <= estimate <= ||product||_F (norms.hpp:38-50,77),
+// so when every pivot exceeds tol_pivot(n) * ||product||_F the verdict is
+// "no ZeroPivot". Only when some pivot falls at or below that bound is the
+// estimate evaluated, in the reference's exact summation order, on a
+// recomputed product (the GEMM is deterministic, so it is bit-identical).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "device_common.cuh"
+#include "kernels.cuh"
+
+extern "C" RL_API rl_status rl_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out);
+
+namespace rl {
+namespace {
+
+__global__ void pivot_scan_kernel(const double* __restrict__ piv, int64_t n, double tol, double* __restrict__ out_min,
+                                  unsigned long long* __restrict__ out_first) {
+    __shared__ double smin[32];
+    __shared__ unsigned long long sfirst[32];
+    double mn = INFINITY;
+    unsigned long long first = ~0ull;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double a = fabs(piv[i]);
+        mn = fmin(mn, a);
+        if (!(a > tol) && static_cast<unsigned long long>(i) < first) first = static_cast<unsigned long long>(i);
+    }
+    mn = warp_min(mn);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long f = __shfl_xor_sync(kFull, first, o);
+        first = f < first ? f : first;
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        smin[w] = mn;
+        sfirst[w] = first;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) {
+            mn = fmin(mn, smin[i]);
+            first = sfirst[i] < first ? sfirst[i] : first;
+        }
+        *out_min = mn;
+        *out_first = first;
+    }
+}
+
+// sum of squares and max |.| over a rows x cols matrix (one block per row);
+// upper_only restricts row i to columns >= i (max |U| of a packed LU)
+__global__ void matrix_stats_kernel(const double* __restrict__ a, int64_t ld, int64_t cols, bool upper_only,
+                                    GemmStats* __restrict__ out) {
+    const int64_t row = blockIdx.x;
+    double s = 0.0, m = 0.0;
+    for (int64_t k = (upper_only ? row : 0) + threadIdx.x; k < cols; k += blockDim.x) {
+        const double v = a[row * ld + k];
+        s = fma(v, v, s);
+        m = fmax(m, fabs(v));
+    }
+    s = warp_sum(s);
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) {
+        if (!upper_only) atomicAdd(&out->sumsq, s);
+        atomicMax(&out->maxabs_bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+    }
+}
+
+__global__ void axpy_kernel(double* __restrict__ x, const double* __restrict__ d, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) x[i] += d[i];
+}
+
+struct Scalars {
+    GemmStats prod;   // ||product||_F^2, max|product|
+    GemmStats upper;  // max|U|
+    double pivmin;
+    unsigned long long first;
+    double bsq[66];   // sumsq scratch, result at [0]
+    double rsq[66];
+};
+
+double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+}
+
+unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+struct Dense {
+    int64_t n = 0, ld = 0;
+    double *A = nullptr, *G = nullptr, *P = nullptr;
+    double *b = nullptr, *x = nullptr, *r = nullptr, *y = nullptr, *d = nullptr, *piv = nullptr, *rinv = nullptr;
+    void* solve_work = nullptr;
+    Scalars* sc = nullptr;
+};
+
+// P = A G (or A), blocked GENP in place, growth, verdict (lu.hpp:44-49).
+rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_info* info) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = D.n;
+    RL_CUDA(cudaMemsetAsync(D.sc, 0, sizeof(Scalars), s));
+    rl_status st;
+    if (have_g) {
+        st = gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, D.P, D.ld, 1.0, false, &D.sc->prod);
+        if (st != RL_OK) return st;
+    } else {
+        RL_CUDA(cudaMemcpy2DAsync(D.P, D.ld * 8, D.A, D.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+        matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(D.P, D.ld, n, false, &D.sc->prod);
+        RL_CHECK_LAUNCH("matrix_stats_kernel");
+    }
+    st = genp_inplace(ctx, n, D.P, D.ld, D.piv, D.rinv);
+    if (st != RL_OK) return st;
+    matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(D.P, D.ld, n, true, &D.sc->upper);
+    RL_CHECK_LAUNCH("matrix_stats_kernel(upper)");
+    Scalars h;
+    RL_CUDA(cudaMemcpyAsync(&h, D.sc, sizeof(GemmStats) * 2, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaStreamSynchronize(s));
+    const double fro = std::sqrt(h.prod.sumsq);
+    const double tol_pivot = 1e-13 * static_cast<double>(n);  // types.hpp:42
+    const double tol_hi = tol_pivot * fro * (1.0 + 1e-10);
+    pivot_scan_kernel<<<1, 1024, 0, s>>>(D.piv, n, tol_hi, &D.sc->pivmin, &D.sc->first);
+    RL_CHECK_LAUNCH("pivot_scan_kernel");
+    RL_CUDA(cudaMemcpyAsync(&h.pivmin, &D.sc->pivmin, 16, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaStreamSynchronize(s));
+    info->min_abs_pivot = h.pivmin;
+    info->max_abs_product = bits_to_double(h.prod.maxabs_bits);
+    info->max_abs_u = bits_to_double(h.upper.maxabs_bits);
+    info->growth = info->max_abs_u / info->max_abs_product;
+    info->norm_frobenius = fro;
+    info->pivot_tolerance = tol_hi;
+    info->norm_estimate = 0.0;
+    info->norm_estimate_evaluated = 0;
+    info->zero_pivot_step = 0;
+    if (h.first == ~0ull) return RL_OK;
+
+    // a pivot at or below tol_pivot * ||P||_F: evaluate the estimate exactly on
+    // a recomputed product and apply the reference's test
+    double* prod = nullptr;  // stream-ordered: D's pointers live in the context workspace
+    RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prod), sizeof(double) * n * D.ld, s));
+    if (have_g)
+        st = gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, prod, D.ld, 1.0, false, nullptr);
+    else
+        RL_CUDA(cudaMemcpy2DAsync(prod, D.ld * 8, D.A, D.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+    double est = 0.0;
+    if (st == RL_OK) st = spectral_norm_estimate_device(ctx, n, n, prod, D.ld, &est);
+    cudaFreeAsync(prod, s);
+    if (st != RL_OK) return st;
+    const double tol = tol_pivot * est;
+    info->norm_estimate = est;
+    info->norm_estimate_evaluated = 1;
+    info->pivot_tolerance = tol;
+    pivot_scan_kernel<<<1, 1024, 0, s>>>(D.piv, n, tol, &D.sc->pivmin, &D.sc->first);
+    RL_CHECK_LAUNCH("pivot_scan_kernel");
+    RL_CUDA(cudaMemcpyAsync(&h.first, &D.sc->first, 8, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaStreamSynchronize(s));
+    if (h.first != ~0ull) {
+        info->zero_pivot_step = static_cast<int64_t>(h.first) + 1;
+        return set_error(RL_ERR_ZERO_PIVOT, "zero pivot at elimination step %lld",
+                         static_cast<long long>(info->zero_pivot_step));
+    }
+    return RL_OK;
+}
+
+// iterative_refine with the chain solver x = G (LU)^-1 r from x0 = 0,
+// refine+1 steps (preprocess.hpp:115-143, :170-178)
+rl_status chain_solve(rl_context* ctx, Dense& D, bool have_g, int64_t refine, rl_solve_info* info) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = D.n;
+    rl_status st = sumsq(ctx, n, D.b, D.sc->bsq);
+    if (st != RL_OK) return st;
+    RL_CUDA(cudaMemsetAsync(D.x, 0, n * 8, s));
+    RL_CUDA(cudaMemcpyAsync(D.r, D.b, n * 8, cudaMemcpyDeviceToDevice, s));  // r = b - A*0
+    double bsq = 0.0;
+    double last = 0.0;
+    int streak = 0;
+    info->history_len = 0;
+    info->diverged = 0;
+    const int64_t steps = refine + 1;
+    for (int64_t k = 0; k < steps; ++k) {
+        st = lu_solve_device(ctx, n, D.P, D.ld, D.rinv, D.r, D.y, D.solve_work);
+        if (st != RL_OK) return st;
+        if (have_g) {
+            st = gemv(ctx, n, n, D.G, D.ld, D.y, D.d, nullptr);
+            if (st != RL_OK) return st;
+        } else {
+            RL_CUDA(cudaMemcpyAsync(D.d, D.y, n * 8, cudaMemcpyDeviceToDevice, s));
+        }
+        axpy_kernel<<<blocks_for(n, 256), 256, 0, s>>>(D.x, D.d, n);
+        RL_CHECK_LAUNCH("axpy_kernel");
+        st = gemv(ctx, n, n, D.A, D.ld, D.x, D.r, D.b);  // r = b - A x
+        if (st != RL_OK) return st;
+        st = sumsq(ctx, n, D.r, D.sc->rsq);
+        if (st != RL_OK) return st;
+        double rsq = 0.0;
+        RL_CUDA(cudaMemcpyAsync(&rsq, D.sc->rsq, 8, cudaMemcpyDeviceToHost, s));
+        if (k == 0) RL_CUDA(cudaMemcpyAsync(&bsq, D.sc->bsq, 8, cudaMemcpyDeviceToHost, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+        if (k == 0) {
+            // history starts at the residual of x0 = 0, which is ||b||/||b|| = 1 (dropped)
+            last = 1.0;
+        }
+        const double rel = std::sqrt(rsq) / std::sqrt(bsq);
+        streak = rel > last ? streak + 1 : 0;
+        if (info->history_len < 8) info->residual_history[info->history_len] = rel;
+        ++info->history_len;
+        last = rel;
+        if (streak >= 2) {
+            info->diverged = 1;
+            break;
+        }
+    }
+    if (info->history_len > 8) info->history_len = 8;
+    return RL_OK;
+}
+
+rl_status dense_alloc(rl_context* ctx, Dense& D, int64_t n, bool need_g, bool own_a, bool own_p) {
+    D.n = n;
+    D.ld = (n + 1) & ~int64_t(1);
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        D.sc = ar.take<Scalars>(1);
+        D.piv = ar.take<double>(n);
+        D.rinv = ar.take<double>(n);
+        D.b = ar.take<double>(n);
+        D.x = ar.take<double>(n);
+        D.r = ar.take<double>(n);
+        D.y = ar.take<double>(n);
+        D.d = ar.take<double>(n);
+        D.solve_work = ar.take<char>(lu_solve_work_bytes(n));
+        if (own_a) D.A = ar.take<double>(n * D.ld);
+        if (need_g) D.G = ar.take<double>(n * D.ld);
+        if (own_p) D.P = ar.take<double>(n * D.ld);
+    });
+    return ok ? RL_OK : RL_ERR_OUT_OF_MEMORY;
+}
+
+rl_status copy_in(rl_context* ctx, double* dst, int64_t ld, const double* src, int64_t rows, int64_t cols, bool host) {
+    RL_CUDA(cudaMemcpy2DAsync(dst, ld * 8, src, cols * 8, cols * 8, rows,
+                              host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->stream));
+    return RL_OK;
+}
+
+rl_status copy_out(rl_context* ctx, double* dst, const double* src, int64_t ld, int64_t rows, int64_t cols, bool host) {
+    RL_CUDA(cudaMemcpy2DAsync(dst, cols * 8, src, ld * 8, cols * 8, rows,
+                              host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+    return RL_OK;
+}
+
+bool aligned_even(const double* p, int64_t ld) {
+    return (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+void clear_info(rl_solve_info* info) { std::memset(info, 0, sizeof(*info)); }
+
+}  // namespace
+}  // namespace rl
+
+using namespace rl;
+
+extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* a,
+                                                       const double* b, const rl_multiplier* post, int64_t refine_steps,
+                                                       double* x, double* lu_out, int32_t want_norm_a,
+                                                       rl_solve_info* info) {
+    rl_solve_info local;
+    if (!info) info = &local;
+    clear_info(info);
+    if (n <= 0) return set_error(RL_ERR_DIMENSION, "preprocess_solve: matrix dimensions must be positive");
+    if (!a || !b || !x) return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: a, b, x are required");
+    if (refine_steps < 0) return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: negative refine_steps");
+    const int kind = post ? post->kind : RL_MULT_NONE;
+    if (kind != RL_MULT_NONE && kind != RL_MULT_GAUSSIAN)
+        return set_error(RL_ERR_UNSUPPORTED, "preprocess_solve: circulant multipliers go through rl_preprocessed_genp_solve_circulant");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    const bool host = mem == RL_HOST;
+    const bool have_g = kind == RL_MULT_GAUSSIAN;
+    const int64_t ld = (n + 1) & ~int64_t(1);
+    // device A can be used in place when it is TMA-compatible (even n, aligned)
+    const bool own_a = host || !((n & 1) == 0 && aligned_even(a, n));
+    const bool g_dev_direct = have_g && !host && post->dense && (n & 1) == 0 && aligned_even(post->dense, n);
+    Dense D;
+    st = dense_alloc(ctx, D, n, have_g && !g_dev_direct, own_a, true);
+    if (st != RL_OK) return st;
+    cudaStream_t s = ctx->stream;
+    if (own_a) {
+        if ((st = copy_in(ctx, D.A, ld, a, n, n, host)) != RL_OK) return st;
+    } else {
+        D.A = const_cast<double*>(a);
+    }
+    std::vector<double> hg;
+    if (have_g) {
+        if (g_dev_direct) {
+            D.G = const_cast<double*>(post->dense);
+        } else if (post->dense) {
+            if ((st = copy_in(ctx, D.G, ld, post->dense, n, n, host)) != RL_OK) return st;
+        } else {
+            // materialize(spec) = gen_gaussian(n, n, seed) (multipliers.hpp:191-192), exact, host
+            hg.resize(static_cast<size_t>(n * n));
+            rl_gen_gaussian(n, n, post->seed, hg.data());
+            if ((st = copy_in(ctx, D.G, ld, hg.data(), n, n, true)) != RL_OK) return st;
+        }
+    }
+    RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    st = factor_and_verdict(ctx, D, have_g, info);
+    if (st != RL_OK) {
+        RL_CUDA(cudaStreamSynchronize(s));
+        return st;
+    }
+    st = chain_solve(ctx, D, have_g, refine_steps, info);
+    if (st != RL_OK) return st;
+    RL_CUDA(cudaMemcpyAsync(x, D.x, n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    if (lu_out && (st = copy_out(ctx, lu_out, D.P, ld, n, n, host)) != RL_OK) return st;
+    if (want_norm_a) {
+        // BASELINE config-1 residual form ||Ax - b|| / (||A||_est ||x||)
+        double na = 0.0;
+        st = spectral_norm_estimate_device(ctx, n, n, D.A, ld, &na);
+        if (st != RL_OK) return st;
+        if ((st = sumsq(ctx, n, D.x, D.sc->bsq)) != RL_OK) return st;  // bsq scratch reused for ||x||^2
+        double sq[2];
+        RL_CUDA(cudaMemcpyAsync(&sq[0], D.sc->rsq, 8, cudaMemcpyDeviceToHost, s));
+        RL_CUDA(cudaMemcpyAsync(&sq[1], D.sc->bsq, 8, cudaMemcpyDeviceToHost, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+        info->residual_rel_a = std::sqrt(sq[0]) / (na * std::sqrt(sq[1]));
+    }
+    RL_CUDA(cudaStreamSynchronize(s));
+    return RL_OK;
+}
+
+extern "C" RL_API rl_status rl_genp_factor(rl_context* ctx, rl_mem mem, int64_t n, const double* a, double* lu,
+                                           rl_solve_info* info) {
+    rl_solve_info local;
+    if (!info) info = &local;
+    clear_info(info);
+    if (n <= 0) return set_error(RL_ERR_DIMENSION, "genp_factor: square input required");
+    if (!a || !lu) return set_error(RL_ERR_INVALID_ARGUMENT, "genp_factor: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    const bool host = mem == RL_HOST;
+    Dense D;
+    st = dense_alloc(ctx, D, n, false, true, true);
+    if (st != RL_OK) return st;
+    if ((st = copy_in(ctx, D.A, D.ld, a, n, n, host)) != RL_OK) return st;
+    st = factor_and_verdict(ctx, D, false, info);
+    if (st != RL_OK && st != RL_ERR_ZERO_PIVOT) return st;
+    const rl_status verdict = st;
+    if ((st = copy_out(ctx, lu, D.P, D.ld, n, n, host)) != RL_OK) return st;
+    RL_CUDA(cudaStreamSynchronize(ctx->stream));
+    return verdict;
+}
+
+extern "C" RL_API rl_status rl_lu_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* lu, const double* b,
+                                        double* x) {
+    if (n <= 0) return set_error(RL_ERR_DIMENSION, "lu_solve: length mismatch");
+    if (!lu || !b || !x) return set_error(RL_ERR_INVALID_ARGUMENT, "lu_solve: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    const bool host = mem == RL_HOST;
+    double *dlu = const_cast<double*>(lu), *db = const_cast<double*>(b), *dx = x;
+    void* work = nullptr;
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        work = ar.take<char>(lu_solve_work_bytes(n));
+        if (host) {
+            dlu = ar.take<double>(n * n);
+            db = ar.take<double>(n);
+            dx = ar.take<double>(n);
+        }
+    });
+    if (!ok) return RL_ERR_OUT_OF_MEMORY;
+    cudaStream_t s = ctx->stream;
+    if (host) {
+        RL_CUDA(cudaMemcpyAsync(dlu, lu, n * n * 8, cudaMemcpyHostToDevice, s));
+        RL_CUDA(cudaMemcpyAsync(db, b, n * 8, cudaMemcpyHostToDevice, s));
+    }
+    st = lu_solve_device(ctx, n, dlu, n, nullptr, db, dx, work);
+    if (st != RL_OK) return st;
+    if (host) {
+        RL_CUDA(cudaMemcpyAsync(x, dx, n * 8, cudaMemcpyDeviceToHost, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+    }
+    return RL_OK;
+}
+
+extern "C" RL_API rl_status rl_spectral_norm_estimate(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                                      double* out) {
+    if (m <= 0 || n <= 0) return set_error(RL_ERR_DIMENSION, "spectral_norm_estimate: empty matrix");
+    if (!a || !out) return set_error(RL_ERR_INVALID_ARGUMENT, "spectral_norm_estimate: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    double* da = const_cast<double*>(a);
+    if (mem == RL_HOST) {
+        RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&da), m * n * 8, ctx->stream));
+        RL_CUDA(cudaMemcpyAsync(da, a, m * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    st = spectral_norm_estimate_device(ctx, m, n, da, n, out);
+    if (mem == RL_HOST) cudaFreeAsync(da, ctx->stream);
+    RL_CUDA(cudaStreamSynchronize(ctx->stream));
+    return st;
+}

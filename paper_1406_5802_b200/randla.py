@@ -248,3 +248,148 @@ def matmul(a, b):
     _sync_stream_for(device)
     _raise(capi.lib().rl_dgemm(_ctx(), _mem(device), m, n, k, capi.addr(a), k, capi.addr(b), n, capi.addr(c), n))
     return c
+
+
+def spectral_norm_estimate(a):
+    """spectral_norm_estimate (norms.hpp:35-78), evaluated on the GPU in the
+    reference's summation order (bit-identical for a given matrix)."""
+    device = _is_device(a)
+    a = _dev(a) if device else _host(a)
+    m, n = a.shape
+    out = ctypes.c_double(0.0)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_spectral_norm_estimate(_ctx(), _mem(device), m, n, capi.addr(a), ctypes.byref(out)))
+    return out.value
+
+
+# ---- GENP (lu.hpp) ---------------------------------------------------------------
+@dataclass
+class LuFactors:
+    """LuFactors (lu.hpp:17-28) held packed: strict lower = L (unit diagonal),
+    upper incl. diagonal = U; perm is always None (no pivoting)."""
+    packed: object
+    perm: object = None
+    info: dict = field(default_factory=dict)
+
+    @property
+    def lower(self):
+        p = self.packed
+        if isinstance(p, np.ndarray):
+            return np.tril(p, -1) + np.eye(p.shape[0])
+        import torch
+        return torch.tril(p, -1) + torch.eye(p.shape[0], dtype=p.dtype, device=p.device)
+
+    @property
+    def upper(self):
+        p = self.packed
+        if isinstance(p, np.ndarray):
+            return np.triu(p)
+        import torch
+        return torch.triu(p)
+
+    def pivots(self):
+        p = self.packed
+        return np.diag(p).copy() if isinstance(p, np.ndarray) else p.diagonal().clone()
+
+
+def genp_factor(a):
+    """genp_factor (lu.hpp:40-58): unpivoted elimination; raises
+    ZeroPivotError(step) exactly when the reference does."""
+    device = _is_device(a)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionError("genp_factor: square input required")
+    n = a.shape[0]
+    a = _dev(a) if device else _host(a)
+    lu = _empty_like_kind(device, (n, n), a)
+    info = capi.rl_solve_info()
+    _sync_stream_for(device)
+    rc = capi.lib().rl_genp_factor(_ctx(), _mem(device), n, capi.addr(a), capi.addr(lu), ctypes.byref(info))
+    _raise(rc, info.zero_pivot_step)
+    return LuFactors(lu, None, info.as_dict())
+
+
+def lu_solve(f, b):
+    """lu_solve (lu.hpp:100-123) on packed factors."""
+    lu = f.packed if isinstance(f, LuFactors) else f
+    device = _is_device(lu, b)
+    n = lu.shape[0]
+    if b.shape[0] != n:
+        raise DimensionError("lu_solve: length mismatch")
+    lu = _dev(lu) if device else _host(lu)
+    b = _dev(b) if device else _host(b)
+    x = _empty_like_kind(device, (n,), b)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_lu_solve(_ctx(), _mem(device), n, capi.addr(lu), capi.addr(b), capi.addr(x)))
+    return x
+
+
+# ---- preprocessed solve (preprocess.hpp) -------------------------------------------
+@dataclass
+class SolveOutcome:
+    """SolveOutcome (preprocess.hpp:9-14) plus the device diagnostics."""
+    x: object
+    residual_history: List[float]
+    diverged: bool
+    info: dict
+    lu: object = None
+
+
+def _multiplier(spec, device):
+    m = capi.rl_multiplier()
+    if spec is None:
+        m.kind = capi.RL_MULT_NONE
+        return m, []
+    m.kind = int(spec.kind)
+    m.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
+    keep = []
+    if spec.dense is not None:
+        d = _dev(spec.dense) if device else _host(spec.dense)
+        keep.append(d)
+        m.dense = capi.addr(d)
+    if spec.column is not None:
+        c = _dev(spec.column) if device else _host(spec.column)
+        keep.append(c)
+        m.column = capi.addr(c)
+    return m, keep
+
+
+def preprocess_solve(a, b, pre_spec=None, post_spec=None, refine_steps=0, want_lu=False, want_norm_a=False):
+    """preprocess_solve(a, b, pre, post, refine) (preprocess.hpp:156-180) with
+    pre = none: product A*H, GENP, x = H (LU)^-1 b, refinement. Raises
+    ZeroPivotError like the reference; retry with preprocess_solve_with_retry."""
+    if pre_spec is not None and pre_spec.kind != MultiplierKind.NONE:
+        raise DimensionError("preprocess_solve: left multipliers are not on the B200 path (pre must be none)")
+    device = _is_device(a, b)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionError("preprocess_solve: square input required")
+    n = a.shape[0]
+    if b.shape[0] != n:
+        raise DimensionError("preprocess_solve: length mismatch")
+    a = _dev(a) if device else _host(a)
+    b = _dev(b) if device else _host(b)
+    x = _empty_like_kind(device, (n,), b)
+    lu = _empty_like_kind(device, (n, n), a) if want_lu else None
+    m, keep = _multiplier(post_spec, device)
+    info = capi.rl_solve_info()
+    _sync_stream_for(device)
+    rc = capi.lib().rl_preprocessed_genp_solve(_ctx(), _mem(device), n, capi.addr(a), capi.addr(b), ctypes.byref(m),
+                                               refine_steps, capi.addr(x), capi.addr(lu), 1 if want_norm_a else 0,
+                                               ctypes.byref(info))
+    del keep
+    _raise(rc, info.zero_pivot_step)
+    d = info.as_dict()
+    return SolveOutcome(x, d["residual_history"], bool(info.diverged), d, lu)
+
+
+def preprocess_solve_with_retry(a, b, pre_spec, post_spec, refine_steps=0, max_retries=3):
+    """preprocess.hpp:182-196: on ZeroPivot reseed with
+    derive_seed(seed, 0x52455452, attempt + 1)."""
+    import copy
+    post = copy.copy(post_spec) if post_spec is not None else MultiplierSpec()
+    for attempt in range(max_retries + 1):
+        try:
+            return preprocess_solve(a, b, pre_spec, post, refine_steps)
+        except ZeroPivotError:
+            if attempt >= max_retries:
+                raise
+            post.seed = derive_seed(post.seed, 0x52455452, attempt + 1)

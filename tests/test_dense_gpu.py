@@ -1,0 +1,142 @@
+"""GPU parity: dense preprocessed GENP (BASELINE config 1 and the headline
+path) through the C ABI vs the CPU oracle on identical seeded inputs.
+
+Tolerances (BASELINE north_star): LU and x within relative Frobenius error
+1e-10 * kappa of the factored product (for LU: of its worst leading minor,
+the quantity GENP's sensitivity follows); verdicts identical; growth to
+rounding."""
+import numpy as np
+import pytest
+
+import paper_1406_5802_b200 as rl
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_genp_kats(cuda):
+    """tests/test_elimination.cpp:29-50"""
+    f = rl.genp_factor(np.eye(3))
+    np.testing.assert_array_equal(f.lower, np.eye(3))
+    np.testing.assert_array_equal(f.upper, np.eye(3))
+    assert f.perm is None
+    with pytest.raises(rl.ZeroPivotError) as e:
+        rl.genp_factor(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert e.value.step == 1
+    f = rl.genp_factor(np.array([[2.0, 1.0], [4.0, 5.0]]))
+    assert f.lower[1, 0] == 2.0 and f.upper[0, 0] == 2.0 and f.upper[0, 1] == 1.0 and f.upper[1, 1] == 3.0
+    assert f.lower[0, 1] == 0.0
+
+
+@pytest.mark.parametrize("n", [5, 64, 65, 200, 511, 1024])
+def test_genp_factor_vs_oracle(cuda, orc, n):
+    a = orc.C.gen_gaussian(n, n, 100 + n)
+    g = orc.C.gen_gaussian(n, n, 200 + n)
+    p = orc.C.matmul(a, g)  # preprocessed product keeps the leading minors healthy
+    lu_ref, zs, _ = orc.C.genp_factor(p)
+    assert zs == 0
+    f = rl.genp_factor(p)
+    kmin = max(np.linalg.cond(p[:k, :k]) for k in range(1, n + 1, max(1, n // 32)))
+    assert _rel(f.packed, lu_ref) <= 1e-10 * kmin
+    b = orc.C.gen_gaussian_vector(n, 7)
+    x = rl.lu_solve(f, b)
+    xr = orc.C.lu_solve(lu_ref, b)
+    assert _rel(x, xr) <= 1e-10 * np.linalg.cond(p)
+
+
+def test_spectral_norm_estimate_bit_exact(cuda, orc):
+    """exact-order device power iteration == the reference's, bit for bit"""
+    rng = np.random.default_rng(11)
+    for shape in [(1, 1), (7, 3), (64, 64), (300, 200), (1024, 1024)]:
+        a = rng.standard_normal(shape)
+        assert rl.spectral_norm_estimate(a) == orc.C.spectral_norm_estimate(a)
+    assert rl.spectral_norm_estimate(np.zeros((4, 4))) == 0.0
+
+
+@pytest.mark.parametrize("refine", [0, 1])
+def test_config1_parity(cuda, orc, golden, refine):
+    """BASELINE config 1: n=1024, A seed 1, G seed 2, b seed 3."""
+    n = 1024
+    a = rl.gen_gaussian(n, n, 1)
+    b = rl.gen_gaussian_vector(n, 3)
+    out = rl.preprocess_solve(a, b, None, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 2), refine, want_lu=True,
+                              want_norm_a=True)
+    ref = orc.C.preprocess_solve(a, b, 1, orc.C.gen_gaussian(n, n, 2), refine=refine, want_lu=True)
+    kap = np.linalg.cond(ref["product"])
+    assert _rel(out.x, ref["x"]) <= 1e-10 * kap
+    assert _rel(out.x, golden[f"cfg1_x_refine{refine}"]) <= 1e-10 * kap
+    assert len(out.residual_history) == refine + 1 and not out.diverged
+    # growth: max|U| / max|AG| within rounding of the reference's
+    assert abs(out.info["growth"] / golden["cfg1_growth"][0] - 1) <= 1e-10 * kap
+    assert out.info["zero_pivot_step"] == 0 and out.info["norm_estimate_evaluated"] == 0
+    # pivots, reference ordering
+    np.testing.assert_allclose(np.diag(out.lu), golden["cfg1_pivots"], rtol=1e-10 * kap)
+    # residual level matches the reference's ||Ax-b||/||b||
+    assert out.residual_history[0] < 10 * golden[f"cfg1_hist_refine{refine}"][0] + 1e-15
+    if refine:
+        assert out.residual_history[1] < 1e-3 * out.residual_history[0]
+    assert 0 < out.info["residual_rel_a"] < 1e-6
+
+
+def test_identity_solve_exact(cuda, orc):
+    """tests/test_elimination.cpp:244-253: preprocessed solve exact on I"""
+    b = orc.C.gen_gaussian_vector(8, 60)
+    out = rl.preprocess_solve(np.eye(8), b, None, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 61), 0)
+    assert len(out.residual_history) == 1 and out.residual_history[0] <= 1e-13
+    np.testing.assert_allclose(out.x, b, rtol=1e-12, atol=1e-12)
+
+
+def test_zero_pivot_verdicts_match_oracle(cuda, orc):
+    """ZeroPivot propagates with the reference's 1-based step, including the
+    ambiguous band that needs the exact estimate."""
+    n = 96
+    cases = []
+    a = np.eye(n)
+    a[0, 0] = 0.0
+    cases.append(a)                       # step 1
+    a = np.eye(n)
+    a[70, 70] = 0.0
+    cases.append(a)                       # step 71 (second base panel)
+    for piv in (5e-11, 9.6e-12, 5e-12):   # tol_pivot(96) * est(=1) = 9.6e-12; ||I||_F bound = 9.4e-11
+        a = np.eye(n)
+        a[40, 40] = piv
+        cases.append(a)
+    for a in cases:
+        _, zs, _ = orc.C.genp_factor(a)
+        if zs:
+            with pytest.raises(rl.ZeroPivotError) as e:
+                rl.genp_factor(a)
+            assert e.value.step == zs
+            with pytest.raises(rl.ZeroPivotError) as e:
+                rl.preprocess_solve(a, np.ones(n), None, None, 0)
+            assert e.value.step == zs
+        else:
+            f = rl.genp_factor(a)
+            assert f.info["norm_estimate_evaluated"] == 1
+
+
+def test_retry_wrapper(cuda, orc):
+    """preprocess.hpp:182-196: identity multipliers keep failing; a Gaussian
+    multiplier rescues the anti-identity immediately."""
+    n = 64
+    a = np.eye(n)[::-1].copy()
+    b = orc.C.gen_gaussian_vector(n, 991)
+    with pytest.raises(rl.ZeroPivotError):
+        rl.preprocess_solve_with_retry(a, b, None, None, 0, 2)
+    out = rl.preprocess_solve_with_retry(a, b, None, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 992), 0, 3)
+    assert out.residual_history[0] <= 1e-3
+
+
+def test_device_pointer_path_matches_host(cuda, orc):
+    torch = cuda
+    n = 512
+    a = rl.gen_gaussian(n, n, 21)
+    b = rl.gen_gaussian_vector(n, 22)
+    g = rl.gen_gaussian(n, n, 23)
+    h = rl.preprocess_solve(a, b, None, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 23), 0)
+    d = rl.preprocess_solve(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), None,
+                            rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 0, dense=torch.from_numpy(g).cuda()), 0)
+    np.testing.assert_array_equal(h.x, d.x.cpu().numpy())
