@@ -39,7 +39,7 @@ __device__ __forceinline__ void wait_flag(const int* flag) {
 template <bool kUpper>
 __global__ void __launch_bounds__(256)
 trsv_kernel(const double* __restrict__ lu, int64_t ld, int64_t n, const double* __restrict__ rinv,
-            const double* __restrict__ rhs, double* __restrict__ out, int* __restrict__ flags, int* __restrict__ ticket) {
+            const double* rhs, double* out, int* __restrict__ flags, int* __restrict__ ticket) {
     __shared__ int s_blk;
     __shared__ double sdiag[TB][TB + 1];
     __shared__ double sacc[TB];
@@ -61,8 +61,11 @@ trsv_kernel(const double* __restrict__ lu, int64_t ld, int64_t n, const double* 
     // off-diagonal contributions: rows r0.., blocks C (C < B lower / C > B upper)
     const int row = tid >> 2, q = tid & 3;
     double acc = 0.0;
-    const int64_t c_begin = kUpper ? B + 1 : 0, c_end = kUpper ? nblk : B;
-    for (int64_t C = c_begin; C < c_end; ++C) {
+    // visit the finished blocks in the order they are produced: ascending for
+    // the forward sweep, descending for the backward one
+    const int64_t ndep = kUpper ? nblk - 1 - B : B;
+    for (int64_t t = 0; t < ndep; ++t) {
+        const int64_t C = kUpper ? nblk - 1 - t : t;
         if (tid == 0) {
             wait_flag(&flags[C]);
             __threadfence();
