@@ -80,11 +80,36 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     if (tid == 0)
         for (int kt = 0; kt < min(STAGES, KT); ++kt) issue(kt);
 
+    // accumulators: 0, or (kAccum) the current C tile, fetched with all loads
+    // in flight at once while the first TMA stages land; alpha = -1 is then
+    // applied by negating the A fragments (C - A B, the Schur update)
     double acc[8][4][2];
+    const bool vec_ok = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (kAccum) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int row = m0 + wm * 64 + 8 * i + fr;
+            if (row >= M) continue;
+            const double* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int col = n0 + wn * 32 + 8 * j + 2 * fc;
+                if (vec_ok && col + 1 < N) {
+                    const double2 o = *reinterpret_cast<const double2*>(crow + col);
+                    acc[i][j][0] = o.x;
+                    acc[i][j][1] = o.y;
+                } else {
+                    if (col < N) acc[i][j][0] = crow[col];
+                    if (col + 1 < N) acc[i][j][1] = crow[col + 1];
+                }
+            }
+        }
+    }
+    const double asign = kAccum ? (alpha < 0.0 ? -1.0 : 1.0) : 1.0;
 
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % STAGES;
@@ -96,7 +121,7 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const int k = 4 * kk + fc;
             double af[8], bf[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = *reinterpret_cast<const double*>(sa + swz128(wm * 64 + 8 * i + fr, k));
+            for (int i = 0; i < 8; ++i) af[i] = asign * *reinterpret_cast<const double*>(sa + swz128(wm * 64 + 8 * i + fr, k));
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int n = wn * 32 + 8 * j + fr;
@@ -113,7 +138,6 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
     // ---- epilogue
     double ssq = 0.0, amax = 0.0;
-    const bool vec_ok = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int row = m0 + wm * 64 + 8 * i + fr;
@@ -122,22 +146,16 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int col = n0 + wn * 32 + 8 * j + 2 * fc;
-            double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+            const double v0 = kAccum ? acc[i][j][0] : alpha * acc[i][j][0];
+            const double v1 = kAccum ? acc[i][j][1] : alpha * acc[i][j][1];
             if (vec_ok && col + 1 < N) {
-                double2* p = reinterpret_cast<double2*>(crow + col);
-                if (kAccum) {
-                    const double2 o = *p;
-                    v0 += o.x;
-                    v1 += o.y;
-                }
-                *p = make_double2(v0, v1);
+                *reinterpret_cast<double2*>(crow + col) = make_double2(v0, v1);
                 if (kStats) {
                     ssq = fma(v0, v0, fma(v1, v1, ssq));
                     amax = fmax(amax, fmax(fabs(v0), fabs(v1)));
                 }
             } else {
                 if (col < N) {
-                    if (kAccum) v0 += crow[col];
                     crow[col] = v0;
                     if (kStats) {
                         ssq = fma(v0, v0, ssq);
@@ -145,7 +163,6 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     }
                 }
                 if (col + 1 < N) {
-                    if (kAccum) v1 += crow[col + 1];
                     crow[col + 1] = v1;
                     if (kStats) {
                         ssq = fma(v1, v1, ssq);
@@ -217,6 +234,8 @@ rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A
     }
     if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm: TMA needs 16-byte aligned operands with even leading dimensions");
+    if (accumulate && alpha != 1.0 && alpha != -1.0)
+        return set_error(RL_ERR_INVALID_ARGUMENT, "gemm: accumulate supports alpha = +1 or -1");
     if (M > (int64_t(1) << 30) || N > (int64_t(1) << 30) || K > (int64_t(1) << 30))
         return set_error(RL_ERR_DIMENSION, "gemm: dimension too large");
     CUtensorMap ta, tb;

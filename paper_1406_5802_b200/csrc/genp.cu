@@ -50,6 +50,47 @@ panel_diag_kernel(double* __restrict__ a, int64_t lda, int w, double* __restrict
     }
 }
 
+// ---- 64 x 64 diagonal block, register-resident: thread i owns row i; the
+// pivot row is broadcast through a double-buffered shared row, one barrier
+// per elimination step (lu.hpp:47-56 order, IEEE division for multipliers)
+template <int W>
+__global__ void __launch_bounds__(W)
+panel_diag_reg_kernel(double* __restrict__ a, int64_t lda, double* __restrict__ piv_out, double* __restrict__ rinv_out) {
+    __shared__ __align__(16) double buf[2][W];
+    const int i = threadIdx.x;
+    double p[W];
+    double2* arow = reinterpret_cast<double2*>(a + i * lda);
+#pragma unroll
+    for (int m = 0; m < W / 2; ++m) {
+        const double2 v = arow[m];
+        p[2 * m] = v.x;
+        p[2 * m + 1] = v.y;
+    }
+    double mypiv = 0.0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        double* row = buf[j & 1];
+        if (i == j) {
+#pragma unroll
+            for (int m = 0; m < W / 2; ++m)
+                if (2 * m + 1 >= j) *reinterpret_cast<double2*>(&row[2 * m]) = make_double2(p[2 * m], p[2 * m + 1]);
+        }
+        __syncthreads();
+        const double piv = row[j];
+        if (i == j) mypiv = piv;
+        const bool below = i > j;
+        const double l = below ? p[j] / piv : 0.0;
+        if (below) p[j] = l;
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+            if (k > j) p[k] = fma(-l, row[k], p[k]);
+    }
+#pragma unroll
+    for (int m = 0; m < W / 2; ++m) arow[m] = make_double2(p[2 * m], p[2 * m + 1]);
+    piv_out[i] = mypiv;
+    rinv_out[i] = 1.0 / mypiv;
+}
+
 // a / b correctly rounded from r = 1/b (one residual correction)
 __device__ __forceinline__ double div_by(double a, double b, double r) {
     const double q0 = a * r;
@@ -80,12 +121,13 @@ panel_rows_kernel(double* __restrict__ rows, int64_t lda, int64_t nrows, const d
         x[2 * j] = v.x;
         x[2 * j + 1] = v.y;
     }
+    // column sweep: x_j final after its division, then folded into every
+    // later column at once (independent FMAs -> short dependency chains)
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-        double acc = x[j];
+        x[j] = div_by(x[j], sp[j], sr[j]);
 #pragma unroll
-        for (int i = 0; i < j; ++i) acc = fma(-x[i], su[i][j], acc);
-        x[j] = div_by(acc, sp[j], sr[j]);
+        for (int k = j + 1; k < W; ++k) x[k] = fma(-x[j], su[j][k], x[k]);
     }
 #pragma unroll
     for (int j = 0; j < W / 2; ++j) row[j] = make_double2(x[2 * j], x[2 * j + 1]);
@@ -103,13 +145,11 @@ trsm_lower_unit_kernel(const double* __restrict__ l, int64_t ldl, double* __rest
     double x[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) x[i] = b[i * ldb + c];
+    // column sweep (x_k final -> update all later rows): short dependency chains
 #pragma unroll
-    for (int i = 1; i < W; ++i) {
-        double acc = x[i];
+    for (int k = 0; k < W - 1; ++k)
 #pragma unroll
-        for (int k = 0; k < i; ++k) acc = fma(-sl[i][k], x[k], acc);
-        x[i] = acc;
-    }
+        for (int i = k + 1; i < W; ++i) x[i] = fma(-sl[i][k], x[k], x[i]);
 #pragma unroll
     for (int i = 0; i < W; ++i) b[i * ldb + c] = x[i];
 }
@@ -137,6 +177,88 @@ trsm_lower_unit_kernel_dyn(const double* __restrict__ l, int64_t ldl, int w, dou
         double acc = b[i * ldb + c];
         for (int k = 0; k < i; ++k) acc = fma(-l[i * ldl + k], b[k * ldb + c], acc);
         b[i * ldb + c] = acc;
+    }
+}
+
+// ---- fused right-looking step for a 64-column panel at c0 ------------------
+// Every CTA factors the 64x64 diagonal block redundantly in shared memory
+// (two threads per row, one barrier per elimination step), then does its
+// share of the panel: row CTAs form L21 = A21 U11^-1 (x U11 = a, column sweep
+// per row, one row per thread), column CTAs form U12 = L11^-1 A12 (column
+// sweep per column, one column per thread, coalesced). CTA 0 writes the
+// factored diagonal block and the pivots. One launch per elimination step;
+// the trailing update A22 -= L21 U12 is one DMMA GEMM (K = 64).
+constexpr int PT = 128;  // threads per CTA
+__global__ void __launch_bounds__(PT)
+lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
+                  double* __restrict__ piv_out, double* __restrict__ rinv_out) {
+    __shared__ double sd[kBase][kBase + 1];
+    __shared__ double sp[kBase], sr[kBase];
+    const int tid = threadIdx.x;
+    double* d = a + c0 * lda + c0;
+    for (int idx = tid; idx < kBase * kBase; idx += PT) sd[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
+    __syncthreads();
+    {
+        const int row = tid >> 1, h = tid & 1;
+        for (int j = 0; j < kBase; ++j) {
+            const double pv = sd[j][j];
+            double l = 0.0;
+            if (row > j) l = sd[row][j] / pv;  // multiplier (lu.hpp:51)
+            __syncwarp();
+            if (row > j) {
+                if ((j & 1) == h) sd[row][j] = l;
+#pragma unroll 4
+                for (int k = j + 1 + ((j + 1 + h) & 1); k < kBase; k += 2) sd[row][k] = fma(-l, sd[j][k], sd[row][k]);
+            }
+            __syncthreads();
+        }
+    }
+    if (tid < kBase) {
+        sp[tid] = sd[tid][tid];
+        sr[tid] = 1.0 / sd[tid][tid];
+    }
+    __syncthreads();
+    const int b = blockIdx.x;
+    if (b == 0) {
+        for (int idx = tid; idx < kBase * kBase; idx += PT) d[(idx >> 6) * lda + (idx & 63)] = sd[idx >> 6][idx & 63];
+        if (tid < kBase) {
+            piv_out[c0 + tid] = sp[tid];
+            rinv_out[c0 + tid] = sr[tid];
+        }
+    }
+    const int64_t rest = n - c0 - kBase;
+    if (b < row_ctas) {
+        const int64_t r = c0 + kBase + static_cast<int64_t>(b) * PT + tid;
+        if (r >= n) return;
+        double2* rowp = reinterpret_cast<double2*>(a + r * lda + c0);
+        double x[kBase];
+#pragma unroll
+        for (int m = 0; m < kBase / 2; ++m) {
+            const double2 v = rowp[m];
+            x[2 * m] = v.x;
+            x[2 * m + 1] = v.y;
+        }
+#pragma unroll
+        for (int j = 0; j < kBase; ++j) {
+            x[j] = div_by(x[j], sp[j], sr[j]);
+#pragma unroll
+            for (int k = j + 1; k < kBase; ++k) x[k] = fma(-x[j], sd[j][k], x[k]);
+        }
+#pragma unroll
+        for (int m = 0; m < kBase / 2; ++m) rowp[m] = make_double2(x[2 * m], x[2 * m + 1]);
+    } else {
+        const int64_t c = c0 + kBase + static_cast<int64_t>(b - row_ctas) * PT + tid;
+        if (c - c0 - kBase >= rest) return;
+        double* col = a + c0 * lda + c;
+        double x[kBase];
+#pragma unroll
+        for (int i = 0; i < kBase; ++i) x[i] = col[i * lda];
+#pragma unroll
+        for (int k = 0; k < kBase - 1; ++k)
+#pragma unroll
+            for (int i = k + 1; i < kBase; ++i) x[i] = fma(-sd[i][k], x[k], x[i]);
+#pragma unroll
+        for (int i = 0; i < kBase; ++i) col[i * lda] = x[i];
     }
 }
 
@@ -176,7 +298,10 @@ rl_status trsm(const Ctx& g, int64_t r0, int64_t w, int64_t c0, int64_t ncols) {
 rl_status panel(const Ctx& g, int64_t c0, int64_t w) {
     const int64_t m = g.n - c0;
     double* d = g.a + c0 * g.lda + c0;
-    panel_diag_kernel<<<1, 256, 0, g.ctx->stream>>>(d, g.lda, static_cast<int>(w), g.piv + c0, g.rinv + c0);
+    if (w == kBase)
+        panel_diag_reg_kernel<kBase><<<1, kBase, 0, g.ctx->stream>>>(d, g.lda, g.piv + c0, g.rinv + c0);
+    else
+        panel_diag_kernel<<<1, 256, 0, g.ctx->stream>>>(d, g.lda, static_cast<int>(w), g.piv + c0, g.rinv + c0);
     RL_CHECK_LAUNCH("panel_diag_kernel");
     const int64_t rows = m - w;
     if (rows > 0) {
@@ -211,7 +336,21 @@ rl_status rec(const Ctx& g, int64_t c0, int64_t w) {
 rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out) {
     if (n <= 0) return RL_OK;
     Ctx g{ctx, a, n, lda, piv_out, rinv_out};
-    return rec(g, 0, n);
+    // right-looking blocked GENP, 64-column panels (see lu_panel64_kernel)
+    int64_t c0 = 0;
+    for (; c0 + kBase <= n; c0 += kBase) {
+        const int64_t rest = n - c0 - kBase;
+        const int blocks = static_cast<int>((rest + PT - 1) / PT);
+        lu_panel64_kernel<<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
+        RL_CHECK_LAUNCH("lu_panel64_kernel");
+        if (rest > 0) {
+            rl_status st = gemm(ctx, rest, rest, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
+                                a + (c0 + kBase) * lda + c0 + kBase, lda, -1.0, true, nullptr);
+            if (st != RL_OK) return st;
+        }
+    }
+    if (c0 < n) return panel(g, c0, n - c0);  // ragged last block (< 64 columns)
+    return RL_OK;
 }
 
 }  // namespace rl
