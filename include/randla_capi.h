@@ -110,6 +110,8 @@ typedef struct rl_solve_info {
     int32_t norm_estimate_evaluated; /* 1 when the verdict needed the power iteration */
     int32_t reserved;
     double pivot_tolerance;      /* tol_pivot(n) * norm used for the verdict (upper bound when lazy) */
+    double stage_ms[4];          /* device time (CUDA events on the context stream): product A*H,
+                                    factor + verdict, chain solve + refinement, whole call */
 } rl_solve_info;
 
 /* Per-batch summary of rl_batched_genp_solve_32. */

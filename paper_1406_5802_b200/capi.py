@@ -55,11 +55,12 @@ class rl_solve_info(ctypes.Structure):
                 ("max_abs_u", ctypes.c_double), ("norm_floor", ctypes.c_double),
                 ("norm_frobenius", ctypes.c_double), ("norm_estimate", ctypes.c_double),
                 ("norm_estimate_evaluated", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("pivot_tolerance", ctypes.c_double)]
+                ("pivot_tolerance", ctypes.c_double), ("stage_ms", ctypes.c_double * 4)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("residual_history", "reserved")}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("residual_history", "reserved", "stage_ms")}
         d["residual_history"] = list(self.residual_history)[: self.history_len]
+        d["stage_ms"] = list(self.stage_ms)
         return d
 
 

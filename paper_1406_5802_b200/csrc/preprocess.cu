@@ -98,6 +98,32 @@ double bits_to_double(unsigned long long b) {
 
 unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
+// CUDA-event stage timer on the context stream (rl_solve_info::stage_ms)
+struct StageTimer {
+    cudaStream_t s;
+    cudaEvent_t ev[5] = {};
+    int n = 0;
+    explicit StageTimer(cudaStream_t st) : s(st) {}
+    void mark() {
+        if (n < 5 && cudaEventCreate(&ev[n]) == cudaSuccess) cudaEventRecord(ev[n++], s);
+    }
+    void fill(double* out) {  // out[0..2] consecutive stages, out[3] total
+        if (n == 0) return;
+        cudaEventSynchronize(ev[n - 1]);
+        for (int i = 0; i + 1 < n && i < 3; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            out[i] = ms;
+        }
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, ev[0], ev[n - 1]);
+        out[3] = tot;
+    }
+    ~StageTimer() {
+        for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+    }
+};
+
 struct Dense {
     int64_t n = 0, ld = 0;
     double *A = nullptr, *G = nullptr, *P = nullptr;
@@ -107,11 +133,12 @@ struct Dense {
 };
 
 // P = A G (or A), blocked GENP in place, growth, verdict (lu.hpp:44-49).
-rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_info* info) {
+rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_info* info, StageTimer* tm = nullptr) {
     cudaStream_t s = ctx->stream;
     const int64_t n = D.n;
     RL_CUDA(cudaMemsetAsync(D.sc, 0, sizeof(Scalars), s));
     rl_status st;
+    if (tm) tm->mark();
     if (have_g) {
         st = gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, D.P, D.ld, 1.0, false, &D.sc->prod);
         if (st != RL_OK) return st;
@@ -120,6 +147,7 @@ rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_in
         matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(D.P, D.ld, n, false, &D.sc->prod);
         RL_CHECK_LAUNCH("matrix_stats_kernel");
     }
+    if (tm) tm->mark();
     st = genp_inplace(ctx, n, D.P, D.ld, D.piv, D.rinv);
     if (st != RL_OK) return st;
     matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(D.P, D.ld, n, true, &D.sc->upper);
@@ -313,13 +341,17 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         }
     }
     RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-    st = factor_and_verdict(ctx, D, have_g, info);
+    StageTimer timer(s);
+    st = factor_and_verdict(ctx, D, have_g, info, &timer);
     if (st != RL_OK) {
         RL_CUDA(cudaStreamSynchronize(s));
         return st;
     }
+    timer.mark();
     st = chain_solve(ctx, D, have_g, refine_steps, info);
     if (st != RL_OK) return st;
+    timer.mark();
+    timer.fill(info->stage_ms);
     RL_CUDA(cudaMemcpyAsync(x, D.x, n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
     if (lu_out && (st = copy_out(ctx, lu_out, D.P, ld, n, n, host)) != RL_OK) return st;
     if (want_norm_a) {
