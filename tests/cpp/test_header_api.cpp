@@ -1,0 +1,93 @@
+// C++ drop-in check: the reference's own test cases for the hot path, written
+// against include/randla_b200/randla.hpp exactly as they read against the
+// reference headers (tests/test_elimination.cpp:29-50, :244-253, :320-332;
+// tests/test_field_core.cpp:52-58). Exit code 0 = all passed.
+#include <cmath>
+#include <cstdio>
+
+#include "randla_b200/randla.hpp"
+
+using namespace randla;
+
+static int failures = 0;
+#define CHECK(c)                                                        \
+    do {                                                                \
+        if (!(c)) {                                                     \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);    \
+            ++failures;                                                 \
+        }                                                               \
+    } while (0)
+
+int main() {
+    // unpivoted factorization of simple matrices (test_elimination.cpp:29-50)
+    const auto id = genp_factor(RealMatrix::identity(3));
+    CHECK(id.lower == RealMatrix::identity(3));
+    CHECK(id.upper == RealMatrix::identity(3));
+    CHECK(!id.perm.has_value());
+    const RealMatrix swap(2, 2, {0, 1, 1, 0});
+    try {
+        genp_factor(swap);
+        CHECK(false);
+    } catch (const ZeroPivotError& e) {
+        CHECK(e.step == 1);
+    }
+    const RealMatrix a(2, 2, {2, 1, 4, 5});
+    const auto f = genp_factor(a);
+    CHECK(f.lower(1, 0) == 2.0);
+    CHECK(f.upper(0, 0) == 2.0);
+    CHECK(f.upper(0, 1) == 1.0);
+    CHECK(f.upper(1, 1) == 3.0);
+    CHECK(f.lower(0, 1) == 0.0);
+
+    // matmul against a triple loop (test_field_core.cpp:18-29, 52-58)
+    const RealMatrix x = gen_gaussian(37, 23, 5), y = gen_gaussian(23, 41, 6);
+    const RealMatrix z = matmul(x, y);
+    double err = 0.0, mx = 0.0;
+    for (std::size_t i = 0; i < 37; ++i)
+        for (std::size_t j = 0; j < 41; ++j) {
+            double acc = 0.0;
+            for (std::size_t k = 0; k < 23; ++k) acc += x(i, k) * y(k, j);
+            err = std::max(err, std::abs(acc - z(i, j)));
+            mx = std::max(mx, std::abs(acc));
+        }
+    CHECK(err <= 1e-13 * mx);
+
+    // preprocessed solve is exact on the identity (test_elimination.cpp:244-253)
+    const std::vector<double> b = gen_gaussian_vector(8, 60);
+    MultiplierSpec post{MultiplierKind::Gaussian};
+    post.seed = 61;
+    const auto out = preprocess_solve(RealMatrix::identity(8), b, MultiplierSpec{}, post, 0);
+    CHECK(out.residual_history.size() == 1);
+    CHECK(out.residual_history[0] <= 1e-13);
+    for (std::size_t i = 0; i < 8; ++i) CHECK(std::abs(out.x[i] - b[i]) <= 1e-12 * std::abs(b[i]) + 1e-12);
+
+    // BASELINE config 1 residual and refinement gain
+    const RealMatrix A = gen_gaussian(1024, 1024, 1);
+    const std::vector<double> rhs = gen_gaussian_vector(1024, 3);
+    MultiplierSpec g{MultiplierKind::Gaussian};
+    g.seed = 2;
+    const auto s1 = preprocess_solve(A, rhs, MultiplierSpec{}, g, 1);
+    CHECK(s1.residual_history.size() == 2);
+    CHECK(s1.residual_history[0] < 1e-4);
+    CHECK(s1.residual_history[1] < 1e-3 * s1.residual_history[0]);
+    CHECK(std::abs(relative_residual(A, s1.x, rhs) - s1.residual_history[1]) <= 0.5 * s1.residual_history[1] + 1e-15);
+
+    // zero pivots propagate; the retry wrapper rescues with a random multiplier
+    // (test_elimination.cpp:320-332, on the anti-identity)
+    RealMatrix anti(64, 64);
+    for (std::size_t i = 0; i < 64; ++i) anti(i, 63 - i) = 1.0;
+    const std::vector<double> b64 = gen_gaussian_vector(64, 991);
+    bool threw = false;
+    try {
+        preprocess_solve_with_retry(anti, b64, MultiplierSpec{}, MultiplierSpec{}, 0, 2);
+    } catch (const ZeroPivotError&) {
+        threw = true;
+    }
+    CHECK(threw);
+    MultiplierSpec post2{MultiplierKind::Gaussian};
+    post2.seed = 992;
+    CHECK(preprocess_solve_with_retry(anti, b64, MultiplierSpec{}, post2, 0, 3).residual_history[0] <= 1e-3);
+
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "all passed", failures);
+    return failures ? 1 : 0;
+}
