@@ -1,0 +1,483 @@
+// Circulant / Toeplitz right products by FFT for sm_100a.
+//
+//   rl_circulant_right_multiply  matmul_by_circulant(A, C(c))      circulant.hpp:171-185
+//   rl_toeplitz_right_multiply   matmul_by_toeplitz_block(A, T)    circulant.hpp:187-203
+//
+// Row i of A C is C^T a_i = Omega^-1 (s .* Omega a_i) with s the spectrum of
+// the transposed circulant's first column c_T[i] = c[(n-i) mod n]
+// (circulant.hpp:40-45, :70-76). The circulant is real, so two real rows
+// travel as one complex row z = a_i + i a_{i+1}; Re/Im of the result are the
+// two output rows (imaginary dust is therefore identically zero and the
+// reference's strip_imag verdict, circulant.hpp:57-68, can never fire — for
+// real inputs it does not fire in the reference either).
+//
+// One CTA per row pair, the row resident in shared memory (n <= 8192 complex
+// = 128 KiB). Forward transform: in-place decimation-in-frequency radix-16
+// passes (+ one radix-2/4/8 pass for the remainder) that leave the spectrum
+// in digit-reversed order; the multiplier spectrum s is produced by the SAME
+// forward transform, so it is in the same order and the pointwise product
+// needs no reordering; the inverse is the transposed (decimation-in-time)
+// sequence of passes with conjugate twiddles, which consumes the permuted
+// spectrum and returns natural order. Twiddles w_n^k = exp(+2 pi i k / n)
+// (the reference's sign, fft.hpp:11-12) come from a sincospi table in L2.
+// Parent length 16384 (BASELINE config 5) runs on a 2-CTA cluster: the
+// first radix-2 DIF pass splits the row into two independent 8192-point
+// halves, one per CTA (both read the row, the second read hits L2); the
+// last inverse radix-2 pass is combined through distributed shared memory for
+// the l output columns the Toeplitz block keeps.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "device_common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rl {
+namespace {
+
+constexpr int FT = 256;          // threads per CTA (255 registers: radix-16 groups stay in registers)
+constexpr int MAXN = 8192;       // complex points per CTA
+
+struct cplx {
+    double x, y;
+};
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return {fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)}; }
+__device__ __forceinline__ cplx cmulc(cplx a, cplx b) {  // a * conj(b)
+    return {fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y)};
+}
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - b.y}; }
+
+__global__ void twiddle_kernel(int64_t n, cplx* __restrict__ tw) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double s, c;
+    sincospi(2.0 * static_cast<double>(k) / static_cast<double>(n), &s, &c);
+    tw[k] = {c, s};
+}
+
+// in-register R-point DFT, forward (w = e^{+2 pi i/R}) or inverse (conjugate);
+// natural-order input, output r lands in v[brev<R>(r)]; w_R^k = tw[k * stride]
+template <int R, bool kInv>
+__device__ __forceinline__ void dft_reg(cplx (&v)[R], const cplx* __restrict__ tw, int64_t stride) {
+    // iterative radix-2 DIF in registers (output bit-reversed)
+#pragma unroll
+    for (int half = R / 2; half >= 1; half >>= 1) {
+#pragma unroll
+        for (int base = 0; base < R; base += 2 * half) {
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const cplx a = v[base + j], b = v[base + j + half];
+                const cplx s = cadd(a, b), d = csub(a, b);
+                v[base + j] = s;
+                if (j == 0) {
+                    v[base + j + half] = d;
+                } else {
+                    const cplx w = tw[j * (R / (2 * half)) * stride];  // w_{2 half}^j
+                    v[base + j + half] = kInv ? cmulc(d, w) : cmul(d, w);
+                }
+            }
+        }
+    }
+}
+
+// position of natural-order output r after dft_reg (bit reversal within R)
+template <int R>
+__host__ __device__ constexpr int brev(int r) {
+    int o = 0;
+    for (int b = 1, ib = R / 2; b < R; b <<= 1, ib >>= 1)
+        if (r & b) o |= ib;
+    return o;
+}
+
+// one forward DIF pass on the full buffer: subarrays of length N, radix R
+template <int R>
+__device__ __forceinline__ void dif_pass(cplx* z, int n, int N, const cplx* __restrict__ tw, int ntw) {
+    const int M = N / R;
+    const int groups = n / R;
+    const int64_t tstride = ntw / N;  // w_N^k = tw[k * ntw / N]
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+        const int o = (g / M) * N, n0 = g % M;
+        cplx v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = z[o + n0 + j * M];
+        dft_reg<R, false>(v, tw, static_cast<int64_t>(ntw / R));
+        z[o + n0] = v[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+            z[o + n0 + r * M] = cmul(v[brev<R>(r)], tw[(static_cast<int64_t>(n0) * r * tstride) % ntw]);
+    }
+}
+
+// transposed (DIT) pass with conjugate twiddles; `scale` folded into outputs
+template <int R>
+__device__ __forceinline__ void dit_pass(cplx* z, int n, int N, const cplx* __restrict__ tw, int ntw, double scale) {
+    const int M = N / R;
+    const int groups = n / R;
+    const int64_t tstride = ntw / N;
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+        const int o = (g / M) * N, n0 = g % M;
+        cplx v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = z[o + n0 + r * M];
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmulc(v[r], tw[(static_cast<int64_t>(n0) * r * tstride) % ntw]);
+        dft_reg<R, true>(v, tw, static_cast<int64_t>(ntw / R));
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const cplx t = v[brev<R>(j)];
+            z[o + n0 + j * M] = {t.x * scale, t.y * scale};
+        }
+    }
+}
+
+// pass plan for n = 2^L: radix-16 passes, then one radix 2/4/8 remainder pass
+__device__ __forceinline__ int plan(int n, int* radix) {
+    int L = 31 - __clz(n), p = 0;
+    while (L >= 4) {
+        radix[p++] = 16;
+        L -= 4;
+    }
+    if (L > 0) radix[p++] = 1 << L;
+    return p;
+}
+
+__device__ void forward_fft(cplx* z, int n, const cplx* tw, int ntw) {
+    int radix[8];
+    const int passes = plan(n, radix);
+    int N = n;
+    for (int p = 0; p < passes; ++p) {
+        switch (radix[p]) {
+            case 16: dif_pass<16>(z, n, N, tw, ntw); break;
+            case 8: dif_pass<8>(z, n, N, tw, ntw); break;
+            case 4: dif_pass<4>(z, n, N, tw, ntw); break;
+            default: dif_pass<2>(z, n, N, tw, ntw); break;
+        }
+        N /= radix[p];
+        __syncthreads();
+    }
+}
+
+__device__ void inverse_fft(cplx* z, int n, const cplx* tw, int ntw, double final_scale) {
+    int radix[8];
+    const int passes = plan(n, radix);
+    int Ns[8];
+    int N = n;
+    for (int p = 0; p < passes; ++p) {
+        Ns[p] = N;
+        N /= radix[p];
+    }
+    for (int p = passes - 1; p >= 0; --p) {
+        const double sc = p == 0 ? final_scale : 1.0;
+        switch (radix[p]) {
+            case 16: dit_pass<16>(z, n, Ns[p], tw, ntw, sc); break;
+            case 8: dit_pass<8>(z, n, Ns[p], tw, ntw, sc); break;
+            case 4: dit_pass<4>(z, n, Ns[p], tw, ntw, sc); break;
+            default: dit_pass<2>(z, n, Ns[p], tw, ntw, sc); break;
+        }
+        __syncthreads();
+    }
+}
+
+// spectrum (digit-reversed) of the transposed circulant: forward DIF of c_T
+__global__ void __launch_bounds__(FT) spectrum_kernel(const double* __restrict__ c, int n, const cplx* __restrict__ tw,
+                                                      cplx* __restrict__ spec) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* z = reinterpret_cast<cplx*>(smem_raw);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) z[i] = {c[(n - i) % n], 0.0};
+    __syncthreads();
+    forward_fft(z, n, tw, n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) spec[i] = z[i];
+}
+
+// rows of A (m x k, lda) times the n-point circulant (first k inputs, zero
+// padded; first l outputs kept), two rows per CTA
+__global__ void __launch_bounds__(FT) circ_rows_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int k, int n,
+                                                       const cplx* __restrict__ spec, const cplx* __restrict__ tw,
+                                                       double* __restrict__ out, int64_t ldo, int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* z = reinterpret_cast<cplx*>(smem_raw);
+    const int64_t r0 = 2 * static_cast<int64_t>(blockIdx.x);
+    const bool two = r0 + 1 < m;
+    const double* a0 = a + r0 * lda;
+    const double* a1 = a + (r0 + 1) * lda;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double re = i < k ? __ldcs(a0 + i) : 0.0;
+        const double im = (two && i < k) ? __ldcs(a1 + i) : 0.0;
+        z[i] = {re, im};
+    }
+    __syncthreads();
+    forward_fft(z, n, tw, n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) z[i] = cmul(z[i], spec[i]);
+    __syncthreads();
+    inverse_fft(z, n, tw, n, 1.0 / static_cast<double>(n));
+    double* o0 = out + r0 * ldo;
+    double* o1 = out + (r0 + 1) * ldo;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) {
+        __stcs(o0 + i, z[i].x);
+        if (two) __stcs(o1 + i, z[i].y);
+    }
+}
+
+// ---- parent length 2*MAXN on a 2-CTA cluster ------------------------------------
+// CTA h keeps half h of the first radix-2 DIF split:
+//   h = 0: y0[j] = z[j] + z[j + H]          h = 1: y1[j] = (z[j] - z[j + H]) w_n^j
+// both halves are then independent H-point problems; the spectrum halves are
+// the same split of the parent spectrum. Inverse: the last DIT radix-2 pass
+// z[j] = (u0[j] + conj(w_n^j) u1[j]) / 2 ... only for the kept j < l, with u1
+// read from the partner CTA's shared memory.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FT)
+circ_rows_split_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int k, int n, const cplx* __restrict__ spec,
+                       const cplx* __restrict__ tw, double* __restrict__ out, int64_t ldo, int l) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* z = reinterpret_cast<cplx*>(smem_raw);
+    cg::cluster_group cluster = cg::this_cluster();
+    const int h = static_cast<int>(cluster.block_rank());
+    const int H = n / 2;
+    const int64_t r0 = 2 * static_cast<int64_t>(blockIdx.x / 2);
+    const bool two = r0 + 1 < m;
+    const double* a0 = a + r0 * lda;
+    const double* a1 = a + (r0 + 1) * lda;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+        const int j2 = j + H;
+        const cplx lo = {j < k ? a0[j] : 0.0, (two && j < k) ? a1[j] : 0.0};
+        const cplx hi = {j2 < k ? a0[j2] : 0.0, (two && j2 < k) ? a1[j2] : 0.0};
+        z[j] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), tw[j]);
+    }
+    __syncthreads();
+    // H-point transform with the parent's twiddle table (w_H^k = w_n^{2k})
+    {
+        int radix[8];
+        const int passes = plan(H, radix);
+        int N = H;
+        for (int p = 0; p < passes; ++p) {
+            switch (radix[p]) {
+                case 16: dif_pass<16>(z, H, N, tw, n); break;
+                case 8: dif_pass<8>(z, H, N, tw, n); break;
+                case 4: dif_pass<4>(z, H, N, tw, n); break;
+                default: dif_pass<2>(z, H, N, tw, n); break;
+            }
+            N /= radix[p];
+            __syncthreads();
+        }
+    }
+    const cplx* sp = spec + static_cast<int64_t>(h) * H;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) z[j] = cmul(z[j], sp[j]);
+    __syncthreads();
+    {
+        int radix[8];
+        const int passes = plan(H, radix);
+        int Ns[8];
+        int N = H;
+        for (int p = 0; p < passes; ++p) {
+            Ns[p] = N;
+            N /= radix[p];
+        }
+        for (int p = passes - 1; p >= 0; --p) {
+            switch (radix[p]) {
+                case 16: dit_pass<16>(z, H, Ns[p], tw, n, 1.0); break;
+                case 8: dit_pass<8>(z, H, Ns[p], tw, n, 1.0); break;
+                case 4: dit_pass<4>(z, H, Ns[p], tw, n, 1.0); break;
+                default: dit_pass<2>(z, H, Ns[p], tw, n, 1.0); break;
+            }
+            __syncthreads();
+        }
+    }
+    cluster.sync();
+    // final inverse radix-2: x[j] = u0[j] + conj(w_n^j) u1[j], x[j+H] = u0[j] - conj(w_n^j) u1[j]
+    const cplx* u0 = cluster.map_shared_rank(z, 0);
+    const cplx* u1 = cluster.map_shared_rank(z, 1);
+    const double scale = 1.0 / static_cast<double>(n);
+    double* o0 = out + r0 * ldo;
+    double* o1 = out + (r0 + 1) * ldo;
+    // CTA h writes outputs j in [h*H, (h+1)*H) intersected with [0, l)
+    for (int jj = threadIdx.x; jj < H; jj += blockDim.x) {
+        const int j = jj + h * H;
+        if (j >= l) break;
+        const cplx t = cmulc(u1[jj], tw[jj]);
+        const cplx v = h == 0 ? cadd(u0[jj], t) : csub(u0[jj], t);
+        __stcs(o0 + j, v.x * scale);
+        if (two) __stcs(o1 + j, v.y * scale);
+    }
+    cluster.sync();
+}
+
+// parent spectrum in split order: CTA h forms half h of the first radix-2
+// DIF split of c_T and runs the H-point forward transform on it
+__global__ void __launch_bounds__(FT) spectrum_split_kernel(const double* __restrict__ c, int n,
+                                                            const cplx* __restrict__ tw, cplx* __restrict__ spec) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* z = reinterpret_cast<cplx*>(smem_raw);
+    const int h = blockIdx.x, H = n / 2;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+        const cplx lo = {c[(n - j) % n], 0.0}, hi = {c[(n - j - H) % n], 0.0};
+        z[j] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), tw[j]);
+    }
+    __syncthreads();
+    int radix[8];
+    const int passes = plan(H, radix);
+    int N = H;
+    for (int p = 0; p < passes; ++p) {
+        switch (radix[p]) {
+            case 16: dif_pass<16>(z, H, N, tw, n); break;
+            case 8: dif_pass<8>(z, H, N, tw, n); break;
+            case 4: dif_pass<4>(z, H, N, tw, n); break;
+            default: dif_pass<2>(z, H, N, tw, n); break;
+        }
+        N /= radix[p];
+        __syncthreads();
+    }
+    for (int j = threadIdx.x; j < H; j += blockDim.x) spec[static_cast<int64_t>(h) * H + j] = z[j];
+}
+
+// dense expansion of the leading k x l block of the np-point circulant
+// (circulant.hpp:143-169: entry (i, j) = c[(i - j) mod np])
+__global__ void circulant_dense_kernel(const double* __restrict__ c, int64_t np, int64_t k, int64_t l,
+                                       double* __restrict__ h, int64_t ldh) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= k * l) return;
+    const int64_t i = idx / l, j = idx % l;
+    h[i * ldh + j] = c[((i - j) % np + np) % np];
+}
+
+struct TwCache {
+    std::mutex mu;
+    std::map<std::pair<int, int64_t>, cplx*> tables;  // (device, n) -> table
+};
+TwCache& tw_cache() {
+    static TwCache* c = new TwCache();  // intentionally leaked (lives for the process)
+    return *c;
+}
+
+rl_status twiddles(rl_context* ctx, int64_t n, cplx** out) {
+    TwCache& c = tw_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto key = std::make_pair(ctx->device, n);
+    auto it = c.tables.find(key);
+    if (it != c.tables.end()) {
+        *out = it->second;
+        return RL_OK;
+    }
+    cplx* t = nullptr;
+    RL_CUDA(cudaMalloc(&t, sizeof(cplx) * n));
+    twiddle_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(n, t);
+    RL_CHECK_LAUNCH("twiddle_kernel");
+    RL_CUDA(cudaStreamSynchronize(ctx->stream));
+    c.tables[key] = t;
+    *out = t;
+    return RL_OK;
+}
+
+bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+
+}  // namespace
+
+// device driver: out (m x l, ldo) = A (m x k, lda) * leading k x l block of
+// the np-point circulant with first column c (device). spec_ws >= np complex.
+rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a, int64_t lda, int64_t np,
+                         const double* c, int64_t l, double* out, int64_t ldo, void* spec_ws) {
+    if (m <= 0) return RL_OK;
+    if (!is_pow2(np) || np > 2 * MAXN || np < 2)
+        return set_error(RL_ERR_UNSUPPORTED, "circulant_rows: parent length %lld (power of two <= %d)",
+                         static_cast<long long>(np), 2 * MAXN);
+    cplx* tw = nullptr;
+    rl_status st = twiddles(ctx, np, &tw);
+    if (st != RL_OK) return st;
+    cplx* spec = static_cast<cplx*>(spec_ws);
+    const int n = static_cast<int>(np);
+    static bool configured = false;
+    if (!configured) {
+        RL_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+        RL_CUDA(cudaFuncSetAttribute(circ_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+        RL_CUDA(cudaFuncSetAttribute(circ_rows_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+        RL_CUDA(cudaFuncSetAttribute(spectrum_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+        configured = true;
+    }
+    if (n <= MAXN) {
+        spectrum_kernel<<<1, FT, n * 16, ctx->stream>>>(c, n, tw, spec);
+        RL_CHECK_LAUNCH("spectrum_kernel");
+        circ_rows_kernel<<<static_cast<unsigned>((m + 1) / 2), FT, n * 16, ctx->stream>>>(
+            a, lda, m, static_cast<int>(k), n, spec, tw, out, ldo, static_cast<int>(l));
+        RL_CHECK_LAUNCH("circ_rows_kernel");
+    } else {
+        spectrum_split_kernel<<<2, FT, (n / 2) * 16, ctx->stream>>>(c, n, tw, spec);
+        RL_CHECK_LAUNCH("spectrum_split_kernel");
+        circ_rows_split_kernel<<<static_cast<unsigned>(2 * ((m + 1) / 2)), FT, (n / 2) * 16, ctx->stream>>>(
+            a, lda, m, static_cast<int>(k), n, spec, tw, out, ldo, static_cast<int>(l));
+        RL_CHECK_LAUNCH("circ_rows_split_kernel");
+    }
+    return RL_OK;
+}
+
+}  // namespace rl
+
+// ---- C ABI -----------------------------------------------------------------
+namespace {
+using namespace rl;
+
+rl_status right_multiply(rl_context* ctx, rl_mem mem, int64_t m, int64_t k, const double* a, int64_t np,
+                         const double* c, int64_t l, double* out) {
+    if (m <= 0 || k <= 0 || np <= 0 || l <= 0) return set_error(RL_ERR_DIMENSION, "matmul_by_circulant: empty shape");
+    if (k > np || l > np) return set_error(RL_ERR_DIMENSION, "toeplitz block exceeds parent dimensions");
+    if (!a || !c || !out) return set_error(RL_ERR_INVALID_ARGUMENT, "matmul_by_circulant: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    const bool host = mem == RL_HOST;
+    const bool fft_path = is_pow2(np) && np <= 2 * MAXN;
+    const double *da = a, *dc = c;
+    double* dout = out;
+    void* spec = nullptr;
+    double* hdense = nullptr;
+    const int64_t ldl = (l + 1) & ~int64_t(1), ldk = (k + 1) & ~int64_t(1);
+    // the GEMM fallback (non power-of-two parents) needs even leading dims
+    const bool stage_a = host || (!fft_path && ((k & 1) || (reinterpret_cast<uintptr_t>(a) & 15)));
+    const bool stage_out = host || (!fft_path && ((l & 1) || (reinterpret_cast<uintptr_t>(out) & 15)));
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        if (stage_a) da = ar.take<double>(m * ldk);
+        if (host) dc = ar.take<double>(np);
+        if (stage_out) dout = ar.take<double>(m * ldl);
+        if (fft_path)
+            spec = ar.take<char>(np * 16);
+        else
+            hdense = ar.take<double>(k * ldl);
+    });
+    if (!ok) return RL_ERR_OUT_OF_MEMORY;
+    cudaStream_t s = ctx->stream;
+    const int64_t lda = stage_a ? ldk : k, ldo = stage_out ? ldl : l;
+    if (stage_a)
+        RL_CUDA(cudaMemcpy2DAsync(const_cast<double*>(da), ldk * 8, a, k * 8, k * 8, m,
+                                  host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    if (host) RL_CUDA(cudaMemcpyAsync(const_cast<double*>(dc), c, np * 8, cudaMemcpyHostToDevice, s));
+    if (fft_path) {
+        st = circulant_rows(ctx, m, k, da, lda, np, dc, l, dout, ldo, spec);
+    } else {
+        circulant_dense_kernel<<<static_cast<unsigned>((k * l + 255) / 256), 256, 0, s>>>(dc, np, k, l, hdense, ldl);
+        RL_CHECK_LAUNCH("circulant_dense_kernel");
+        st = gemm(ctx, m, l, k, da, lda, hdense, ldl, dout, ldo, 1.0, false, nullptr);
+    }
+    if (st != RL_OK) return st;
+    if (stage_out)
+        RL_CUDA(cudaMemcpy2DAsync(out, l * 8, dout, ldl * 8, l * 8, m,
+                                  host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    if (host) RL_CUDA(cudaStreamSynchronize(s));
+    return RL_OK;
+}
+}  // namespace
+
+extern "C" RL_API rl_status rl_circulant_right_multiply(rl_context* ctx, rl_mem mem, int64_t m, int64_t n,
+                                                        const double* a, const double* c, double* out) {
+    return right_multiply(ctx, mem, m, n, a, n, c, n, out);
+}
+
+extern "C" RL_API rl_status rl_toeplitz_right_multiply(rl_context* ctx, rl_mem mem, int64_t m, int64_t k,
+                                                       const double* a, int64_t np, const double* c, int64_t l,
+                                                       double* out) {
+    return right_multiply(ctx, mem, m, k, a, np, c, l, out);
+}

@@ -44,6 +44,11 @@ rl_status sumsq(rl_context* ctx, int64_t n, const double* v, double* out);
 rl_status spectral_norm_estimate_device(rl_context* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
                                         double* out);
 
+// out (m x l) = A (m x k) * leading k x l block of the np-point circulant with
+// first column c (device); np a power of two <= 16384. spec_ws >= 16*np bytes.
+rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a, int64_t lda, int64_t np,
+                         const double* c, int64_t l, double* out, int64_t ldo, void* spec_ws);
+
 // batched 32x32 kernel (batched32.cu)
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,
                                 double* lu, double* x, double* r, double* growth, int32_t* status, int refine,

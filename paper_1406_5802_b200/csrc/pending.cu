@@ -8,16 +8,6 @@
 
 extern "C" {
 
-RL_API rl_status rl_circulant_right_multiply(rl_context*, rl_mem, int64_t, int64_t, const double*, const double*,
-                                             double*) {
-    RL_PENDING("rl_circulant_right_multiply");
-}
-
-RL_API rl_status rl_toeplitz_right_multiply(rl_context*, rl_mem, int64_t, int64_t, const double*, int64_t,
-                                            const double*, int64_t, double*) {
-    RL_PENDING("rl_toeplitz_right_multiply");
-}
-
 RL_API rl_status rl_cholqr2(rl_context*, rl_mem, int64_t, int64_t, const double*, double*, double*, int64_t*) {
     RL_PENDING("rl_cholqr2");
 }

@@ -393,3 +393,38 @@ def preprocess_solve_with_retry(a, b, pre_spec, post_spec, refine_steps=0, max_r
             if attempt >= max_retries:
                 raise
             post.seed = derive_seed(post.seed, 0x52455452, attempt + 1)
+
+
+# ---- structured multipliers (circulant.hpp) -------------------------------------
+def matmul_by_circulant(a, c):
+    """matmul_by_circulant(A, C(c)) (circulant.hpp:171-185): A (m x n) times the
+    real circulant with first column c, by FFT on the GPU."""
+    device = _is_device(a, c)
+    m, n = a.shape
+    if c.shape[0] != n:
+        raise DimensionError("matmul_by_circulant: shape mismatch")
+    a = _dev(a) if device else _host(a)
+    c = _dev(c) if device else _host(c)
+    out = _empty_like_kind(device, (m, n), a)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_circulant_right_multiply(_ctx(), _mem(device), m, n, capi.addr(a), capi.addr(c),
+                                                  capi.addr(out)))
+    return out
+
+
+def matmul_by_toeplitz_block(a, c, cols):
+    """matmul_by_toeplitz_block(A, ToeplitzBlock(C(c), k, cols))
+    (circulant.hpp:187-203): A (m x k) times the leading k x cols block of the
+    circulant with first column c (parent length len(c) >= k)."""
+    device = _is_device(a, c)
+    m, k = a.shape
+    np_ = c.shape[0]
+    if k > np_ or cols > np_ or cols < 1:
+        raise DimensionError("toeplitz block exceeds parent dimensions")
+    a = _dev(a) if device else _host(a)
+    c = _dev(c) if device else _host(c)
+    out = _empty_like_kind(device, (m, cols), a)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_toeplitz_right_multiply(_ctx(), _mem(device), m, k, capi.addr(a), np_, capi.addr(c), cols,
+                                                 capi.addr(out)))
+    return out
