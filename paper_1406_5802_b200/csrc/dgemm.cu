@@ -36,10 +36,15 @@ constexpr int GROUP_M = 8;
 // element (r, k) of a 128-byte-swizzled tile with 16 doubles per row
 __device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3); }
 
-template <bool kAccum, bool kStats>
+// kAccum: accumulators start from C (C +- A B); kStats: fold ||.||_F^2 / max|.|
+// of the result into *stats; kStore = false: statistics only (e.g. the
+// low-rank residual A - Q (Q^T A) is never materialised). Split-K: blockIdx.y
+// takes k-tiles [y*ktc, (y+1)*ktc) and writes its partial at C + y*split_stride.
+template <bool kAccum, bool kStats, bool kStore>
 __global__ void __launch_bounds__(THREADS, 1)
 dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
-             int64_t ldc, int M, int N, int K, double alpha, GemmStats* __restrict__ stats) {
+             int64_t ldc, int M, int N, int K, double alpha, GemmStats* __restrict__ stats, int ktc,
+             int64_t split_stride) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle, keeping the pointer in the
     // shared window so operand reads compile to LDS (not generic LD)
@@ -59,7 +64,10 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const int tm_ = first_m + (t % (GROUP_M * tiles_n)) % gsize;
     const int tn_ = (t % (GROUP_M * tiles_n)) / gsize;
     const int m0 = tm_ * BM, n0 = tn_ * BN;
-    const int KT = (K + BK - 1) / BK;
+    const int KT_all = (K + BK - 1) / BK;
+    const int kt0 = ktc > 0 ? static_cast<int>(blockIdx.y) * ktc : 0;
+    const int KT = ktc > 0 ? min(ktc, KT_all - kt0) : KT_all;
+    C += static_cast<int64_t>(blockIdx.y) * split_stride;
 
     if (tid == 0) {
         tma_prefetch_desc(&tmA);
@@ -73,9 +81,10 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         const int s = kt % STAGES;
         unsigned char* st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(st, &tmA, kt * BK, m0, &full[s]);
+        tma_load_2d(st, &tmA, (kt0 + kt) * BK, m0, &full[s]);
 #pragma unroll
-        for (int j = 0; j < BN / 16; ++j) tma_load_2d(st + A_STAGE + j * 2048, &tmB, n0 + 16 * j, kt * BK, &full[s]);
+        for (int j = 0; j < BN / 16; ++j)
+            tma_load_2d(st + A_STAGE + j * 2048, &tmB, n0 + 16 * j, (kt0 + kt) * BK, &full[s]);
     };
     if (tid == 0)
         for (int kt = 0; kt < min(STAGES, KT); ++kt) issue(kt);
@@ -149,21 +158,21 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const double v0 = kAccum ? acc[i][j][0] : alpha * acc[i][j][0];
             const double v1 = kAccum ? acc[i][j][1] : alpha * acc[i][j][1];
             if (vec_ok && col + 1 < N) {
-                *reinterpret_cast<double2*>(crow + col) = make_double2(v0, v1);
+                if (kStore) *reinterpret_cast<double2*>(crow + col) = make_double2(v0, v1);
                 if (kStats) {
                     ssq = fma(v0, v0, fma(v1, v1, ssq));
                     amax = fmax(amax, fmax(fabs(v0), fabs(v1)));
                 }
             } else {
                 if (col < N) {
-                    crow[col] = v0;
+                    if (kStore) crow[col] = v0;
                     if (kStats) {
                         ssq = fma(v0, v0, ssq);
                         amax = fmax(amax, fabs(v0));
                     }
                 }
                 if (col + 1 < N) {
-                    crow[col + 1] = v1;
+                    if (kStore) crow[col + 1] = v1;
                     if (kStats) {
                         ssq = fma(v1, v1, ssq);
                         amax = fmax(amax, fabs(v1));
@@ -199,13 +208,31 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-template <bool A, bool S>
+template <bool A, bool S, bool T>
 void configure_once() {
     static bool done = false;
     if (!done) {
-        cudaFuncSetAttribute(dgemm_kernel<A, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM_BYTES));
+        cudaFuncSetAttribute(dgemm_kernel<A, S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(SMEM_BYTES));
         done = true;
     }
+}
+
+template <bool A, bool S, bool T>
+void launch(dim3 grid, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, double* C, int64_t ldc, int m,
+            int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride) {
+    configure_once<A, S, T>();
+    dgemm_kernel<A, S, T><<<grid, THREADS, SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc, split_stride);
+}
+
+__global__ void reduce_splits_kernel(const double* __restrict__ part, int splits, int64_t slab, int64_t M, int64_t N,
+                                     int64_t ldp, double* __restrict__ C, int64_t ldc, bool accumulate, double alpha) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= M * N) return;
+    const int64_t i = idx / N, j = idx % N;
+    double s = 0.0;
+    for (int q = 0; q < splits; ++q) s += part[q * slab + i * ldp + j];
+    C[i * ldc + j] = accumulate ? C[i * ldc + j] + alpha * s : alpha * s;
 }
 
 }  // namespace
@@ -243,26 +270,67 @@ rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A
         return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
     const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     if (tiles > 0x7fffffff) return set_error(RL_ERR_DIMENSION, "gemm: too many tiles");
-    const dim3 grid(static_cast<unsigned>(tiles)), block(THREADS);
+    const dim3 grid(static_cast<unsigned>(tiles));
     const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+    cudaStream_t st = ctx->stream;
     if (accumulate) {
-        if (stats) {
-            configure_once<true, true>();
-            dgemm_kernel<true, true><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
-        } else {
-            configure_once<true, false>();
-            dgemm_kernel<true, false><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
-        }
+        if (stats)
+            launch<true, true, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
+        else
+            launch<true, false, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
     } else {
-        if (stats) {
-            configure_once<false, true>();
-            dgemm_kernel<false, true><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
-        } else {
-            configure_once<false, false>();
-            dgemm_kernel<false, false><<<grid, block, SMEM_BYTES, ctx->stream>>>(ta, tb, C, ldc, m, n, k, alpha, stats);
-        }
+        if (stats)
+            launch<false, true, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
+        else
+            launch<false, false, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
     }
     RL_CHECK_LAUNCH("dgemm_kernel");
+    return RL_OK;
+}
+
+rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                              const double* B, int64_t ldb, const double* C, int64_t ldc, GemmStats* stats) {
+    if (M <= 0 || N <= 0) return RL_OK;
+    if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+        return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_residual_stats: misaligned operands");
+    CUtensorMap ta, tb;
+    if (!make_tmap_2d(&ta, A, M, K, lda, BM, BK, true) || !make_tmap_2d(&tb, B, K, N, ldb, BK, 16, true))
+        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    launch<true, true, false>(dim3(static_cast<unsigned>(tiles)), ctx->stream, ta, tb, const_cast<double*>(C), ldc,
+                              static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), -1.0, stats, 0, 0);
+    RL_CHECK_LAUNCH("dgemm_kernel(residual stats)");
+    return RL_OK;
+}
+
+size_t gemm_splitk_work_bytes(int64_t M, int64_t N, int splits) {
+    return static_cast<size_t>(splits) * static_cast<size_t>(M) * static_cast<size_t>((N + 1) & ~int64_t(1)) * 8 + 256;
+}
+
+rl_status gemm_splitk(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                      int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, int splits, void* work) {
+    if (M <= 0 || N <= 0) return RL_OK;
+    const int KT = static_cast<int>((K + BK - 1) / BK);
+    splits = std::max(1, std::min(splits, KT));
+    if (splits == 1) return gemm(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, accumulate, nullptr);
+    if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+        return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_splitk: misaligned operands");
+    const int ktc = (KT + splits - 1) / splits;
+    splits = (KT + ktc - 1) / ktc;
+    CUtensorMap ta, tb;
+    if (!make_tmap_2d(&ta, A, M, K, lda, BM, BK, true) || !make_tmap_2d(&tb, B, K, N, ldb, BK, 16, true))
+        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+    const int64_t ldp = (N + 1) & ~int64_t(1);
+    const int64_t slab = M * ldp;
+    double* part = static_cast<double*>(work);
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    launch<false, false, true>(dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), ctx->stream, ta, tb,
+                               part, ldp, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), 1.0, nullptr,
+                               ktc, slab);
+    RL_CHECK_LAUNCH("dgemm_kernel(split-k)");
+    reduce_splits_kernel<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, ctx->stream>>>(
+        part, splits, slab, M, N, ldp, C, ldc, accumulate, alpha);
+    RL_CHECK_LAUNCH("reduce_splits_kernel");
     return RL_OK;
 }
 

@@ -62,10 +62,37 @@ __global__ void twiddle_kernel(int64_t n, cplx* __restrict__ tw) {
     tw[k] = {c, s};
 }
 
-// in-register R-point DFT, forward (w = e^{+2 pi i/R}) or inverse (conjugate);
-// natural-order input, output r lands in v[brev<R>(r)]; w_R^k = tw[k * stride]
+// w_R^j = exp(+2 pi i j / R) for R <= 16 as exact double literals (the
+// in-register butterflies then fold multiplications by 0, +-1)
+__device__ __forceinline__ cplx wconst(int R, int j) {
+    constexpr double c1 = 0.92387953251128674;  // cos(pi/8)
+    constexpr double s1 = 0.38268343236508977;  // sin(pi/8)
+    constexpr double h = 0.70710678118654757;   // sqrt(1/2)
+    const int k = (j * 16 / R) & 15;            // as a power of w_16
+    switch (k) {
+        case 0: return {1.0, 0.0};
+        case 1: return {c1, s1};
+        case 2: return {h, h};
+        case 3: return {s1, c1};
+        case 4: return {0.0, 1.0};
+        case 5: return {-s1, c1};
+        case 6: return {-h, h};
+        case 7: return {-c1, s1};
+        case 8: return {-1.0, 0.0};
+        case 9: return {-c1, -s1};
+        case 10: return {-h, -h};
+        case 11: return {-s1, -c1};
+        case 12: return {0.0, -1.0};
+        case 13: return {s1, -c1};
+        case 14: return {h, -h};
+        default: return {c1, -s1};
+    }
+}
+
+// in-register R-point DFT (R <= 16), forward (w = e^{+2 pi i/R}) or inverse
+// (conjugate); natural-order input, output r lands in v[brev<R>(r)]
 template <int R, bool kInv>
-__device__ __forceinline__ void dft_reg(cplx (&v)[R], const cplx* __restrict__ tw, int64_t stride) {
+__device__ __forceinline__ void dft_reg(cplx (&v)[R]) {
     // iterative radix-2 DIF in registers (output bit-reversed)
 #pragma unroll
     for (int half = R / 2; half >= 1; half >>= 1) {
@@ -74,12 +101,12 @@ __device__ __forceinline__ void dft_reg(cplx (&v)[R], const cplx* __restrict__ t
 #pragma unroll
             for (int j = 0; j < half; ++j) {
                 const cplx a = v[base + j], b = v[base + j + half];
-                const cplx s = cadd(a, b), d = csub(a, b);
-                v[base + j] = s;
+                const cplx d = csub(a, b);
+                v[base + j] = cadd(a, b);
                 if (j == 0) {
                     v[base + j + half] = d;
                 } else {
-                    const cplx w = tw[j * (R / (2 * half)) * stride];  // w_{2 half}^j
+                    const cplx w = wconst(2 * half, j);  // w_{2 half}^j
                     v[base + j + half] = kInv ? cmulc(d, w) : cmul(d, w);
                 }
             }
@@ -96,22 +123,42 @@ __host__ __device__ constexpr int brev(int r) {
     return o;
 }
 
+// twiddles w_N^{n0 r}, r = 1..R-1, from four table loads (r = 1, 2, 4, 8)
+// and at most three products (|error| <= ~3 ulp)
+template <int R>
+__device__ __forceinline__ void pass_twiddles(cplx (&w)[R], const cplx* __restrict__ tw, int64_t base, int64_t mask) {
+    w[0] = {1.0, 0.0};
+    if (R > 1) w[1] = tw[base & mask];
+    if (R > 2) w[2] = tw[(2 * base) & mask];
+    if (R > 4) w[4] = tw[(4 * base) & mask];
+    if (R > 8) w[8] = tw[(8 * base) & mask];
+#pragma unroll
+    for (int r = 3; r < R; ++r) {
+        if (r == 4 || r == 8) continue;
+        const int hi = r >= 8 ? 8 : (r >= 4 ? 4 : 2);
+        w[r] = cmul(w[hi], w[r - hi]);
+    }
+}
+
 // one forward DIF pass on the full buffer: subarrays of length N, radix R
 template <int R>
 __device__ __forceinline__ void dif_pass(cplx* z, int n, int N, const cplx* __restrict__ tw, int ntw) {
     const int M = N / R;
+    const int lgM = 31 - __clz(M);
     const int groups = n / R;
     const int64_t tstride = ntw / N;  // w_N^k = tw[k * ntw / N]
+    const int64_t mask = ntw - 1;
     for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-        const int o = (g / M) * N, n0 = g % M;
+        const int n0 = g & (M - 1), o = (g >> lgM) * N;
         cplx v[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) v[j] = z[o + n0 + j * M];
-        dft_reg<R, false>(v, tw, static_cast<int64_t>(ntw / R));
+        dft_reg<R, false>(v);
+        cplx w[R];
+        pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, mask);
         z[o + n0] = v[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r)
-            z[o + n0 + r * M] = cmul(v[brev<R>(r)], tw[(static_cast<int64_t>(n0) * r * tstride) % ntw]);
+        for (int r = 1; r < R; ++r) z[o + n0 + r * M] = cmul(v[brev<R>(r)], w[r]);
     }
 }
 
@@ -119,16 +166,19 @@ __device__ __forceinline__ void dif_pass(cplx* z, int n, int N, const cplx* __re
 template <int R>
 __device__ __forceinline__ void dit_pass(cplx* z, int n, int N, const cplx* __restrict__ tw, int ntw, double scale) {
     const int M = N / R;
+    const int lgM = 31 - __clz(M);
     const int groups = n / R;
     const int64_t tstride = ntw / N;
+    const int64_t mask = ntw - 1;
     for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-        const int o = (g / M) * N, n0 = g % M;
+        const int n0 = g & (M - 1), o = (g >> lgM) * N;
+        cplx w[R];
+        pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, mask);
         cplx v[R];
+        v[0] = z[o + n0];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = z[o + n0 + r * M];
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmulc(v[r], tw[(static_cast<int64_t>(n0) * r * tstride) % ntw]);
-        dft_reg<R, true>(v, tw, static_cast<int64_t>(ntw / R));
+        for (int r = 1; r < R; ++r) v[r] = cmulc(z[o + n0 + r * M], w[r]);
+        dft_reg<R, true>(v);
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const cplx t = v[brev<R>(j)];

@@ -22,6 +22,17 @@ struct GemmStats {
 rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, GemmStats* stats);
 
+// Split-K variant for small M x N with long K (Gram matrices, Q^T A): partial
+// products per K-slice into `work` (>= gemm_splitk_work_bytes), then an
+// ordered (deterministic) reduction into C.
+rl_status gemm_splitk(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                      int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, int splits, void* work);
+size_t gemm_splitk_work_bytes(int64_t M, int64_t N, int splits);
+
+// Statistics of C - A B (||.||_F^2, max|.|) without storing it.
+rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                              const double* B, int64_t ldb, const double* C, int64_t ldc, GemmStats* stats);
+
 // In-place blocked GENP of the n x n row-major matrix `a` (ld = lda, even,
 // 16-byte aligned) into its packed LU. piv_out / rinv_out (device, n) receive
 // u_jj and 1/u_jj. No pivoting, no verdict (the caller decides it).

@@ -8,13 +8,4 @@
 
 extern "C" {
 
-RL_API rl_status rl_cholqr2(rl_context*, rl_mem, int64_t, int64_t, const double*, double*, double*, int64_t*) {
-    RL_PENDING("rl_cholqr2");
-}
-
-RL_API rl_status rl_range_find_residual(rl_context*, rl_mem, int64_t, int64_t, const double*, int64_t,
-                                        const rl_multiplier*, double*, rl_lowrank_info*) {
-    RL_PENDING("rl_range_find_residual");
-}
-
 }  // extern "C"

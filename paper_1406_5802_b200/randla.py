@@ -428,3 +428,68 @@ def matmul_by_toeplitz_block(a, c, cols):
     _raise(capi.lib().rl_toeplitz_right_multiply(_ctx(), _mem(device), m, k, capi.addr(a), np_, capi.addr(c), cols,
                                                  capi.addr(out)))
     return out
+
+
+# ---- low-rank (qr.hpp, lowrank.hpp) ---------------------------------------------
+def qr(y):
+    """Thin QR with positive diagonal (qr.hpp:21-47) by CholeskyQR2 on the GPU;
+    raises RankDeficiencyError(column) per qr.hpp:33-38."""
+    device = _is_device(y)
+    m, l = y.shape
+    y = _dev(y) if device else _host(y)
+    q = _empty_like_kind(device, (m, l), y)
+    r = _empty_like_kind(device, (l, l), y)
+    bad = ctypes.c_int64(0)
+    _sync_stream_for(device)
+    rc = capi.lib().rl_cholqr2(_ctx(), _mem(device), m, l, capi.addr(y), capi.addr(q), capi.addr(r), ctypes.byref(bad))
+    _raise(rc, bad.value)
+    return q, r
+
+
+def orthonormal_basis(y):
+    """qr.hpp:51-54"""
+    return qr(y)[0]
+
+
+@dataclass
+class LowRankResult:
+    """LowRankResult (lowrank.hpp:21-43) plus the residual norms evaluated on the
+    device against the same A."""
+    q: object
+    rank: int
+    oversample: int
+    power_steps: int
+    info: dict
+
+    def sketch_width(self):
+        return self.q.shape[1]
+
+
+def range_find(a, r, p, spec, power_steps=0):
+    """range_find (lowrank.hpp:62-83): Y = A H (Gaussian H, or the Toeplitz block
+    of a circulant through the FFT), Q = orthonormal_basis(Y); also evaluates
+    ||A - Q Q^T A||_F and the power-iteration ||.||_2 (lowrank.hpp:99-102)."""
+    if power_steps:
+        raise DimensionError("range_find: power steps are not on the B200 path")
+    device = _is_device(a)
+    m, n = a.shape
+    l = r + p
+    if r < 1 or l > min(m, n):
+        raise DimensionError("range_find: rank plus oversampling exceeds matrix size")
+    a = _dev(a) if device else _host(a)
+    q = _empty_like_kind(device, (m, l), a)
+    mlt, keep = _multiplier(spec, device)
+    info = capi.rl_lowrank_info()
+    _sync_stream_for(device)
+    rc = capi.lib().rl_range_find_residual(_ctx(), _mem(device), m, n, capi.addr(a), l, ctypes.byref(mlt),
+                                           capi.addr(q), ctypes.byref(info))
+    del keep
+    _raise(rc, info.rank_deficient_column)
+    d = {k: getattr(info, k) for k, _ in info._fields_ if k != "reserved"}
+    return LowRankResult(q, r, p, power_steps, d)
+
+
+def approximation_residual(a, result):
+    """||A - Q (Q^T A)||_2 of a range_find result (lowrank.hpp:99-102), from the
+    device power iteration on the implicit residual operator."""
+    return result.info["residual_spectral"]

@@ -1,0 +1,108 @@
+"""GPU parity: CholeskyQR2 orthonormal basis (qr.hpp:21-54) and the range
+finder + residual (lowrank.hpp:62-102) vs the oracle, including the
+reference's own low-rank test cases (tests/test_lowrank.cpp:20-52)."""
+import numpy as np
+import pytest
+
+import paper_1406_5802_b200 as rl
+
+pytestmark = pytest.mark.gpu
+
+
+def _lownumrank(n, r, seed, tail=1e-10):
+    """testbed/inputs.hpp:67-83 pattern: Q(Gaussian) diag(1/j, tail) Q(Gaussian)^T"""
+    rng = np.random.default_rng(seed)
+    s, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    t, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = np.array([1.0 / (j + 1) if j < r else tail for j in range(n)])
+    return (s * sig) @ t.T, sig
+
+
+def test_qr_matches_oracle_householder(cuda, orc):
+    for m, l in [(64, 8), (200, 30), (1000, 64), (4096, 256), (37, 37)]:
+        y = orc.C.gen_gaussian(m, l, m + l)
+        q, r = rl.qr(y)
+        qo, ro, st, _ = orc.C.qr(y)
+        assert st == 0
+        kap = np.linalg.cond(y)
+        assert np.abs(q - qo).max() <= 1e-13 * kap * np.sqrt(m), np.abs(q - qo).max()
+        assert np.abs(r - ro).max() <= 1e-12 * kap * np.abs(ro).max()
+        assert np.linalg.norm(q.T @ q - np.eye(l)) <= 1e-10 * max(m, l)  # tol_orth (types.hpp:39)
+        assert (np.diag(r) > 0).all()
+
+
+def test_qr_kat_and_rank_deficiency(cuda, orc):
+    """tests/test_field_core.cpp:80-86: QR of (3,4)^T; duplicated column ->
+    RankDeficiencyError at that column (qr.hpp:37-38)."""
+    q, r = rl.qr(np.array([[3.0], [4.0]]))
+    np.testing.assert_allclose(q[:, 0], [0.6, 0.8], atol=1e-15)
+    assert abs(r[0, 0] - 5.0) < 1e-14
+    y = orc.C.gen_gaussian(300, 20, 3)
+    y[:, 11] = y[:, 4]
+    _, _, st, bad = orc.C.qr(y)
+    assert st == 4
+    with pytest.raises(rl.RankDeficiencyError) as e:
+        rl.qr(y)
+    assert e.value.column == bad == 12
+
+
+def test_range_finder_exact_low_rank(cuda, orc):
+    """tests/test_lowrank.cpp:20-29"""
+    n, r = 24, 5
+    a, sig = _lownumrank(n, r, 11, tail=0.0)
+    res = rl.range_find(a, r, 0, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 12))
+    assert res.sketch_width() == r
+    assert rl.approximation_residual(a, res) <= 1e-10 * np.linalg.norm(a, 2)
+    assert np.linalg.norm(res.q.T @ res.q - np.eye(r)) <= 1e-10 * n
+
+
+def test_axis_aligned_residual(cuda):
+    """tests/test_lowrank.cpp:31-39: residual == the dropped singular value"""
+    a = np.diag([1.0, 1e-10])
+    h = np.array([[1.0], [0.0]])
+    res = rl.range_find(a, 1, 0, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 0, dense=h))
+    assert abs(rl.approximation_residual(a, res) - 1e-10) <= 1e-12 * 1e-10
+    assert abs(res.info["residual_frobenius"] - 1e-10) <= 1e-12 * 1e-10
+
+
+def test_mean_residual_known_rank_ensemble(cuda):
+    """tests/test_lowrank.cpp:41-52 analogue (20 trials, n=64, r=8)"""
+    tot = 0.0
+    for t in range(20):
+        a, _ = _lownumrank(64, 8, 1000 + t)
+        res = rl.range_find(a, 8, 0, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, rl.derive_seed(22, t)))
+        tot += rl.approximation_residual(a, res)
+    assert tot / 20 <= 1e-6
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "toeplitz"])
+def test_range_find_residual_vs_oracle(cuda, orc, kind):
+    """Y, Q and the residual against the oracle's Householder path on the same
+    inputs; ||R||_2 against numpy's SVD of the oracle's residual."""
+    m = n = 1024
+    r = 32
+    rng = np.random.default_rng(4)
+    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    sig = np.logspace(0, -2, r)
+    a = (u * sig) @ v.T + 1e-10 * rng.standard_normal((m, n))
+    if kind == "gaussian":
+        spec = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 77)
+        y_ref = orc.C.matmul(a, orc.C.gen_gaussian(n, r, 77))
+    else:
+        spec = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN_CIRCULANT, 21)
+        y_ref, st = orc.C.matmul_by_toeplitz_block(a, orc.C.gen_gaussian_vector(n, 21), r)
+        assert st == 0
+    res = rl.range_find(a, r, 0, spec)
+    q_ref, _, st, _ = orc.C.qr(y_ref)
+    assert st == 0
+    # same subspace: compare projectors through Q^T Q_ref (sign-free)
+    assert np.abs(np.abs(np.linalg.svd(res.q.T @ q_ref, compute_uv=False)) - 1).max() < 1e-6
+    resid_ref = a - q_ref @ (q_ref.T @ a)
+    s_ref = np.linalg.svd(resid_ref, compute_uv=False)
+    floor = 2.2e-16 * np.linalg.norm(a, 2) / s_ref[0]  # rounding floor of the comparison (SURVEY finding 9)
+    assert abs(res.info["residual_frobenius"] / np.linalg.norm(resid_ref) - 1) <= max(1e-6, 100 * floor)
+    # power iteration: a lower bound of sigma_1 converging to it
+    rel = abs(res.info["residual_spectral"] / s_ref[0] - 1)
+    print(kind, "sigma1", s_ref[0], "est", res.info["residual_spectral"], "rel", rel, "its", res.info["power_iterations"])
+    assert rel <= 0.05
