@@ -467,6 +467,17 @@ rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a,
 
 }  // namespace rl
 
+namespace rl {
+// dense expansion (device) of the leading k x l block of the np-point circulant
+rl_status circulant_dense(rl_context* ctx, const double* c, int64_t np, int64_t k, int64_t l, double* h, int64_t ldh) {
+    circulant_dense_kernel<<<static_cast<unsigned>((k * l + 255) / 256), 256, 0, ctx->stream>>>(c, np, k, l, h, ldh);
+    RL_CHECK_LAUNCH("circulant_dense_kernel");
+    return RL_OK;
+}
+
+bool circulant_fft_ok(int64_t np) { return is_pow2(np) && np <= 2 * MAXN; }
+}  // namespace rl
+
 // ---- C ABI -----------------------------------------------------------------
 namespace {
 using namespace rl;

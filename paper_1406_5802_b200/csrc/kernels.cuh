@@ -60,6 +60,11 @@ rl_status spectral_norm_estimate_device(rl_context* ctx, int64_t m, int64_t n, c
 rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a, int64_t lda, int64_t np,
                          const double* c, int64_t l, double* out, int64_t ldo, void* spec_ws);
 
+// dense expansion of the leading k x l block of the np-point circulant (device)
+rl_status circulant_dense(rl_context* ctx, const double* c, int64_t np, int64_t k, int64_t l, double* h, int64_t ldh);
+// whether circulant_rows handles parent length np
+bool circulant_fft_ok(int64_t np);
+
 // batched 32x32 kernel (batched32.cu)
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,
                                 double* lu, double* x, double* r, double* growth, int32_t* status, int refine,

@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 
 extern "C" RL_API rl_status rl_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out);
+extern "C" RL_API rl_status rl_gen_real_circulant_column(int64_t n, uint64_t seed, double* out);
 
 namespace rl {
 namespace {
@@ -124,8 +125,14 @@ struct StageTimer {
     }
 };
 
+enum PostKind { POST_NONE, POST_DENSE, POST_CIRC };
+
 struct Dense {
     int64_t n = 0, ld = 0;
+    PostKind post = POST_NONE;
+    double* c = nullptr;   // circulant first column (device)
+    double* ct = nullptr;  // transposed circulant's first column c[(n-i) mod n]
+    void* spec = nullptr;  // FFT spectrum workspace (16 n bytes)
     double *A = nullptr, *G = nullptr, *P = nullptr;
     double *b = nullptr, *x = nullptr, *r = nullptr, *y = nullptr, *d = nullptr, *piv = nullptr, *rinv = nullptr;
     void* solve_work = nullptr;
@@ -133,20 +140,32 @@ struct Dense {
 };
 
 // P = A G (or A), blocked GENP in place, growth, verdict (lu.hpp:44-49).
-rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_info* info, StageTimer* tm = nullptr) {
+// product P = A H by the multiplier's own method (deterministic: the rare
+// exact-verdict path recomputes it bit for bit)
+rl_status form_product(rl_context* ctx, Dense& D, double* P, GemmStats* stats) {
+    const int64_t n = D.n;
+    if (D.post == POST_DENSE) return gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, P, D.ld, 1.0, false, stats);
+    if (D.post == POST_CIRC) {
+        // matmul_by_circulant (circulant.hpp:171-185), SideMultiplier::right_multiply (preprocess.hpp:65-73)
+        rl_status st = circulant_rows(ctx, n, n, D.A, D.ld, n, D.c, n, P, D.ld, D.spec);
+        if (st != RL_OK) return st;
+    } else {
+        RL_CUDA(cudaMemcpy2DAsync(P, D.ld * 8, D.A, D.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (stats) {
+        matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, ctx->stream>>>(P, D.ld, n, false, stats);
+        RL_CHECK_LAUNCH("matrix_stats_kernel");
+    }
+    return RL_OK;
+}
+
+rl_status factor_and_verdict(rl_context* ctx, Dense& D, rl_solve_info* info, StageTimer* tm = nullptr) {
     cudaStream_t s = ctx->stream;
     const int64_t n = D.n;
     RL_CUDA(cudaMemsetAsync(D.sc, 0, sizeof(Scalars), s));
     rl_status st;
     if (tm) tm->mark();
-    if (have_g) {
-        st = gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, D.P, D.ld, 1.0, false, &D.sc->prod);
-        if (st != RL_OK) return st;
-    } else {
-        RL_CUDA(cudaMemcpy2DAsync(D.P, D.ld * 8, D.A, D.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
-        matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(D.P, D.ld, n, false, &D.sc->prod);
-        RL_CHECK_LAUNCH("matrix_stats_kernel");
-    }
+    if ((st = form_product(ctx, D, D.P, &D.sc->prod)) != RL_OK) return st;
     if (tm) tm->mark();
     st = genp_inplace(ctx, n, D.P, D.ld, D.piv, D.rinv);
     if (st != RL_OK) return st;
@@ -177,10 +196,7 @@ rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_in
     // a recomputed product and apply the reference's test
     double* prod = nullptr;  // stream-ordered: D's pointers live in the context workspace
     RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&prod), sizeof(double) * n * D.ld, s));
-    if (have_g)
-        st = gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, prod, D.ld, 1.0, false, nullptr);
-    else
-        RL_CUDA(cudaMemcpy2DAsync(prod, D.ld * 8, D.A, D.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, s));
+    st = form_product(ctx, D, prod, nullptr);
     double est = 0.0;
     if (st == RL_OK) st = spectral_norm_estimate_device(ctx, n, n, prod, D.ld, &est);
     cudaFreeAsync(prod, s);
@@ -203,7 +219,7 @@ rl_status factor_and_verdict(rl_context* ctx, Dense& D, bool have_g, rl_solve_in
 
 // iterative_refine with the chain solver x = G (LU)^-1 r from x0 = 0,
 // refine+1 steps (preprocess.hpp:115-143, :170-178)
-rl_status chain_solve(rl_context* ctx, Dense& D, bool have_g, int64_t refine, rl_solve_info* info) {
+rl_status chain_solve(rl_context* ctx, Dense& D, int64_t refine, rl_solve_info* info) {
     cudaStream_t s = ctx->stream;
     const int64_t n = D.n;
     rl_status st = sumsq(ctx, n, D.b, D.sc->bsq);
@@ -219,8 +235,12 @@ rl_status chain_solve(rl_context* ctx, Dense& D, bool have_g, int64_t refine, rl
     for (int64_t k = 0; k < steps; ++k) {
         st = lu_solve_device(ctx, n, D.P, D.ld, D.rinv, D.r, D.y, D.solve_work);
         if (st != RL_OK) return st;
-        if (have_g) {
+        if (D.post == POST_DENSE) {  // H y = matvec (preprocess.hpp:88-94)
             st = gemv(ctx, n, n, D.G, D.ld, D.y, D.d, nullptr);
+            if (st != RL_OK) return st;
+        } else if (D.post == POST_CIRC) {
+            // H y = circulant_apply(C, y) (circulant.hpp:85-91): the row y^T times C^T
+            st = circulant_rows(ctx, 1, n, D.y, n, n, D.ct, n, D.d, n, D.spec);
             if (st != RL_OK) return st;
         } else {
             RL_CUDA(cudaMemcpyAsync(D.d, D.y, n * 8, cudaMemcpyDeviceToDevice, s));
@@ -307,19 +327,25 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     if (!a || !b || !x) return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: a, b, x are required");
     if (refine_steps < 0) return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: negative refine_steps");
     const int kind = post ? post->kind : RL_MULT_NONE;
-    if (kind != RL_MULT_NONE && kind != RL_MULT_GAUSSIAN)
-        return set_error(RL_ERR_UNSUPPORTED, "preprocess_solve: circulant multipliers go through rl_preprocessed_genp_solve_circulant");
+    if (kind < RL_MULT_NONE || kind > RL_MULT_GAUSSIAN_CIRCULANT)
+        return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: unknown multiplier kind %d", kind);
     rl_status st;
     ctx = resolve(ctx, &st);
     if (!ctx) return st;
     const bool host = mem == RL_HOST;
-    const bool have_g = kind == RL_MULT_GAUSSIAN;
+    const bool circ = kind == RL_MULT_REAL_CIRCULANT || kind == RL_MULT_GAUSSIAN_CIRCULANT;
+    // SideMultiplier::make (preprocess.hpp:27-60): circulants stay structured
+    // (FFT products) when the FFT kernel covers n; otherwise their dense
+    // expansion goes through the GEMM path
+    const bool circ_fft = circ && circulant_fft_ok(n);
+    const bool dense = kind == RL_MULT_GAUSSIAN || (circ && !circ_fft);
     const int64_t ld = (n + 1) & ~int64_t(1);
     // device A can be used in place when it is TMA-compatible (even n, aligned)
     const bool own_a = host || !((n & 1) == 0 && aligned_even(a, n));
-    const bool g_dev_direct = have_g && !host && post->dense && (n & 1) == 0 && aligned_even(post->dense, n);
+    const bool g_dev_direct = kind == RL_MULT_GAUSSIAN && !host && post->dense && (n & 1) == 0 && aligned_even(post->dense, n);
     Dense D;
-    st = dense_alloc(ctx, D, n, have_g && !g_dev_direct, own_a, true);
+    D.post = dense ? POST_DENSE : (circ ? POST_CIRC : POST_NONE);
+    st = dense_alloc(ctx, D, n, dense && !g_dev_direct, own_a, true);
     if (st != RL_OK) return st;
     cudaStream_t s = ctx->stream;
     if (own_a) {
@@ -328,7 +354,37 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         D.A = const_cast<double*>(a);
     }
     std::vector<double> hg;
-    if (have_g) {
+    struct Col {
+        double* p = nullptr;
+        cudaStream_t s;
+        ~Col() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } colbuf{nullptr, s};
+    if (circ) {
+        // first column: explicit, or drawn by the family's generator
+        std::vector<double> col(static_cast<size_t>(n));
+        if (post->column) {
+            if (host)
+                std::memcpy(col.data(), post->column, n * 8);
+            else
+                RL_CUDA(cudaMemcpy(col.data(), post->column, n * 8, cudaMemcpyDeviceToHost));
+        } else if (kind == RL_MULT_GAUSSIAN_CIRCULANT) {
+            rl_gen_gaussian(n, 1, post->seed, col.data());  // gen_gaussian_vector (testbed/inputs.hpp:85-90)
+        } else {
+            rl_gen_real_circulant_column(n, post->seed, col.data());  // multipliers.hpp:67-73
+        }
+        std::vector<double> colt(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) colt[i] = col[(n - i) % n];  // circulant.hpp:40-45
+        RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&colbuf.p), sizeof(double) * 2 * n + 16 * n + 256, s));
+        D.c = colbuf.p;
+        D.ct = colbuf.p + n;
+        D.spec = colbuf.p + 2 * n;
+        RL_CUDA(cudaMemcpyAsync(D.c, col.data(), n * 8, cudaMemcpyHostToDevice, s));
+        RL_CUDA(cudaMemcpyAsync(D.ct, colt.data(), n * 8, cudaMemcpyHostToDevice, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+        if (dense && (st = circulant_dense(ctx, D.c, n, n, n, D.G, ld)) != RL_OK) return st;
+    } else if (kind == RL_MULT_GAUSSIAN) {
         if (g_dev_direct) {
             D.G = const_cast<double*>(post->dense);
         } else if (post->dense) {
@@ -342,13 +398,13 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     }
     RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
     StageTimer timer(s);
-    st = factor_and_verdict(ctx, D, have_g, info, &timer);
+    st = factor_and_verdict(ctx, D, info, &timer);
     if (st != RL_OK) {
         RL_CUDA(cudaStreamSynchronize(s));
         return st;
     }
     timer.mark();
-    st = chain_solve(ctx, D, have_g, refine_steps, info);
+    st = chain_solve(ctx, D, refine_steps, info);
     if (st != RL_OK) return st;
     timer.mark();
     timer.fill(info->stage_ms);
@@ -385,7 +441,7 @@ extern "C" RL_API rl_status rl_genp_factor(rl_context* ctx, rl_mem mem, int64_t 
     st = dense_alloc(ctx, D, n, false, true, true);
     if (st != RL_OK) return st;
     if ((st = copy_in(ctx, D.A, D.ld, a, n, n, host)) != RL_OK) return st;
-    st = factor_and_verdict(ctx, D, false, info);
+    st = factor_and_verdict(ctx, D, info);
     if (st != RL_OK && st != RL_ERR_ZERO_PIVOT) return st;
     const rl_status verdict = st;
     if ((st = copy_out(ctx, lu, D.P, D.ld, n, n, host)) != RL_OK) return st;
