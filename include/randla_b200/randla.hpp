@@ -202,9 +202,9 @@ inline LuFactors genp_factor(const RealMatrix& a) {
     const std::size_t n = a.rows();
     if (a.cols() != n) throw DimensionError("genp_factor: square input required");
     RealMatrix packed(n, n);
-    rl_solve_info info;
-    detail::check(rl_genp_factor(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), packed.data(), &info),
-                  info.zero_pivot_step);
+    rl_solve_info info{};
+    const rl_status st = rl_genp_factor(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), packed.data(), &info);
+    detail::check(st, info.zero_pivot_step);  // step read after the call
     return detail::unpack(packed);
 }
 
@@ -249,9 +249,10 @@ inline SolveOutcome preprocess_solve(const RealMatrix& a, const std::vector<doub
     m.seed = post_spec.seed;
     SolveOutcome out;
     out.x.resize(n);
-    detail::check(rl_preprocessed_genp_solve(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), b.data(), &m,
-                                             static_cast<int64_t>(refine_steps), out.x.data(), nullptr, 0, &out.info),
-                  out.info.zero_pivot_step);
+    const rl_status st = rl_preprocessed_genp_solve(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), b.data(), &m,
+                                                    static_cast<int64_t>(refine_steps), out.x.data(), nullptr, 0,
+                                                    &out.info);
+    detail::check(st, out.info.zero_pivot_step);
     out.residual_history.assign(out.info.residual_history, out.info.residual_history + out.info.history_len);
     out.diverged = out.info.diverged != 0;
     return out;
