@@ -26,12 +26,23 @@
 namespace rl {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
-constexpr int A_STAGE = BM * BK * 8;  // 16 KiB
-constexpr int B_STAGE = BK * BN * 8;  // 16 KiB (8 boxes of 16 x 16)
-constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 64;
-constexpr int GROUP_M = 8;
+constexpr int BK = 16, THREADS = 256, GROUP_M = 8;
+
+// Tile configurations. Big: 128x128 CTA tile, 8 warps of 64x32, one CTA per
+// SM (long-K products such as A*G). Small: 128x64 tile, 8 warps of 32x32,
+// two CTAs per SM so one CTA's epilogue (C read-modify-write) overlaps the
+// other's MMA main loop — the short-K Schur updates of blocked GENP.
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+struct Cfg {
+    static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+    static constexpr int MI = BM / WM / 8, NJ = BN / WN / 8;  // 8x8 fragments per warp
+    static constexpr int A_STAGE = BM * BK * 8, B_STAGE = BK * BN * 8;
+    static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+    static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 64;
+    static_assert(WM * WN * 32 == THREADS, "8 warps");
+};
+using BigCfg = Cfg<128, 128, 2, 4, 4, 1>;
+using SmallCfg = Cfg<128, 64, 4, 2, 4, 2>;
 
 // element (r, k) of a 128-byte-swizzled tile with 16 doubles per row
 __device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3); }
@@ -40,20 +51,22 @@ __device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 
 // of the result into *stats; kStore = false: statistics only (e.g. the
 // low-rank residual A - Q (Q^T A) is never materialised). Split-K: blockIdx.y
 // takes k-tiles [y*ktc, (y+1)*ktc) and writes its partial at C + y*split_stride.
-template <bool kAccum, bool kStats, bool kStore>
-__global__ void __launch_bounds__(THREADS, 1)
+template <class CF, bool kAccum, bool kStats, bool kStore>
+__global__ void __launch_bounds__(THREADS, CF::MINB)
 dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
              int64_t ldc, int M, int N, int K, double alpha, GemmStats* __restrict__ stats, int ktc,
              int64_t split_stride) {
+    constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, MI = CF::MI, NJ = CF::NJ;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle, keeping the pointer in the
     // shared window so operand reads compile to LDS (not generic LD)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wm = warp >> 2, wn = warp & 3;
+    const int wm = warp / CF::WN, wn = warp % CF::WN;
     const int fr = lane >> 2, fc = lane & 3;
+    const int rbase = wm * (MI * 8), cbase = wn * (NJ * 8);
 
     // grouped raster over (tiles_m x tiles_n)
     const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
@@ -79,12 +92,12 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 
     auto issue = [&](int kt) {
         const int s = kt % STAGES;
-        unsigned char* st = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
+        unsigned char* st = smem + s * CF::STAGE_BYTES;
+        mbar_expect_tx(&full[s], CF::STAGE_BYTES);
         tma_load_2d(st, &tmA, (kt0 + kt) * BK, m0, &full[s]);
 #pragma unroll
         for (int j = 0; j < BN / 16; ++j)
-            tma_load_2d(st + A_STAGE + j * 2048, &tmB, n0 + 16 * j, (kt0 + kt) * BK, &full[s]);
+            tma_load_2d(st + CF::A_STAGE + j * 2048, &tmB, n0 + 16 * j, (kt0 + kt) * BK, &full[s]);
     };
     if (tid == 0)
         for (int kt = 0; kt < min(STAGES, KT); ++kt) issue(kt);
@@ -92,21 +105,21 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     // accumulators: 0, or (kAccum) the current C tile, fetched with all loads
     // in flight at once while the first TMA stages land; alpha = -1 is then
     // applied by negating the A fragments (C - A B, the Schur update)
-    double acc[8][4][2];
+    double acc[MI][NJ][2];
     const bool vec_ok = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     if (kAccum) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int row = m0 + wm * 64 + 8 * i + fr;
+        for (int i = 0; i < MI; ++i) {
+            const int row = m0 + rbase + 8 * i + fr;
             if (row >= M) continue;
             const double* crow = C + static_cast<int64_t>(row) * ldc;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int col = n0 + wn * 32 + 8 * j + 2 * fc;
+            for (int j = 0; j < NJ; ++j) {
+                const int col = n0 + cbase + 8 * j + 2 * fc;
                 if (vec_ok && col + 1 < N) {
                     const double2 o = *reinterpret_cast<const double2*>(crow + col);
                     acc[i][j][0] = o.x;
@@ -123,23 +136,24 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % STAGES;
         mbar_wait(&full[s], (kt / STAGES) & 1);
-        const unsigned char* sa = smem + s * STAGE_BYTES;
-        const unsigned char* sb = sa + A_STAGE;
+        const unsigned char* sa = smem + s * CF::STAGE_BYTES;
+        const unsigned char* sb = sa + CF::A_STAGE;
 #pragma unroll
         for (int kk = 0; kk < BK / 4; ++kk) {
             const int k = 4 * kk + fc;
-            double af[8], bf[4];
+            double af[MI], bf[NJ];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = asign * *reinterpret_cast<const double*>(sa + swz128(wm * 64 + 8 * i + fr, k));
+            for (int i = 0; i < MI; ++i)
+                af[i] = asign * *reinterpret_cast<const double*>(sa + swz128(rbase + 8 * i + fr, k));
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int n = wn * 32 + 8 * j + fr;
+            for (int j = 0; j < NJ; ++j) {
+                const int n = cbase + 8 * j + fr;
                 bf[j] = *reinterpret_cast<const double*>(sb + (n >> 4) * 2048 + swz128(k, n & 15));
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                for (int j = 0; j < NJ; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         __syncthreads();
         if (tid == 0 && kt + STAGES < KT) issue(kt + STAGES);
@@ -148,13 +162,13 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     // ---- epilogue
     double ssq = 0.0, amax = 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int row = m0 + wm * 64 + 8 * i + fr;
+    for (int i = 0; i < MI; ++i) {
+        const int row = m0 + rbase + 8 * i + fr;
         if (row >= M) continue;
         double* crow = C + static_cast<int64_t>(row) * ldc;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int col = n0 + wn * 32 + 8 * j + 2 * fc;
+        for (int j = 0; j < NJ; ++j) {
+            const int col = n0 + cbase + 8 * j + 2 * fc;
             const double v0 = kAccum ? acc[i][j][0] : alpha * acc[i][j][0];
             const double v1 = kAccum ? acc[i][j][1] : alpha * acc[i][j][1];
             if (vec_ok && col + 1 < N) {
@@ -208,21 +222,39 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-template <bool A, bool S, bool T>
+template <class CF, bool A, bool S, bool T>
 void configure_once() {
     static bool done = false;
     if (!done) {
-        cudaFuncSetAttribute(dgemm_kernel<A, S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(SMEM_BYTES));
+        cudaFuncSetAttribute(dgemm_kernel<CF, A, S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(CF::SMEM_BYTES));
         done = true;
     }
 }
 
-template <bool A, bool S, bool T>
-void launch(dim3 grid, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, double* C, int64_t ldc, int m,
-            int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride) {
-    configure_once<A, S, T>();
-    dgemm_kernel<A, S, T><<<grid, THREADS, SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc, split_stride);
+template <class CF, bool A, bool S, bool T>
+void launch_cfg(dim3 grid, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, double* C, int64_t ldc, int m,
+                int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride) {
+    configure_once<CF, A, S, T>();
+    dgemm_kernel<CF, A, S, T><<<grid, THREADS, CF::SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc,
+                                                                       split_stride);
+}
+
+// encode the operand maps for configuration CF and launch over all tiles
+template <class CF, bool A, bool S, bool T>
+rl_status run_cfg(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* Ap, int64_t lda, const double* Bp,
+                  int64_t ldb, double* C, int64_t ldc, double alpha, GemmStats* stats, int splits, int ktc,
+                  int64_t split_stride) {
+    CUtensorMap ta, tb;
+    if (!make_tmap_2d(&ta, Ap, M, K, lda, CF::BM, BK, true) || !make_tmap_2d(&tb, Bp, K, N, ldb, BK, 16, true))
+        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
+    const int64_t tiles = ((M + CF::BM - 1) / CF::BM) * ((N + CF::BN - 1) / CF::BN);
+    if (tiles > 0x7fffffff) return set_error(RL_ERR_DIMENSION, "gemm: too many tiles");
+    launch_cfg<CF, A, S, T>(dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), ctx->stream, ta, tb, C,
+                            ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), alpha, stats, ktc,
+                            split_stride);
+    RL_CHECK_LAUNCH("dgemm_kernel");
+    return RL_OK;
 }
 
 __global__ void reduce_splits_kernel(const double* __restrict__ part, int splits, int64_t slab, int64_t M, int64_t N,
@@ -265,27 +297,20 @@ rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm: accumulate supports alpha = +1 or -1");
     if (M > (int64_t(1) << 30) || N > (int64_t(1) << 30) || K > (int64_t(1) << 30))
         return set_error(RL_ERR_DIMENSION, "gemm: dimension too large");
-    CUtensorMap ta, tb;
-    if (!make_tmap_2d(&ta, A, M, K, lda, BM, BK, true) || !make_tmap_2d(&tb, B, K, N, ldb, BK, 16, true))
-        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    if (tiles > 0x7fffffff) return set_error(RL_ERR_DIMENSION, "gemm: too many tiles");
-    const dim3 grid(static_cast<unsigned>(tiles));
-    const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
-    cudaStream_t st = ctx->stream;
+    // short K (Schur updates): the two-CTAs-per-SM configuration
+    const bool small = K <= 256;
     if (accumulate) {
         if (stats)
-            launch<true, true, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
-        else
-            launch<true, false, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
-    } else {
-        if (stats)
-            launch<false, true, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
-        else
-            launch<false, false, true>(grid, st, ta, tb, C, ldc, m, n, k, alpha, stats, 0, 0);
+            return small ? run_cfg<SmallCfg, true, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
+                         : run_cfg<BigCfg, true, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
+        return small ? run_cfg<SmallCfg, true, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
+                     : run_cfg<BigCfg, true, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
     }
-    RL_CHECK_LAUNCH("dgemm_kernel");
-    return RL_OK;
+    if (stats)
+        return small ? run_cfg<SmallCfg, false, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
+                     : run_cfg<BigCfg, false, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
+    return small ? run_cfg<SmallCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
+                 : run_cfg<BigCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
 }
 
 rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
@@ -293,14 +318,11 @@ rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, 
     if (M <= 0 || N <= 0) return RL_OK;
     if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_residual_stats: misaligned operands");
-    CUtensorMap ta, tb;
-    if (!make_tmap_2d(&ta, A, M, K, lda, BM, BK, true) || !make_tmap_2d(&tb, B, K, N, ldb, BK, 16, true))
-        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    launch<true, true, false>(dim3(static_cast<unsigned>(tiles)), ctx->stream, ta, tb, const_cast<double*>(C), ldc,
-                              static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), -1.0, stats, 0, 0);
-    RL_CHECK_LAUNCH("dgemm_kernel(residual stats)");
-    return RL_OK;
+    const bool small = K <= 256;
+    return small ? run_cfg<SmallCfg, true, true, false>(ctx, M, N, K, A, lda, B, ldb, const_cast<double*>(C), ldc, -1.0,
+                                                        stats, 1, 0, 0)
+                 : run_cfg<BigCfg, true, true, false>(ctx, M, N, K, A, lda, B, ldb, const_cast<double*>(C), ldc, -1.0,
+                                                      stats, 1, 0, 0);
 }
 
 size_t gemm_splitk_work_bytes(int64_t M, int64_t N, int splits) {
@@ -317,17 +339,12 @@ rl_status gemm_splitk(rl_context* ctx, int64_t M, int64_t N, int64_t K, const do
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_splitk: misaligned operands");
     const int ktc = (KT + splits - 1) / splits;
     splits = (KT + ktc - 1) / ktc;
-    CUtensorMap ta, tb;
-    if (!make_tmap_2d(&ta, A, M, K, lda, BM, BK, true) || !make_tmap_2d(&tb, B, K, N, ldb, BK, 16, true))
-        return set_error(RL_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed");
     const int64_t ldp = (N + 1) & ~int64_t(1);
     const int64_t slab = M * ldp;
     double* part = static_cast<double*>(work);
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    launch<false, false, true>(dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), ctx->stream, ta, tb,
-                               part, ldp, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), 1.0, nullptr,
-                               ktc, slab);
-    RL_CHECK_LAUNCH("dgemm_kernel(split-k)");
+    rl_status st = run_cfg<BigCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, part, ldp, 1.0, nullptr, splits,
+                                                       ktc, slab);
+    if (st != RL_OK) return st;
     reduce_splits_kernel<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, ctx->stream>>>(
         part, splits, slab, M, N, ldp, C, ldc, accumulate, alpha);
     RL_CHECK_LAUNCH("reduce_splits_kernel");

@@ -91,6 +91,16 @@ panel_diag_reg_kernel(double* __restrict__ a, int64_t lda, double* __restrict__ 
     rinv_out[i] = 1.0 / mypiv;
 }
 
+// 1/x: MUFU seed + two Newton steps (no division subroutine on the critical path)
+__device__ __forceinline__ double rcp64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 // a / b correctly rounded from r = 1/b (one residual correction)
 __device__ __forceinline__ double div_by(double a, double b, double r) {
     const double q0 = a * r;
@@ -189,30 +199,57 @@ trsm_lower_unit_kernel_dyn(const double* __restrict__ l, int64_t ldl, int w, dou
 // factored diagonal block and the pivots. One launch per elimination step;
 // the trailing update A22 -= L21 U12 is one DMMA GEMM (K = 64).
 constexpr int PT = 128;  // threads per CTA
+
+// GENP of the 64x64 block in sd (lu.hpp:47-56 order), register-resident:
+// thread t owns row t>>1, columns of parity t&1 (32 values). The pivot row is
+// published through a double-buffered shared row (one barrier per step), the
+// multiplier's column value comes from the parity partner by shuffle. No
+// shared-memory read-after-write chains inside a step.
+__device__ __forceinline__ void factor64_regs(double (*sd)[kBase + 1], double (*pbuf)[kBase], int tid) {
+    const int row = tid >> 1, h = tid & 1;
+    double r[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) r[q] = sd[row][2 * q + h];
+#pragma unroll
+    for (int j = 0; j < kBase; ++j) {
+        double* prow = pbuf[j & 1];
+        if (row == j) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) prow[2 * q + h] = r[q];
+        }
+        __syncthreads();
+        const double pv = prow[j];
+        const double mine = r[j >> 1];
+        const double other = __shfl_xor_sync(kFull, mine, 1);
+        const double colj = (h == (j & 1)) ? mine : other;
+        const bool below = row > j;
+        const double l = below ? div_by(colj, pv, rcp64(pv)) : 0.0;  // multiplier (lu.hpp:51)
+        if (below && h == (j & 1)) r[j >> 1] = l;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            if (2 * q + 1 > j) {  // columns k = 2q + h > j (static bound first, parity at run time)
+                const int k = 2 * q + h;
+                if (k > j) r[q] = fma(-l, prow[k], r[q]);
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) sd[row][2 * q + h] = r[q];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(PT)
 lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
                   double* __restrict__ piv_out, double* __restrict__ rinv_out) {
     __shared__ double sd[kBase][kBase + 1];
+    __shared__ __align__(16) double pbuf[2][kBase];
     __shared__ double sp[kBase], sr[kBase];
     const int tid = threadIdx.x;
     double* d = a + c0 * lda + c0;
     for (int idx = tid; idx < kBase * kBase; idx += PT) sd[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
     __syncthreads();
-    {
-        const int row = tid >> 1, h = tid & 1;
-        for (int j = 0; j < kBase; ++j) {
-            const double pv = sd[j][j];
-            double l = 0.0;
-            if (row > j) l = sd[row][j] / pv;  // multiplier (lu.hpp:51)
-            __syncwarp();
-            if (row > j) {
-                if ((j & 1) == h) sd[row][j] = l;
-#pragma unroll 4
-                for (int k = j + 1 + ((j + 1 + h) & 1); k < kBase; k += 2) sd[row][k] = fma(-l, sd[j][k], sd[row][k]);
-            }
-            __syncthreads();
-        }
-    }
+    factor64_regs(sd, pbuf, tid);
     if (tid < kBase) {
         sp[tid] = sd[tid][tid];
         sr[tid] = 1.0 / sd[tid][tid];
