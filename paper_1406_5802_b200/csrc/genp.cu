@@ -299,6 +299,31 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     }
 }
 
+// ---- U12 = L11^-1 A12 for the trailing columns of a 64-row panel ---------
+// (the column half of the fused step, split out so it can run after the
+// trailing update of the previous step while the next panel factors on the
+// lookahead stream); L11 comes from the already factored diagonal block.
+__global__ void __launch_bounds__(PT)
+lu_u12_kernel(double* __restrict__ a, int64_t lda, int64_t c0, int64_t col_begin, int64_t ncols) {
+    __shared__ double sl[kBase][kBase + 1];
+    const int tid = threadIdx.x;
+    const double* d = a + c0 * lda + c0;
+    for (int idx = tid; idx < kBase * kBase; idx += PT) sl[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
+    __syncthreads();
+    const int64_t cidx = static_cast<int64_t>(blockIdx.x) * PT + tid;
+    if (cidx >= ncols) return;
+    double* col = a + c0 * lda + col_begin + cidx;
+    double x[kBase];
+#pragma unroll
+    for (int i = 0; i < kBase; ++i) x[i] = col[i * lda];
+#pragma unroll
+    for (int k = 0; k < kBase - 1; ++k)
+#pragma unroll
+        for (int i = k + 1; i < kBase; ++i) x[i] = fma(-sl[i][k], x[k], x[i]);
+#pragma unroll
+    for (int i = 0; i < kBase; ++i) col[i * lda] = x[i];
+}
+
 struct Ctx {
     rl_context* ctx;
     double* a;
@@ -373,7 +398,73 @@ rl_status rec(const Ctx& g, int64_t c0, int64_t w) {
 rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out) {
     if (n <= 0) return RL_OK;
     Ctx g{ctx, a, n, lda, piv_out, rinv_out};
-    // right-looking blocked GENP, 64-column panels (see lu_panel64_kernel)
+    const int64_t K = n / kBase;  // full 64-column panels
+    rl_status st;
+    if (K >= 3) {
+        // right-looking GENP with a one-panel lookahead on two streams:
+        //   hi: GEMM_a(k) (next panel's 64 columns) -> panel_L(k+1)
+        //   lo: U12(k) -> GEMM_b(k) (all later columns)
+        // so the latency-bound panel factorisation of step k+1 runs under the
+        // bulk trailing update of step k.
+        constexpr int kRing = 8;
+        if ((st = side_resources(ctx, kRing + 2)) != RL_OK) return st;
+        cudaStream_t lo = ctx->stream, hi = ctx->hi_stream;
+        cudaEvent_t* ev = ctx->events;
+        int e = 0;
+        auto next_event = [&]() { return ev[2 + (e++ % kRing)]; };
+        RL_CUDA(cudaEventRecord(ev[0], lo));  // prior work on the caller's stream
+        RL_CUDA(cudaStreamWaitEvent(hi, ev[0], 0));
+        auto panel_l = [&](int64_t c0) -> rl_status {
+            const int64_t rest = n - c0 - kBase;
+            const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
+            lu_panel64_kernel<<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
+            RL_CHECK_LAUNCH("lu_panel64_kernel");
+            return RL_OK;
+        };
+        if ((st = panel_l(0)) != RL_OK) return st;
+        cudaEvent_t el = next_event();
+        RL_CUDA(cudaEventRecord(el, hi));
+        for (int64_t k = 0; k < K; ++k) {
+            const int64_t c0 = k * kBase, rest = n - c0 - kBase;
+            if (rest <= 0) break;
+            // lo: U12(k) for all trailing columns
+            RL_CUDA(cudaStreamWaitEvent(lo, el, 0));
+            lu_u12_kernel<<<static_cast<unsigned>((rest + PT - 1) / PT), PT, 0, lo>>>(a, lda, c0, c0 + kBase, rest);
+            RL_CHECK_LAUNCH("lu_u12_kernel");
+            cudaEvent_t eu = next_event();
+            RL_CUDA(cudaEventRecord(eu, lo));
+            const int64_t wa = std::min<int64_t>(kBase, rest);  // next panel's columns
+            const bool next_full = (k + 1 < K);
+            // hi: GEMM_a(k) -> panel_L(k+1)
+            RL_CUDA(cudaStreamWaitEvent(hi, eu, 0));
+            if (next_full) {
+                cudaStream_t keep = ctx->stream;
+                ctx->stream = hi;
+                st = gemm(ctx, rest, wa, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
+                          a + (c0 + kBase) * lda + c0 + kBase, lda, -1.0, true, nullptr);
+                ctx->stream = keep;
+                if (st != RL_OK) return st;
+                if ((st = panel_l(c0 + kBase)) != RL_OK) return st;
+                el = next_event();
+                RL_CUDA(cudaEventRecord(el, hi));
+            }
+            // lo: GEMM_b(k) on the remaining columns (or all of them when the
+            // ragged tail follows)
+            const int64_t cb = next_full ? c0 + 2 * kBase : c0 + kBase;
+            const int64_t nb = n - cb;
+            if (nb > 0) {
+                st = gemm(ctx, rest, nb, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + cb, lda,
+                          a + (c0 + kBase) * lda + cb, lda, -1.0, true, nullptr);
+                if (st != RL_OK) return st;
+            }
+        }
+        RL_CUDA(cudaEventRecord(ev[1], hi));
+        RL_CUDA(cudaStreamWaitEvent(lo, ev[1], 0));
+        const int64_t c0 = K * kBase;
+        if (c0 < n) return panel(g, c0, n - c0);  // ragged last block (< 64 columns)
+        return RL_OK;
+    }
+    // small matrices: fused steps on one stream
     int64_t c0 = 0;
     for (; c0 + kBase <= n; c0 += kBase) {
         const int64_t rest = n - c0 - kBase;
@@ -381,8 +472,8 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         lu_panel64_kernel<<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         if (rest > 0) {
-            rl_status st = gemm(ctx, rest, rest, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
-                                a + (c0 + kBase) * lda + c0 + kBase, lda, -1.0, true, nullptr);
+            st = gemm(ctx, rest, rest, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
+                      a + (c0 + kBase) * lda + c0 + kBase, lda, -1.0, true, nullptr);
             if (st != RL_OK) return st;
         }
     }

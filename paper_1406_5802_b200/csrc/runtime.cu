@@ -53,6 +53,9 @@ static void destroy_context(rl_context* c) {
     if (c->ws) cudaFree(c->ws);
     if (c->flags) cudaFree(c->flags);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->hi_stream) cudaStreamDestroy(c->hi_stream);
+    for (int i = 0; i < c->num_events; ++i) cudaEventDestroy(c->events[i]);
+    delete[] c->events;
     delete c;
 }
 
@@ -100,6 +103,23 @@ rl_context* resolve(rl_context* ctx, rl_status* st) {
     }
     cudaSetDevice(t_default.ctx->device);
     return t_default.ctx;
+}
+
+rl_status side_resources(rl_context* ctx, int count) {
+    if (!ctx->hi_stream) {
+        int lo = 0, hi = 0;
+        RL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        RL_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, hi));
+    }
+    if (ctx->num_events < count) {
+        cudaEvent_t* ev = new cudaEvent_t[count];
+        for (int i = 0; i < ctx->num_events; ++i) ev[i] = ctx->events[i];
+        for (int i = ctx->num_events; i < count; ++i) RL_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        delete[] ctx->events;
+        ctx->events = ev;
+        ctx->num_events = count;
+    }
+    return RL_OK;
 }
 
 void* workspace(rl_context* ctx, size_t bytes) {

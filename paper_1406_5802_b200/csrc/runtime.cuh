@@ -22,6 +22,11 @@ struct rl_context {
     size_t ws_bytes = 0;
     void* flags = nullptr;  // small zero-initialised device scratch for verdicts / counters
     size_t flags_bytes = 0;
+    // lookahead stream (high priority) and an event pool for intra-call
+    // dependencies between it and `stream` (created on first use)
+    cudaStream_t hi_stream = nullptr;
+    cudaEvent_t* events = nullptr;
+    int num_events = 0;
 };
 
 namespace rl {
@@ -37,6 +42,9 @@ rl_context* resolve(rl_context* ctx, rl_status* st);
 
 // Grow-only device workspace; returns nullptr on OOM (error already set).
 void* workspace(rl_context* ctx, size_t bytes);
+
+// High-priority side stream and at least `count` reusable timing-free events.
+rl_status side_resources(rl_context* ctx, int count);
 
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
