@@ -152,13 +152,13 @@ __device__ __forceinline__ void dif_pass(cplx* z, int n, int N, const cplx* __re
         const int n0 = g & (M - 1), o = (g >> lgM) * N;
         cplx v[R];
 #pragma unroll
-        for (int j = 0; j < R; ++j) v[j] = z[o + n0 + j * M];
+        for (int j = 0; j < R; ++j) v[j] = z[(o + n0 + j * M)];
         dft_reg<R, false>(v);
         cplx w[R];
         pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, mask);
-        z[o + n0] = v[0];
+        z[(o + n0)] = v[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r) z[o + n0 + r * M] = cmul(v[brev<R>(r)], w[r]);
+        for (int r = 1; r < R; ++r) z[(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
     }
 }
 
@@ -175,14 +175,14 @@ __device__ __forceinline__ void dit_pass(cplx* z, int n, int N, const cplx* __re
         cplx w[R];
         pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, mask);
         cplx v[R];
-        v[0] = z[o + n0];
+        v[0] = z[(o + n0)];
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmulc(z[o + n0 + r * M], w[r]);
+        for (int r = 1; r < R; ++r) v[r] = cmulc(z[(o + n0 + r * M)], w[r]);
         dft_reg<R, true>(v);
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const cplx t = v[brev<R>(j)];
-            z[o + n0 + j * M] = {t.x * scale, t.y * scale};
+            z[(o + n0 + j * M)] = {t.x * scale, t.y * scale};
         }
     }
 }
@@ -396,6 +396,253 @@ __global__ void circulant_dense_kernel(const double* __restrict__ c, int64_t np,
     h[i * ldh + j] = c[((i - j) % np + np) % np];
 }
 
+// ---- real-input path: one real row per CTA through a half-length complex
+// transform (m = n/2 points, 16 m bytes of shared memory: two CTAs per SM at
+// n = 8192). z[j] = x[2j] + i x[2j+1]; after the DIF passes the spectrum sits
+// in digit-reversed order; pairs (k, m-k) are unpacked to the real spectrum
+// X_k, multiplied by the multiplier spectrum S_k (natural order), re-packed
+// for the half-length inverse, and the DIT passes return y[2j] + i y[2j+1].
+// Everything is specialised on L = log2 m, so pass loops, strides and the
+// digit reversal are compile-time constants.
+namespace r2c {
+
+template <int L>
+struct Shape {
+    static constexpr int m = 1 << L, n = 2 * m;
+    static constexpr int full = L / 4, rem = L % 4;
+    static constexpr int passes = full + (rem ? 1 : 0);
+    static constexpr int T = L >= 13 ? 512 : 256;  // threads per CTA
+    static constexpr int minb = L >= 13 ? 1 : 2;
+    __host__ __device__ static constexpr int radix(int p) { return p < full ? 16 : 1 << rem; }
+    __host__ __device__ static constexpr int sub(int p) { return m >> (4 * p); }  // subarray length entering pass p
+};
+
+// shared-memory slot of element i: XOR swizzle of the 16-byte slot index so
+// that the stride-16 (last radix-16 pass) and stride-256 (digit-reversed
+// unpack) patterns hit distinct bank groups within a quarter-warp
+__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 4) ^ (i >> 8)) & 7); }
+
+// position of frequency k after the DIF passes: base-16 digit reversal
+template <int L>
+__device__ __forceinline__ int dif_pos(int k) {
+    constexpr int full = L / 4;
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < full; ++i) p |= ((k >> (4 * i)) & 15) << (L - 4 * (i + 1));
+    return p | (k >> (4 * full));
+}
+
+// one DIF pass over subarrays of length N (radix R); kGlobal: the input is the
+// real row x (length k, zero padded), read straight from global memory
+template <int L, int R, int N, bool kGlobal>
+__device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k, const cplx* __restrict__ tw) {
+    using S = Shape<L>;
+    constexpr int M = N / R, groups = S::m / R;
+    constexpr int64_t tstride = S::n / N;
+#pragma unroll
+    for (int g0 = 0; g0 < groups; g0 += S::T) {
+        const int g = g0 + threadIdx.x;
+        if (groups % S::T != 0 && g >= groups) break;
+        const int n0 = g % M, o = (g / M) * N;
+        cplx v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int q = o + n0 + j * M;
+            if (kGlobal) {
+                if (2 * q + 1 < k) {
+                    const double2 t = __ldcs(reinterpret_cast<const double2*>(x) + q);
+                    v[j] = {t.x, t.y};
+                } else {
+                    v[j] = {2 * q < k ? x[2 * q] : 0.0, 0.0};
+                }
+            } else {
+                v[j] = z[swz(q)];
+            }
+        }
+        dft_reg<R, false>(v);
+        cplx w[R];
+        pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+        z[swz(o + n0)] = v[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) z[swz(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
+    }
+}
+
+// one DIT pass with conjugate twiddles; kGlobal: the last pass, writing
+// y[2q] = Re, y[2q+1] = Im (scaled) for 2q < l straight to global memory
+template <int L, int R, int N, bool kGlobal>
+__device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, double scale,
+                                    const cplx* __restrict__ tw) {
+    using S = Shape<L>;
+    constexpr int M = N / R, groups = S::m / R;
+    constexpr int64_t tstride = S::n / N;
+#pragma unroll
+    for (int g0 = 0; g0 < groups; g0 += S::T) {
+        const int g = g0 + threadIdx.x;
+        if (groups % S::T != 0 && g >= groups) break;
+        const int n0 = g % M, o = (g / M) * N;
+        cplx w[R];
+        pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+        cplx v[R];
+        v[0] = z[swz(o + n0)];
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmulc(z[swz(o + n0 + r * M)], w[r]);
+        dft_reg<R, true>(v);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const cplx t = v[brev<R>(j)];
+            const int q = o + n0 + j * M;
+            if (kGlobal) {
+                if (2 * q + 1 < l) {
+                    __stcs(reinterpret_cast<double2*>(y) + q, make_double2(t.x * scale, t.y * scale));
+                } else if (2 * q < l) {
+                    y[2 * q] = t.x * scale;
+                }
+            } else {
+                z[swz(q)] = t;
+            }
+        }
+    }
+}
+
+template <int L, int P>
+__device__ __forceinline__ void dif_from(cplx* z, const double* x, int k, const cplx* tw) {
+    using S = Shape<L>;
+    if constexpr (P < S::passes) {
+        dif<L, S::radix(P), S::sub(P), P == 0>(z, x, k, tw);
+        __syncthreads();
+        dif_from<L, P + 1>(z, x, k, tw);
+    }
+}
+
+template <int L, int P>
+__device__ __forceinline__ void dit_down(cplx* z, double* y, int l, double scale, const cplx* tw) {
+    using S = Shape<L>;
+    if constexpr (P >= 0) {
+        dit<L, S::radix(P), S::sub(P), P == 0>(z, y, l, scale, tw);
+        if constexpr (P > 0) {
+            __syncthreads();
+            dit_down<L, P - 1>(z, y, l, scale, tw);
+        }
+    }
+}
+
+// real spectrum X_k and X_{m-k} (k <= m/2) from the packed half-length
+// transform Z (digit-reversed in z): E = (Z_k + conj Z_{m-k})/2,
+// O = (Z_k - conj Z_{m-k})/(2i), X_k = E + w_n^k O, X_{m-k} = conj(E - w_n^k O);
+// k = 0 yields X_0 and X_m
+template <int L>
+__device__ __forceinline__ void unpack_pair(const cplx* z, int k, const cplx* __restrict__ tw, cplx& xk, cplx& xmk) {
+    constexpr int m = Shape<L>::m;
+    const cplx zk = z[swz(dif_pos<L>(k))];
+    const cplx zm = z[swz(dif_pos<L>((m - k) & (m - 1)))];
+    const cplx e = {0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y)};
+    const cplx o = {0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x)};
+    if (k == 0) {
+        xk = {e.x + o.x, e.y + o.y};
+        xmk = {e.x - o.x, e.y - o.y};
+        return;
+    }
+    const cplx wo = cmul(tw[k], o);
+    xk = cadd(e, wo);
+    const cplx d = csub(e, wo);
+    xmk = {d.x, -d.y};
+}
+
+// Z'_k = (Y_k + conj Y_{m-k}) + i (Y_k - conj Y_{m-k}) conj(w_n^k)
+__device__ __forceinline__ cplx repack(cplx yk, cplx partner, cplx wk) {
+    const cplx ee = cadd(yk, partner);
+    const cplx oo = cmulc(csub(yk, partner), wk);
+    return {ee.x - oo.y, ee.y + oo.x};
+}
+
+// spectrum S_k (k = 0..m, natural order) of c_T, c_T[i] = c[(n-i) mod n]
+template <int L>
+__global__ void __launch_bounds__(Shape<L>::T) spectrum_kernel(const double* __restrict__ c,
+                                                                const cplx* __restrict__ tw, cplx* __restrict__ spec) {
+    using S = Shape<L>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* z = reinterpret_cast<cplx*>(smem_raw);
+    constexpr int m = S::m, n = S::n;
+    for (int j = threadIdx.x; j < m; j += S::T) z[swz(j)] = {c[(n - 2 * j) % n], c[(n - 2 * j - 1) % n]};
+    __syncthreads();
+    // first pass from shared memory: reuse dif<> with kGlobal = false
+    dif<L, S::radix(0), S::sub(0), false>(z, nullptr, 0, tw);
+    __syncthreads();
+    dif_from<L, 1>(z, nullptr, 0, tw);
+    for (int k = threadIdx.x; k <= m / 2; k += S::T) {
+        cplx xk, xmk;
+        unpack_pair<L>(z, k, tw, xk, xmk);
+        spec[k] = xk;
+        spec[m - k] = xmk;
+    }
+}
+
+// one real row of A (k inputs) per CTA times the n-point real circulant,
+// first l outputs
+template <int L>
+__global__ void __launch_bounds__(Shape<L>::T, Shape<L>::minb)
+    rows_kernel(const double* __restrict__ a, int64_t lda, int k, const cplx* __restrict__ spec,
+                const cplx* __restrict__ tw, double* __restrict__ out, int64_t ldo, int l) {
+    using S = Shape<L>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* z = reinterpret_cast<cplx*>(smem_raw);
+    constexpr int m = S::m;
+    const int64_t row = blockIdx.x;
+    dif_from<L, 0>(z, a + row * lda, k, tw);
+#pragma unroll 1
+    for (int q = threadIdx.x; q <= m / 2; q += S::T) {
+        cplx xk, xmk;
+        unpack_pair<L>(z, q, tw, xk, xmk);
+        const cplx yk = cmul(spec[q], xk), ymk = cmul(spec[m - q], xmk);
+        const int pk = swz(dif_pos<L>(q)), pm = swz(dif_pos<L>((m - q) & (m - 1)));
+        if (q == 0) {
+            // Ee_0 = Y_0 + Y_m, Oo_0 = Y_0 - Y_m
+            z[pk] = {(yk.x + ymk.x) - (yk.y - ymk.y), (yk.y + ymk.y) + (yk.x - ymk.x)};
+        } else {
+            const cplx cym = {ymk.x, -ymk.y}, cyk = {yk.x, -yk.y};
+            const cplx zk = repack(yk, cym, tw[q]);
+            const cplx zm = repack(ymk, cyk, tw[m - q]);
+            z[pk] = zk;
+            z[pm] = zm;
+        }
+    }
+    __syncthreads();
+    dit_down<L, S::passes - 1>(z, out + row * ldo, l, 1.0 / static_cast<double>(S::n), tw);
+}
+
+template <int L>
+rl_status launch_L(rl_context* ctx, int64_t rows, int k, const double* a, int64_t lda, const double* c,
+                   const cplx* tw, cplx* spec, double* out, int64_t ldo, int l) {
+    using S = Shape<L>;
+    constexpr int smem = S::m * 16;
+    static bool configured = false;
+    if (!configured) {
+        RL_CUDA(cudaFuncSetAttribute(spectrum_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RL_CUDA(cudaFuncSetAttribute(rows_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = true;
+    }
+    spectrum_kernel<L><<<1, S::T, smem, ctx->stream>>>(c, tw, spec);
+    RL_CHECK_LAUNCH("r2c::spectrum_kernel");
+    rows_kernel<L><<<static_cast<unsigned>(rows), S::T, smem, ctx->stream>>>(a, lda, k, spec, tw, out, ldo, l);
+    RL_CHECK_LAUNCH("r2c::rows_kernel");
+    return RL_OK;
+}
+
+rl_status launch(rl_context* ctx, int L, int64_t rows, int k, const double* a, int64_t lda, const double* c,
+                 const cplx* tw, cplx* spec, double* out, int64_t ldo, int l) {
+    switch (L) {
+#define RL_R2C_CASE(LL) \
+    case LL: return launch_L<LL>(ctx, rows, k, a, lda, c, tw, spec, out, ldo, l);
+        RL_R2C_CASE(1) RL_R2C_CASE(2) RL_R2C_CASE(3) RL_R2C_CASE(4) RL_R2C_CASE(5) RL_R2C_CASE(6) RL_R2C_CASE(7)
+        RL_R2C_CASE(8) RL_R2C_CASE(9) RL_R2C_CASE(10) RL_R2C_CASE(11) RL_R2C_CASE(12) RL_R2C_CASE(13)
+#undef RL_R2C_CASE
+        default: return set_error(RL_ERR_UNSUPPORTED, "r2c: log2 half length %d", L);
+    }
+}
+
+}  // namespace r2c
+
 struct TwCache {
     std::mutex mu;
     std::map<std::pair<int, int64_t>, cplx*> tables;  // (device, n) -> table
@@ -449,7 +696,14 @@ rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a,
         RL_CUDA(cudaFuncSetAttribute(spectrum_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
         configured = true;
     }
-    if (n <= MAXN) {
+    const bool aligned = (lda % 2 == 0) && (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (aligned && n >= 4) {
+        int L = 0;
+        while ((2 << L) < n) ++L;
+        st = r2c::launch(ctx, L, m, static_cast<int>(k), a, lda, c, tw, spec, out, ldo, static_cast<int>(l));
+        if (st != RL_OK) return st;
+    } else if (n <= MAXN) {
         spectrum_kernel<<<1, FT, n * 16, ctx->stream>>>(c, n, tw, spec);
         RL_CHECK_LAUNCH("spectrum_kernel");
         circ_rows_kernel<<<static_cast<unsigned>((m + 1) / 2), FT, n * 16, ctx->stream>>>(
