@@ -150,6 +150,13 @@ RL_API uint64_t rl_hash_label(const char* label);
 RL_API rl_status rl_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out);
 /* `count` independent gen_gaussian(m, n, seeds[i]) into out[i*m*n ...] */
 RL_API rl_status rl_gen_gaussian_batch(int64_t count, int64_t m, int64_t n, const uint64_t* seeds, double* out);
+/* gen_gaussian(m, n, seed) generated on the device into `out` (device, leading
+ * dimension ld >= n), bit-identical to rl_gen_gaussian: the polar method runs on
+ * the GPU; the ~6% of log(s) evaluations too close to a rounding boundary to
+ * match glibc by construction are finished on the host with glibc. Synchronises
+ * the context stream. hard_cases (nullable) = attempts finished on the host. */
+RL_API rl_status rl_gen_gaussian_device(rl_context* ctx, int64_t m, int64_t n, uint64_t seed, double* out, int64_t ld,
+                                        int64_t* hard_cases);
 /* gen_real_circulant first column (multipliers.hpp:67-73) */
 RL_API rl_status rl_gen_real_circulant_column(int64_t n, uint64_t seed, double* out);
 

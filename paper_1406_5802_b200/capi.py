@@ -91,6 +91,7 @@ SIGNATURES = {
     "rl_hash_label": (u64, [ctypes.c_char_p]),
     "rl_gen_gaussian": (ctypes.c_int, [i64, i64, u64, _vp]),
     "rl_gen_gaussian_batch": (ctypes.c_int, [i64, i64, i64, _vp, _vp]),
+    "rl_gen_gaussian_device": (ctypes.c_int, [_vp, i64, i64, u64, _vp, i64, ctypes.POINTER(i64)]),
     "rl_gen_real_circulant_column": (ctypes.c_int, [i64, u64, _vp]),
     "rl_dgemm": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, i64, _vp, i64, _vp, i64, _vp, i64]),
     "rl_spectral_norm_estimate": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _dp]),

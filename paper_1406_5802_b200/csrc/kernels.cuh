@@ -65,6 +65,27 @@ rl_status circulant_dense(rl_context* ctx, const double* c, int64_t np, int64_t 
 // whether circulant_rows handles parent length np
 bool circulant_fft_ok(int64_t np);
 
+// gen_gaussian(rows, cols, seed) into device memory (ld), bit-identical to the
+// reference stream (rng_device.cu). begin() only enqueues work on ctx->stream;
+// finish() synchronises it and completes the host-decided attempts.
+struct GaussJob {
+    rl_context* ctx = nullptr;
+    int64_t rows = 0, cols = 0, ld = 0, count = 0, nb = 0, cap = 0;
+    uint64_t seed = 0;
+    double* out = nullptr;
+    char* base = nullptr;
+    int64_t *counts = nullptr, *offsets = nullptr, *pair = nullptr;
+    unsigned long long* hcount = nullptr;
+    uint64_t* attempts = nullptr;
+    double* vals = nullptr;
+    int64_t h_total = 0, h_hard = 0;  // host copies (pageable; valid after finish's sync)
+    rl_status begin(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld);
+    rl_status finish(int64_t* hard_cases);
+    ~GaussJob();
+};
+rl_status gen_gaussian_device(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld,
+                              int64_t* hard_cases);
+
 // batched 32x32 kernel (batched32.cu)
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,
                                 double* lu, double* x, double* r, double* growth, int32_t* status, int refine,

@@ -12,6 +12,9 @@
 // estimate evaluated, in the reference's exact summation order, on a
 // recomputed product (the GEMM is deterministic, so it is bit-identical).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -137,6 +140,11 @@ struct Dense {
     double *b = nullptr, *x = nullptr, *r = nullptr, *y = nullptr, *d = nullptr, *piv = nullptr, *rinv = nullptr;
     void* solve_work = nullptr;
     Scalars* sc = nullptr;
+    // host-mode pipelining: A arrives in a_chunks row blocks of a_chunk_rows,
+    // block c resident once a_ready[c] has fired (0 chunks: A fully resident)
+    int a_chunks = 0;
+    int64_t a_chunk_rows = 0;
+    cudaEvent_t* a_ready = nullptr;
 };
 
 // P = A G (or A), blocked GENP in place, growth, verdict (lu.hpp:44-49).
@@ -144,15 +152,29 @@ struct Dense {
 // exact-verdict path recomputes it bit for bit)
 rl_status form_product(rl_context* ctx, Dense& D, double* P, GemmStats* stats) {
     const int64_t n = D.n;
-    if (D.post == POST_DENSE) return gemm(ctx, n, n, n, D.A, D.ld, D.G, D.ld, P, D.ld, 1.0, false, stats);
-    if (D.post == POST_CIRC) {
-        // matmul_by_circulant (circulant.hpp:171-185), SideMultiplier::right_multiply (preprocess.hpp:65-73)
-        rl_status st = circulant_rows(ctx, n, n, D.A, D.ld, n, D.c, n, P, D.ld, D.spec);
+    // row blocks of A (all of A when it is already resident); every block's
+    // product rows are computed exactly as in one call (per-tile K order)
+    const int chunks = D.a_chunks > 0 ? D.a_chunks : 1;
+    const int64_t rows = D.a_chunks > 0 ? D.a_chunk_rows : n;
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t r0 = c * rows, rc = std::min(rows, n - r0);
+        if (rc <= 0) break;
+        if (D.a_chunks > 0) RL_CUDA(cudaStreamWaitEvent(ctx->stream, D.a_ready[c], 0));
+        const double* Ac = D.A + r0 * D.ld;
+        double* Pc = P + r0 * D.ld;
+        rl_status st = RL_OK;
+        if (D.post == POST_DENSE) {
+            st = gemm(ctx, rc, n, n, Ac, D.ld, D.G, D.ld, Pc, D.ld, 1.0, false, stats);
+        } else if (D.post == POST_CIRC) {
+            // matmul_by_circulant (circulant.hpp:171-185), SideMultiplier::right_multiply (preprocess.hpp:65-73)
+            st = circulant_rows(ctx, rc, n, Ac, D.ld, n, D.c, n, Pc, D.ld, D.spec);
+        } else if (Pc != Ac) {
+            RL_CUDA(cudaMemcpy2DAsync(Pc, D.ld * 8, Ac, D.ld * 8, n * 8, rc, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
         if (st != RL_OK) return st;
-    } else {
-        RL_CUDA(cudaMemcpy2DAsync(P, D.ld * 8, D.A, D.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    if (stats) {
+    D.a_chunks = 0;  // resident from here on (the exact-verdict recompute reuses A)
+    if (stats && D.post != POST_DENSE) {
         matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, ctx->stream>>>(P, D.ld, n, false, stats);
         RL_CHECK_LAUNCH("matrix_stats_kernel");
     }
@@ -348,12 +370,50 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     st = dense_alloc(ctx, D, n, dense && !g_dev_direct, own_a, true);
     if (st != RL_OK) return st;
     cudaStream_t s = ctx->stream;
+    static const bool dbg = std::getenv("RANDLA_DEBUG_GEN") != nullptr;
+    auto now = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t_start = dbg ? now() : 0.0;
+    // seeded dense multiplier: generated on the device (exact); its kernels are
+    // enqueued first so that they run under the upload of A
+    GaussJob gjob;
+    const bool gen_g = kind == RL_MULT_GAUSSIAN && !post->dense;
+    if (gen_g && (st = gjob.begin(ctx, n, n, post->seed, D.G, ld)) != RL_OK) return st;
+    const double t_begun = dbg ? now() : 0.0;
+    int a_issued = 0;
+    auto upload_a_block = [&](int c) -> rl_status {
+        const int64_t r0 = c * D.a_chunk_rows, rc = std::min(D.a_chunk_rows, n - r0);
+        if (rc > 0)
+            RL_CUDA(cudaMemcpy2DAsync(D.A + r0 * ld, ld * 8, a + r0 * n, n * 8, n * 8, rc, cudaMemcpyHostToDevice,
+                                      ctx->hi_stream));
+        RL_CUDA(cudaEventRecord(ctx->events[c], ctx->hi_stream));
+        return RL_OK;
+    };
     if (own_a) {
-        if ((st = copy_in(ctx, D.A, ld, a, n, n, host)) != RL_OK) return st;
+        // host A: uploaded in row blocks on the side stream; the product of
+        // block c starts as soon as block c has landed
+        constexpr int kChunks = 4;
+        if (host && n >= 1024 && side_resources(ctx, kChunks) == RL_OK) {
+            cudaEvent_t start = ctx->events[kChunks - 1];
+            RL_CUDA(cudaEventRecord(start, s));  // workspace reuse: after this stream's earlier work
+            RL_CUDA(cudaStreamWaitEvent(ctx->hi_stream, start, 0));
+            D.a_chunks = kChunks;
+            D.a_chunk_rows = (n + kChunks - 1) / kChunks;
+            D.a_ready = ctx->events;
+            // block 0 now; when the generator still has host-decided values to
+            // upload, the other blocks are enqueued after them (same copy
+            // engine: those few MB must not queue behind 3/4 of A)
+            a_issued = gen_g ? 1 : kChunks;
+            for (int c = 0; c < a_issued; ++c)
+                if ((st = upload_a_block(c)) != RL_OK) return st;
+        } else if ((st = copy_in(ctx, D.A, ld, a, n, n, host)) != RL_OK) {
+            return st;
+        }
     } else {
         D.A = const_cast<double*>(a);
     }
-    std::vector<double> hg;
+    const double t_aq = dbg ? now() : 0.0;
     struct Col {
         double* p = nullptr;
         cudaStream_t s;
@@ -389,14 +449,16 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
             D.G = const_cast<double*>(post->dense);
         } else if (post->dense) {
             if ((st = copy_in(ctx, D.G, ld, post->dense, n, n, host)) != RL_OK) return st;
-        } else {
-            // materialize(spec) = gen_gaussian(n, n, seed) (multipliers.hpp:191-192), exact, host
-            hg.resize(static_cast<size_t>(n * n));
-            rl_gen_gaussian(n, n, post->seed, hg.data());
-            if ((st = copy_in(ctx, D.G, ld, hg.data(), n, n, true)) != RL_OK) return st;
+        } else if ((st = gjob.finish(nullptr)) != RL_OK) {
+            // materialize(spec) = gen_gaussian(n, n, seed) (multipliers.hpp:191-192)
+            return st;
         }
     }
+    // b before the remaining blocks of A (the stream s work must not queue behind them)
     RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    for (; a_issued > 0 && a_issued < D.a_chunks; ++a_issued)
+        if ((st = upload_a_block(a_issued)) != RL_OK) return st;
+    const double t_gen = dbg ? now() : 0.0;
     StageTimer timer(s);
     st = factor_and_verdict(ctx, D, info, &timer);
     if (st != RL_OK) {
@@ -408,6 +470,7 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     if (st != RL_OK) return st;
     timer.mark();
     timer.fill(info->stage_ms);
+    const double t_solved = dbg ? now() : 0.0;
     RL_CUDA(cudaMemcpyAsync(x, D.x, n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
     if (lu_out && (st = copy_out(ctx, lu_out, D.P, ld, n, n, host)) != RL_OK) return st;
     if (want_norm_a) {
@@ -423,6 +486,9 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         info->residual_rel_a = std::sqrt(sq[0]) / (na * std::sqrt(sq[1]));
     }
     RL_CUDA(cudaStreamSynchronize(s));
+    if (dbg)
+        std::fprintf(stderr, "[solve] begin %.2f, A enqueue %.2f, gen finish %.2f ms, stages %.2f ms (wall %.2f), tail %.2f ms\n",
+                     t_begun - t_start, t_aq - t_begun, t_gen - t_aq, info->stage_ms[3], t_solved - t_gen, now() - t_solved);
     return RL_OK;
 }
 

@@ -142,6 +142,27 @@ void gaussian_parallel(uint64_t seed, int64_t count, double* out) {
 
 }  // namespace
 
+namespace rl {
+uint64_t host_stream_state(uint64_t seed) { return stream_state(seed); }
+
+// finish listed polar attempts with glibc's log (rng_device.cu hard cases):
+// out2[2i], out2[2i+1] = u f, v f of attempt attempts[i]
+void host_polar_pairs(uint64_t seed, const uint64_t* attempts, int64_t count, double* out2) {
+    const uint64_t s0 = stream_state(seed);
+    constexpr int64_t kGroup = 4096;
+    parallel_for((count + kGroup - 1) / kGroup, [&](int64_t g) {
+        const int64_t hi = std::min(count, (g + 1) * kGroup);
+        for (int64_t i = g * kGroup; i < hi; ++i) {
+            double u, v, s;
+            attempt(s0, attempts[i], u, v, s);
+            const double f = std::sqrt(-2.0 * std::log(s) / s);
+            out2[2 * i] = u * f;
+            out2[2 * i + 1] = v * f;
+        }
+    });
+}
+}  // namespace rl
+
 extern "C" {
 
 RL_API void rl_set_host_threads(int threads) { g_threads = threads; }

@@ -43,6 +43,14 @@ static rl_status init_context(rl_context* c, int device) {
     c->flags_bytes = 4096;
     RL_CUDA(cudaMalloc(&c->flags, c->flags_bytes));
     RL_CUDA(cudaMemset(c->flags, 0, c->flags_bytes));
+    RL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->host_scalars), 4096, cudaHostAllocDefault));
+    // call-scoped scratch comes from cudaMallocAsync: keep the pool's memory
+    // mapped between calls instead of returning it at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     return RL_OK;
 }
 
@@ -52,6 +60,8 @@ static void destroy_context(rl_context* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->ws) cudaFree(c->ws);
     if (c->flags) cudaFree(c->flags);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->host_scalars) cudaFreeHost(c->host_scalars);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->hi_stream) cudaStreamDestroy(c->hi_stream);
     for (int i = 0; i < c->num_events; ++i) cudaEventDestroy(c->events[i]);
@@ -120,6 +130,22 @@ rl_status side_resources(rl_context* ctx, int count) {
         ctx->num_events = count;
     }
     return RL_OK;
+}
+
+void* pinned_staging(rl_context* ctx, size_t bytes) {
+    if (bytes <= ctx->pinned_bytes) return ctx->pinned;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    const size_t want = align_up(bytes, size_t(1) << 20);
+    if (cudaHostAlloc(&ctx->pinned, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->pinned = nullptr;
+        return nullptr;
+    }
+    ctx->pinned_bytes = want;
+    return ctx->pinned;
 }
 
 void* workspace(rl_context* ctx, size_t bytes) {
