@@ -31,7 +31,8 @@ def _headers_mtime():
 
 def _compile(src, obj):
     if src.endswith(".cu"):
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        # RANDLA_NVCC_EXTRA: developer switches (e.g. -DRL_PHASES), never set in the product build
+        cmd = [NVCC] + NVCC_FLAGS + os.environ.get("RANDLA_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj]
     else:
         cmd = ["g++"] + CXX_FLAGS + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

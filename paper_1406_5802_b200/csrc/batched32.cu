@@ -1,27 +1,31 @@
 // Batched small GENP — BASELINE config 2: many independent 32x32 systems,
 // each preprocess_solve(A_i, b_i, none, {Gaussian, G_i}, refine)
-// (preprocess.hpp:156-180) on one warp, register-resident.
+// (preprocess.hpp:156-180) on one warp.
 //
-// Per system (one warp):
-//   1. A_i, G_i -> shared memory (coalesced 16-byte streaming loads).
-//   2. P = A_i G_i with FP64 tensor-core MMA (mma.sync m8n8k4, 128 DMMA).
-//   3. P row-per-lane in registers; exact-order row/column norms
-//      (norms.hpp:38-50 floor) and ||P||_F bound the pivot tolerance.
-//   4. GENP (lu.hpp:47-56): 31 unrolled elimination steps; the pivot row is
-//      broadcast through a 256-byte shared row buffer, every lane divides its
-//      own multiplier. All pivots are seen by every lane (warp-uniform).
-//   5. Verdict: tol = tol_pivot(32) * spectral_norm_estimate(P) (lu.hpp:44).
+// Per system (one warp, 9,984 B of shared memory, 128 registers: 16 resident
+// warps per SM; the next system's A and G are prefetched into L2):
+//   1. G_i -> the warp's P region (cp.async, swizzled); A_i row blocks as MMA
+//      A-fragments straight from global.
+//   2. P = A_i G_i on the FP64 tensor path (128 DMMA m8n8k4), held in
+//      registers until every DMMA has read G, then written over it; ||P||_F
+//      and max|P| fold over the registers.
+//   3. Blocked GENP (lu.hpp:47-56): 8-column panels eliminated row-per-lane
+//      with the pivot row broadcast through shared memory, U12 by forward
+//      substitution, trailing Schur update on DMMA. Pivots are warp-uniform.
+//   4. Verdict: tol = tol_pivot(32) * spectral_norm_estimate(P) (lu.hpp:44).
 //      floor <= estimate <= ||P||_F, so the power iteration runs only when a
 //      pivot lies in the band (tol_pivot*floor, tol_pivot*||P||_F]; it then
-//      runs in the reference's exact summation order (no FMA), so the verdict
-//      is the reference's.
-//   6. Solves (lu.hpp:110-122) with shuffle broadcasts, x = G y, residual
-//      ||b - A x|| / ||b|| (lu.hpp:155-161 / preprocess.hpp:122-128),
-//      growth max|U| / max|P|, packed LU written back coalesced.
+//      runs in the reference's exact summation order (no FMA) in
+//      verdict_fixup_kernel, so the verdict is the reference's.
+//   5. Solves (lu.hpp:110-122) with shuffle broadcasts; x = G y and the
+//      residual ||b - A x|| / ||b|| (lu.hpp:155-161 / preprocess.hpp:122-128)
+//      on DMMA with G and A re-read from L2; growth max|U| / max|P|; packed
+//      LU written back coalesced.
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 
 #include "device_common.cuh"
 #include "runtime.cuh"
@@ -33,17 +37,6 @@ constexpr int D = 32;
 constexpr int WARPS = 4;
 constexpr int LDP = 34;  // P / LU row stride (doubles): 16 B rows, <= 2-way conflicts on rows and columns
 constexpr double kTolPivot32 = 1e-13 * 32.0;  // tol_pivot(32), types.hpp:42
-
-// Per-warp shared memory: 18,176 B -> 12 resident warps per SM (3 CTAs x 4).
-struct __align__(16) WarpSmem {
-    double G[D * D];   // multiplier, swizzled (swz_g)
-    double P[D * LDP]; // product A G, then its packed LU in place
-    double vec[2][D];  // double-buffered broadcast rows / vectors
-    double b[D];
-    double rinv[D];    // 1 / u_jj
-    double piv[D];     // u_jj
-};
-constexpr size_t kSmemBytes = sizeof(WarpSmem) * WARPS;
 
 // G element (k, n): XOR-swizzled columns so the DMMA B-fragment loads (4 rows
 // 2q+e x 8 columns) hit distinct banks.
@@ -153,7 +146,73 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
     }
 }
 
-__global__ void __launch_bounds__(WARPS * 32, 3)
+// Main-kernel shared memory: only P (then its LU) and a few vectors per warp
+// (9,984 B): 5 CTAs x 4 warps = 20 resident warps per SM. G never touches
+// shared memory: its B fragments go from global straight into registers, and
+// the two late passes that need A and G again (x = G y, r = b - A x) re-read
+// them from L2 with evict-first loads.
+struct __align__(16) MainSmem {
+    double P[D * LDP];  // product A G, then its packed LU in place
+    double vec[2][D];   // double-buffered broadcast rows / vectors
+    double b[D];
+    double rinv[D];     // 1 / u_jj
+    double piv[D];      // u_jj
+};
+constexpr size_t kMainSmemBytes = sizeof(MainSmem) * WARPS;
+constexpr int kMainCtasPerSm = 4;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// A (or G) row block ti as MMA A-fragments: f[kk] = M[8 ti + l/4][kidx(kk, l%4)]
+template <bool kStream>
+__device__ __forceinline__ void load_rowblock_frags(const double* gM, int ti, int lane, double (&f)[8]) {
+    const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const double2* p = reinterpret_cast<const double2*>(gM + (8 * ti + fr) * D + 8 * m + 2 * fc);
+        const double2 v = kStream ? __ldcs(p) : __ldcg(p);
+        f[2 * m] = v.x;
+        f[2 * m + 1] = v.y;
+    }
+}
+
+// C = M v for a 32 x 32 row-major M in global memory (A-fragment loads, DMMA
+// with v in the first B column); returns C[8 ti + fr] in lanes fc == 0 via cb
+__device__ __forceinline__ void matvec_dmma(const double* gM, const double* sv, int lane, double (&cb)[4]) {
+    const int fc = lane & 3;
+    double bv[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) bv[kk] = lane < 4 ? sv[kidx(kk, fc)] : 0.0;
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti) {
+        double f[8];
+        load_rowblock_frags<true>(gM, ti, lane, f);
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma(c0, c1, f[kk], bv[kk]);
+        cb[ti] = c0;
+    }
+}
+
+#ifdef RL_PHASES
+__device__ unsigned long long g_phase[8];
+#define PH(i)                                \
+    do {                                     \
+        __syncwarp();                        \
+        const long long t_ = clock64();      \
+        acc[i] += t_ - t_prev;               \
+        t_prev = t_;                         \
+    } while (0)
+#else
+#define PH(i) \
+    do {      \
+    } while (0)
+#endif
+__global__ void __launch_bounds__(WARPS * 32, kMainCtasPerSm)
 batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ gG, const double* __restrict__ gB,
                       double* __restrict__ gLU, double* __restrict__ gX, double* __restrict__ gR,
                       double* __restrict__ gGrowth, int32_t* __restrict__ gStatus, int64_t batch, int refine,
@@ -161,25 +220,72 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fr = lane >> 2, fc = lane & 3;
-    WarpSmem& s = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
-
+    MainSmem& s = reinterpret_cast<MainSmem*>(smem_raw)[warp];
+#ifdef RL_PHASES
+    long long t_prev = clock64();
+    long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    const int64_t sys_stride = static_cast<int64_t>(gridDim.x) * WARPS;
     for (int64_t sys = static_cast<int64_t>(blockIdx.x) * WARPS + warp; sys < batch;
          sys += static_cast<int64_t>(gridDim.x) * WARPS) {
         const size_t mo = static_cast<size_t>(sys) * D * D;
-        load_g_async(s.G, gG + mo, lane);
-        double a[4][8];
-        load_a_frags(gA + mo, lane, a);
+        const double* A = gA + mo;
+        const double* G = gG + mo;
+        // G staged (swizzled) in the P region: the product is held in registers
+        // until the last DMMA has read G, then written over it
+        load_g_async(s.P, G, lane);
+        double af[8];
+        load_rowblock_frags<false>(A, 0, lane, af);
         const double bl = __ldcs(gB + sys * D + lane);
         s.b[lane] = bl;
+        // the next system's A and G (8 KiB each, contiguous) into L2 while this one runs
+        if (lane < 2 && sys + sys_stride < batch) {
+            const double* nxt = (lane == 0 ? gA : gG) + static_cast<size_t>(sys + sys_stride) * D * D;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 8192;\n" ::"l"(nxt));
+        }
         cp_async_wait_all();
         __syncwarp();
+        PH(0);
 
-        // ---- P = A G (DMMA), ||P||_F bounds spectral_norm_estimate (norms.hpp:77)
-        double sumsq, amax;
-        product_to_smem(a, s.G, s.P, lane, sumsq, amax);
+        // ---- P = A G (DMMA, same per-tile k order as product_to_smem), ||P||_F
+        // bounds spectral_norm_estimate (norms.hpp:77)
+        double c[4][4][2];
+#pragma unroll
+        for (int ti = 0; ti < 4; ++ti) {
+            double an[8];
+            if (ti < 3) load_rowblock_frags<false>(A, ti + 1, lane, an);
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) c[ti][tj][0] = c[ti][tj][1] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                double bf[4];
+#pragma unroll
+                for (int tj = 0; tj < 4; ++tj) bf[tj] = s.P[swz_g(kidx(kk, fc), 8 * tj + fr)];
+#pragma unroll
+                for (int tj = 0; tj < 4; ++tj) dmma(c[ti][tj][0], c[ti][tj][1], af[kk], bf[tj]);
+            }
+            if (ti < 3) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) af[kk] = an[kk];
+            }
+        }
+        __syncwarp();  // every lane's DMMAs have consumed G
+        double sumsq = 0.0, amax = 0.0;
+#pragma unroll
+        for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) {
+                *reinterpret_cast<double2*>(&s.P[(8 * ti + fr) * LDP + 8 * tj + 2 * fc]) =
+                    make_double2(c[ti][tj][0], c[ti][tj][1]);
+                sumsq = fma(c[ti][tj][0], c[ti][tj][0], sumsq);
+                sumsq = fma(c[ti][tj][1], c[ti][tj][1], sumsq);
+                amax = max_abs(max_abs(amax, c[ti][tj][0]), c[ti][tj][1]);
+            }
+        PH(1);
         const double tol_hi = kTolPivot32 * sqrt(warp_sum(sumsq)) * (1.0 + 1e-10);
         const double max_p = warp_max(amax);
         __syncwarp();
+        PH(2);
 
         // ---- blocked GENP on P (lu.hpp:47-56 reorganised: 8-column panels
         // eliminated in natural order, U12 by forward substitution, trailing
@@ -252,16 +358,16 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                 const int nt = R / 8;
 #pragma unroll
                 for (int ti = 0; ti < nt; ++ti) {
-                    double af[2];
+                    double lf[2];
 #pragma unroll
-                    for (int ks = 0; ks < 2; ++ks) af[ks] = -s.P[(J + 8 + 8 * ti + fr) * LDP + J + 4 * ks + fc];
+                    for (int ks = 0; ks < 2; ++ks) lf[ks] = -s.P[(J + 8 + 8 * ti + fr) * LDP + J + 4 * ks + fc];
 #pragma unroll
                     for (int tj = 0; tj < nt; ++tj) {
                         double2* cp = reinterpret_cast<double2*>(&s.P[(J + 8 + 8 * ti + fr) * LDP + J + 8 + 8 * tj + 2 * fc]);
                         double2 cv = *cp;
 #pragma unroll
                         for (int ks = 0; ks < 2; ++ks)
-                            dmma_884(cv.x, cv.y, af[ks], s.P[(J + 4 * ks + fc) * LDP + J + 8 + 8 * tj + fr]);
+                            dmma(cv.x, cv.y, lf[ks], s.P[(J + 4 * ks + fc) * LDP + J + 8 + 8 * tj + fr]);
                         *cp = cv;
                     }
                 }
@@ -269,6 +375,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             }
         }
 
+        PH(3);
         // ---- growth numerator max|U|: lane i scans the U part of row i
         double umax = 0.0;
 #pragma unroll
@@ -287,6 +394,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             fix_piv[static_cast<size_t>(idx) * D + lane] = s.piv[lane];
         }
 
+        PH(4);
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
         const double my_rinv = s.rinv[lane], my_piv = s.piv[lane];
@@ -305,29 +413,26 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             }
             s.vec[0][lane] = y;
             __syncwarp();
-            double d = 0.0;  // d = G y (matvec, matrix.hpp:146-156)
+            // d = G y (matvec, matrix.hpp:146-156), G re-read from L2
+            double cb[4];
+            matvec_dmma(G, s.vec[0], lane, cb);
+            __syncwarp();
+            if (fc == 0) {
 #pragma unroll
-            for (int m = 0; m < D / 2; ++m) {
-                const double2 gv = *reinterpret_cast<const double2*>(&s.G[swz_g(lane, 2 * m)]);
-                const double2 yv = *reinterpret_cast<const double2*>(&s.vec[0][2 * m]);
-                d = fma(gv.x, yv.x, d);
-                d = fma(gv.y, yv.y, d);
+                for (int ti = 0; ti < 4; ++ti) s.vec[1][8 * ti + fr] = cb[ti];
             }
-            x += d;
+            __syncwarp();
+            x += s.vec[1][lane];
+            __syncwarp();
             s.vec[1][lane] = x;
             __syncwarp();
-            // residual b - A x (preprocess.hpp:122-126) with A in MMA fragments
+            // residual b - A x (preprocess.hpp:122-126), A re-read from L2
+            matvec_dmma(A, s.vec[1], lane, cb);
             double rsq = 0.0;
+            if (fc == 0) {
 #pragma unroll
-            for (int ti = 0; ti < 4; ++ti) {
-                double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const double xv = s.vec[1][kidx(kk, fc)];
-                    dmma_884(c0, c1, a[ti][kk], lane < 4 ? xv : 0.0);
-                }
-                if (fc == 0) {
-                    const double r = s.b[8 * ti + fr] - c0;
+                for (int ti = 0; ti < 4; ++ti) {
+                    const double r = s.b[8 * ti + fr] - cb[ti];
                     rsq = fma(r, r, rsq);
                     s.vec[0][8 * ti + fr] = r;
                 }
@@ -338,6 +443,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             __syncwarp();
         }
 
+        PH(5);
         // ---- outputs
         if (gLU) {
             double2* dst = reinterpret_cast<double2*>(gLU + mo);
@@ -355,7 +461,12 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             if (gStatus) gStatus[sys] = 0;
         }
         __syncwarp();
+        PH(6);
     }
+#ifdef RL_PHASES
+    if (lane == 0)
+        for (int i = 0; i < 7; ++i) atomicAdd(&g_phase[i], static_cast<unsigned long long>(acc[i]));
+#endif
 }
 
 // ---- verdict fix-up (rare path): exact spectral_norm_estimate of P = A G
@@ -510,7 +621,7 @@ rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a,
     static bool configured = false;
     if (!configured) {
         RL_CUDA(cudaFuncSetAttribute(batched_genp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kSmemBytes)));
+                                     static_cast<int>(kMainSmemBytes)));
         RL_CUDA(cudaFuncSetAttribute(verdict_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sizeof(FixSmem) * WARPS)));
         configured = true;
@@ -520,10 +631,21 @@ rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a,
     double* fix_piv = reinterpret_cast<double*>(static_cast<char*>(fix_ws) + align_up(16 + 8 * batch));
     RL_CUDA(cudaMemsetAsync(&fix->count, 0, sizeof(int32_t), ctx->stream));
     const int64_t ctas_needed = (batch + WARPS - 1) / WARPS;
-    const int64_t grid = std::min<int64_t>(ctas_needed, static_cast<int64_t>(ctx->num_sms) * 3);
-    batched_genp32_kernel<<<static_cast<unsigned>(grid), WARPS * 32, kSmemBytes, ctx->stream>>>(
+    const int64_t grid = std::min<int64_t>(ctas_needed, static_cast<int64_t>(ctx->num_sms) * kMainCtasPerSm);
+    batched_genp32_kernel<<<static_cast<unsigned>(grid), WARPS * 32, kMainSmemBytes, ctx->stream>>>(
         a, g, b, lu, x, r, growth, status, batch, refine, fix, fix_piv);
     RL_CHECK_LAUNCH("batched_genp32_kernel");
+#ifdef RL_PHASES
+    {
+        unsigned long long h[8];
+        cudaMemcpyFromSymbol(h, g_phase, sizeof(h));
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+        const double sy = static_cast<double>(batch);
+        std::fprintf(stderr, "[phases cycles/system] load %.0f product %.0f stats %.0f lu %.0f verdict %.0f solve %.0f out %.0f\n",
+                     h[0] / sy, h[1] / sy, h[2] / sy, h[3] / sy, h[4] / sy, h[5] / sy, h[6] / sy);
+    }
+#endif
     verdict_fixup_kernel<<<static_cast<unsigned>(ctx->num_sms), WARPS * 32, sizeof(FixSmem) * WARPS, ctx->stream>>>(
         a, g, x, r, growth, status, fix, fix_piv);
     RL_CHECK_LAUNCH("verdict_fixup_kernel");
