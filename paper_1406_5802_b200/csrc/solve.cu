@@ -36,12 +36,19 @@ __device__ __forceinline__ void wait_flag(const int* flag) {
 }
 
 // kUpper = false: y = L^-1 b (unit lower); true: x = U^-1 y (upper, diagonal)
+// Block B (64 rows, claimed in dependency order through the ticket) keeps the
+// next dependency tile of L/U in registers while it waits for the current
+// one's flag, so the HBM read of the tile is off the critical path; the
+// diagonal block, its reciprocal pivots and the finished x blocks go through
+// shared memory.
 template <bool kUpper>
 __global__ void __launch_bounds__(256)
 trsv_kernel(const double* __restrict__ lu, int64_t ld, int64_t n, const double* __restrict__ rinv,
             const double* rhs, double* out, int* __restrict__ flags, int* __restrict__ ticket) {
     __shared__ int s_blk;
     __shared__ double sdiag[TB][TB + 1];
+    __shared__ double sri[TB];
+    __shared__ double sx[TB];
     __shared__ double sacc[TB];
     const int tid = threadIdx.x;
     const int64_t nblk = (n + TB - 1) / TB;
@@ -53,19 +60,33 @@ trsv_kernel(const double* __restrict__ lu, int64_t ld, int64_t n, const double* 
     const int64_t r0 = B * TB;
     const int nr = static_cast<int>(min(static_cast<int64_t>(TB), n - r0));
 
-    // diagonal block into smem while the dependencies finish
+    // diagonal block (identity-padded past nr) and 1/u_jj while the dependencies finish
     for (int idx = tid; idx < TB * TB; idx += 256) {
         const int i = idx / TB, k = idx % TB;
-        sdiag[i][k] = (i < nr && k < nr) ? lu[(r0 + i) * ld + r0 + k] : 0.0;
+        sdiag[i][k] = (i < nr && k < nr) ? lu[(r0 + i) * ld + r0 + k] : (i == k ? 1.0 : 0.0);
     }
-    // off-diagonal contributions: rows r0.., blocks C (C < B lower / C > B upper)
+    if (kUpper && tid < TB) sri[tid] = tid < nr ? (rinv ? __ldcg(rinv + r0 + tid) : 1.0 / lu[(r0 + tid) * ld + r0 + tid]) : 1.0;
+    // off-diagonal contributions: thread (row, q) takes columns q, q+4, ... of each tile
     const int row = tid >> 2, q = tid & 3;
+    const bool live = row < nr;
     double acc = 0.0;
-    // visit the finished blocks in the order they are produced: ascending for
-    // the forward sweep, descending for the backward one
     const int64_t ndep = kUpper ? nblk - 1 - B : B;
+    double cur[TB / 4], nxt[TB / 4];
+    auto load_tile = [&](int64_t t, double (&v)[TB / 4]) {
+        const int64_t C = kUpper ? nblk - 1 - t : t;
+        const int64_t c0 = C * TB;
+        const int nc = static_cast<int>(min(static_cast<int64_t>(TB), n - c0));
+        const double* lrow = lu + (r0 + row) * ld + c0;
+#pragma unroll
+        for (int j = 0; j < TB / 4; ++j) {
+            const int k = q + 4 * j;
+            v[j] = (live && k < nc) ? __ldcs(lrow + k) : 0.0;
+        }
+    };
+    if (ndep > 0) load_tile(0, cur);
     for (int64_t t = 0; t < ndep; ++t) {
         const int64_t C = kUpper ? nblk - 1 - t : t;
+        if (t + 1 < ndep) load_tile(t + 1, nxt);
         if (tid == 0) {
             wait_flag(&flags[C]);
             __threadfence();
@@ -73,32 +94,36 @@ trsv_kernel(const double* __restrict__ lu, int64_t ld, int64_t n, const double* 
         __syncthreads();
         const int64_t c0 = C * TB;
         const int nc = static_cast<int>(min(static_cast<int64_t>(TB), n - c0));
-        if (row < nr) {
-            const double* lrow = lu + (r0 + row) * ld + c0;
-#pragma unroll 4
-            for (int k = q; k < nc; k += 4) acc = fma(lrow[k], __ldcg(out + c0 + k), acc);
-        }
+        if (tid < TB) sx[tid] = tid < nc ? __ldcg(out + c0 + tid) : 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < TB / 4; ++j) acc = fma(cur[j], sx[q + 4 * j], acc);
+        __syncthreads();  // sx is rewritten by the next dependency
+#pragma unroll
+        for (int j = 0; j < TB / 4; ++j) cur[j] = nxt[j];
     }
     acc += __shfl_xor_sync(kFull, acc, 1);
     acc += __shfl_xor_sync(kFull, acc, 2);
-    if (q == 0 && row < nr) sacc[row] = __ldcg(rhs + r0 + row) - acc;
+    if (q == 0) sacc[row] = live ? __ldcg(rhs + r0 + row) - acc : 0.0;
     __syncthreads();
 
-    // diagonal block: column sweep on warp 0, two rows per lane
+    // diagonal block: column sweep on warp 0, two rows per lane, fully unrolled
     if (tid < 32) {
         const int lane = tid;
-        double v0 = lane < nr ? sacc[lane] : 0.0;
-        double v1 = lane + 32 < nr ? sacc[lane + 32] : 0.0;
+        double v0 = sacc[lane];
+        double v1 = sacc[lane + 32];
         if (!kUpper) {
-            for (int k = 0; k < nr; ++k) {
+#pragma unroll
+            for (int k = 0; k < TB; ++k) {
                 const double yk = __shfl_sync(kFull, k < 32 ? v0 : v1, k & 31);
                 if (lane > k) v0 = fma(-sdiag[lane][k], yk, v0);
                 if (lane + 32 > k) v1 = fma(-sdiag[lane + 32][k], yk, v1);
             }
         } else {
-            for (int k = nr - 1; k >= 0; --k) {
+#pragma unroll
+            for (int k = TB - 1; k >= 0; --k) {
                 const double d = sdiag[k][k];
-                const double ri = rinv ? __ldcg(rinv + r0 + k) : 1.0 / d;
+                const double ri = sri[k];
                 if (lane == k) v0 = div_by(v0, d, ri);
                 if (lane + 32 == k) v1 = div_by(v1, d, ri);
                 const double xk = __shfl_sync(kFull, k < 32 ? v0 : v1, k & 31);
