@@ -395,11 +395,113 @@ rl_status rec(const Ctx& g, int64_t c0, int64_t w) {
 
 }  // namespace
 
+// Right-looking GENP in 128-column super-panels, each factored as two
+// 64-column sub-panels, so that the bulk trailing update is one K = 128 GEMM
+// per super-panel (half the C read/write traffic per flop of K = 64), with a
+// one-super-panel lookahead on two streams:
+//   hi: GEMM_a(s) (the next super-panel's 128 columns) -> factor_super(s+1)
+//   lo: U12(s) for the trailing columns -> GEMM_b(s) (all later columns)
+// factor_super(c0): panel_L(c0); U12 of the first half onto the second half's
+// 64 columns; their K = 64 update; panel_L(c0 + 64).
+// U12(s) = L11^-1 A12 with the 128x128 unit-lower L11 in two 64-row steps:
+// top = La^-1 A12_top; A12_bot -= L_ba top (K = 64 GEMM); bot = Lb^-1 A12_bot.
+static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out,
+                               double* rinv_out) {
+    constexpr int64_t W = 2 * kBase;
+    const int64_t S = n / W;  // full super-panels
+    Ctx g{ctx, a, n, lda, piv_out, rinv_out};
+    rl_status st;
+    constexpr int kRing = 8;
+    if ((st = side_resources(ctx, kRing + 2)) != RL_OK) return st;
+    cudaStream_t lo = ctx->stream, hi = ctx->hi_stream;
+    cudaEvent_t* ev = ctx->events;
+    int e = 0;
+    auto next_event = [&]() { return ev[2 + (e++ % kRing)]; };
+    auto at = [&](int64_t r, int64_t c) { return a + r * lda + c; };
+    // GEMM C -= A B on stream sm (ctx->stream is what gemm() launches on)
+    auto update = [&](cudaStream_t sm, int64_t M, int64_t N, int64_t Kd, const double* A, const double* B,
+                      double* C) -> rl_status {
+        if (M <= 0 || N <= 0) return RL_OK;
+        cudaStream_t keep = ctx->stream;
+        ctx->stream = sm;
+        const rl_status r = gemm(ctx, M, N, Kd, A, lda, B, lda, C, lda, -1.0, true, nullptr);
+        ctx->stream = keep;
+        return r;
+    };
+    auto panel_l = [&](cudaStream_t sm, int64_t c0) -> rl_status {
+        const int64_t rest = n - c0 - kBase;
+        const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
+        lu_panel64_kernel<<<blocks, PT, 0, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
+        RL_CHECK_LAUNCH("lu_panel64_kernel");
+        return RL_OK;
+    };
+    auto u12 = [&](cudaStream_t sm, int64_t r0, int64_t cb, int64_t ncols) -> rl_status {
+        if (ncols <= 0) return RL_OK;
+        lu_u12_kernel<<<static_cast<unsigned>((ncols + PT - 1) / PT), PT, 0, sm>>>(a, lda, r0, cb, ncols);
+        RL_CHECK_LAUNCH("lu_u12_kernel");
+        return RL_OK;
+    };
+    auto factor_super = [&](cudaStream_t sm, int64_t c0) -> rl_status {
+        rl_status r;
+        if ((r = panel_l(sm, c0)) != RL_OK) return r;
+        if ((r = u12(sm, c0, c0 + kBase, kBase)) != RL_OK) return r;
+        if ((r = update(sm, n - c0 - kBase, kBase, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase),
+                        at(c0 + kBase, c0 + kBase))) != RL_OK)
+            return r;
+        return panel_l(sm, c0 + kBase);
+    };
+    RL_CUDA(cudaEventRecord(ev[0], lo));  // prior work on the caller's stream
+    RL_CUDA(cudaStreamWaitEvent(hi, ev[0], 0));
+    if ((st = factor_super(hi, 0)) != RL_OK) return st;
+    cudaEvent_t el = next_event();
+    RL_CUDA(cudaEventRecord(el, hi));
+    for (int64_t sp = 0; sp < S; ++sp) {
+        const int64_t c0 = sp * W, rest = n - c0 - W;
+        if (rest <= 0) break;
+        // lo: U12 of this super-panel for every trailing column
+        RL_CUDA(cudaStreamWaitEvent(lo, el, 0));
+        if ((st = u12(lo, c0, c0 + W, rest)) != RL_OK) return st;
+        if ((st = update(lo, kBase, rest, kBase, at(c0 + kBase, c0), at(c0, c0 + W), at(c0 + kBase, c0 + W))) != RL_OK)
+            return st;
+        if ((st = u12(lo, c0 + kBase, c0 + W, rest)) != RL_OK) return st;
+        cudaEvent_t eu = next_event();
+        RL_CUDA(cudaEventRecord(eu, lo));
+        const bool next_full = sp + 1 < S;
+        // hi: GEMM_a(s) -> factor_super(s+1)
+        RL_CUDA(cudaStreamWaitEvent(hi, eu, 0));
+        if (next_full) {
+            if ((st = update(hi, rest, W, W, at(c0 + W, c0), at(c0, c0 + W), at(c0 + W, c0 + W))) != RL_OK) return st;
+            if ((st = factor_super(hi, c0 + W)) != RL_OK) return st;
+            el = next_event();
+            RL_CUDA(cudaEventRecord(el, hi));
+        }
+        // lo: GEMM_b(s) on the remaining columns (all of them before the tail)
+        const int64_t cb = next_full ? c0 + 2 * W : c0 + W;
+        if ((st = update(lo, rest, n - cb, W, at(c0 + W, c0), at(c0, cb), at(c0 + W, cb))) != RL_OK) return st;
+    }
+    RL_CUDA(cudaEventRecord(ev[1], hi));
+    RL_CUDA(cudaStreamWaitEvent(lo, ev[1], 0));
+    // tail (< 128 columns, fully updated): one 64-column step, then the ragged rest
+    int64_t c0 = S * W;
+    if (n - c0 >= kBase) {
+        if ((st = panel_l(lo, c0)) != RL_OK) return st;
+        const int64_t rest = n - c0 - kBase;
+        if ((st = u12(lo, c0, c0 + kBase, rest)) != RL_OK) return st;
+        if ((st = update(lo, rest, rest, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase), at(c0 + kBase, c0 + kBase))) !=
+            RL_OK)
+            return st;
+        c0 += kBase;
+    }
+    if (c0 < n) return panel(g, c0, n - c0);
+    return RL_OK;
+}
+
 rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out) {
     if (n <= 0) return RL_OK;
     Ctx g{ctx, a, n, lda, piv_out, rinv_out};
     const int64_t K = n / kBase;  // full 64-column panels
     rl_status st;
+    if (K >= 4) return genp_super128(ctx, n, a, lda, piv_out, rinv_out);
     if (K >= 3) {
         // right-looking GENP with a one-panel lookahead on two streams:
         //   hi: GEMM_a(k) (next panel's 64 columns) -> panel_L(k+1)
