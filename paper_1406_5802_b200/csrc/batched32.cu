@@ -81,6 +81,17 @@ __device__ __forceinline__ void fma_if(bool pred, double& y, double l, double v)
         : "+d"(y) : "d"(-l), "d"(v), "r"(static_cast<unsigned>(pred)));
 }
 
+// max over the warp of a non-negative double (bit patterns order like the
+// values): max of the high words, then of the low words among the lanes that
+// hold that high word — two REDUX instead of five shuffle/fmax rounds
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned hi = static_cast<unsigned>(b >> 32), lo = static_cast<unsigned>(b);
+    const unsigned mhi = __reduce_max_sync(kFull, hi);
+    const unsigned mlo = __reduce_max_sync(kFull, hi == mhi ? lo : 0u);
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
+}
+
 // a / b correctly rounded from r = 1/b: one residual correction
 __device__ __forceinline__ double div_by(double a, double b, double r) {
     const double q0 = a * r;
@@ -147,7 +158,7 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
 }
 
 // Main-kernel shared memory: only P (then its LU) and a few vectors per warp
-// (9,984 B): 5 CTAs x 4 warps = 20 resident warps per SM. G never touches
+// (9,472 B): 5 CTAs x 4 warps = 20 resident warps per SM. G never touches
 // shared memory: its B fragments go from global straight into registers, and
 // the two late passes that need A and G again (x = G y, r = b - A x) re-read
 // them from L2 with evict-first loads.
@@ -155,8 +166,6 @@ struct __align__(16) MainSmem {
     double P[D * LDP];  // product A G, then its packed LU in place
     double vec[2][D];   // double-buffered broadcast rows / vectors
     double b[D];
-    double rinv[D];     // 1 / u_jj
-    double piv[D];      // u_jj
 };
 constexpr size_t kMainSmemBytes = sizeof(MainSmem) * WARPS;
 constexpr int kMainCtasPerSm = 4;
@@ -283,14 +292,13 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             }
         PH(1);
         const double tol_hi = kTolPivot32 * sqrt(warp_sum(sumsq)) * (1.0 + 1e-10);
-        const double max_p = warp_max(amax);
+        const double max_p = warp_max_nonneg(amax);
         __syncwarp();
         PH(2);
 
         // ---- blocked GENP on P (lu.hpp:47-56 reorganised: 8-column panels
         // eliminated in natural order, U12 by forward substitution, trailing
         // Schur update on the FP64 tensor path). No row exchanges.
-        bool flagged = false;
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
             const int J = 8 * kb, rows = D - J, R = D - J - 8;
@@ -321,11 +329,6 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                 }
                 const double piv = rw[t];
                 const double inv = rcp64(piv);
-                flagged |= !(fabs(piv) > tol_hi);
-                if (lane == 0) {
-                    s.piv[J + t] = piv;
-                    s.rinv[J + t] = inv;
-                }
                 const bool below = lane > t && lane < rows;
                 const double l = below ? div_by(pr[t], piv, inv) : 0.0;
                 if (below) pr[t] = l;
@@ -375,6 +378,11 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             }
         }
 
+        // pivot u_ii, its reciprocal (the same rcp64 the elimination used) and
+        // the verdict bound, one row per lane
+        const double my_piv = s.P[lane * LDP + lane];
+        const double my_rinv = rcp64(my_piv);
+        const bool flagged = __any_sync(kFull, !(fabs(my_piv) > tol_hi));
         PH(3);
         // ---- growth numerator max|U|: lane i scans the U part of row i
         double umax = 0.0;
@@ -391,25 +399,31 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             if (lane == 0) idx = atomicAdd(&fix->count, 1);
             idx = __shfl_sync(kFull, idx, 0);
             if (lane == 0) fix->sys[idx] = sys;
-            fix_piv[static_cast<size_t>(idx) * D + lane] = s.piv[lane];
+            fix_piv[static_cast<size_t>(idx) * D + lane] = my_piv;
         }
 
         PH(4);
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
-        const double my_rinv = s.rinv[lane], my_piv = s.piv[lane];
         double x = 0.0, rel = 0.0, y = bl;
+        double prow[D];  // this lane's LU row, off the substitution chains
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) {
+            const double2 v = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
+            prow[2 * m] = v.x;
+            prow[2 * m + 1] = v.y;
+        }
         for (int step = 0; step <= refine; ++step) {
 #pragma unroll
             for (int k = 0; k < D; ++k) {  // forward, unit L (lu.hpp:110-115)
                 const double yk = __shfl_sync(kFull, y, k);
-                fma_if(lane > k, y, s.P[lane * LDP + k], yk);
+                fma_if(lane > k, y, prow[k], yk);
             }
 #pragma unroll
             for (int k = D - 1; k >= 0; --k) {  // backward, U (lu.hpp:116-121)
                 if (lane == k) y = div_by(y, my_piv, my_rinv);
                 const double xk = __shfl_sync(kFull, y, k);
-                fma_if(lane < k, y, s.P[lane * LDP + k], xk);
+                fma_if(lane < k, y, prow[k], xk);
             }
             s.vec[0][lane] = y;
             __syncwarp();
@@ -454,7 +468,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             }
         }
         __stcs(gX + sys * D + lane, x);
-        umax = warp_max(umax);  // identical in every lane
+        umax = warp_max_nonneg(umax);  // identical in every lane
         if (lane == 0) {
             if (gR) gR[sys] = rel;
             if (gGrowth) gGrowth[sys] = umax / max_p;
