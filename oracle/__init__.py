@@ -214,6 +214,7 @@ class _Ref:
         self._normest = s("ref_spectral_norm_estimate", ctypes.c_double, [i64, i64, _dp])
         self._genp = s("ref_genp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p])
         self._solve = s("ref_lu_solve", None, [i64, _dp, _dp, _dp])
+        self._schur = s("ref_schur_complement", ctypes.c_int, [i64, _dp, i64, _dp])
         self._fft = s("ref_fft", ctypes.c_int, [i64, _dp, ctypes.c_int])
         self._capply = s("ref_circulant_apply", ctypes.c_int, [i64, _dp, _dp, _dp])
         self._mcirc = s("ref_matmul_by_circulant", ctypes.c_int, [i64, i64, _dp, _dp, _dp])
@@ -256,6 +257,16 @@ class _Ref:
         zs = np.zeros(1, np.int64)
         st = self._genp(a.shape[0], ptr(a), ptr(lu), ptr(zs))
         return lu, int(zs[0]) if st == 2 else 0
+
+    def schur_complement(self, a, k):
+        """block_ge.hpp:202-218: E - D B^-1 C of the leading k x k block (GEPP)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        n = a.shape[0]
+        out = np.empty((n - k, n - k))
+        st = self._schur(n, ptr(a), k, ptr(out))
+        if st != 0:
+            raise RuntimeError(f"ref_schur_complement failed ({st})")
+        return out
 
     def lu_solve(self, lu, b):
         lu = np.ascontiguousarray(lu, dtype=np.float64)

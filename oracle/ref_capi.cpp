@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "oracle.h"
+#include "randla/block_ge.hpp"
 #include "randla/circulant.hpp"
 #include "randla/fft.hpp"
 #include "randla/lu.hpp"
@@ -121,6 +122,15 @@ int ref_genp_factor(int64_t n, const double* a, double* lu, int64_t* zero_step) 
                                             : f.upper(static_cast<std::size_t>(i), static_cast<std::size_t>(j));
         },
         zero_step);
+}
+
+// schur_complement (block_ge.hpp:202-218): E - D B^-1 C for the leading k x k
+// block (GEPP on B, so independent of the elimination path)
+int ref_schur_complement(int64_t n, const double* a, int64_t k, double* out) {
+    return guarded([&] {
+        const RealMatrix sc = schur_complement(wrap(n, n, a), static_cast<std::size_t>(k));
+        std::memcpy(out, sc.data(), sizeof(double) * (n - k) * (n - k));
+    });
 }
 
 // lu_solve (lu.hpp:100-123) on packed factors

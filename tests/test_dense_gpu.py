@@ -203,3 +203,24 @@ def test_config3_full_size_device(cuda, orc):
     ref, st = orc.C.matmul_by_circulant(a[rows].cpu().numpy(), c)
     got = rl.matmul_by_circulant(a[rows].contiguous(), torch.from_numpy(c).cuda()).cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("n,ks", [(1024, (256, 512, 768)), (700, (256, 512))])
+def test_schur_blocks_vs_reference_block_ge(cuda, orc, n, ks):
+    """SURVEY §8(a) a27 / config 3's block size 256: the trailing factors of the
+    device's blocked GENP give the Schur complement of every leading k x k block,
+    which is elimination-path independent; it must match the reference's own
+    schur_complement (block_ge.hpp:202-218, GEPP on the pivot block), the
+    quantity block_ge_factor's Schur children hold (tests/test_elimination.cpp:
+    141-153, tests/acceptance.cpp:246-259)."""
+    if orc.REF is None:
+        pytest.skip("reference build (oracle/_ref) not present")
+    a = orc.C.gen_gaussian(n, n, 1)
+    g = orc.C.gen_gaussian(n, n, 2)
+    p = orc.C.matmul(a, g)
+    f = rl.genp_factor(p)
+    for k in ks:
+        s_dev = f.lower[k:, k:] @ f.upper[k:, k:]
+        s_ref = orc.REF.schur_complement(p, k)
+        kb = np.linalg.cond(p[:k, :k])
+        assert _rel(s_dev, s_ref) <= 1e-10 * kb, (k, _rel(s_dev, s_ref), kb)
