@@ -17,10 +17,12 @@
 //      pivot lies in the band (tol_pivot*floor, tol_pivot*||P||_F]; it then
 //      runs in the reference's exact summation order (no FMA) in
 //      verdict_fixup_kernel, so the verdict is the reference's.
-//   5. Solves (lu.hpp:110-122) with shuffle broadcasts; x = G y and the
-//      residual ||b - A x|| / ||b|| (lu.hpp:155-161 / preprocess.hpp:122-128)
-//      on DMMA with G and A re-read from L2; growth max|U| / max|P|; packed
-//      LU written back coalesced.
+//   5. The packed LU is final: written back coalesced, and the P region takes
+//      G again (cp.async, in flight during the sweeps). Solves (lu.hpp:
+//      110-122) with shuffle broadcasts over the lane's LU row in registers;
+//      x = G y by row dots from shared memory; the residual ||b - A x|| / ||b||
+//      (lu.hpp:155-161 / preprocess.hpp:122-128) on DMMA with A re-read from
+//      L2; growth max|U| / max|P|.
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
@@ -413,6 +415,22 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             prow[2 * m] = v.x;
             prow[2 * m + 1] = v.y;
         }
+        // the LU is final: store it now and reuse the P region for G (rows at
+        // stride LDP: conflict-free row reads), in flight during the sweeps
+        if (gLU) {
+            double2* dst = reinterpret_cast<double2*>(gLU + mo);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int p = lane + 32 * q;
+                st_stream(dst + p, *reinterpret_cast<const double2*>(&s.P[(p >> 4) * LDP + 2 * (p & 15)]));
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int p = lane + 32 * q;
+            cp_async16(&s.P[(p >> 4) * LDP + 2 * (p & 15)], G + 2 * p);
+        }
         for (int step = 0; step <= refine; ++step) {
 #pragma unroll
             for (int k = 0; k < D; ++k) {  // forward, unit L (lu.hpp:110-115)
@@ -426,21 +444,22 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                 fma_if(lane < k, y, prow[k], xk);
             }
             s.vec[0][lane] = y;
+            cp_async_wait_all();
             __syncwarp();
-            // d = G y (matvec, matrix.hpp:146-156), G re-read from L2
-            double cb[4];
-            matvec_dmma(G, s.vec[0], lane, cb);
-            __syncwarp();
-            if (fc == 0) {
+            // d = G y (matvec, matrix.hpp:146-156): lane i dots row i of G
+            double d = 0.0;
 #pragma unroll
-                for (int ti = 0; ti < 4; ++ti) s.vec[1][8 * ti + fr] = cb[ti];
+            for (int m = 0; m < D / 2; ++m) {
+                const double2 gv = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
+                const double2 yv = *reinterpret_cast<const double2*>(&s.vec[0][2 * m]);
+                d = fma(gv.x, yv.x, d);
+                d = fma(gv.y, yv.y, d);
             }
-            __syncwarp();
-            x += s.vec[1][lane];
-            __syncwarp();
+            x += d;
             s.vec[1][lane] = x;
             __syncwarp();
             // residual b - A x (preprocess.hpp:122-126), A re-read from L2
+            double cb[4];
             matvec_dmma(A, s.vec[1], lane, cb);
             double rsq = 0.0;
             if (fc == 0) {
@@ -459,14 +478,6 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
 
         PH(5);
         // ---- outputs
-        if (gLU) {
-            double2* dst = reinterpret_cast<double2*>(gLU + mo);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int p = lane + 32 * q;
-                st_stream(dst + p, *reinterpret_cast<const double2*>(&s.P[(p >> 4) * LDP + 2 * (p & 15)]));
-            }
-        }
         __stcs(gX + sys * D + lane, x);
         umax = warp_max_nonneg(umax);  // identical in every lane
         if (lane == 0) {
