@@ -386,14 +386,19 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         const double my_rinv = rcp64(my_piv);
         const bool flagged = __any_sync(kFull, !(fabs(my_piv) > tol_hi));
         PH(3);
-        // ---- growth numerator max|U|: lane i scans the U part of row i
-        double umax = 0.0;
+        // ---- this lane's LU row into registers (the sweeps' operands) and the
+        // growth numerator max|U| over its U part
+        double prow[D];
 #pragma unroll
         for (int m = 0; m < D / 2; ++m) {
             const double2 v = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
-            if (2 * m >= lane) umax = max_abs(umax, v.x);
-            if (2 * m + 1 >= lane) umax = max_abs(umax, v.y);
+            prow[2 * m] = v.x;
+            prow[2 * m + 1] = v.y;
         }
+        double umax = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+            if (k >= lane) umax = max_abs(umax, prow[k]);
 
         // ---- verdict: pivots <= tol_pivot * ||P||_F need the exact estimate
         if (flagged) {
@@ -408,13 +413,6 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
         double x = 0.0, rel = 0.0, y = bl;
-        double prow[D];  // this lane's LU row, off the substitution chains
-#pragma unroll
-        for (int m = 0; m < D / 2; ++m) {
-            const double2 v = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
-            prow[2 * m] = v.x;
-            prow[2 * m + 1] = v.y;
-        }
         // the LU is final: store it now and reuse the P region for G (rows at
         // stride LDP: conflict-free row reads), in flight during the sweeps
         if (gLU) {
