@@ -324,6 +324,68 @@ lu_u12_kernel(double* __restrict__ a, int64_t lda, int64_t c0, int64_t col_begin
     for (int i = 0; i < kBase; ++i) col[i * lda] = x[i];
 }
 
+// ---- L11^-1 of a factored 64x64 diagonal block (U12 as a GEMM) -----------
+// Recursive doubling on the unit-lower L11: the eight 8x8 diagonal blocks are
+// inverted by forward substitution (one thread per column), then pairs merge,
+// inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 (B A^-1), C^-1]], at 8, 16, 32.
+// One CTA, small rolled loops (a single CTA running fully unrolled 64-step
+// code is instruction-fetch bound). The U12 = L11^-1 A12 product then runs on
+// the DMMA GEMM instead of a latency-bound substitution kernel; keeping L21 by
+// substitution (U11^-1 loses an order of magnitude of residual on config 1).
+constexpr int IT = 256;
+constexpr int kInvSmem = 3 * kBase * (kBase + 1) * 8;
+__global__ void __launch_bounds__(IT)
+linv64_kernel(const double* __restrict__ a, int64_t lda, int64_t c0, double* __restrict__ linv) {
+    extern __shared__ double ism[];
+    double(*L)[kBase + 1] = reinterpret_cast<double(*)[kBase + 1]>(ism);
+    double(*X)[kBase + 1] = reinterpret_cast<double(*)[kBase + 1]>(ism + kBase * (kBase + 1));
+    double(*T)[kBase + 1] = reinterpret_cast<double(*)[kBase + 1]>(ism + 2 * kBase * (kBase + 1));
+    const int tid = threadIdx.x;
+    const double* d = a + c0 * lda + c0;
+    for (int idx = tid; idx < kBase * kBase; idx += IT) {
+        const int i = idx >> 6, j = idx & 63;
+        L[i][j] = j < i ? d[i * lda + j] : (i == j ? 1.0 : 0.0);
+        X[i][j] = 0.0;
+    }
+    __syncthreads();
+    if (tid < kBase) {  // level 0: column j of the inverse of diagonal block b (8x8)
+        const int b = tid >> 3, j = tid & 7, o = 8 * b;
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = i == j ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+#pragma unroll
+            for (int i = k + 1; i < 8; ++i) x[i] = fma(-L[o + i][o + k], x[k], x[i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) X[o + i][o + j] = x[i];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int h = 8; h < kBase; h *= 2) {
+        const int pairs = kBase / (2 * h), outs = pairs * h * h;
+        // T = B A^-1 for every pair (B: L rows [o+h, o+2h), cols [o, o+h))
+        for (int e = tid; e < outs; e += IT) {
+            const int p = e / (h * h), r = (e / h) % h, cidx = e % h, o = 2 * h * p;
+            double acc = 0.0;
+#pragma unroll 4
+            for (int k = cidx; k < h; ++k) acc = fma(L[o + h + r][o + k], X[o + k][o + cidx], acc);  // X_a lower
+            T[o + h + r][o + cidx] = acc;
+        }
+        __syncthreads();
+        // X_off = -C^-1 T
+        for (int e = tid; e < outs; e += IT) {
+            const int p = e / (h * h), r = (e / h) % h, cidx = e % h, o = 2 * h * p;
+            double acc = 0.0;
+#pragma unroll 4
+            for (int k = 0; k <= r; ++k) acc = fma(X[o + h + r][o + h + k], T[o + h + k][o + cidx], acc);  // X_c lower
+            X[o + h + r][o + cidx] = -acc;
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < kBase * kBase; idx += IT) linv[idx] = X[idx >> 6][idx & 63];
+}
+
 struct Ctx {
     rl_context* ctx;
     double* a;
@@ -428,18 +490,41 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         ctx->stream = keep;
         return r;
     };
+    static bool inv_configured = false;
+    if (!inv_configured) {
+        RL_CUDA(cudaFuncSetAttribute(linv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem));
+        inv_configured = true;
+    }
+    // per 64-block L11^-1 (32 KiB each), stream-ordered scratch
+    double* inv = nullptr;
+    RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&inv), sizeof(double) * kBase * kBase * (n / kBase), lo));
+    struct Free {
+        double* p;
+        cudaStream_t s;
+        ~Free() { cudaFreeAsync(p, s); }
+    } inv_guard{inv, lo};
+    auto linv = [&](int64_t c0) { return inv + (c0 / kBase) * kBase * kBase; };
+    // panel: factor the diagonal block and L21 = A21 U11^-1 by substitution,
+    // then L11^-1 for the U12 GEMMs
     auto panel_l = [&](cudaStream_t sm, int64_t c0) -> rl_status {
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
         lu_panel64_kernel<<<blocks, PT, 0, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
+        linv64_kernel<<<1, IT, kInvSmem, sm>>>(a, lda, c0, linv(c0));
+        RL_CHECK_LAUNCH("linv64_kernel");
         return RL_OK;
     };
+    // U12 = L11^-1 A12 in place (each output column block reads only its own
+    // input block, all of it, before any store)
     auto u12 = [&](cudaStream_t sm, int64_t r0, int64_t cb, int64_t ncols) -> rl_status {
         if (ncols <= 0) return RL_OK;
-        lu_u12_kernel<<<static_cast<unsigned>((ncols + PT - 1) / PT), PT, 0, sm>>>(a, lda, r0, cb, ncols);
-        RL_CHECK_LAUNCH("lu_u12_kernel");
-        return RL_OK;
+        cudaStream_t keep = ctx->stream;
+        ctx->stream = sm;
+        const rl_status r = gemm(ctx, kBase, ncols, kBase, linv(r0), kBase, at(r0, cb), lda, at(r0, cb), lda, 1.0,
+                                 false, nullptr);
+        ctx->stream = keep;
+        return r;
     };
     auto factor_super = [&](cudaStream_t sm, int64_t c0) -> rl_status {
         rl_status r;
