@@ -727,8 +727,7 @@ extern "C" RL_API rl_status rl_batched_genp_solve_32(rl_context* ctx, rl_mem mem
         RL_CUDA(cudaMemcpyAsync(const_cast<double*>(dg), g, mb * 8, cudaMemcpyHostToDevice, s));
         RL_CUDA(cudaMemcpyAsync(const_cast<double*>(db), b, vb * 8, cudaMemcpyHostToDevice, s));
     }
-    static const int dbg_refine = getenv("RANDLA_DEBUG_REFINE") ? atoi(getenv("RANDLA_DEBUG_REFINE")) : 0;
-    st = launch_batched_genp32(ctx, batch, da, dg, db, dlu, dx, dr, dgr, dst, dbg_refine, fix_ws);
+    st = launch_batched_genp32(ctx, batch, da, dg, db, dlu, dx, dr, dgr, dst, /*refine=*/0, fix_ws);
     if (st != RL_OK) return st;
     SummaryAccum hsum{};
     if (summary) {

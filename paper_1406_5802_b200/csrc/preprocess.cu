@@ -370,17 +370,11 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     st = dense_alloc(ctx, D, n, dense && !g_dev_direct, own_a, true);
     if (st != RL_OK) return st;
     cudaStream_t s = ctx->stream;
-    static const bool dbg = std::getenv("RANDLA_DEBUG_GEN") != nullptr;
-    auto now = [] {
-        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-    };
-    const double t_start = dbg ? now() : 0.0;
     // seeded dense multiplier: generated on the device (exact); its kernels are
     // enqueued first so that they run under the upload of A
     GaussJob gjob;
     const bool gen_g = kind == RL_MULT_GAUSSIAN && !post->dense;
     if (gen_g && (st = gjob.begin(ctx, n, n, post->seed, D.G, ld)) != RL_OK) return st;
-    const double t_begun = dbg ? now() : 0.0;
     int a_issued = 0;
     auto upload_a_block = [&](int c) -> rl_status {
         const int64_t r0 = c * D.a_chunk_rows, rc = std::min(D.a_chunk_rows, n - r0);
@@ -413,7 +407,6 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     } else {
         D.A = const_cast<double*>(a);
     }
-    const double t_aq = dbg ? now() : 0.0;
     struct Col {
         double* p = nullptr;
         cudaStream_t s;
@@ -458,7 +451,6 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
     for (; a_issued > 0 && a_issued < D.a_chunks; ++a_issued)
         if ((st = upload_a_block(a_issued)) != RL_OK) return st;
-    const double t_gen = dbg ? now() : 0.0;
     StageTimer timer(s);
     st = factor_and_verdict(ctx, D, info, &timer);
     if (st != RL_OK) {
@@ -470,7 +462,6 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     if (st != RL_OK) return st;
     timer.mark();
     timer.fill(info->stage_ms);
-    const double t_solved = dbg ? now() : 0.0;
     RL_CUDA(cudaMemcpyAsync(x, D.x, n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
     if (lu_out && (st = copy_out(ctx, lu_out, D.P, ld, n, n, host)) != RL_OK) return st;
     if (want_norm_a) {
@@ -486,9 +477,6 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         info->residual_rel_a = std::sqrt(sq[0]) / (na * std::sqrt(sq[1]));
     }
     RL_CUDA(cudaStreamSynchronize(s));
-    if (dbg)
-        std::fprintf(stderr, "[solve] begin %.2f, A enqueue %.2f, gen finish %.2f ms, stages %.2f ms (wall %.2f), tail %.2f ms\n",
-                     t_begun - t_start, t_aq - t_begun, t_gen - t_aq, info->stage_ms[3], t_solved - t_gen, now() - t_solved);
     return RL_OK;
 }
 

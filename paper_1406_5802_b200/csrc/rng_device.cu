@@ -325,13 +325,9 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
     if (count <= 0) return RL_OK;
     cudaStream_t s = ctx->stream;
     const int64_t pairs = (count + 1) / 2;
-    static const bool dbg = std::getenv("RANDLA_DEBUG_GEN") != nullptr;
-    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    const double t0 = dbg ? now() : 0.0;
     RL_CUDA(cudaStreamSynchronize(s));
     h_total = ctx->host_scalars[0];
     h_hard = static_cast<int64_t>(ctx->host_scalars[1]);
-    const double t1 = dbg ? now() : 0.0;
     if (h_total < pairs || h_hard > cap) {
         // astronomically unlikely: too few accepted attempts, or too many hard
         // cases for the list; generate on the host and upload
@@ -362,9 +358,7 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
         }
         RL_CUDA(cudaMemcpyAsync(att, attempts, 8 * nh, cudaMemcpyDeviceToHost, s));
         RL_CUDA(cudaStreamSynchronize(s));
-        const double t2 = dbg ? now() : 0.0;
         host_polar_pairs(seed, att, nh, hv);
-        if (dbg) std::fprintf(stderr, "[gen] kernels %.2f ms, d2h %.2f ms, host %.2f ms\n", t1 - t0, t2 - t1, now() - t2);
         RL_CUDA(cudaMemcpyAsync(vals, hv, 16 * nh, cudaMemcpyHostToDevice, s));
         scatter_kernel<<<static_cast<unsigned>((nh + 255) / 256), 256, 0, s>>>(pair, vals, nh, count, out,
                                                                                Pos{rows, cols, ld});
