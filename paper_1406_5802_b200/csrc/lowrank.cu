@@ -436,11 +436,9 @@ extern "C" RL_API rl_status rl_range_find_residual(rl_context* ctx, rl_mem mem, 
         if (h->dense) {
             RL_CUDA(cudaMemcpy2DAsync(bh.p, ldq * 8, h->dense, l * 8, l * 8, n,
                                       host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-        } else {
-            std::vector<double> hg(static_cast<size_t>(n * l));
-            rl_gen_gaussian(n, l, h->seed, hg.data());  // materialize: gen_gaussian(n, l, seed)
-            RL_CUDA(cudaMemcpy2DAsync(bh.p, ldq * 8, hg.data(), l * 8, l * 8, n, cudaMemcpyHostToDevice, s));
-            RL_CUDA(cudaStreamSynchronize(s));
+        } else if ((st = gen_gaussian_device(ctx, n, l, h->seed, bh.p, ldq, nullptr)) != RL_OK) {
+            // materialize: gen_gaussian(n, l, seed) (multipliers.hpp:191-192), exact, on the device
+            return st;
         }
         const int64_t tiles = ((m + 127) / 128) * ((l + 127) / 128);
         const int splits = splits_for(tiles, (n + 15) / 16, ctx->num_sms);
