@@ -8,8 +8,9 @@
 // Y = A H: dense Gaussian H (n x l, materialize -> gen_gaussian(n, l, seed),
 //   multipliers.hpp:191-192) by the DMMA GEMM (split-K: N = l is narrow), or
 //   the Toeplitz block of a circulant by the FFT kernel (fft.cu).
-// Q: CholeskyQR2. W = Y^T Y (split-K DMMA GEMM over Y^T), W = R^T R
-//   (one-CTA Cholesky), Q1 = Y R^-1 (DMMA GEMM with the triangular inverse),
+// Q: CholeskyQR2. W = Y^T Y (split-K DMMA GEMM over Y^T), W = R^T R and
+//   R^-1 blocked by 64 (shared-memory diagonal blocks, DMMA GEMM panels and
+//   updates), Q1 = Y R^-1 (DMMA GEMM),
 //   repeated once; R = R2 R1. The R of a full-rank QR with positive diagonal is
 //   unique, so R_jj is Householder's |r_jj| up to rounding and the reference's
 //   rank verdict |r_jj| <= tol_rank(m, l) * spectral_norm_estimate(Y)
@@ -52,51 +53,85 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int
     }
 }
 
-// W = R^T R in place (upper triangle of w holds R afterwards, lower zeroed).
-// *fail = first 1-based step with a non-positive pivot, 0 on success.
-__global__ void __launch_bounds__(1024) cholesky_kernel(double* __restrict__ w, int64_t ld, int l, int* __restrict__ fail) {
+
+// ---- blocked Cholesky / triangular inverse (l up to a few hundred) ---------
+// 64x64 diagonal block at (J, J): Cholesky W_JJ = R^T R in shared memory
+// (lu.hpp-style right-looking, rolled loops), R written back upper with zeros
+// below, X = R^-1 (column sweeps) into xd (Rinv's diagonal block) and X^T
+// into xt (64 x 64, the operand of the panel GEMM). fail <- 1-based global
+// index of the first non-positive pivot (first block that breaks down).
+constexpr int CB = 64, CT = 256;
+constexpr int kCholSmem = 2 * CB * (CB + 1) * 8;
+__global__ void __launch_bounds__(CT) chol_block_kernel(double* __restrict__ w, int64_t ld, int J, int bw,
+                                                        int* __restrict__ fail, double* __restrict__ xd, int64_t ldx,
+                                                        double* __restrict__ xt) {
+    extern __shared__ double cbm[];
+    double(*a)[CB + 1] = reinterpret_cast<double(*)[CB + 1]>(cbm);
+    double(*x)[CB + 1] = reinterpret_cast<double(*)[CB + 1]>(cbm + CB * (CB + 1));
     __shared__ int s_fail;
-    if (threadIdx.x == 0) s_fail = 0;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_fail = 0;
+    for (int idx = tid; idx < CB * CB; idx += CT) {
+        const int i = idx >> 6, k = idx & 63;
+        a[i][k] = (i < bw && k < bw) ? w[(J + i) * ld + J + k] : (i == k ? 1.0 : 0.0);
+        x[i][k] = 0.0;
+    }
     __syncthreads();
-    for (int j = 0; j < l; ++j) {
-        const double d = w[j * ld + j];
-        if (!(d > 0.0)) {
-            if (threadIdx.x == 0) s_fail = j + 1;
+    const int r = tid >> 2, q = tid & 3;  // trailing row j+1+r... (r < 64), columns q, q+4, ...
+#pragma unroll 1
+    for (int j = 0; j < bw; ++j) {
+        const double d = a[j][j];
+        if (!(d > 0.0)) {  // uniform: every thread reads the same value
+            if (tid == 0) s_fail = J + j + 1;
             break;
         }
-        const double r = sqrt(d);
-        const double ri = 1.0 / r;
+        const double rt = sqrt(d), ri = 1.0 / rt;
         __syncthreads();
-        for (int k = j + 1 + threadIdx.x; k < l; k += blockDim.x) w[j * ld + k] *= ri;
+        if (tid > j && tid < bw) a[j][tid] *= ri;
+        if (tid == 0) a[j][j] = rt;
         __syncthreads();
-        if (threadIdx.x == 0) w[j * ld + j] = r;
-        const int rest = l - j - 1;
-        for (int idx = threadIdx.x; idx < rest * rest; idx += blockDim.x) {
-            const int i = j + 1 + idx / rest, k = j + 1 + idx % rest;
-            if (k >= i) w[i * ld + k] = fma(-w[j * ld + i], w[j * ld + k], w[i * ld + k]);
+        const int i = j + 1 + r;
+        if (i < bw) {
+            const double l = a[j][i];
+#pragma unroll 4
+            for (int k = j + 1 + q; k < bw; k += 4) a[i][k] = fma(-l, a[j][k], a[i][k]);
         }
         __syncthreads();
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) {
-        const int i = idx / l, k = idx % l;
-        if (k < i) w[i * ld + k] = 0.0;
+    if (s_fail) {
+        if (tid == 0) atomicCAS(fail, 0, s_fail);
+        return;
     }
-    if (threadIdx.x == 0) *fail = s_fail;
+    // X = R^-1, thread c < bw owns column c (axpy back substitution)
+    if (tid < bw) {
+        const int c = tid;
+        x[c][c] = 1.0;
+#pragma unroll 1
+        for (int k = c; k >= 0; --k) {
+            const double xk = x[k][c] / a[k][k];
+            x[k][c] = xk;
+#pragma unroll 4
+            for (int i = 0; i < k; ++i) x[i][c] = fma(-a[i][k], xk, x[i][c]);
+        }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < bw * bw; idx += CT) {
+        const int i = idx / bw, k = idx % bw;
+        w[(J + i) * ld + J + k] = k >= i ? a[i][k] : 0.0;
+        xd[i * ldx + k] = x[i][k];
+    }
+    for (int idx = tid; idx < CB * CB; idx += CT) {
+        const int i = idx >> 6, k = idx & 63;
+        xt[i * CB + k] = (i < bw && k < bw) ? x[k][i] : 0.0;
+    }
 }
 
-// X = R^-1 for upper triangular R (l x l): one column per thread, back
-// substitution (rows below the column's index are zero)
-__global__ void tri_inv_upper_kernel(const double* __restrict__ r, int64_t ldr, int l, double* __restrict__ x,
-                                     int64_t ldx) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= l) return;
-    for (int i = l - 1; i > j; --i) x[i * ldx + j] = 0.0;
-    for (int i = j; i >= 0; --i) {
-        double acc = i == j ? 1.0 : 0.0;
-        for (int k = i + 1; k <= j; ++k) acc = fma(-r[i * ldr + k], x[k * ldx + j], acc);
-        x[i * ldx + j] = acc / r[i * ldr + i];
-    }
+__global__ void zero_lower_kernel(double* __restrict__ w, int64_t ld, int l) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<int64_t>(l) * l) return;
+    const int i = static_cast<int>(idx / l), k = static_cast<int>(idx % l);
+    if (k < i) w[i * ld + k] = 0.0;
 }
 
 __global__ void add_diag_kernel(double* __restrict__ w, int64_t ld, int l, double s) {
@@ -177,7 +212,61 @@ struct Buf {
 }  // namespace
 
 // C (l x l, ldc) = Y^T Y for Y (m x l, ldy): transpose + split-K DMMA GEMM
-static rl_status gram(rl_context* ctx, int64_t m, int64_t l, const double* y, int64_t ldy, double* c, int64_t ldc,
+static // Blocked Cholesky W = R^T R (upper R, in place, zeros below) and X = R^-1
+// (upper, zeros below) for the Gram matrix of CholeskyQR: 64-wide diagonal
+// blocks in chol_block_kernel, panel R_J* = R_JJ^-T W_J* and trailing update
+// W -= R_J*^T R_J* on the DMMA GEMM; X's off-diagonal block columns
+// X[0:J, J] = -X[0:J, 0:J] R[0:J, J] X_JJ by two GEMMs each. flags[0] <- the
+// 1-based breakdown index (0 = none; caller reads it).
+size_t chol_inv_work_bytes(int64_t l) {
+    const int64_t ldl = (l + 1) & ~int64_t(1);
+    return sizeof(double) * (CB * CB + 2 * l * ldl) + 256;
+}
+
+rl_status chol_inv_blocked(rl_context* ctx, double* W, int64_t ldl, int64_t l, double* X, int* flags, void* work) {
+    cudaStream_t s = ctx->stream;
+    double* xt = static_cast<double*>(work);
+    double* pt = xt + CB * CB;    // transposed panel (rest x CB)
+    double* tt = pt + l * ldl;    // T = X[0:J,0:J] R[0:J, J] (J x CB)
+    RL_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
+    RL_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * l * ldl, s));
+    static bool configured = false;
+    if (!configured) {
+        RL_CUDA(cudaFuncSetAttribute(chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem));
+        configured = true;
+    }
+    rl_status e;
+    for (int64_t J = 0; J < l; J += CB) {
+        const int bw = static_cast<int>(std::min<int64_t>(CB, l - J));
+        chol_block_kernel<<<1, CT, kCholSmem, s>>>(W, ldl, static_cast<int>(J), bw, flags, X + J * ldl + J, ldl, xt);
+        RL_CHECK_LAUNCH("chol_block_kernel");
+        const int64_t rest = l - J - bw;
+        if (rest > 0) {
+            // panel: R[J:J+bw, J+bw:] = (R_JJ^-1)^T W[J:J+bw, J+bw:]  (in place)
+            if ((e = gemm(ctx, bw, rest, bw, xt, CB, W + J * ldl + J + bw, ldl, W + J * ldl + J + bw, ldl, 1.0, false,
+                          nullptr)) != RL_OK)
+                return e;
+            // trailing: W[J+bw:, J+bw:] -= panel^T panel
+            transpose_kernel<<<dim3(nblk(rest, 32), nblk(bw, 32)), dim3(32, 8), 0, s>>>(W + J * ldl + J + bw, ldl, bw,
+                                                                                        rest, pt, ldl);
+            RL_CHECK_LAUNCH("transpose_kernel");
+            if ((e = gemm(ctx, rest, rest, bw, pt, ldl, W + J * ldl + J + bw, ldl, W + (J + bw) * ldl + J + bw, ldl,
+                          -1.0, true, nullptr)) != RL_OK)
+                return e;
+        }
+        if (J > 0) {
+            // X[0:J, J:J+bw] = -(X[0:J, 0:J] R[0:J, J:J+bw]) X_JJ
+            if ((e = gemm(ctx, J, bw, J, X, ldl, W + J, ldl, tt, ldl, 1.0, false, nullptr)) != RL_OK) return e;
+            if ((e = gemm(ctx, J, bw, bw, tt, ldl, X + J * ldl + J, ldl, X + J, ldl, -1.0, false, nullptr)) != RL_OK)
+                return e;
+        }
+    }
+    zero_lower_kernel<<<nblk(l * l, 256), 256, 0, s>>>(W, ldl, static_cast<int>(l));
+    RL_CHECK_LAUNCH("zero_lower_kernel");
+    return RL_OK;
+}
+
+rl_status gram(rl_context* ctx, int64_t m, int64_t l, const double* y, int64_t ldy, double* c, int64_t ldc,
                       double* yt, int64_t ldyt, void* work, int splits) {
     transpose_kernel<<<dim3(nblk(l, 32), nblk(m, 32)), dim3(32, 8), 0, ctx->stream>>>(y, ldy, m, l, yt, ldyt);
     RL_CHECK_LAUNCH("transpose_kernel");
@@ -201,6 +290,8 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
     if ((st = byt.alloc(sizeof(double) * l * ldm)) != RL_OK) return st;
     if ((st = bsplit.alloc(gemm_splitk_work_bytes(l, l, splits))) != RL_OK) return st;
     if ((st = bscal.alloc(sizeof(double) * 80)) != RL_OK) return st;
+    Buf cws(s);
+    if ((st = cws.alloc(chol_inv_work_bytes(l))) != RL_OK) return st;
     double* W = bw.p;
     double* Rinv = bw.p + l * ldl;
     double* Racc = bw.p + 2 * l * ldl;
@@ -226,13 +317,10 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
             add_diag_kernel<<<nblk(l, 256), 256, 0, s>>>(W, ldl, static_cast<int>(l), sh);
             RL_CHECK_LAUNCH("add_diag_kernel");
         }
-        cholesky_kernel<<<1, 1024, 0, s>>>(W, ldl, static_cast<int>(l), flags);
-        RL_CHECK_LAUNCH("cholesky_kernel");
+        if ((e = chol_inv_blocked(ctx, W, ldl, l, Rinv, flags, cws.p)) != RL_OK) return e;
         RL_CUDA(cudaMemcpyAsync(fail, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
         RL_CUDA(cudaStreamSynchronize(s));
         if (*fail) return RL_OK;
-        tri_inv_upper_kernel<<<nblk(l, 128), 128, 0, s>>>(W, ldl, static_cast<int>(l), Rinv, ldl);
-        RL_CHECK_LAUNCH("tri_inv_upper_kernel");
         if ((e = gemm(ctx, m, l, l, in, ldq, Rinv, ldl, out, ldq, 1.0, false, nullptr)) != RL_OK) return e;
         if (npass == 0) {
             RL_CUDA(cudaMemcpy2DAsync(Racc, ldl * 8, W, ldl * 8, l * 8, l, cudaMemcpyDeviceToDevice, s));
