@@ -256,3 +256,21 @@ def test_headline_full_size_properties(cuda):
     umax = torch.triu(dev.lu).abs().max()
     growth = (umax / p.abs().max()).item()
     assert abs(growth / dev.info["growth"] - 1) < 1e-12, (growth, dev.info["growth"])
+
+
+@pytest.mark.parametrize("n", [1031, 2050])
+def test_host_chunked_upload_odd_sizes(cuda, orc, n):
+    """Host-buffer calls upload A in row blocks under the product (n >= 1024);
+    odd n (padded leading dimension) and uneven blocks must give the same x as
+    the device-resident call, and match the oracle within tolerance."""
+    torch = cuda
+    a = orc.C.gen_gaussian(n, n, 31)
+    b = orc.C.gen_gaussian_vector(n, 32)
+    g = orc.C.gen_gaussian(n, n, 33)
+    h = rl.preprocess_solve(a, b, None, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 33), 0)
+    d = rl.preprocess_solve(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), None,
+                            rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 0, dense=torch.from_numpy(g).cuda()), 0)
+    np.testing.assert_array_equal(h.x, d.x.cpu().numpy())
+    if n <= 1100:
+        ref = orc.C.preprocess_solve(a, b, 1, g, refine=0, want_lu=True)
+        assert _rel(h.x, ref["x"]) <= 1e-10 * np.linalg.cond(ref["product"])
