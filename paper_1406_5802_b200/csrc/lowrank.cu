@@ -145,8 +145,15 @@ __global__ void gemvt_partial_kernel(const double* __restrict__ a, int64_t lda, 
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const int64_t i0 = static_cast<int64_t>(blockIdx.y) * chunk, i1 = min(m, i0 + chunk);
-    double s = 0.0;
-    for (int64_t i = i0; i < i1; ++i) s = fma(a[i * lda + j], u[i], s);
+    // eight rows per step with independent accumulators: eight loads in flight
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int64_t i = i0;
+    for (; i + 8 <= i1; i += 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] = fma(__ldcs(a + (i + r) * lda + j), u[i + r], acc[r]);
+    }
+    for (; i < i1; ++i) acc[0] = fma(a[i * lda + j], u[i], acc[0]);
+    const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     part[static_cast<int64_t>(blockIdx.y) * n + j] = s;
 }
 

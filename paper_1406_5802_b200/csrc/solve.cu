@@ -152,10 +152,23 @@ gemv_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n, con
         const double2* a2 = reinterpret_cast<const double2*>(ar);
         const double2* x2 = reinterpret_cast<const double2*>(x);
         const int64_t n2 = n / 2;
-        for (int64_t k = lane; k < n2; k += 32) {
+        // four independent accumulators: four 16-byte loads in flight per lane
+        double c1 = 0.0, c2 = 0.0, c3 = 0.0;
+        int64_t k = lane;
+        for (; k + 96 < n2; k += 128) {
+            const double2 a0 = __ldcs(a2 + k), a1 = __ldcs(a2 + k + 32), a2v = __ldcs(a2 + k + 64),
+                          a3 = __ldcs(a2 + k + 96);
+            const double2 x0 = x2[k], x1 = x2[k + 32], x2v = x2[k + 64], x3 = x2[k + 96];
+            acc = fma(a0.x, x0.x, fma(a0.y, x0.y, acc));
+            c1 = fma(a1.x, x1.x, fma(a1.y, x1.y, c1));
+            c2 = fma(a2v.x, x2v.x, fma(a2v.y, x2v.y, c2));
+            c3 = fma(a3.x, x3.x, fma(a3.y, x3.y, c3));
+        }
+        for (; k < n2; k += 32) {
             const double2 av = __ldcs(a2 + k), xv = x2[k];
             acc = fma(av.x, xv.x, fma(av.y, xv.y, acc));
         }
+        acc = (acc + c1) + (c2 + c3);
         if ((n & 1) && lane == 0) acc = fma(ar[n - 1], x[n - 1], acc);
     } else {
         for (int64_t k = lane; k < n; k += 32) acc = fma(ar[k], x[k], acc);
