@@ -239,17 +239,60 @@ __device__ __forceinline__ void factor64_regs(double (*sd)[kBase + 1], double (*
     __syncthreads();
 }
 
+// GENP of the 64x64 block in sd (lu.hpp:47-56 order) with a rolled loop: a
+// panel kernel runs this code once per CTA, so the fully unrolled
+// factor64_regs is instruction-fetch bound (~1.2k cycles per step). Thread t
+// owns row t>>1, columns of parity t&1, in a window that shifts by one pair of
+// columns per pair of steps, so the current column is always slot 0 (static
+// register indices only). Same operations in the same order.
+__device__ __forceinline__ void factor64_shift(double (*sd)[kBase + 1], double (*pbuf)[2 * kBase], int tid) {
+    const int row = tid >> 1, h = tid & 1;
+    double r[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) r[q] = sd[row][2 * q + h];
+#pragma unroll 1
+    for (int sp = 0; sp < kBase / 2; ++sp) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {  // step j = 2 sp + e
+            const int j = 2 * sp + e;
+            double* prow = pbuf[e];
+            if (row == j) {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) prow[2 * (sp + q) + h] = r[q];
+            }
+            __syncthreads();
+            const double pv = prow[j];
+            const double other = __shfl_xor_sync(kFull, r[0], 1);
+            const double colj = (h == e) ? r[0] : other;  // column j sits in slot 0 of parity e
+            const bool below = row > j;
+            const double l = below ? div_by(colj, pv, rcp64(pv)) : 0.0;  // multiplier (lu.hpp:51)
+            if (below && h == e) r[0] = l;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                if (q == 0 && !(h > e)) continue;  // columns 2(sp+q)+h > j only
+                r[q] = fma(-l, prow[2 * (sp + q) + h], r[q]);
+            }
+        }
+        sd[row][2 * sp + h] = r[0];  // column 2 sp + h is final
+#pragma unroll
+        for (int q = 0; q < 31; ++q) r[q] = r[q + 1];
+        r[31] = 0.0;
+        __syncthreads();  // both broadcast rows are rewritten in the next pair
+    }
+}
+
 __global__ void __launch_bounds__(PT)
 lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
                   double* __restrict__ piv_out, double* __restrict__ rinv_out) {
     __shared__ double sd[kBase][kBase + 1];
-    __shared__ __align__(16) double pbuf[2][kBase];
+    __shared__ __align__(16) double pbuf[2][2 * kBase];
     __shared__ double sp[kBase], sr[kBase];
     const int tid = threadIdx.x;
     double* d = a + c0 * lda + c0;
     for (int idx = tid; idx < kBase * kBase; idx += PT) sd[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
+    for (int idx = tid; idx < 4 * kBase; idx += PT) (&pbuf[0][0])[idx] = 0.0;
     __syncthreads();
-    factor64_regs(sd, pbuf, tid);
+    factor64_shift(sd, pbuf, tid);
     if (tid < kBase) {
         sp[tid] = sd[tid][tid];
         sr[tid] = 1.0 / sd[tid][tid];
