@@ -420,7 +420,16 @@ struct Shape {
 // shared-memory slot of element i: XOR swizzle of the 16-byte slot index so
 // that the stride-16 (last radix-16 pass) and stride-256 (digit-reversed
 // unpack) patterns hit distinct bank groups within a quarter-warp
-__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 4) ^ (i >> 8)) & 7); }
+// Specialised per length: the digit-reversed unpack varies bits L-4..L-2 of the
+// index (the top radix-16 digit); for L = 1 mod 4 the final radix-2 pass reads
+// stride-2 pairs, separated by folding bit 3 in as well.
+template <int L>
+__device__ __forceinline__ int swz(int i) {
+    constexpr int hi = L >= 8 ? L - 4 : 4;
+    int f = (i >> 4) ^ (i >> hi);
+    if (L % 4 == 1) f ^= (i >> 3) & 1;
+    return i ^ (f & 7);
+}
 
 // position of frequency k after the DIF passes: base-16 digit reversal
 template <int L>
@@ -456,15 +465,15 @@ __device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k
                     v[j] = {2 * q < k ? x[2 * q] : 0.0, 0.0};
                 }
             } else {
-                v[j] = z[swz(q)];
+                v[j] = z[swz<L>(q)];
             }
         }
         dft_reg<R, false>(v);
         cplx w[R];
         pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
-        z[swz(o + n0)] = v[0];
+        z[swz<L>(o + n0)] = v[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r) z[swz(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
+        for (int r = 1; r < R; ++r) z[swz<L>(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
     }
 }
 
@@ -484,9 +493,9 @@ __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, doub
         cplx w[R];
         pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
         cplx v[R];
-        v[0] = z[swz(o + n0)];
+        v[0] = z[swz<L>(o + n0)];
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmulc(z[swz(o + n0 + r * M)], w[r]);
+        for (int r = 1; r < R; ++r) v[r] = cmulc(z[swz<L>(o + n0 + r * M)], w[r]);
         dft_reg<R, true>(v);
 #pragma unroll
         for (int j = 0; j < R; ++j) {
@@ -499,7 +508,7 @@ __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, doub
                     y[2 * q] = t.x * scale;
                 }
             } else {
-                z[swz(q)] = t;
+                z[swz<L>(q)] = t;
             }
         }
     }
@@ -534,8 +543,8 @@ __device__ __forceinline__ void dit_down(cplx* z, double* y, int l, double scale
 template <int L>
 __device__ __forceinline__ void unpack_pair(const cplx* z, int k, const cplx* __restrict__ tw, cplx& xk, cplx& xmk) {
     constexpr int m = Shape<L>::m;
-    const cplx zk = z[swz(dif_pos<L>(k))];
-    const cplx zm = z[swz(dif_pos<L>((m - k) & (m - 1)))];
+    const cplx zk = z[swz<L>(dif_pos<L>(k))];
+    const cplx zm = z[swz<L>(dif_pos<L>((m - k) & (m - 1)))];
     const cplx e = {0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y)};
     const cplx o = {0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x)};
     if (k == 0) {
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(Shape<L>::T) spectrum_kernel(const double* __r
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* z = reinterpret_cast<cplx*>(smem_raw);
     constexpr int m = S::m, n = S::n;
-    for (int j = threadIdx.x; j < m; j += S::T) z[swz(j)] = {c[(n - 2 * j) % n], c[(n - 2 * j - 1) % n]};
+    for (int j = threadIdx.x; j < m; j += S::T) z[swz<L>(j)] = {c[(n - 2 * j) % n], c[(n - 2 * j - 1) % n]};
     __syncthreads();
     // first pass from shared memory: reuse dif<> with kGlobal = false
     dif<L, S::radix(0), S::sub(0), false>(z, nullptr, 0, tw);
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(Shape<L>::T, Shape<L>::minb)
         cplx xk, xmk;
         unpack_pair<L>(z, q, tw, xk, xmk);
         const cplx yk = cmul(spec[q], xk), ymk = cmul(spec[m - q], xmk);
-        const int pk = swz(dif_pos<L>(q)), pm = swz(dif_pos<L>((m - q) & (m - 1)));
+        const int pk = swz<L>(dif_pos<L>(q)), pm = swz<L>(dif_pos<L>((m - q) & (m - 1)));
         if (q == 0) {
             // Ee_0 = Y_0 + Y_m, Oo_0 = Y_0 - Y_m
             z[pk] = {(yk.x + ymk.x) - (yk.y - ymk.y), (yk.y + ymk.y) + (yk.x - ymk.x)};
