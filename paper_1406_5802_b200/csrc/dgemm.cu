@@ -26,7 +26,7 @@
 namespace rl {
 namespace {
 
-constexpr int BK = 16, THREADS = 256, GROUP_M = 8;
+constexpr int BK = 16, GROUP_M = 8;
 
 // Tile configurations. Big: 128x128 CTA tile, 8 warps of 64x32, one CTA per
 // SM (long-K products such as A*G). Small: 128x64 tile, 8 warps of 32x32,
@@ -39,7 +39,7 @@ struct Cfg {
     static constexpr int A_STAGE = BM * BK * 8, B_STAGE = BK * BN * 8;
     static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
     static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 64;
-    static_assert(WM * WN * 32 == THREADS, "8 warps");
+    static constexpr int THREADS = WM * WN * 32;
 };
 using BigCfg = Cfg<128, 128, 2, 4, 4, 1>;
 using SmallCfg = Cfg<128, 64, 4, 2, 4, 2>;
@@ -52,7 +52,7 @@ __device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 
 // low-rank residual A - Q (Q^T A) is never materialised). Split-K: blockIdx.y
 // takes k-tiles [y*ktc, (y+1)*ktc) and writes its partial at C + y*split_stride.
 template <class CF, bool kAccum, bool kStats, bool kStore>
-__global__ void __launch_bounds__(THREADS, CF::MINB)
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
              int64_t ldc, int M, int N, int K, double alpha, GemmStats* __restrict__ stats, int ktc,
              int64_t split_stride) {
@@ -236,7 +236,7 @@ template <class CF, bool A, bool S, bool T>
 void launch_cfg(dim3 grid, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, double* C, int64_t ldc, int m,
                 int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride) {
     configure_once<CF, A, S, T>();
-    dgemm_kernel<CF, A, S, T><<<grid, THREADS, CF::SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc,
+    dgemm_kernel<CF, A, S, T><<<grid, CF::THREADS, CF::SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc,
                                                                        split_stride);
 }
 
