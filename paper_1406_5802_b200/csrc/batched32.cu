@@ -641,13 +641,16 @@ __global__ void batch_summary_kernel(const double* __restrict__ r, const double*
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,
                                 double* lu, double* x, double* r, double* growth, int32_t* status, int refine,
                                 void* fix_ws) {
-    static bool configured = false;
-    if (!configured) {
-        RL_CUDA(cudaFuncSetAttribute(batched_genp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kMainSmemBytes)));
-        RL_CUDA(cudaFuncSetAttribute(verdict_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(sizeof(FixSmem) * WARPS)));
-        configured = true;
+    static PerDeviceOnce configured_once;
+    {
+        const rl_status cst = once_per_device(configured_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(batched_genp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMainSmemBytes)));
+            RL_CUDA(cudaFuncSetAttribute(verdict_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(FixSmem) * WARPS)));
+            return RL_OK;
+        });
+        if (cst != RL_OK) return cst;
     }
     if (batch == 0) return RL_OK;
     FixList* fix = static_cast<FixList*>(fix_ws);

@@ -224,12 +224,13 @@ EncodeFn encode_fn() {
 
 template <class CF, bool A, bool S, bool T>
 void configure_once() {
-    static bool done = false;
-    if (!done) {
-        cudaFuncSetAttribute(dgemm_kernel<CF, A, S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(CF::SMEM_BYTES));
-        done = true;
-    }
+    static PerDeviceOnce once;
+    once_per_device(once, [] {
+        return cudaFuncSetAttribute(dgemm_kernel<CF, A, S, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(CF::SMEM_BYTES)) == cudaSuccess
+                   ? RL_OK
+                   : RL_ERR_CUDA;  // a failure surfaces at the launch
+    });
 }
 
 template <class CF, bool A, bool S, bool T>

@@ -625,11 +625,14 @@ rl_status launch_L(rl_context* ctx, int64_t rows, int k, const double* a, int64_
                    const cplx* tw, cplx* spec, double* out, int64_t ldo, int l) {
     using S = Shape<L>;
     constexpr int smem = S::m * 16;
-    static bool configured = false;
-    if (!configured) {
-        RL_CUDA(cudaFuncSetAttribute(spectrum_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        RL_CUDA(cudaFuncSetAttribute(rows_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = true;
+    static PerDeviceOnce configured_once;
+    {
+        const rl_status cst = once_per_device(configured_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(spectrum_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            RL_CUDA(cudaFuncSetAttribute(rows_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            return RL_OK;
+        });
+        if (cst != RL_OK) return cst;
     }
     spectrum_kernel<L><<<1, S::T, smem, ctx->stream>>>(c, tw, spec);
     RL_CHECK_LAUNCH("r2c::spectrum_kernel");
@@ -697,13 +700,16 @@ rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a,
     if (st != RL_OK) return st;
     cplx* spec = static_cast<cplx*>(spec_ws);
     const int n = static_cast<int>(np);
-    static bool configured = false;
-    if (!configured) {
-        RL_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
-        RL_CUDA(cudaFuncSetAttribute(circ_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
-        RL_CUDA(cudaFuncSetAttribute(circ_rows_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
-        RL_CUDA(cudaFuncSetAttribute(spectrum_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
-        configured = true;
+    static PerDeviceOnce configured_once;
+    {
+        const rl_status cst = once_per_device(configured_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+            RL_CUDA(cudaFuncSetAttribute(circ_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+            RL_CUDA(cudaFuncSetAttribute(circ_rows_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+            RL_CUDA(cudaFuncSetAttribute(spectrum_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+            return RL_OK;
+        });
+        if (cst != RL_OK) return cst;
     }
     const bool aligned = (lda % 2 == 0) && (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);

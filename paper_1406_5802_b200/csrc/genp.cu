@@ -533,10 +533,13 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         ctx->stream = keep;
         return r;
     };
-    static bool inv_configured = false;
-    if (!inv_configured) {
-        RL_CUDA(cudaFuncSetAttribute(linv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem));
-        inv_configured = true;
+    static PerDeviceOnce inv_configured_once;
+    {
+        const rl_status cst = once_per_device(inv_configured_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(linv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem));
+            return RL_OK;
+        });
+        if (cst != RL_OK) return cst;
     }
     // per 64-block L11^-1 (32 KiB each), stream-ordered scratch
     double* inv = nullptr;

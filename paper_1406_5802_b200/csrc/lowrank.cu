@@ -237,10 +237,13 @@ rl_status chol_inv_blocked(rl_context* ctx, double* W, int64_t ldl, int64_t l, d
     double* tt = pt + l * ldl;    // T = X[0:J,0:J] R[0:J, J] (J x CB)
     RL_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), s));
     RL_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * l * ldl, s));
-    static bool configured = false;
-    if (!configured) {
-        RL_CUDA(cudaFuncSetAttribute(chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem));
-        configured = true;
+    static PerDeviceOnce configured_once;
+    {
+        const rl_status cst = once_per_device(configured_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(chol_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmem));
+            return RL_OK;
+        });
+        if (cst != RL_OK) return cst;
     }
     rl_status e;
     for (int64_t J = 0; J < l; J += CB) {

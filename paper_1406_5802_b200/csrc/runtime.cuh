@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <cstdarg>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -71,6 +72,25 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
     } while (0)
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// One-time per-device setup (kernel attributes such as the dynamic shared
+// memory limit are per device): runs f() the first time for the current
+// device, under a lock so that no caller launches before it has finished.
+struct PerDeviceOnce {
+    std::mutex mu;
+    uint64_t done = 0;
+};
+template <typename F>
+rl_status once_per_device(PerDeviceOnce& o, F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> lk(o.mu);
+    if (o.done & bit) return RL_OK;
+    const rl_status st = f();
+    if (st == RL_OK) o.done |= bit;
+    return st;
+}
 
 // Bump allocator over the context workspace for one call.
 struct Arena {
