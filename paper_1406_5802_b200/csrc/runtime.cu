@@ -44,11 +44,11 @@ static rl_status init_context(rl_context* c, int device) {
     RL_CUDA(cudaMalloc(&c->flags, c->flags_bytes));
     RL_CUDA(cudaMemset(c->flags, 0, c->flags_bytes));
     RL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->host_scalars), 4096, cudaHostAllocDefault));
-    // call-scoped scratch comes from cudaMallocAsync: keep the pool's memory
-    // mapped between calls instead of returning it at every synchronisation
+    // call-scoped scratch comes from cudaMallocAsync: keep up to 2 GiB of the
+    // pool mapped between calls instead of returning it at every synchronisation
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
+        uint64_t keep = uint64_t(2) << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     return RL_OK;
