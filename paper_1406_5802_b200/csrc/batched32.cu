@@ -170,7 +170,10 @@ struct __align__(16) MainSmem {
     double b[D];
 };
 constexpr size_t kMainSmemBytes = sizeof(MainSmem) * WARPS;
-constexpr int kMainCtasPerSm = 4;
+#ifndef RL_BATCH_CTAS
+#define RL_BATCH_CTAS 4
+#endif
+constexpr int kMainCtasPerSm = RL_BATCH_CTAS;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

@@ -281,9 +281,65 @@ __device__ __forceinline__ void factor64_shift(double (*sd)[kBase + 1], double (
     }
 }
 
+// X = L^-1 for the unit-lower part of a factored 64x64 block (strictly lower
+// entries of sd, implicit unit diagonal) by recursive doubling: the eight 8x8
+// diagonal blocks by forward substitution (one thread per column), then pairs
+// merge, inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 (B A^-1), C^-1]], at 8, 16
+// and 32, each product on DMMA 8x8x4 tiles (one warp per tile).
+constexpr int LDX = 66, LDT = 34;
+constexpr int kInvFusedSmem = (kBase * LDX + 32 * LDT) * 8;
+__device__ __forceinline__ void inv_unit_lower64(const double (*sd)[kBase + 1], double* __restrict__ X,
+                                                 double* __restrict__ T, int tid) {
+    for (int idx = tid; idx < kBase * LDX; idx += PT) X[idx] = 0.0;
+    __syncthreads();
+    if (tid < kBase) {
+        const int o = 8 * (tid >> 3), j = tid & 7;
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = i == j ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+#pragma unroll
+            for (int i = k + 1; i < 8; ++i) x[i] = fma(-sd[o + i][o + k], x[k], x[i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) X[(o + i) * LDX + o + j] = x[i];
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+#pragma unroll 1
+    for (int h = 8; h < kBase; h *= 2) {
+        const int tn = h / 8, tiles = (kBase / (2 * h)) * tn * tn;
+        // T = B A^-1 (B: rows [o+h, o+2h), cols [o, o+h) of L)
+        for (int t = warp; t < tiles; t += PT / 32) {
+            const int p = t / (tn * tn), ti = (t / tn) % tn, tj = t % tn, o = 2 * h * p;
+            double c0 = 0.0, c1 = 0.0;
+            for (int k = 0; k < h; k += 4)
+                dmma_884(c0, c1, sd[o + h + 8 * ti + fr][o + k + fc], X[(o + k + fc) * LDX + o + 8 * tj + fr]);
+            double* tr = T + (p * h + 8 * ti + fr) * LDT + 8 * tj + 2 * fc;
+            tr[0] = c0;
+            tr[1] = c1;
+        }
+        __syncthreads();
+        // X_off = -C^-1 T
+        for (int t = warp; t < tiles; t += PT / 32) {
+            const int p = t / (tn * tn), ti = (t / tn) % tn, tj = t % tn, o = 2 * h * p;
+            double c0 = 0.0, c1 = 0.0;
+            for (int k = 0; k < h; k += 4)
+                dmma_884(c0, c1, X[(o + h + 8 * ti + fr) * LDX + o + h + k + fc], T[(p * h + k + fc) * LDT + 8 * tj + fr]);
+            double* xr = X + (o + h + 8 * ti + fr) * LDX + o + 8 * tj + 2 * fc;
+            xr[0] = -c0;
+            xr[1] = -c1;
+        }
+        __syncthreads();
+    }
+}
+
+// linv_out != nullptr: one extra CTA (the last) writes L11^-1 (64x64, ld 64)
+// from its factored copy instead of doing rows, with kInvFusedSmem of dynamic
+// shared memory, concurrently with the L21 rows.
 __global__ void __launch_bounds__(PT)
 lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
-                  double* __restrict__ piv_out, double* __restrict__ rinv_out) {
+                  double* __restrict__ piv_out, double* __restrict__ rinv_out, double* __restrict__ linv_out) {
     __shared__ double sd[kBase][kBase + 1];
     __shared__ __align__(16) double pbuf[2][2 * kBase];
     __shared__ double sp[kBase], sr[kBase];
@@ -299,6 +355,12 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     }
     __syncthreads();
     const int b = blockIdx.x;
+    if (linv_out && b == static_cast<int>(gridDim.x) - 1) {
+        extern __shared__ double inv_smem[];
+        inv_unit_lower64(sd, inv_smem, inv_smem + kBase * LDX, tid);
+        for (int idx = tid; idx < kBase * kBase; idx += PT) linv_out[idx] = inv_smem[(idx >> 6) * LDX + (idx & 63)];
+        return;
+    }
     if (b == 0) {
         for (int idx = tid; idx < kBase * kBase; idx += PT) d[(idx >> 6) * lda + (idx & 63)] = sd[idx >> 6][idx & 63];
         if (tid < kBase) {
@@ -365,68 +427,6 @@ lu_u12_kernel(double* __restrict__ a, int64_t lda, int64_t c0, int64_t col_begin
         for (int i = k + 1; i < kBase; ++i) x[i] = fma(-sl[i][k], x[k], x[i]);
 #pragma unroll
     for (int i = 0; i < kBase; ++i) col[i * lda] = x[i];
-}
-
-// ---- L11^-1 of a factored 64x64 diagonal block (U12 as a GEMM) -----------
-// Recursive doubling on the unit-lower L11: the eight 8x8 diagonal blocks are
-// inverted by forward substitution (one thread per column), then pairs merge,
-// inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 (B A^-1), C^-1]], at 8, 16, 32.
-// One CTA, small rolled loops (a single CTA running fully unrolled 64-step
-// code is instruction-fetch bound). The U12 = L11^-1 A12 product then runs on
-// the DMMA GEMM instead of a latency-bound substitution kernel; keeping L21 by
-// substitution (U11^-1 loses an order of magnitude of residual on config 1).
-constexpr int IT = 256;
-constexpr int kInvSmem = 3 * kBase * (kBase + 1) * 8;
-__global__ void __launch_bounds__(IT)
-linv64_kernel(const double* __restrict__ a, int64_t lda, int64_t c0, double* __restrict__ linv) {
-    extern __shared__ double ism[];
-    double(*L)[kBase + 1] = reinterpret_cast<double(*)[kBase + 1]>(ism);
-    double(*X)[kBase + 1] = reinterpret_cast<double(*)[kBase + 1]>(ism + kBase * (kBase + 1));
-    double(*T)[kBase + 1] = reinterpret_cast<double(*)[kBase + 1]>(ism + 2 * kBase * (kBase + 1));
-    const int tid = threadIdx.x;
-    const double* d = a + c0 * lda + c0;
-    for (int idx = tid; idx < kBase * kBase; idx += IT) {
-        const int i = idx >> 6, j = idx & 63;
-        L[i][j] = j < i ? d[i * lda + j] : (i == j ? 1.0 : 0.0);
-        X[i][j] = 0.0;
-    }
-    __syncthreads();
-    if (tid < kBase) {  // level 0: column j of the inverse of diagonal block b (8x8)
-        const int b = tid >> 3, j = tid & 7, o = 8 * b;
-        double x[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = i == j ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < 7; ++k)
-#pragma unroll
-            for (int i = k + 1; i < 8; ++i) x[i] = fma(-L[o + i][o + k], x[k], x[i]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) X[o + i][o + j] = x[i];
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int h = 8; h < kBase; h *= 2) {
-        const int pairs = kBase / (2 * h), outs = pairs * h * h;
-        // T = B A^-1 for every pair (B: L rows [o+h, o+2h), cols [o, o+h))
-        for (int e = tid; e < outs; e += IT) {
-            const int p = e / (h * h), r = (e / h) % h, cidx = e % h, o = 2 * h * p;
-            double acc = 0.0;
-#pragma unroll 4
-            for (int k = cidx; k < h; ++k) acc = fma(L[o + h + r][o + k], X[o + k][o + cidx], acc);  // X_a lower
-            T[o + h + r][o + cidx] = acc;
-        }
-        __syncthreads();
-        // X_off = -C^-1 T
-        for (int e = tid; e < outs; e += IT) {
-            const int p = e / (h * h), r = (e / h) % h, cidx = e % h, o = 2 * h * p;
-            double acc = 0.0;
-#pragma unroll 4
-            for (int k = 0; k <= r; ++k) acc = fma(X[o + h + r][o + h + k], T[o + h + k][o + cidx], acc);  // X_c lower
-            X[o + h + r][o + cidx] = -acc;
-        }
-        __syncthreads();
-    }
-    for (int idx = tid; idx < kBase * kBase; idx += IT) linv[idx] = X[idx >> 6][idx & 63];
 }
 
 struct Ctx {
@@ -536,7 +536,7 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     static PerDeviceOnce inv_configured_once;
     {
         const rl_status cst = once_per_device(inv_configured_once, [&]() -> rl_status {
-            RL_CUDA(cudaFuncSetAttribute(linv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem));
+            RL_CUDA(cudaFuncSetAttribute(lu_panel64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvFusedSmem));
             return RL_OK;
         });
         if (cst != RL_OK) return cst;
@@ -555,10 +555,8 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     auto panel_l = [&](cudaStream_t sm, int64_t c0) -> rl_status {
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-        lu_panel64_kernel<<<blocks, PT, 0, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
+        lu_panel64_kernel<<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, linv(c0));
         RL_CHECK_LAUNCH("lu_panel64_kernel");
-        linv64_kernel<<<1, IT, kInvSmem, sm>>>(a, lda, c0, linv(c0));
-        RL_CHECK_LAUNCH("linv64_kernel");
         return RL_OK;
     };
     // U12 = L11^-1 A12 in place (each output column block reads only its own
@@ -650,7 +648,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         auto panel_l = [&](int64_t c0) -> rl_status {
             const int64_t rest = n - c0 - kBase;
             const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-            lu_panel64_kernel<<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
+            lu_panel64_kernel<<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr);
             RL_CHECK_LAUNCH("lu_panel64_kernel");
             return RL_OK;
         };
@@ -702,7 +700,8 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
     for (; c0 + kBase <= n; c0 += kBase) {
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>((rest + PT - 1) / PT);
-        lu_panel64_kernel<<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out);
+        lu_panel64_kernel<<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out,
+                                                                        nullptr);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         if (rest > 0) {
             st = gemm(ctx, rest, rest, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
