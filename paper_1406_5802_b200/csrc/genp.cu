@@ -15,6 +15,8 @@
 // unit-lower TRSM is recursive the same way down to a 64-row base kernel.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <vector>
 
 #include "device_common.cuh"
 #include "kernels.cuh"
@@ -200,48 +202,9 @@ trsm_lower_unit_kernel_dyn(const double* __restrict__ l, int64_t ldl, int w, dou
 // the trailing update A22 -= L21 U12 is one DMMA GEMM (K = 64).
 constexpr int PT = 128;  // threads per CTA
 
-// GENP of the 64x64 block in sd (lu.hpp:47-56 order), register-resident:
-// thread t owns row t>>1, columns of parity t&1 (32 values). The pivot row is
-// published through a double-buffered shared row (one barrier per step), the
-// multiplier's column value comes from the parity partner by shuffle. No
-// shared-memory read-after-write chains inside a step.
-__device__ __forceinline__ void factor64_regs(double (*sd)[kBase + 1], double (*pbuf)[kBase], int tid) {
-    const int row = tid >> 1, h = tid & 1;
-    double r[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) r[q] = sd[row][2 * q + h];
-#pragma unroll
-    for (int j = 0; j < kBase; ++j) {
-        double* prow = pbuf[j & 1];
-        if (row == j) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) prow[2 * q + h] = r[q];
-        }
-        __syncthreads();
-        const double pv = prow[j];
-        const double mine = r[j >> 1];
-        const double other = __shfl_xor_sync(kFull, mine, 1);
-        const double colj = (h == (j & 1)) ? mine : other;
-        const bool below = row > j;
-        const double l = below ? div_by(colj, pv, rcp64(pv)) : 0.0;  // multiplier (lu.hpp:51)
-        if (below && h == (j & 1)) r[j >> 1] = l;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            if (2 * q + 1 > j) {  // columns k = 2q + h > j (static bound first, parity at run time)
-                const int k = 2 * q + h;
-                if (k > j) r[q] = fma(-l, prow[k], r[q]);
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 32; ++q) sd[row][2 * q + h] = r[q];
-    __syncthreads();
-}
-
 // GENP of the 64x64 block in sd (lu.hpp:47-56 order) with a rolled loop: a
-// panel kernel runs this code once per CTA, so the fully unrolled
-// factor64_regs is instruction-fetch bound (~1.2k cycles per step). Thread t
+// panel kernel runs this code once per CTA, so a fully unrolled version is
+// instruction-fetch bound (~1.2k cycles per step). Thread t
 // owns row t>>1, columns of parity t&1, in a window that shifts by one pair of
 // columns per pair of steps, so the current column is always slot 0 (static
 // register indices only). Same operations in the same order.
@@ -287,7 +250,7 @@ __device__ __forceinline__ void factor64_shift(double (*sd)[kBase + 1], double (
 // merge, inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 (B A^-1), C^-1]], at 8, 16
 // and 32, each product on DMMA 8x8x4 tiles (one warp per tile).
 constexpr int LDX = 66, LDT = 34;
-constexpr int kInvFusedSmem = (kBase * LDX + 32 * LDT) * 8;
+constexpr int kInvFusedSmem = 2 * kBase * LDX * 8;  // X and Y (Y also the 32 x LDT merge scratch)
 __device__ __forceinline__ void inv_unit_lower64(const double (*sd)[kBase + 1], double* __restrict__ X,
                                                  double* __restrict__ T, int tid) {
     for (int idx = tid; idx < kBase * LDX; idx += PT) X[idx] = 0.0;
@@ -334,12 +297,40 @@ __device__ __forceinline__ void inv_unit_lower64(const double (*sd)[kBase + 1], 
     }
 }
 
-// linv_out != nullptr: one extra CTA (the last) writes L11^-1 (64x64, ld 64)
-// from its factored copy instead of doing rows, with kInvFusedSmem of dynamic
-// shared memory, concurrently with the L21 rows.
+// 8x8 tiles (ti0 + {0,1}, 0..7) of S = M N for 64x64 operands in shared
+// memory (M row-major with stride ldm, N with stride ldn), one warp
+__device__ __forceinline__ void mm64_rows2(const double* M, int ldm, const double* N, int ldn, int ti0, int lane,
+                                           double (&acc)[2][8][2]) {
+    const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < kBase; k += 4) {
+        double bf[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bf[j] = N[(k + fc) * ldn + 8 * j + fr];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double af = M[(8 * (ti0 + i) + fr) * ldm + k + fc];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af, bf[j]);
+        }
+    }
+}
+
+// inv128 != nullptr: one extra CTA (the last) builds this 64-column
+// sub-panel's share of the super-panel's 128x128 unit-lower inverse (ld 128)
+// from its factored copy, concurrently with the L21 rows, with kInvFusedSmem of
+// dynamic shared memory:
+//   half 0: [La^-1, 0] in rows 0..63
+//   half 1: [-Lb^-1 (L_ba La^-1), Lb^-1] in rows 64..127 (L_ba: rows c0.., the
+//           previous sub-panel's L21 columns; La^-1 from the half-0 launch)
+// so U12 of the super-panel is one K = 128 GEMM.
 __global__ void __launch_bounds__(PT)
 lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
-                  double* __restrict__ piv_out, double* __restrict__ rinv_out, double* __restrict__ linv_out) {
+                  double* __restrict__ piv_out, double* __restrict__ rinv_out, double* __restrict__ inv128, int half) {
     __shared__ double sd[kBase][kBase + 1];
     __shared__ __align__(16) double pbuf[2][2 * kBase];
     __shared__ double sp[kBase], sr[kBase];
@@ -355,10 +346,46 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     }
     __syncthreads();
     const int b = blockIdx.x;
-    if (linv_out && b == static_cast<int>(gridDim.x) - 1) {
+    if (inv128 && b == static_cast<int>(gridDim.x) - 1) {
         extern __shared__ double inv_smem[];
-        inv_unit_lower64(sd, inv_smem, inv_smem + kBase * LDX, tid);
-        for (int idx = tid; idx < kBase * kBase; idx += PT) linv_out[idx] = inv_smem[(idx >> 6) * LDX + (idx & 63)];
+        double* X = inv_smem;
+        double* Y = inv_smem + kBase * LDX;
+        inv_unit_lower64(sd, X, Y, tid);  // X = L^-1 of this block (Y as scratch)
+        double* dst = inv128 + half * (kBase * 128 + kBase);
+        for (int idx = tid; idx < kBase * kBase; idx += PT) dst[(idx >> 6) * 128 + (idx & 63)] = X[(idx >> 6) * LDX + (idx & 63)];
+        if (half == 0) {
+            for (int idx = tid; idx < kBase * kBase; idx += PT) inv128[(idx >> 6) * 128 + kBase + (idx & 63)] = 0.0;
+            return;
+        }
+        // off-diagonal block -Lb^-1 (L_ba La^-1)
+        const double* lba = a + c0 * lda + (c0 - kBase);
+        for (int idx = tid; idx < kBase * kBase; idx += PT) {
+            const int i = idx >> 6, k = idx & 63;
+            sd[i][k] = lba[i * lda + k];
+            Y[i * LDX + k] = inv128[i * 128 + k];
+        }
+        __syncthreads();
+        const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+        double acc[2][8][2];
+        mm64_rows2(&sd[0][0], kBase + 1, Y, LDX, 2 * warp, lane, acc);  // T = L_ba La^-1
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                sd[8 * (2 * warp + i) + fr][8 * j + 2 * fc] = acc[i][j][0];
+                sd[8 * (2 * warp + i) + fr][8 * j + 2 * fc + 1] = acc[i][j][1];
+            }
+        __syncthreads();
+        mm64_rows2(X, LDX, &sd[0][0], kBase + 1, 2 * warp, lane, acc);  // Lb^-1 T
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                double* o = inv128 + (kBase + 8 * (2 * warp + i) + fr) * 128 + 8 * j + 2 * fc;
+                o[0] = -acc[i][j][0];
+                o[1] = -acc[i][j][1];
+            }
         return;
     }
     if (b == 0) {
@@ -508,8 +535,38 @@ rl_status rec(const Ctx& g, int64_t c0, int64_t w) {
 //   lo: U12(s) for the trailing columns -> GEMM_b(s) (all later columns)
 // factor_super(c0): panel_L(c0); U12 of the first half onto the second half's
 // 64 columns; their K = 64 update; panel_L(c0 + 64).
-// U12(s) = L11^-1 A12 with the 128x128 unit-lower L11 in two 64-row steps:
-// top = La^-1 A12_top; A12_bot -= L_ba top (K = 64 GEMM); bot = Lb^-1 A12_bot.
+// U12(s) = L11^-1 A12 is one K = 128 GEMM with the super-panel's 128x128
+// unit-lower inverse, assembled by the two panel launches' extra CTAs.
+#ifdef RL_GENP_TRACE
+// developer timeline of the lookahead schedule (never in the product build):
+// one-thread kernels stamp %globaltimer into a managed buffer
+__global__ void stamp_kernel(unsigned long long* slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *slot = t;
+}
+struct GenpTrace {
+    unsigned long long* buf = nullptr;
+    std::vector<int> tags;
+    GenpTrace() { cudaMallocManaged(&buf, 8 * 4096); }
+    void mark(int tag, cudaStream_t s) {
+        if (tags.size() >= 4096) return;
+        stamp_kernel<<<1, 1, 0, s>>>(buf + tags.size());
+        tags.push_back(tag);
+    }
+    ~GenpTrace() {
+        cudaDeviceSynchronize();
+        for (size_t i = 0; i < tags.size(); ++i)
+            std::fprintf(stderr, "T %d %.1f\n", tags[i], (buf[i] - buf[0]) * 1e-3);
+        cudaFree(buf);
+    }
+};
+#define TRACE(tag, s) trace.mark(tag, s)
+#else
+#define TRACE(tag, s) \
+    do {              \
+    } while (0)
+#endif
 static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out,
                                double* rinv_out) {
     constexpr int64_t W = 2 * kBase;
@@ -541,44 +598,52 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         });
         if (cst != RL_OK) return cst;
     }
-    // per 64-block L11^-1 (32 KiB each), stream-ordered scratch
+    // per super-panel 128x128 unit-lower L11^-1 (128 KiB each, ld 128; the
+    // ragged tail's 64-column step uses the top-left block of one more),
+    // stream-ordered scratch
     double* inv = nullptr;
-    RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&inv), sizeof(double) * kBase * kBase * (n / kBase), lo));
+    RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&inv), sizeof(double) * W * W * (S + 1), lo));
     struct Free {
         double* p;
         cudaStream_t s;
         ~Free() { cudaFreeAsync(p, s); }
     } inv_guard{inv, lo};
-    auto linv = [&](int64_t c0) { return inv + (c0 / kBase) * kBase * kBase; };
-    // panel: factor the diagonal block and L21 = A21 U11^-1 by substitution,
-    // then L11^-1 for the U12 GEMMs
+    auto inv_of = [&](int64_t c0) { return inv + (c0 / W) * W * W; };  // super-panel containing column c0
+    // panel: factor the diagonal block and L21 = A21 U11^-1 by substitution;
+    // the extra CTA fills this half of the super-panel's L11^-1
     auto panel_l = [&](cudaStream_t sm, int64_t c0) -> rl_status {
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-        lu_panel64_kernel<<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, linv(c0));
+        lu_panel64_kernel<<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0),
+                                                                  static_cast<int>((c0 / kBase) & 1));
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         return RL_OK;
     };
-    // U12 = L11^-1 A12 in place (each output column block reads only its own
-    // input block, all of it, before any store)
-    auto u12 = [&](cudaStream_t sm, int64_t r0, int64_t cb, int64_t ncols) -> rl_status {
+    // U12 = L11^-1 A12 in place for rows [r0, r0 + rows), rows = 64 (the
+    // top-left block) or 128 (the whole super-panel inverse): one CTA tile row,
+    // so each output column block reads all of its own input before any store
+    auto u12 = [&](cudaStream_t sm, int64_t r0, int64_t rows, int64_t cb, int64_t ncols) -> rl_status {
         if (ncols <= 0) return RL_OK;
         cudaStream_t keep = ctx->stream;
         ctx->stream = sm;
-        const rl_status r = gemm(ctx, kBase, ncols, kBase, linv(r0), kBase, at(r0, cb), lda, at(r0, cb), lda, 1.0,
-                                 false, nullptr);
+        const rl_status r =
+            gemm(ctx, rows, ncols, rows, inv_of(r0), W, at(r0, cb), lda, at(r0, cb), lda, 1.0, false, nullptr);
         ctx->stream = keep;
         return r;
     };
     auto factor_super = [&](cudaStream_t sm, int64_t c0) -> rl_status {
         rl_status r;
         if ((r = panel_l(sm, c0)) != RL_OK) return r;
-        if ((r = u12(sm, c0, c0 + kBase, kBase)) != RL_OK) return r;
+        if ((r = u12(sm, c0, kBase, c0 + kBase, kBase)) != RL_OK) return r;
         if ((r = update(sm, n - c0 - kBase, kBase, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase),
                         at(c0 + kBase, c0 + kBase))) != RL_OK)
             return r;
         return panel_l(sm, c0 + kBase);
     };
+#ifdef RL_GENP_TRACE
+    GenpTrace trace;
+#endif
+    TRACE(0, lo);
     RL_CUDA(cudaEventRecord(ev[0], lo));  // prior work on the caller's stream
     RL_CUDA(cudaStreamWaitEvent(hi, ev[0], 0));
     if ((st = factor_super(hi, 0)) != RL_OK) return st;
@@ -589,24 +654,26 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         if (rest <= 0) break;
         // lo: U12 of this super-panel for every trailing column
         RL_CUDA(cudaStreamWaitEvent(lo, el, 0));
-        if ((st = u12(lo, c0, c0 + W, rest)) != RL_OK) return st;
-        if ((st = update(lo, kBase, rest, kBase, at(c0 + kBase, c0), at(c0, c0 + W), at(c0 + kBase, c0 + W))) != RL_OK)
-            return st;
-        if ((st = u12(lo, c0 + kBase, c0 + W, rest)) != RL_OK) return st;
+        TRACE(1, lo);
+        if ((st = u12(lo, c0, W, c0 + W, rest)) != RL_OK) return st;
         cudaEvent_t eu = next_event();
         RL_CUDA(cudaEventRecord(eu, lo));
         const bool next_full = sp + 1 < S;
         // hi: GEMM_a(s) -> factor_super(s+1)
         RL_CUDA(cudaStreamWaitEvent(hi, eu, 0));
+        TRACE(2, lo);
         if (next_full) {
             if ((st = update(hi, rest, W, W, at(c0 + W, c0), at(c0, c0 + W), at(c0 + W, c0 + W))) != RL_OK) return st;
+            TRACE(3, hi);
             if ((st = factor_super(hi, c0 + W)) != RL_OK) return st;
+            TRACE(4, hi);
             el = next_event();
             RL_CUDA(cudaEventRecord(el, hi));
         }
         // lo: GEMM_b(s) on the remaining columns (all of them before the tail)
         const int64_t cb = next_full ? c0 + 2 * W : c0 + W;
         if ((st = update(lo, rest, n - cb, W, at(c0 + W, c0), at(c0, cb), at(c0 + W, cb))) != RL_OK) return st;
+        TRACE(5, lo);
     }
     RL_CUDA(cudaEventRecord(ev[1], hi));
     RL_CUDA(cudaStreamWaitEvent(lo, ev[1], 0));
@@ -615,7 +682,7 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     if (n - c0 >= kBase) {
         if ((st = panel_l(lo, c0)) != RL_OK) return st;
         const int64_t rest = n - c0 - kBase;
-        if ((st = u12(lo, c0, c0 + kBase, rest)) != RL_OK) return st;
+        if ((st = u12(lo, c0, kBase, c0 + kBase, rest)) != RL_OK) return st;
         if ((st = update(lo, rest, rest, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase), at(c0 + kBase, c0 + kBase))) !=
             RL_OK)
             return st;
@@ -648,7 +715,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         auto panel_l = [&](int64_t c0) -> rl_status {
             const int64_t rest = n - c0 - kBase;
             const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-            lu_panel64_kernel<<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr);
+            lu_panel64_kernel<<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr, 0);
             RL_CHECK_LAUNCH("lu_panel64_kernel");
             return RL_OK;
         };
@@ -701,7 +768,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>((rest + PT - 1) / PT);
         lu_panel64_kernel<<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out,
-                                                                        nullptr);
+                                                                        nullptr, 0);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         if (rest > 0) {
             st = gemm(ctx, rest, rest, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
