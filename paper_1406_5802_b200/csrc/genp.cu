@@ -204,10 +204,13 @@ constexpr int PT = 128;  // threads per CTA
 
 // GENP of the 64x64 block in sd (lu.hpp:47-56 order) with a rolled loop: a
 // panel kernel runs this code once per CTA, so a fully unrolled version is
-// instruction-fetch bound (~1.2k cycles per step). Thread t
-// owns row t>>1, columns of parity t&1, in a window that shifts by one pair of
-// columns per pair of steps, so the current column is always slot 0 (static
-// register indices only). Same operations in the same order.
+// instruction-fetch bound (~1.2k cycles per step). Thread t owns row t>>1,
+// columns of parity t&1, in a window that shifts by one pair of columns per
+// pair of steps, so the current columns always sit in slot 0 (static register
+// indices only). Two steps per barrier: the owners of rows j0 = 2sp and
+// j1 = 2sp+1 publish both rows, and every thread forms row j1's step-j0 update
+// for its parity half itself (the same FMAs the owner performs), so the
+// factors are bit-identical to one step per barrier.
 __device__ __forceinline__ void factor64_shift(double (*sd)[kBase + 1], double (*pbuf)[2 * kBase], int tid) {
     const int row = tid >> 1, h = tid & 1;
     double r[32];
@@ -215,33 +218,52 @@ __device__ __forceinline__ void factor64_shift(double (*sd)[kBase + 1], double (
     for (int q = 0; q < 32; ++q) r[q] = sd[row][2 * q + h];
 #pragma unroll 1
     for (int sp = 0; sp < kBase / 2; ++sp) {
+        const int j0 = 2 * sp, j1 = j0 + 1;
+        // [0, 64): row j0, [64, 128): row j1, each as window-relative parity
+        // halves ([32 h + q] = column 2 (sp + q) + h). Buffer sp & 1 is
+        // rewritten two pairs later, after every reader passed a barrier.
+        double* pb = pbuf[sp & 1];
+        if (row == j0 || row == j1) {
+            double2* dst = reinterpret_cast<double2*>(pb + (row == j1 ? 64 : 0) + 32 * h);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {  // step j = 2 sp + e
-            const int j = 2 * sp + e;
-            double* prow = pbuf[e];
-            if (row == j) {
-#pragma unroll
-                for (int q = 0; q < 32; ++q) prow[2 * (sp + q) + h] = r[q];
-            }
-            __syncthreads();
-            const double pv = prow[j];
-            const double other = __shfl_xor_sync(kFull, r[0], 1);
-            const double colj = (h == e) ? r[0] : other;  // column j sits in slot 0 of parity e
-            const bool below = row > j;
-            const double l = below ? div_by(colj, pv, rcp64(pv)) : 0.0;  // multiplier (lu.hpp:51)
-            if (below && h == e) r[0] = l;
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                if (q == 0 && !(h > e)) continue;  // columns 2(sp+q)+h > j only
-                r[q] = fma(-l, prow[2 * (sp + q) + h], r[q]);
-            }
+            for (int m = 0; m < 16; ++m) dst[m] = make_double2(r[2 * m], r[2 * m + 1]);
         }
+        __syncthreads();
+        const double pv0 = pb[0];                    // u(j0, j0): parity 0, slot 0
+        const double rinv0 = rcp64(pv0);
+        const double l10 = div_by(pb[64], pv0, rinv0);  // row j1's multiplier at step j0 (lu.hpp:51)
+        const double pv1 = fma(-l10, pb[32], pb[96]);   // u(j1, j1) after step j0 (lu.hpp:53)
+        const double rinv1 = rcp64(pv1);
+        const bool below0 = row > j0, below1 = row > j1;
+        const double other0 = __shfl_xor_sync(kFull, r[0], 1);
+        const double l0 = below0 ? div_by(h == 0 ? r[0] : other0, pv0, rinv0) : 0.0;
+        if (below0 && h == 0) r[0] = l0;
+        const double2* A = reinterpret_cast<const double2*>(pb + 32 * h);
+        const double2* B = reinterpret_cast<const double2*>(pb + 64 + 32 * h);
+        double bp[32];  // row j1 after step j0, this parity
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const double2 av = A[m], bv = B[m];
+            if (m > 0 || h > 0) {  // columns > j0: all but slot 0 of parity 0
+                r[2 * m] = fma(-l0, av.x, r[2 * m]);
+                bp[2 * m] = fma(-l10, av.x, bv.x);
+            } else {
+                bp[0] = bv.x;
+            }
+            r[2 * m + 1] = fma(-l0, av.y, r[2 * m + 1]);
+            bp[2 * m + 1] = fma(-l10, av.y, bv.y);
+        }
+        const double other1 = __shfl_xor_sync(kFull, r[0], 1);
+        const double l1 = below1 ? div_by(h == 1 ? r[0] : other1, pv1, rinv1) : 0.0;
+        if (below1 && h == 1) r[0] = l1;
+#pragma unroll
+        for (int q = 1; q < 32; ++q) r[q] = fma(-l1, bp[q], r[q]);  // slot 0 holds columns j0, j1 only
         sd[row][2 * sp + h] = r[0];  // column 2 sp + h is final
 #pragma unroll
         for (int q = 0; q < 31; ++q) r[q] = r[q + 1];
         r[31] = 0.0;
-        __syncthreads();  // both broadcast rows are rewritten in the next pair
     }
+    __syncthreads();
 }
 
 // X = L^-1 for the unit-lower part of a factored 64x64 block (strictly lower
@@ -297,6 +319,9 @@ __device__ __forceinline__ void inv_unit_lower64(const double (*sd)[kBase + 1], 
     }
 }
 
+#ifdef RL_PANEL_PHASES
+__device__ unsigned long long g_panel_phase[4];
+#endif
 // 8x8 tiles (ti0 + {0,1}, 0..7) of S = M N for 64x64 operands in shared
 // memory (M row-major with stride ldm, N with stride ldn), one warp
 __device__ __forceinline__ void mm64_rows2(const double* M, int ldm, const double* N, int ldn, int ti0, int lane,
@@ -335,10 +360,16 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     __shared__ __align__(16) double pbuf[2][2 * kBase];
     __shared__ double sp[kBase], sr[kBase];
     const int tid = threadIdx.x;
+#ifdef RL_PANEL_PHASES
+    const long long t0 = clock64();
+#endif
     double* d = a + c0 * lda + c0;
     for (int idx = tid; idx < kBase * kBase; idx += PT) sd[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
     for (int idx = tid; idx < 4 * kBase; idx += PT) (&pbuf[0][0])[idx] = 0.0;
     __syncthreads();
+#ifdef RL_PANEL_PHASES
+    const long long t1 = clock64();
+#endif
     factor64_shift(sd, pbuf, tid);
     if (tid < kBase) {
         sp[tid] = sd[tid][tid];
@@ -346,6 +377,14 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     }
     __syncthreads();
     const int b = blockIdx.x;
+#ifdef RL_PANEL_PHASES
+    const long long t2 = clock64();
+    if (tid == 0 && b == 0) {
+        atomicExch(&g_panel_phase[0], static_cast<unsigned long long>(t1 - t0));
+        atomicExch(&g_panel_phase[1], static_cast<unsigned long long>(t2 - t1));
+        atomicExch(&g_panel_phase[3], 1ull);
+    }
+#endif
     if (inv128 && b == static_cast<int>(gridDim.x) - 1) {
         extern __shared__ double inv_smem[];
         double* X = inv_smem;
@@ -415,6 +454,9 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
         }
 #pragma unroll
         for (int m = 0; m < kBase / 2; ++m) rowp[m] = make_double2(x[2 * m], x[2 * m + 1]);
+#ifdef RL_PANEL_PHASES
+        if (tid == 0 && b == 0) atomicExch(&g_panel_phase[2], static_cast<unsigned long long>(clock64() - t2));
+#endif
     } else {
         const int64_t c = c0 + kBase + static_cast<int64_t>(b - row_ctas) * PT + tid;
         if (c - c0 - kBase >= rest) return;
@@ -556,6 +598,12 @@ struct GenpTrace {
     }
     ~GenpTrace() {
         cudaDeviceSynchronize();
+#ifdef RL_PANEL_PHASES
+        unsigned long long ph[4];
+        cudaMemcpyFromSymbol(ph, g_panel_phase, sizeof(ph));
+        std::fprintf(stderr, "P load %.0f factor %.0f rows %.0f cycles per launch (%llu)\n", double(ph[0]) / ph[3],
+                     double(ph[1]) / ph[3], double(ph[2]) / ph[3], ph[3]);
+#endif
         for (size_t i = 0; i < tags.size(); ++i)
             std::fprintf(stderr, "T %d %.1f\n", tags[i], (buf[i] - buf[0]) * 1e-3);
         cudaFree(buf);
@@ -631,18 +679,21 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         ctx->stream = keep;
         return r;
     };
-    auto factor_super = [&](cudaStream_t sm, int64_t c0) -> rl_status {
-        rl_status r;
-        if ((r = panel_l(sm, c0)) != RL_OK) return r;
-        if ((r = u12(sm, c0, kBase, c0 + kBase, kBase)) != RL_OK) return r;
-        if ((r = update(sm, n - c0 - kBase, kBase, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase),
-                        at(c0 + kBase, c0 + kBase))) != RL_OK)
-            return r;
-        return panel_l(sm, c0 + kBase);
-    };
 #ifdef RL_GENP_TRACE
     GenpTrace trace;
 #endif
+    auto factor_super = [&](cudaStream_t sm, int64_t c0) -> rl_status {
+        rl_status r;
+        if ((r = panel_l(sm, c0)) != RL_OK) return r;
+        TRACE(6, sm);
+        if ((r = u12(sm, c0, kBase, c0 + kBase, kBase)) != RL_OK) return r;
+        TRACE(7, sm);
+        if ((r = update(sm, n - c0 - kBase, kBase, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase),
+                        at(c0 + kBase, c0 + kBase))) != RL_OK)
+            return r;
+        TRACE(8, sm);
+        return panel_l(sm, c0 + kBase);
+    };
     TRACE(0, lo);
     RL_CUDA(cudaEventRecord(ev[0], lo));  // prior work on the caller's stream
     RL_CUDA(cudaStreamWaitEvent(hi, ev[0], 0));
