@@ -105,6 +105,8 @@ __device__ __forceinline__ void dft_reg(cplx (&v)[R]) {
                 v[base + j] = cadd(a, b);
                 if (j == 0) {
                     v[base + j + half] = d;
+                } else if (j * 2 == half) {  // w = i: a swap and a sign (the FMA form would not fold the 0 and 1)
+                    v[base + j + half] = kInv ? cplx{d.y, -d.x} : cplx{-d.y, d.x};
                 } else {
                     const cplx w = wconst(2 * half, j);  // w_{2 half}^j
                     v[base + j + half] = kInv ? cmulc(d, w) : cmul(d, w);
@@ -135,6 +137,25 @@ __device__ __forceinline__ void pass_twiddles(cplx (&w)[R], const cplx* __restri
 #pragma unroll
     for (int r = 3; r < R; ++r) {
         if (r == 4 || r == 8) continue;
+        const int hi = r >= 8 ? 8 : (r >= 4 ? 4 : 2);
+        w[r] = cmul(w[hi], w[r - hi]);
+    }
+}
+
+// the same twiddles formed lazily: base_twiddles loads r = 1, 2, 4, 8 and
+// lazy_twiddle(w, r) forms w[r] = w[hi] w[r - hi] just before its first use
+// (the products of pass_twiddles, in the same order), so the fifteen values
+// are not all live at once
+template <int R>
+__device__ __forceinline__ void base_twiddles(cplx (&w)[R], const cplx* __restrict__ tw, int64_t base, int64_t mask) {
+    if (R > 1) w[1] = tw[base & mask];
+    if (R > 2) w[2] = tw[(2 * base) & mask];
+    if (R > 4) w[4] = tw[(4 * base) & mask];
+    if (R > 8) w[8] = tw[(8 * base) & mask];
+}
+template <int R>
+__device__ __forceinline__ void lazy_twiddle(cplx (&w)[R], int r) {
+    if (r >= 3 && r != 4 && r != 8) {
         const int hi = r >= 8 ? 8 : (r >= 4 ? 4 : 2);
         w[r] = cmul(w[hi], w[r - hi]);
     }
@@ -411,8 +432,17 @@ struct Shape {
     static constexpr int m = 1 << L, n = 2 * m;
     static constexpr int full = L / 4, rem = L % 4;
     static constexpr int passes = full + (rem ? 1 : 0);
-    static constexpr int T = L >= 13 ? 512 : 256;  // threads per CTA
-    static constexpr int minb = L >= 13 ? 1 : 2;
+#ifndef RL_FFT_T13
+#define RL_FFT_T13 512
+#endif
+#ifndef RL_FFT_T12
+#define RL_FFT_T12 256
+#endif
+#ifndef RL_FFT_MINB12
+#define RL_FFT_MINB12 2
+#endif
+    static constexpr int T = L >= 13 ? RL_FFT_T13 : RL_FFT_T12;  // threads per CTA
+    static constexpr int minb = L >= 13 ? 1 : RL_FFT_MINB12;
     __host__ __device__ static constexpr int radix(int p) { return p < full ? 16 : 1 << rem; }
     __host__ __device__ static constexpr int sub(int p) { return m >> (4 * p); }  // subarray length entering pass p
 };
@@ -468,12 +498,15 @@ __device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k
                 v[j] = z[swz<L>(q)];
             }
         }
-        dft_reg<R, false>(v);
         cplx w[R];
-        pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+        base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+        dft_reg<R, false>(v);
         z[swz<L>(o + n0)] = v[0];
 #pragma unroll
-        for (int r = 1; r < R; ++r) z[swz<L>(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
+        for (int r = 1; r < R; ++r) {
+            lazy_twiddle<R>(w, r);
+            z[swz<L>(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
+        }
     }
 }
 
@@ -491,11 +524,14 @@ __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, doub
         if (groups % S::T != 0 && g >= groups) break;
         const int n0 = g % M, o = (g / M) * N;
         cplx w[R];
-        pass_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+        base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
         cplx v[R];
         v[0] = z[swz<L>(o + n0)];
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmulc(z[swz<L>(o + n0 + r * M)], w[r]);
+        for (int r = 1; r < R; ++r) {
+            lazy_twiddle<R>(w, r);
+            v[r] = cmulc(z[swz<L>(o + n0 + r * M)], w[r]);
+        }
         dft_reg<R, true>(v);
 #pragma unroll
         for (int j = 0; j < R; ++j) {
