@@ -20,14 +20,21 @@
 // Residual R = A - Q (Q^T A) (association of lowrank.hpp:35-37): B = Q^T A by
 //   split-K GEMM; ||R||_F from a GEMM epilogue that never stores R; ||R||_2 by
 //   the restated power iteration of norms.hpp:52-77 applied to the implicit
-//   operator R v = A v - Q (B v), R^T u = A^T u - B^T (Q^T u).
+//   operator R v = A v - Q (B v), R^T u = A^T u - B^T (Q^T u), each step one
+//   read of A (power_pass_kernel: thread-block clusters exchanging per-row
+//   partial dot products through distributed shared memory).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "device_common.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 extern "C" RL_API rl_status rl_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out);
 extern "C" RL_API rl_status rl_gen_real_circulant_column(int64_t n, uint64_t seed, double* out);
@@ -392,6 +399,161 @@ static rl_status gemvt(rl_context* ctx, int64_t m, int64_t n, const double* a, i
     return RL_OK;
 }
 
+// ---- one pass over A per power step ------------------------------------
+// u = R x = A x - Q t (t = B x) and the partial sums of A^T u, Q^T u and
+// ||u||^2 in a single read of A: a cluster of kPC CTAs (one per SM) owns a
+// range of rows, each CTA a quarter of the columns in registers (x, its share
+// of A^T u, the rows in flight). Per pair of rows the CTAs exchange their
+// partial dot products through distributed shared memory, so every CTA forms
+// the same u_i (ranks summed in order) before accumulating u_i a_i.
+#ifndef RL_PW_ROWS
+#define RL_PW_ROWS 4
+#endif
+#ifndef RL_PW_AHEAD
+#define RL_PW_AHEAD 1
+#endif
+constexpr int kPT = 512, kPC = 4, kPR = RL_PW_ROWS;  // threads, cluster CTAs, rows per exchange
+constexpr int kPA = RL_PW_AHEAD;                      // exchanges of rows prefetched into L2 ahead
+namespace cg = cooperative_groups;
+
+// remote store of one double into CTA `rank`'s shared memory that completes
+// 8 bytes of that CTA's mbarrier transaction count (no cluster barrier)
+__device__ __forceinline__ void st_async_f64(double* local_slot, uint64_t* local_bar, unsigned rank, double v) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_slot)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(local_bar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
+                 "l"(__double_as_longlong(v)), "r"(rb)
+                 : "memory");
+}
+
+template <int NP>  // double2 column pairs per thread: the cluster covers kPC * kPT * 2 * NP columns
+__global__ void __cluster_dims__(kPC, 1, 1) __launch_bounds__(kPT, 1)
+power_pass_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int64_t n, const double* __restrict__ q,
+                  int64_t ldq, int l, const double* __restrict__ x, const double* __restrict__ t,
+                  int64_t rows_per_cluster, double* __restrict__ ypart, double* __restrict__ spart,
+                  double* __restrict__ sqpart) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int64_t cl = blockIdx.x / kPC;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double red[2][kPR][kPT / 32];
+    __shared__ __align__(8) double xch[2][kPC][kPR];
+    __shared__ __align__(8) uint64_t xbar[2];  // exchange parity p lands when kPC * kPR * 8 bytes arrived
+    if (tid == 0) {
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        mbar_fence_init();
+    }
+    cluster.sync();  // barriers initialised before any peer signals them
+    const int64_t c0 = static_cast<int64_t>(rank) * kPT * 2 * NP;  // first column of this CTA
+    double2 xv[NP], yv[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        const int64_t c = c0 + 2 * (tid + static_cast<int64_t>(kPT) * k);
+        xv[k] = c < n ? *reinterpret_cast<const double2*>(x + c) : make_double2(0.0, 0.0);
+        yv[k] = make_double2(0.0, 0.0);
+    }
+    const bool qlane = rank == 0 && tid < l;
+    const double tq = qlane ? t[tid] : 0.0;
+    double sacc = 0.0, usq = 0.0;
+    const int64_t r0 = cl * rows_per_cluster, r1 = std::min<int64_t>(m, r0 + rows_per_cluster);
+    int par = 0;
+    for (int64_t i = r0; i < r1; i += kPR, par ^= 1) {
+        if (tid == 0 && i + kPA * kPR < r1)  // rows kPA exchanges ahead into L2
+            for (int r = 0; r < kPR; ++r) {
+                const double* nx = a + (i + kPA * kPR + r) * lda + c0;
+                const int64_t bytes = std::min<int64_t>(n - c0, static_cast<int64_t>(kPT) * 2 * NP) * 8;
+                if (bytes > 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(nx), "r"(static_cast<unsigned>(bytes & ~15ll)));
+            }
+        double2 av[kPR][NP];
+        double qv[kPR], d[kPR];
+#pragma unroll
+        for (int r = 0; r < kPR; ++r) {
+            const bool live = i + r < r1;
+            const double* row = a + (i + r) * lda;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const int64_t c = c0 + 2 * (tid + static_cast<int64_t>(kPT) * k);
+                av[r][k] = live && c < n ? __ldcs(reinterpret_cast<const double2*>(row + c)) : make_double2(0.0, 0.0);
+            }
+            qv[r] = live && qlane ? q[(i + r) * ldq + tid] : 0.0;
+            double acc = -qv[r] * tq;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) acc = fma(av[r][k].x, xv[k].x, fma(av[r][k].y, xv[k].y, acc));
+            d[r] = warp_sum(acc);
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int r = 0; r < kPR; ++r) red[par][r][warp] = d[r];
+        if (tid == 0) mbar_expect_tx(&xbar[par], kPC * kPR * 8);
+        __syncthreads();
+        if (tid < kPR) {  // this CTA's partial of row i + tid, to every CTA of the cluster
+            double v = 0.0;
+            for (int w = 0; w < kPT / 32; ++w) v += red[par][tid][w];
+            for (int dst = 0; dst < kPC; ++dst) st_async_f64(&xch[par][rank][tid], &xbar[par], dst, v);
+        }
+        // a peer writes slot par again only after this CTA's next exchange reached it,
+        // which follows these reads in program order
+        mbar_wait(&xbar[par], static_cast<uint32_t>(((i - r0) / kPR >> 1) & 1));
+#pragma unroll
+        for (int r = 0; r < kPR; ++r) {
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < kPC; ++c) v += xch[par][c][r];
+            usq = fma(v, v, usq);
+            sacc = fma(v, qv[r], sacc);
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                yv[k].x = fma(v, av[r][k].x, yv[k].x);
+                yv[k].y = fma(v, av[r][k].y, yv[k].y);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        const int64_t c = c0 + 2 * (tid + static_cast<int64_t>(kPT) * k);
+        if (c < n) *reinterpret_cast<double2*>(ypart + cl * n + c) = yv[k];
+    }
+    if (qlane) spart[cl * l + tid] = sacc;
+    if (rank == 0 && tid == 0) sqpart[cl] = usq;
+    cluster.sync();  // no CTA leaves while a peer may still write its exchange slots
+}
+
+// y = sum over clusters of the partial A^T u (and s = Q^T u, ||u||^2), fixed order
+__global__ void power_reduce_kernel(const double* __restrict__ ypart, const double* __restrict__ spart,
+                                    const double* __restrict__ sqpart, int clusters, int64_t n, int l,
+                                    double* __restrict__ y, double* __restrict__ s, double* __restrict__ usq) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c < n) {
+        double v = 0.0;
+        for (int k = 0; k < clusters; ++k) v += ypart[k * n + c];
+        y[c] = v;
+    }
+    if (c < l) {
+        double v = 0.0;
+        for (int k = 0; k < clusters; ++k) v += spart[static_cast<int64_t>(k) * l + c];
+        s[c] = v;
+    }
+    if (c == 0) {
+        double v = 0.0;
+        for (int k = 0; k < clusters; ++k) v += sqpart[k];
+        *usq = v;
+    }
+}
+
+template <int NP>
+rl_status launch_power_pass(rl_context* ctx, int clusters, const double* a, int64_t lda, int64_t m, int64_t n,
+                            const double* q, int64_t ldq, int l, const double* x, const double* t, double* ypart,
+                            double* spart, double* sqpart) {
+    const int64_t rows = (m + clusters - 1) / clusters;
+    power_pass_kernel<NP><<<clusters * kPC, kPT, 0, ctx->stream>>>(a, lda, m, n, q, ldq, l, x, t,
+                                                                  (rows + kPR - 1) / kPR * kPR, ypart, spart, sqpart);
+    RL_CHECK_LAUNCH("power_pass_kernel");
+    return RL_OK;
+}
+
 // ||R||_2 estimate, R = A - Q B (A m x n, Q m x l, B l x n): the power
 // iteration of norms.hpp:52-77 (start x_j = 1 + j/(n+1), <= 200 steps, stop
 // when |‖Rx‖ - est| <= 1e-9 ‖Rx‖) on the implicit operator
@@ -424,9 +586,76 @@ rl_status residual_power_iteration(rl_context* ctx, int64_t m, int64_t n, int64_
     }();
     init_x_kernel<<<nblk(n, 256), 256, 0, s>>>(x, n, 1.0 / std::sqrt(nx2));
     RL_CHECK_LAUNCH("init_x_kernel");
+    // one pass over A per step when a cluster of kPC CTAs holds a row in registers
+    const int np = n <= 4096 ? 1 : n <= 8192 ? 2 : n <= 16384 ? 4 : 0;
+    const bool fused = np > 0 && l <= kPT && (n & 1) == 0 && (lda & 1) == 0 &&
+                       (reinterpret_cast<uintptr_t>(a) & 15) == 0 && ctx->num_sms >= kPC;
+    int clusters = 0;
+    Buf fbuf(s);
+    double *ypart = nullptr, *spart = nullptr, *sqpart = nullptr;
+    if (fused) {
+        // all clusters co-resident (a second wave would re-run whole row ranges)
+        int active = 0;
+        {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(ctx->num_sms / kPC * kPC), 1, 1);
+            cfg.blockDim = dim3(kPT, 1, 1);
+            cudaLaunchAttribute attr;
+            attr.id = cudaLaunchAttributeClusterDimension;
+            attr.val.clusterDim.x = kPC;
+            attr.val.clusterDim.y = 1;
+            attr.val.clusterDim.z = 1;
+            cfg.attrs = &attr;
+            cfg.numAttrs = 1;
+            const cudaError_t e = np == 1   ? cudaOccupancyMaxActiveClusters(&active, power_pass_kernel<1>, &cfg)
+                                  : np == 2 ? cudaOccupancyMaxActiveClusters(&active, power_pass_kernel<2>, &cfg)
+                                            : cudaOccupancyMaxActiveClusters(&active, power_pass_kernel<4>, &cfg);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                active = ctx->num_sms / kPC / 2;
+            }
+            if (std::getenv("RL_DEBUG_POWER")) std::fprintf(stderr, "power_pass: %d active clusters\n", active);
+        }
+        clusters = static_cast<int>(std::min<int64_t>(std::max(1, active), (m + kPR - 1) / kPR));
+        if ((st = fbuf.alloc(sizeof(double) * (static_cast<size_t>(clusters) * (n + l + 1) + 8))) != RL_OK) return st;
+        ypart = fbuf.p;
+        spart = ypart + static_cast<size_t>(clusters) * n;
+        sqpart = spart + static_cast<size_t>(clusters) * l;
+    }
     double est = 0.0;
     int it = 0;
     for (; it < 200; ++it) {
+        if (fused) {
+            // t = B x; one pass: u = A x - Q t, partial A^T u, Q^T u, ||u||^2;
+            // y = A^T u - B^T (Q^T u)
+            if ((st = gemv(ctx, l, n, b, ldb, x, tl, nullptr)) != RL_OK) return st;
+            switch (np) {
+                case 1: st = launch_power_pass<1>(ctx, clusters, a, lda, m, n, q, ldq, static_cast<int>(l), x, tl, ypart, spart, sqpart); break;
+                case 2: st = launch_power_pass<2>(ctx, clusters, a, lda, m, n, q, ldq, static_cast<int>(l), x, tl, ypart, spart, sqpart); break;
+                default: st = launch_power_pass<4>(ctx, clusters, a, lda, m, n, q, ldq, static_cast<int>(l), x, tl, ypart, spart, sqpart); break;
+            }
+            if (st != RL_OK) return st;
+            power_reduce_kernel<<<nblk(std::max<int64_t>(n, l), 256), 256, 0, s>>>(ypart, spart, sqpart, clusters, n,
+                                                                                 static_cast<int>(l), y, sl, sc);
+            RL_CHECK_LAUNCH("power_reduce_kernel");
+            if ((st = gemvt(ctx, l, n, b, ldb, sl, y, -1.0, true, part, chunks_l)) != RL_OK) return st;
+            if ((st = sumsq(ctx, n, y, sc + 70)) != RL_OK) return st;
+            scale_by_kernel<<<nblk(n, 256), 256, 0, s>>>(x, y, n, sc + 70);
+            RL_CHECK_LAUNCH("scale_by_kernel");
+            double h[2];
+            RL_CUDA(cudaMemcpyAsync(&h[0], sc, 8, cudaMemcpyDeviceToHost, s));
+            RL_CUDA(cudaMemcpyAsync(&h[1], sc + 70, 8, cudaMemcpyDeviceToHost, s));
+            RL_CUDA(cudaStreamSynchronize(s));
+            const double nax = std::sqrt(h[0]);
+            if (nax == 0.0 || h[1] == 0.0) break;
+            if (std::fabs(nax - est) <= 1e-9 * nax) {
+                est = nax;
+                ++it;
+                break;
+            }
+            est = nax;
+            continue;
+        }
         // u = R x = A x - Q (B x)
         if ((st = gemv(ctx, m, n, a, lda, x, u, nullptr)) != RL_OK) return st;
         if ((st = gemv(ctx, l, n, b, ldb, x, tl, nullptr)) != RL_OK) return st;

@@ -106,3 +106,21 @@ def test_range_find_residual_vs_oracle(cuda, orc, kind):
     rel = abs(res.info["residual_spectral"] / s_ref[0] - 1)
     print(kind, "sigma1", s_ref[0], "est", res.info["residual_spectral"], "rel", rel, "its", res.info["power_iterations"])
     assert rel <= 0.05
+
+
+@pytest.mark.parametrize("m,n,r", [(1000, 998, 17), (2050, 4100, 40), (3001, 640, 64), (513, 9000, 8)])
+def test_power_iteration_one_pass_shapes(cuda, m, n, r):
+    """||A - Q Q^T A||_2 by the one-pass power step (a cluster of CTAs per row
+    range, rows not a multiple of the exchange size, columns ragged against the
+    cluster's column split): a lower bound of sigma_1 that converges to it."""
+    rng = np.random.default_rng(m + n + r)
+    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    a = (u * np.logspace(0, -3, r)) @ v.T + 1e-6 * rng.standard_normal((m, n))
+    res = rl.range_find(a, r, 0, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 5))
+    resid = a - res.q @ (res.q.T @ a)
+    s1 = np.linalg.norm(resid, 2)
+    est = res.info["residual_spectral"]
+    assert est <= s1 * (1 + 1e-12)
+    assert abs(est / s1 - 1) <= 1e-3, (est, s1, res.info["power_iterations"])
+    assert abs(res.info["residual_frobenius"] / np.linalg.norm(resid) - 1) <= 1e-6
