@@ -55,7 +55,7 @@ template <class CF, bool kAccum, bool kStats, bool kStore>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, double* __restrict__ C,
              int64_t ldc, int M, int N, int K, double alpha, GemmStats* __restrict__ stats, int ktc,
-             int64_t split_stride) {
+             int64_t split_stride, int c_ahead) {
     constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, MI = CF::MI, NJ = CF::NJ;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B swizzle, keeping the pointer in the
@@ -131,7 +131,24 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
         }
     }
-    const double asign = kAccum ? (alpha < 0.0 ? -1.0 : 1.0) : 1.0;
+    // alpha = -1: flip the sign bit of the A fragments (an integer op, exact)
+    const int sign_hi = kAccum && alpha < 0.0 ? static_cast<int>(0x80000000u) : 0;
+    // the C tile of the tile one resident wave ahead into L2, so that its
+    // up-front C read (above) hits L2 instead of drawing on HBM in a burst
+    // with every other tile of its wave
+    if (kAccum && c_ahead > 0 && ktc == 0) {
+        const int ta = t + c_ahead;
+        if (ta < tiles_m * tiles_n && tid < BM) {
+            const int ga = ta / (GROUP_M * tiles_n), fa = ga * GROUP_M, sa = min(tiles_m - fa, GROUP_M);
+            const int ma = (fa + (ta % (GROUP_M * tiles_n)) % sa) * BM, na = ((ta % (GROUP_M * tiles_n)) / sa) * BN;
+            const int row = ma + tid;
+            const int cols = min(BN, N - na);
+            if (row < M && cols > 0 && vec_ok) {
+                const double* p = C + static_cast<int64_t>(row) * ldc + na;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(static_cast<unsigned>(cols * 8) & ~15u));
+            }
+        }
+    }
 
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % STAGES;
@@ -144,7 +161,9 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             double af[MI], bf[NJ];
 #pragma unroll
             for (int i = 0; i < MI; ++i)
-                af[i] = asign * *reinterpret_cast<const double*>(sa + swz128(rbase + 8 * i + fr, k));
+                af[i] = __hiloint2double(
+                    __double2hiint(*reinterpret_cast<const double*>(sa + swz128(rbase + 8 * i + fr, k))) ^ sign_hi,
+                    __double2loint(*reinterpret_cast<const double*>(sa + swz128(rbase + 8 * i + fr, k))));
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 const int n = cbase + 8 * j + fr;
@@ -235,10 +254,10 @@ void configure_once() {
 
 template <class CF, bool A, bool S, bool T>
 void launch_cfg(dim3 grid, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, double* C, int64_t ldc, int m,
-                int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride) {
+                int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride, int c_ahead) {
     configure_once<CF, A, S, T>();
     dgemm_kernel<CF, A, S, T><<<grid, CF::THREADS, CF::SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc,
-                                                                       split_stride);
+                                                                       split_stride, c_ahead);
 }
 
 // encode the operand maps for configuration CF and launch over all tiles
@@ -253,7 +272,7 @@ rl_status run_cfg(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double
     if (tiles > 0x7fffffff) return set_error(RL_ERR_DIMENSION, "gemm: too many tiles");
     launch_cfg<CF, A, S, T>(dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), ctx->stream, ta, tb, C,
                             ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), alpha, stats, ktc,
-                            split_stride);
+                            split_stride, A ? ctx->num_sms * CF::MINB : 0);
     RL_CHECK_LAUNCH("dgemm_kernel");
     return RL_OK;
 }
