@@ -38,7 +38,7 @@ struct Cfg {
     static constexpr int MI = BM / WM / 8, NJ = BN / WN / 8;  // 8x8 fragments per warp
     static constexpr int A_STAGE = BM * BK * 8, B_STAGE = BK * BN * 8;
     static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-    static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 64;
+    static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 128;
     static constexpr int THREADS = WM * WN * 32;
 };
 using BigCfg = Cfg<128, 128, 2, 4, 4, 1>;
@@ -62,6 +62,7 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     // shared window so operand reads compile to LDS (not generic LD)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;  // stage drained by every MMA warp
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = warp / CF::WN, wn = warp % CF::WN;
@@ -82,10 +83,14 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const int KT = ktc > 0 ? min(ktc, KT_all - kt0) : KT_all;
     C += static_cast<int64_t>(blockIdx.y) * split_stride;
 
+    constexpr int MMA_WARPS = CF::THREADS / 32;
     if (tid == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], MMA_WARPS);
+        }
         mbar_fence_init();
     }
     __syncthreads();
@@ -174,8 +179,16 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
-        __syncthreads();
-        if (tid == 0 && kt + STAGES < KT) issue(kt + STAGES);
+        // release the stage; thread 0 refills it once every warp has (the
+        // other warps run ahead on the stages already landed, no CTA barrier)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (tid == 0 && kt + STAGES < KT) {
+            mbar_wait(&empty[s], (kt / STAGES) & 1);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(kt + STAGES);
+        }
+        __syncwarp();  // warp 0 reconverges before its next mma.sync (.aligned)
     }
 
     // ---- epilogue

@@ -36,3 +36,27 @@ def test_matmul_kat_and_device(cuda):
 def test_matmul_dimension_error(cuda):
     with pytest.raises(rl.DimensionError):
         rl.matmul(np.zeros((3, 4)), np.zeros((5, 2)))
+
+
+@pytest.mark.parametrize("n", [4096, 6000])
+def test_many_wave_genp_updates_exact_and_deterministic(cuda, n):
+    """The multi-wave trailing-update GEMMs of blocked GENP (C -= A B with
+    K = 64 / 128, thousands of tiles, two CTAs per SM, stage ring refilled as
+    the MMA warps release stages): L U reproduces A to rounding and two calls
+    return identical bits. (A missing generic->async proxy fence before the
+    refill once corrupted a few fragments per call at this size.)"""
+    torch = cuda
+    import ctypes
+    from paper_1406_5802_b200 import capi
+    L = capi.lib()
+    g = torch.Generator(device="cuda").manual_seed(n)
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    lu1, lu2 = torch.empty_like(a), torch.empty_like(a)
+    info = capi.rl_solve_info()
+    assert L.rl_genp_factor(None, capi.RL_DEVICE, n, a.data_ptr(), lu1.data_ptr(), ctypes.byref(info)) == 0
+    assert L.rl_genp_factor(None, capi.RL_DEVICE, n, a.data_ptr(), lu2.data_ptr(), ctypes.byref(info)) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(lu1, lu2)
+    lo = torch.tril(lu1, -1) + torch.eye(n, dtype=torch.float64, device="cuda")
+    rel = (torch.linalg.matrix_norm(lo @ torch.triu(lu1) - a) / torch.linalg.matrix_norm(a)).item()
+    assert rel <= 1e-13 * n * info.growth, (rel, info.growth)
