@@ -43,6 +43,10 @@ struct Cfg {
 };
 using BigCfg = Cfg<128, 128, 2, 4, 4, 1>;
 using SmallCfg = Cfg<128, 64, 4, 2, 4, 2>;
+// latency-bound small products (the GENP tail's U12, GEMM_a and panel
+// updates): 64x32 tiles, 4 warps of 32x16, four CTAs per SM, so a problem of a
+// few 128x64 tiles still spreads over the SMs
+using TinyCfg = Cfg<64, 32, 2, 2, 4, 4>;
 
 // element (r, k) of a 128-byte-swizzled tile with 16 doubles per row
 __device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3); }
@@ -330,20 +334,22 @@ rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm: accumulate supports alpha = +1 or -1");
     if (M > (int64_t(1) << 30) || N > (int64_t(1) << 30) || K > (int64_t(1) << 30))
         return set_error(RL_ERR_DIMENSION, "gemm: dimension too large");
-    // short K (Schur updates): the two-CTAs-per-SM configuration
+    // short K (Schur updates): the two-CTAs-per-SM configuration; problems
+    // that would not fill the SMs with it: 64x32 tiles
     const bool small = K <= 256;
+    const int64_t small_tiles = ((M + 127) / 128) * ((N + 63) / 64);
+    const bool tiny = small && small_tiles < ctx->num_sms;
+#define RL_GEMM_DISPATCH(AC, ST)                                                                                   \
+    return tiny    ? run_cfg<TinyCfg, AC, ST, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)  \
+           : small ? run_cfg<SmallCfg, AC, ST, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0) \
+                   : run_cfg<BigCfg, AC, ST, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
     if (accumulate) {
-        if (stats)
-            return small ? run_cfg<SmallCfg, true, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
-                         : run_cfg<BigCfg, true, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
-        return small ? run_cfg<SmallCfg, true, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
-                     : run_cfg<BigCfg, true, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
+        if (stats) RL_GEMM_DISPATCH(true, true);
+        RL_GEMM_DISPATCH(true, false);
     }
-    if (stats)
-        return small ? run_cfg<SmallCfg, false, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
-                     : run_cfg<BigCfg, false, true, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
-    return small ? run_cfg<SmallCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)
-                 : run_cfg<BigCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0);
+    if (stats) RL_GEMM_DISPATCH(false, true);
+    RL_GEMM_DISPATCH(false, false);
+#undef RL_GEMM_DISPATCH
 }
 
 rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
