@@ -8,8 +8,11 @@ import numpy as np
 import torch
 import paper_1406_5802_b200 as rl
 from paper_1406_5802_b200 import capi
+if os.environ.get('RANDLA_VARIANT_LIB'):  # dev A/B: a variant library from tools/build_variant.sh
+    capi.LIB_PATH = os.environ['RANDLA_VARIANT_LIB']
+    capi._lib = None
 
-n = 65536
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 t0 = time.time()
 seeds = np.array([[rl.derive_seed(7 + i, k) for k in (1, 2, 3)] for i in range(n)], dtype=np.uint64)
 a = rl.gen_gaussian_batch(n, 32, 32, seeds[:, 0])
@@ -30,11 +33,12 @@ def run():
 for _ in range(3): run()
 torch.cuda.synchronize()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-K = 20
+K = int(os.environ.get("TB_K", "20"))
 e0.record()
 for _ in range(K): run()
 e1.record(); e1.synchronize()
 ms = e0.elapsed_time(e1) / K
 byts = n * 25104
 print(f"batched32: {ms:.4f} ms/batch, {n/ms*1e3:.3e} solves/s, {byts/ms/1e6:.1f} GB/s ({byts/ms/1e6/6534.5*100:.1f}% of 6534.5)")
+print("checksum x", float(x.abs().sum()), "lu", float(lu.abs().sum()))
 print("zero pivots", int((st != 0).sum()), "max resid", float(r.max()), "median", float(r.median()))
