@@ -445,6 +445,18 @@ struct Shape {
     static constexpr int minb = L >= 13 ? 1 : RL_FFT_MINB12;
     __host__ __device__ static constexpr int radix(int p) { return p < full ? 16 : 1 << rem; }
     __host__ __device__ static constexpr int sub(int p) { return m >> (4 * p); }  // subarray length entering pass p
+    // base twiddles w_N^{n0 2^j} (j < log2 R) of the passes with M = N/R > 1,
+    // cached per CTA in shared memory behind z as [pass][j][n0]
+    __host__ __device__ static constexpr int lgr(int p) { return p < full ? 4 : rem; }
+    __host__ __device__ static constexpr int tw_m(int p) { return sub(p) >> lgr(p); }
+    __host__ __device__ static constexpr int tw_entries(int p) { return tw_m(p) > 1 ? tw_m(p) * lgr(p) : 0; }
+    __host__ __device__ static constexpr int tw_off(int p) { return p == 0 ? 0 : tw_off(p - 1) + tw_entries(p - 1); }
+    static constexpr int tw_total = tw_off(passes);
+    // w_n^q (q < m/2) for the spectrum unpack / repack also cached when it
+    // still fits minb CTAs per SM (228 KiB per SM, 1 KiB reserved per CTA)
+    static constexpr int smem_base = (m + tw_total) * 16;
+    static constexpr bool unpack_cache = minb * (smem_base + (m / 2) * 16 + 1024) <= 228 * 1024;
+    static constexpr int smem_rows = smem_base + (unpack_cache ? (m / 2) * 16 : 0);
 };
 
 // shared-memory slot of element i: XOR swizzle of the 16-byte slot index so
@@ -473,8 +485,18 @@ __device__ __forceinline__ int dif_pos(int k) {
 
 // one DIF pass over subarrays of length N (radix R); kGlobal: the input is the
 // real row x (length k, zero padded), read straight from global memory
+// base twiddles of a pass from the shared-memory cache (see Shape::tw_off)
+template <int R>
+__device__ __forceinline__ void cached_twiddles(cplx (&w)[R], const cplx* twc, int n0, int M) {
+    if (R > 1) w[1] = twc[n0];
+    if (R > 2) w[2] = twc[M + n0];
+    if (R > 4) w[4] = twc[2 * M + n0];
+    if (R > 8) w[8] = twc[3 * M + n0];
+}
+
 template <int L, int R, int N, bool kGlobal>
-__device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k, const cplx* __restrict__ tw) {
+__device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k, const cplx* __restrict__ tw,
+                                    const cplx* twc = nullptr) {
     using S = Shape<L>;
     constexpr int M = N / R, groups = S::m / R;
     constexpr int64_t tstride = S::n / N;
@@ -498,14 +520,23 @@ __device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k
                 v[j] = z[swz<L>(q)];
             }
         }
-        cplx w[R];
-        base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
         dft_reg<R, false>(v);
         z[swz<L>(o + n0)] = v[0];
+        if constexpr (M == 1) {
+            // last pass: every twiddle is w^0 = 1
 #pragma unroll
-        for (int r = 1; r < R; ++r) {
-            lazy_twiddle<R>(w, r);
-            z[swz<L>(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
+            for (int r = 1; r < R; ++r) z[swz<L>(o + r)] = v[brev<R>(r)];
+        } else {
+            cplx w[R];
+            if (twc)
+                cached_twiddles<R>(w, twc, n0, M);
+            else
+                base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                lazy_twiddle<R>(w, r);
+                z[swz<L>(o + n0 + r * M)] = cmul(v[brev<R>(r)], w[r]);
+            }
         }
     }
 }
@@ -514,7 +545,7 @@ __device__ __forceinline__ void dif(cplx* z, const double* __restrict__ x, int k
 // y[2q] = Re, y[2q+1] = Im (scaled) for 2q < l straight to global memory
 template <int L, int R, int N, bool kGlobal>
 __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, double scale,
-                                    const cplx* __restrict__ tw) {
+                                    const cplx* __restrict__ tw, const cplx* twc = nullptr) {
     using S = Shape<L>;
     constexpr int M = N / R, groups = S::m / R;
     constexpr int64_t tstride = S::n / N;
@@ -523,14 +554,23 @@ __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, doub
         const int g = g0 + threadIdx.x;
         if (groups % S::T != 0 && g >= groups) break;
         const int n0 = g % M, o = (g / M) * N;
-        cplx w[R];
-        base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
         cplx v[R];
         v[0] = z[swz<L>(o + n0)];
+        if constexpr (M == 1) {
+            // first inverse pass: every twiddle is w^0 = 1
 #pragma unroll
-        for (int r = 1; r < R; ++r) {
-            lazy_twiddle<R>(w, r);
-            v[r] = cmulc(z[swz<L>(o + n0 + r * M)], w[r]);
+            for (int r = 1; r < R; ++r) v[r] = z[swz<L>(o + r)];
+        } else {
+            cplx w[R];
+            if (twc)
+                cached_twiddles<R>(w, twc, n0, M);
+            else
+                base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                lazy_twiddle<R>(w, r);
+                v[r] = cmulc(z[swz<L>(o + n0 + r * M)], w[r]);
+            }
         }
         dft_reg<R, true>(v);
 #pragma unroll
@@ -551,24 +591,40 @@ __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, doub
 }
 
 template <int L, int P>
-__device__ __forceinline__ void dif_from(cplx* z, const double* x, int k, const cplx* tw) {
+__device__ __forceinline__ void dif_from(cplx* z, const double* x, int k, const cplx* tw, const cplx* twc = nullptr) {
     using S = Shape<L>;
     if constexpr (P < S::passes) {
-        dif<L, S::radix(P), S::sub(P), P == 0>(z, x, k, tw);
+        dif<L, S::radix(P), S::sub(P), P == 0>(z, x, k, tw, twc ? twc + S::tw_off(P) : nullptr);
         __syncthreads();
-        dif_from<L, P + 1>(z, x, k, tw);
+        dif_from<L, P + 1>(z, x, k, tw, twc);
     }
 }
 
 template <int L, int P>
-__device__ __forceinline__ void dit_down(cplx* z, double* y, int l, double scale, const cplx* tw) {
+__device__ __forceinline__ void dit_down(cplx* z, double* y, int l, double scale, const cplx* tw,
+                                         const cplx* twc = nullptr) {
     using S = Shape<L>;
     if constexpr (P >= 0) {
-        dit<L, S::radix(P), S::sub(P), P == 0>(z, y, l, scale, tw);
+        dit<L, S::radix(P), S::sub(P), P == 0>(z, y, l, scale, tw, twc ? twc + S::tw_off(P) : nullptr);
         if constexpr (P > 0) {
             __syncthreads();
-            dit_down<L, P - 1>(z, y, l, scale, tw);
+            dit_down<L, P - 1>(z, y, l, scale, tw, twc);
         }
+    }
+}
+
+// fill the per-CTA twiddle cache: entry [tw_off(p) + j M + n0] = w_N^{n0 2^j}
+template <int L, int P>
+__device__ __forceinline__ void fill_twiddle_cache(cplx* twc, const cplx* __restrict__ tw) {
+    using S = Shape<L>;
+    if constexpr (P < S::passes) {
+        constexpr int M = S::tw_m(P), E = S::tw_entries(P);
+        constexpr int64_t tstride = S::n / S::sub(P);
+        for (int e = threadIdx.x; e < E; e += S::T) {
+            const int j = e / M, n0 = e % M;
+            twc[S::tw_off(P) + e] = tw[((static_cast<int64_t>(n0) << j) * tstride) & (S::n - 1)];
+        }
+        fill_twiddle_cache<L, P + 1>(twc, tw);
     }
 }
 
@@ -577,7 +633,7 @@ __device__ __forceinline__ void dit_down(cplx* z, double* y, int l, double scale
 // O = (Z_k - conj Z_{m-k})/(2i), X_k = E + w_n^k O, X_{m-k} = conj(E - w_n^k O);
 // k = 0 yields X_0 and X_m
 template <int L>
-__device__ __forceinline__ void unpack_pair(const cplx* z, int k, const cplx* __restrict__ tw, cplx& xk, cplx& xmk) {
+__device__ __forceinline__ void unpack_pair(const cplx* z, int k, cplx wk, cplx& xk, cplx& xmk) {
     constexpr int m = Shape<L>::m;
     const cplx zk = z[swz<L>(dif_pos<L>(k))];
     const cplx zm = z[swz<L>(dif_pos<L>((m - k) & (m - 1)))];
@@ -588,7 +644,7 @@ __device__ __forceinline__ void unpack_pair(const cplx* z, int k, const cplx* __
         xmk = {e.x - o.x, e.y - o.y};
         return;
     }
-    const cplx wo = cmul(tw[k], o);
+    const cplx wo = cmul(wk, o);
     xk = cadd(e, wo);
     const cplx d = csub(e, wo);
     xmk = {d.x, -d.y};
@@ -617,7 +673,7 @@ __global__ void __launch_bounds__(Shape<L>::T) spectrum_kernel(const double* __r
     dif_from<L, 1>(z, nullptr, 0, tw);
     for (int k = threadIdx.x; k <= m / 2; k += S::T) {
         cplx xk, xmk;
-        unpack_pair<L>(z, k, tw, xk, xmk);
+        unpack_pair<L>(z, k, tw[k], xk, xmk);
         spec[k] = xk;
         spec[m - k] = xmk;
     }
@@ -627,18 +683,43 @@ __global__ void __launch_bounds__(Shape<L>::T) spectrum_kernel(const double* __r
 // first l outputs
 template <int L>
 __global__ void __launch_bounds__(Shape<L>::T, Shape<L>::minb)
-    rows_kernel(const double* __restrict__ a, int64_t lda, int k, const cplx* __restrict__ spec,
+    rows_kernel(const double* __restrict__ a, int64_t rows, int64_t lda, int k, const cplx* __restrict__ spec,
                 const cplx* __restrict__ tw, double* __restrict__ out, int64_t ldo, int l) {
     using S = Shape<L>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx* z = reinterpret_cast<cplx*>(smem_raw);
     constexpr int m = S::m;
-    const int64_t row = blockIdx.x;
-    dif_from<L, 0>(z, a + row * lda, k, tw);
+    cplx* twc = z + m;
+    fill_twiddle_cache<L, 0>(twc, tw);
+    cplx* twu = twc + S::tw_total;  // w_n^q, q < m/2 (unpack_cache)
+    if constexpr (S::unpack_cache)
+        for (int q = threadIdx.x; q < m / 2; q += S::T) twu[q] = tw[q];
+    __syncthreads();
+    // persistent: each CTA walks rows blockIdx.x, + gridDim.x, ...; the next
+    // row is prefetched into L2 while this one is transformed, so the first
+    // pass's loads hit L2 instead of waiting on HBM
+#pragma unroll 1
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    if (threadIdx.x == 0 && row + gridDim.x < rows) {
+        const char* nxt = reinterpret_cast<const char*>(a + (row + gridDim.x) * lda);
+        const int bytes = ((k * 8) + 15) & ~15;
+        for (int off = 0; off < bytes; off += 32768)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(nxt + off), "r"(min(32768, bytes - off)));
+    }
+    dif_from<L, 0>(z, a + row * lda, k, tw, twc);
 #pragma unroll 1
     for (int q = threadIdx.x; q <= m / 2; q += S::T) {
+        // w_n^q and w_n^{m-q} = -conj(w_n^q) (w_n^m = -1); w_n^{m/2} = i
+        cplx wq, wmq;
+        if constexpr (S::unpack_cache) {
+            wq = q < m / 2 ? twu[q] : cplx{0.0, 1.0};
+            wmq = {-wq.x, wq.y};
+        } else {
+            wq = tw[q];
+            wmq = tw[m - q];
+        }
         cplx xk, xmk;
-        unpack_pair<L>(z, q, tw, xk, xmk);
+        unpack_pair<L>(z, q, wq, xk, xmk);
         const cplx yk = cmul(spec[q], xk), ymk = cmul(spec[m - q], xmk);
         const int pk = swz<L>(dif_pos<L>(q)), pm = swz<L>(dif_pos<L>((m - q) & (m - 1)));
         if (q == 0) {
@@ -646,14 +727,16 @@ __global__ void __launch_bounds__(Shape<L>::T, Shape<L>::minb)
             z[pk] = {(yk.x + ymk.x) - (yk.y - ymk.y), (yk.y + ymk.y) + (yk.x - ymk.x)};
         } else {
             const cplx cym = {ymk.x, -ymk.y}, cyk = {yk.x, -yk.y};
-            const cplx zk = repack(yk, cym, tw[q]);
-            const cplx zm = repack(ymk, cyk, tw[m - q]);
+            const cplx zk = repack(yk, cym, wq);
+            const cplx zm = repack(ymk, cyk, wmq);
             z[pk] = zk;
             z[pm] = zm;
         }
     }
     __syncthreads();
-    dit_down<L, S::passes - 1>(z, out + row * ldo, l, 1.0 / static_cast<double>(S::n), tw);
+    dit_down<L, S::passes - 1>(z, out + row * ldo, l, 1.0 / static_cast<double>(S::n), tw, twc);
+    __syncthreads();  // the last pass has read z before the next row's first pass writes it
+    }
 }
 
 template <int L>
@@ -661,18 +744,20 @@ rl_status launch_L(rl_context* ctx, int64_t rows, int k, const double* a, int64_
                    const cplx* tw, cplx* spec, double* out, int64_t ldo, int l) {
     using S = Shape<L>;
     constexpr int smem = S::m * 16;
+    constexpr int smem_rows = S::smem_rows;
     static PerDeviceOnce configured_once;
     {
         const rl_status cst = once_per_device(configured_once, [&]() -> rl_status {
             RL_CUDA(cudaFuncSetAttribute(spectrum_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            RL_CUDA(cudaFuncSetAttribute(rows_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            RL_CUDA(cudaFuncSetAttribute(rows_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_rows));
             return RL_OK;
         });
         if (cst != RL_OK) return cst;
     }
     spectrum_kernel<L><<<1, S::T, smem, ctx->stream>>>(c, tw, spec);
     RL_CHECK_LAUNCH("r2c::spectrum_kernel");
-    rows_kernel<L><<<static_cast<unsigned>(rows), S::T, smem, ctx->stream>>>(a, lda, k, spec, tw, out, ldo, l);
+    const int64_t grid = std::min<int64_t>(rows, static_cast<int64_t>(ctx->num_sms) * S::minb);
+    rows_kernel<L><<<static_cast<unsigned>(grid), S::T, smem_rows, ctx->stream>>>(a, rows, lda, k, spec, tw, out, ldo, l);
     RL_CHECK_LAUNCH("r2c::rows_kernel");
     return RL_OK;
 }
