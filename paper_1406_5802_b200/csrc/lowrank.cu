@@ -62,75 +62,112 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int
 
 
 // ---- blocked Cholesky / triangular inverse (l up to a few hundred) ---------
-// 64x64 diagonal block at (J, J): Cholesky W_JJ = R^T R in shared memory
-// (lu.hpp-style right-looking, rolled loops), R written back upper with zeros
-// below, X = R^-1 (column sweeps) into xd (Rinv's diagonal block) and X^T
-// into xt (64 x 64, the operand of the panel GEMM). fail <- 1-based global
-// index of the first non-positive pivot (first block that breaks down).
+// 64x64 diagonal block at (J, J): Cholesky W_JJ = R^T R (lu.hpp-style
+// right-looking order), R written back upper with zeros below, X = R^-1
+// (column sweeps) into xd (Rinv's diagonal block) and X^T into xt (64 x 64,
+// the operand of the panel GEMM). fail <- 1-based global index of the first
+// non-positive pivot (first block that breaks down).
+// Thread t holds row t/4 of the block, columns = t mod 4 (16 registers); one
+// barrier per elimination step: the pivot row's four threads scale it and
+// publish it to a double-buffered shared row.
 constexpr int CB = 64, CT = 256;
-constexpr int kCholSmem = 2 * CB * (CB + 1) * 8;
+constexpr int kCholSmem = 2 * CB * (CB + 1) * 8 + 2 * CB * 8;  // R, rb, X
 __global__ void __launch_bounds__(CT) chol_block_kernel(double* __restrict__ w, int64_t ld, int J, int bw,
                                                         int* __restrict__ fail, double* __restrict__ xd, int64_t ldx,
                                                         double* __restrict__ xt) {
     extern __shared__ double cbm[];
-    double(*a)[CB + 1] = reinterpret_cast<double(*)[CB + 1]>(cbm);
-    double(*x)[CB + 1] = reinterpret_cast<double(*)[CB + 1]>(cbm + CB * (CB + 1));
-    __shared__ int s_fail;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_fail = 0;
-    for (int idx = tid; idx < CB * CB; idx += CT) {
-        const int i = idx >> 6, k = idx & 63;
-        a[i][k] = (i < bw && k < bw) ? w[(J + i) * ld + J + k] : (i == k ? 1.0 : 0.0);
-        x[i][k] = 0.0;
+    double(*R)[CB + 1] = reinterpret_cast<double(*)[CB + 1]>(cbm);
+    double(*rb)[CB] = reinterpret_cast<double(*)[CB]>(cbm + CB * (CB + 1));
+    const int tid = threadIdx.x, i = tid >> 2, q = tid & 3, warp = tid >> 5;
+    double v[16];  // v[s] = W(i, q + 4 s)
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int k = q + 4 * s;
+        v[s] = (i < bw && k < bw) ? w[(J + i) * ld + J + k] : (i == k ? 1.0 : 0.0);
     }
-    __syncthreads();
-    const int r = tid >> 2, q = tid & 3;  // trailing row j+1+r... (r < 64), columns q, q+4, ...
+    int failed = 0;
 #pragma unroll 1
     for (int j = 0; j < bw; ++j) {
-        const double d = a[j][j];
-        if (!(d > 0.0)) {  // uniform: every thread reads the same value
-            if (tid == 0) s_fail = J + j + 1;
+        double* row = rb[j & 1];
+        if (warp == (j >> 3)) {  // the pivot row's warp: d = W(j, j) from its owner lane
+            // v[j / 4] by a select tree on the bits of j / 4 (a dynamic index
+            // would send v to local memory)
+            const int sel = j >> 2;
+            double t8[8], t4[4], t2[2];
+#pragma unroll
+            for (int s = 0; s < 8; ++s) t8[s] = (sel & 1) ? v[2 * s + 1] : v[2 * s];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) t4[s] = (sel & 2) ? t8[2 * s + 1] : t8[2 * s];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) t2[s] = (sel & 4) ? t4[2 * s + 1] : t4[2 * s];
+            const double dl = (sel & 8) ? t2[1] : t2[0];
+            const double d = __shfl_sync(0xffffffffu, dl, 4 * (j & 7) + (j & 3));
+            if (i == j) {
+                const double rt = sqrt(d), ri = 1.0 / rt;
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int k = q + 4 * s;
+                    if (k > j) {
+                        v[s] *= ri;  // R(j, k) = W(j, k) / R(j, j) as 1/rt products
+                        row[k] = v[s];
+                    } else if (k == j) {
+                        v[s] = rt;
+                        row[j] = d;  // the unscaled pivot for the breakdown test
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const double dj = row[j];
+        if (!(dj > 0.0)) {  // uniform: every thread reads the same value
+            failed = J + j + 1;
             break;
         }
-        const double rt = sqrt(d), ri = 1.0 / rt;
-        __syncthreads();
-        if (tid > j && tid < bw) a[j][tid] *= ri;
-        if (tid == 0) a[j][j] = rt;
-        __syncthreads();
-        const int i = j + 1 + r;
-        if (i < bw) {
-            const double l = a[j][i];
-#pragma unroll 4
-            for (int k = j + 1 + q; k < bw; k += 4) a[i][k] = fma(-l, a[j][k], a[i][k]);
+        if (i > j) {
+            const double l = row[i];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int k = q + 4 * s;
+                if (k >= i) v[s] = fma(-l, row[k], v[s]);
+            }
         }
-        __syncthreads();
     }
-    __syncthreads();
-    if (s_fail) {
-        if (tid == 0) atomicCAS(fail, 0, s_fail);
+    if (failed) {
+        if (tid == 0) atomicCAS(fail, 0, failed);
         return;
     }
-    // X = R^-1, thread c < bw owns column c (axpy back substitution)
-    if (tid < bw) {
-        const int c = tid;
-        x[c][c] = 1.0;
-#pragma unroll 1
-        for (int k = c; k >= 0; --k) {
-            const double xk = x[k][c] / a[k][k];
-            x[k][c] = xk;
-#pragma unroll 4
-            for (int i = 0; i < k; ++i) x[i][c] = fma(-a[i][k], xk, x[i][c]);
-        }
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int k = q + 4 * s;
+        R[i][k] = k >= i ? v[s] : 0.0;
+        if (i < bw && k < bw) w[(J + i) * ld + J + k] = k >= i ? v[s] : 0.0;
     }
     __syncthreads();
-    for (int idx = tid; idx < bw * bw; idx += CT) {
-        const int i = idx / bw, k = idx % bw;
-        w[(J + i) * ld + J + k] = k >= i ? a[i][k] : 0.0;
-        xd[i * ldx + k] = x[i][k];
-    }
-    for (int idx = tid; idx < CB * CB; idx += CT) {
-        const int i = idx >> 6, k = idx & 63;
-        xt[i * CB + k] = (i < bw && k < bw) ? x[k][i] : 0.0;
+    // X = R^-1 by column sweeps (axpy back substitution, the reference order
+    // per column): four threads per column c (one warp holds 8 columns), thread
+    // p updating rows r = p mod 4; rolled over k (an unrolled sweep is
+    // instruction-fetch bound)
+    {
+        const int c = tid >> 2, p = tid & 3;
+        const unsigned gm = 0xFu << (tid & 28);  // the column's four lanes (same trip count)
+        double* X = &rb[0][0] + 2 * CB;  // X[r * (CB + 1) + c] (behind R and rb)
+        for (int r = p; r < CB; r += 4) X[r * (CB + 1) + c] = r == c ? 1.0 : 0.0;
+        __syncwarp(gm);
+        const int kmax = min(c, bw - 1);
+#pragma unroll 1
+        for (int k = kmax; k >= 0; --k) {
+            const double xk = X[k * (CB + 1) + c] / R[k][k];
+            __syncwarp(gm);
+            if (p == (k & 3)) X[k * (CB + 1) + c] = xk;
+            for (int r = p; r < k; r += 4) X[r * (CB + 1) + c] = fma(-R[r][k], xk, X[r * (CB + 1) + c]);
+            __syncwarp(gm);
+        }
+        for (int r = p; r < CB; r += 4) {
+            const bool in = r < bw && c < bw;
+            const double xv = X[r * (CB + 1) + c];
+            if (in) xd[r * ldx + c] = xv;
+            xt[c * CB + r] = in ? xv : 0.0;
+        }
     }
 }
 

