@@ -178,6 +178,35 @@ RL_API rl_status rl_genp_factor(rl_context* ctx, rl_mem mem, int64_t n, const do
 /* lu_solve (lu.hpp:100-123) on packed factors */
 RL_API rl_status rl_lu_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* lu, const double* b, double* x);
 
+/* ---- block elimination (block_ge.hpp), the reference's arithmetic order -- */
+/* gepp_factor (lu.hpp:62-98): packed L\U with partial pivoting (first maximal
+ * |u_ij|), perm[i] = original row at position i; RL_ERR_SINGULAR_MATRIX with
+ * *singular_step (1-based) when the best pivot <= tol_pivot(n) *
+ * spectral_norm_estimate(a). Bit-identical to the reference. */
+RL_API rl_status rl_gepp_factor(rl_context* ctx, rl_mem mem, int64_t n, const double* a, double* lu, int64_t* perm,
+                                int64_t* singular_step);
+/* lu_solve (lu.hpp:100-123) or, transpose != 0, lu_solve_transpose
+ * (lu.hpp:127-147) with GEPP factors, for nrhs right-hand sides: the columns
+ * of the n x nrhs row-major b; x likewise (x must not alias b) */
+RL_API rl_status rl_gepp_solve(rl_context* ctx, rl_mem mem, int64_t n, int64_t nrhs, const double* lu,
+                               const int64_t* perm, const double* b, double* x, int32_t transpose);
+/* block_ge_factor(a, split) (block_ge.hpp:168-181): split = pivot block sizes
+ * in elimination order (sum n). The right-spine factorisation is returned
+ * flat: level at offset o with block size k holds its leaf's packed GEPP
+ * factors in factors[o:o+k, o:o+k], B^-1 C in factors[o:o+k, o+k:n], D B^-1 in
+ * factors[o+k:n, o:o+k], the leaf's local permutation in perm[o:o+k].
+ * leaf_blocks (nullable, n x n): each leaf's block matrix (the Schur complement
+ * it factors) on its diagonal block. RL_ERR_DIMENSION on a bad split;
+ * RL_ERR_SINGULAR_PIVOT_BLOCK with *position = offset + 1 when
+ * svd_values(B).back() <= tol_pivot(n) * spectral_norm_estimate(a);
+ * RL_ERR_SINGULAR_MATRIX from a leaf's GEPP. */
+RL_API rl_status rl_block_ge_factor(rl_context* ctx, rl_mem mem, int64_t n, const double* a, int64_t nsplit,
+                                   const int64_t* split, double* factors, int64_t* perm, double* leaf_blocks,
+                                   int64_t* position);
+/* block_solve (block_ge.hpp:198-201) on rl_block_ge_factor's output */
+RL_API rl_status rl_block_solve(rl_context* ctx, rl_mem mem, int64_t n, int64_t nsplit, const int64_t* split,
+                               const double* factors, const int64_t* perm, const double* b, double* x);
+
 /* preprocess_solve(a, b, none, post, refine_steps) (preprocess.hpp:156-180):
  * product = A*H (dense GEMM or circulant FFT), GENP, chain solve
  * x = H (LU)^-1 b, refinement. lu_out (n x n, nullable) receives the packed

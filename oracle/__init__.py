@@ -72,6 +72,7 @@ class _C:
     def __init__(self, lib):
         self.lib = lib
         s = lambda n, r, a: _sig(lib, n, r, a)
+        s("or_singular_values", None, [i64, i64, _dp, _dp])
         self.hash_label = s("or_hash_label", u64, [ctypes.c_char_p])
         self.derive_seed = s("or_derive_seed", u64, [u64, u64, u64])
         self._gen = s("or_gen_gaussian", None, [i64, i64, u64, _dp])
@@ -223,6 +224,48 @@ class _Ref:
                       [i64, _dp, _dp, ctypes.c_int, u64, i64, _dp, _dp, _i32p, _i64p])
         self._batch = s("ref_batched_config2", i64, [i64, u64, i64, i64, _dp, _dp])
         self._trials = s("ref_parallel_dense_trials", i64, [i64, i64, _dp, _dp, _u64p, _dp])
+        self._gepp = s("ref_gepp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p])
+        self._gepp_solve = s("ref_gepp_solve", ctypes.c_int, [i64, _dp, _dp, _dp, ctypes.c_int])
+        self._block_ge = s("ref_block_ge", ctypes.c_int, [i64, _dp, i64, _i64p, _dp, _dp, _dp, _dp, _dp, _i64p])
+
+    # status codes of the ref_* entry points (ref_capi.cpp)
+    DIM, ZERO_PIVOT, SINGULAR_BLOCK, SINGULAR = 1, 2, 3, 6
+
+    def gepp_factor(self, a):
+        """gepp_factor (lu.hpp:62-98): (packed L\\U, perm, status)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        n = a.shape[0]
+        packed = np.empty_like(a)
+        perm = np.empty(n, np.int64)
+        st = self._gepp(n, ptr(a), ptr(packed), ptr(perm))
+        return packed, perm, st
+
+    def gepp_solve(self, a, b, transpose=False):
+        """lu_solve / lu_solve_transpose (lu.hpp:100-147) with gepp_factor(a)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b)
+        st = self._gepp_solve(a.shape[0], ptr(a), ptr(b), ptr(x), 1 if transpose else 0)
+        if st != 0:
+            raise RuntimeError(f"ref_gepp_solve failed ({st})")
+        return x
+
+    def block_ge(self, a, split, b):
+        """block_ge_factor(a, split) (block_ge.hpp:168-181): dict with pivots,
+        reassembled, x = block_solve(b), last_leaf (the deepest Schur leaf's
+        block_matrix), status and position."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        n = a.shape[0]
+        sp = np.ascontiguousarray(split, dtype=np.int64)
+        k = int(sp[-1]) if len(sp) else 0
+        out = {"pivots": np.empty(n), "reassembled": np.empty((n, n)), "x": np.empty(n),
+               "last_leaf": np.empty((max(k, 1), max(k, 1)))}
+        pos = np.zeros(1, np.int64)
+        st = self._block_ge(n, ptr(a), len(sp), ptr(sp) if len(sp) else None, ptr(b), ptr(out["pivots"]),
+                            ptr(out["reassembled"]), ptr(out["x"]), ptr(out["last_leaf"]), ptr(pos))
+        out["status"], out["position"] = st, int(pos[0])
+        return out
 
     def golden_draws(self, label, seed, trials):
         d = np.empty(trials)

@@ -710,3 +710,55 @@ int or_qr(int64_t m, int64_t l, const double* a, double* q, double* r, int64_t* 
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------------ singular values --- */
+/* One-sided Jacobi on the columns of A (or of A^T when m < n), cyclic pair
+ * order, until no pair has |a_p . a_q| > 1e-15 sqrt(|a_p|^2 |a_q|^2); the
+ * singular values are the column norms, sorted non-increasing. */
+static int cmp_desc(const void* x, const void* y) {
+    const double a = *(const double*)x, b = *(const double*)y;
+    return a < b ? 1 : (a > b ? -1 : 0);
+}
+
+void or_singular_values(int64_t m, int64_t n, const double* a, double* out) {
+    const int tr = m < n;
+    const int64_t rows = tr ? n : m, cols = tr ? m : n;
+    double* w = (double*)malloc(sizeof(double) * rows * cols); /* column p at w + p * rows */
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            if (tr) w[i * rows + j] = a[i * n + j];
+            else w[j * rows + i] = a[i * n + j];
+        }
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        int rotated = 0;
+        for (int64_t p = 0; p + 1 < cols; ++p)
+            for (int64_t q = p + 1; q < cols; ++q) {
+                double* wp = w + p * rows;
+                double* wq = w + q * rows;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int64_t i = 0; i < rows; ++i) {
+                    al += wp[i] * wp[i];
+                    be += wq[i] * wq[i];
+                    ga += wp[i] * wq[i];
+                }
+                if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+                rotated = 1;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                for (int64_t i = 0; i < rows; ++i) {
+                    const double xp = wp[i], xq = wq[i];
+                    wp[i] = c * xp - s * xq;
+                    wq[i] = s * xp + c * xq;
+                }
+            }
+        if (!rotated) break;
+    }
+    for (int64_t p = 0; p < cols; ++p) {
+        double s2 = 0.0;
+        for (int64_t i = 0; i < rows; ++i) s2 += w[p * rows + i] * w[p * rows + i];
+        out[p] = sqrt(s2);
+    }
+    qsort(out, (size_t)cols, sizeof(double), cmp_desc);
+    free(w);
+}

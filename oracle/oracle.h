@@ -101,6 +101,10 @@ void or_batched_config2(int64_t dim, uint64_t base, int64_t i0, int64_t count, i
 /* Householder thin QR with positive diagonal and rank check (qr.hpp:21-47).
  * q: m x l, r: l x l. Returns OR_OK or OR_RANK_DEFICIENCY (*bad_col 1-based). */
 int or_qr(int64_t m, int64_t l, const double* a, double* q, double* r, int64_t* bad_col);
+/* singular values (non-increasing) of a row-major m x n matrix by one-sided
+ * (Hestenes) Jacobi: the stand-in for Eigen's JacobiSVD/BDCSVD values
+ * (svd.hpp:76-88), a third-party dependency absent here */
+void or_singular_values(int64_t m, int64_t n, const double* a, double* out);
 
 #ifdef __cplusplus
 }

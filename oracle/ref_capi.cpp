@@ -37,12 +37,13 @@ void gemm_rowmajor(const std::complex<double>* a, const std::complex<double>* b,
             c[i * n + j] = acc;
         }
 }
+void singular_values(const double* a, Index m, Index n, double* out) { or_singular_values(m, n, a, out); }
 }  // namespace Eigen::shim
 
 using namespace randla;
 
 namespace {
-enum { RS_OK = 0, RS_DIM = 1, RS_ZERO_PIVOT = 2, RS_LOGIC = 5, RS_OTHER = 9 };
+enum { RS_OK = 0, RS_DIM = 1, RS_ZERO_PIVOT = 2, RS_SINGULAR_BLOCK = 3, RS_LOGIC = 5, RS_SINGULAR = 6, RS_OTHER = 9 };
 
 RealMatrix wrap(int64_t m, int64_t n, const double* p) {
     return RealMatrix(static_cast<std::size_t>(m), static_cast<std::size_t>(n), std::vector<double>(p, p + m * n));
@@ -56,6 +57,11 @@ int guarded(F&& f, int64_t* step = nullptr) {
     } catch (const ZeroPivotError& e) {
         if (step) *step = static_cast<int64_t>(e.step);
         return RS_ZERO_PIVOT;
+    } catch (const SingularPivotBlockError& e) {
+        if (step) *step = static_cast<int64_t>(e.position);
+        return RS_SINGULAR_BLOCK;
+    } catch (const SingularMatrixError&) {
+        return RS_SINGULAR;
     } catch (const DimensionError&) {
         return RS_DIM;
     } catch (const std::logic_error&) {
@@ -267,4 +273,49 @@ int64_t ref_parallel_dense_trials(int64_t n, int64_t trials, const double* a_all
     return nf;
 }
 
+// gepp_factor (lu.hpp:62-98): packed factors (strict lower of `lower`,
+// `upper` on and above the diagonal) and the row permutation
+int ref_gepp_factor(int64_t n, const double* a, double* packed, int64_t* perm) {
+    return guarded([&] {
+        const auto f = gepp_factor(wrap(n, n, a));
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < n; ++j) packed[i * n + j] = j < i ? f.lower(i, j) : f.upper(i, j);
+        for (int64_t i = 0; i < n; ++i) perm[i] = static_cast<int64_t>((*f.perm)[i]);
+    });
+}
+
+// lu_solve / lu_solve_transpose (lu.hpp:100-147) on ref_gepp_factor's output
+int ref_gepp_solve(int64_t n, const double* a, const double* b, double* x, int transpose) {
+    return guarded([&] {
+        const auto f = gepp_factor(wrap(n, n, a));
+        const std::vector<double> bv(b, b + n);
+        const auto y = transpose ? lu_solve_transpose(f, bv) : lu_solve(f, bv);
+        for (int64_t i = 0; i < n; ++i) x[i] = y[i];
+    });
+}
+
+// block_ge_factor(a, split) (block_ge.hpp:168-181) with pivots(), reassemble(),
+// block_solve(b) and the deepest leaf's block_matrix (split.back() squared);
+// *position: SingularPivotBlockError's position
+int ref_block_ge(int64_t n, const double* a, int64_t nsplit, const int64_t* split, const double* b, double* pivots,
+                 double* reassembled, double* x, double* last_leaf, int64_t* position) {
+    return guarded(
+        [&] {
+            std::vector<std::size_t> sp(split, split + nsplit);
+            const auto f = block_ge_factor(wrap(n, n, a), sp);
+            const auto pv = f.pivots();
+            for (int64_t i = 0; i < n; ++i) pivots[i] = pv[i];
+            const RealMatrix r = f.reassemble();
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t j = 0; j < n; ++j) reassembled[i * n + j] = r(i, j);
+            const auto xv = block_solve(f, std::vector<double>(b, b + n));
+            for (int64_t i = 0; i < n; ++i) x[i] = xv[i];
+            const BlockNode<double>* node = f.root.get();
+            while (!node->leaf()) node = node->schur_child.get();
+            const int64_t k = static_cast<int64_t>(node->dim);
+            for (int64_t i = 0; i < k; ++i)
+                for (int64_t j = 0; j < k; ++j) last_leaf[i * k + j] = node->block_matrix(i, j);
+        },
+        position);
+}
 }  // extern "C"

@@ -97,6 +97,10 @@ SIGNATURES = {
     "rl_spectral_norm_estimate": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _dp]),
     "rl_genp_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, ctypes.POINTER(rl_solve_info)]),
     "rl_lu_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
+    "rl_gepp_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp, _vp]),
+    "rl_gepp_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp, _vp, _vp, ctypes.c_int32]),
+    "rl_block_ge_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, i64, _vp, _vp, _vp, _vp, _vp]),
+    "rl_block_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp, _vp, _vp, _vp]),
     "rl_preprocessed_genp_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, ctypes.POINTER(rl_multiplier),
                                                   i64, _vp, _vp, i32, ctypes.POINTER(rl_solve_info)]),
     "rl_batched_genp_solve_32": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

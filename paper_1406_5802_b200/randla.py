@@ -309,7 +309,10 @@ def genp_factor(a):
 
 
 def lu_solve(f, b):
-    """lu_solve (lu.hpp:100-123) on packed factors."""
+    """lu_solve (lu.hpp:100-123) on packed factors (GENP, or GEPP when f.perm
+    is set)."""
+    if isinstance(f, LuFactors) and f.perm is not None:
+        return _gepp_solve(f, b, False)
     lu = f.packed if isinstance(f, LuFactors) else f
     device = _is_device(lu, b)
     n = lu.shape[0]
@@ -321,6 +324,208 @@ def lu_solve(f, b):
     _sync_stream_for(device)
     _raise(capi.lib().rl_lu_solve(_ctx(), _mem(device), n, capi.addr(lu), capi.addr(b), capi.addr(x)))
     return x
+
+
+# ---- block elimination (block_ge.hpp) ----------------------------------------------
+def _index_like(device, n, ref=None):
+    if device:
+        import torch
+        return torch.empty(n, dtype=torch.int64, device=ref.device if ref is not None else "cuda")
+    return np.empty(n, dtype=np.int64)
+
+
+def gepp_factor(a):
+    """gepp_factor (lu.hpp:62-98): partial pivoting (first maximal |u_ij|),
+    bit-identical to the reference; raises SingularMatrixError when the best
+    pivot is <= tol_pivot(n) * spectral_norm_estimate(a)."""
+    device = _is_device(a)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionError("gepp_factor: square input required")
+    n = a.shape[0]
+    a = _dev(a) if device else _host(a)
+    lu = _empty_like_kind(device, (n, n), a)
+    perm = _index_like(device, n, a)
+    step = ctypes.c_int64(0)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_gepp_factor(_ctx(), _mem(device), n, capi.addr(a), capi.addr(lu), capi.addr(perm),
+                                     ctypes.byref(step)), step.value)
+    return LuFactors(lu, perm)
+
+
+def _gepp_solve(f, b, transpose):
+    lu, perm = f.packed, f.perm
+    device = _is_device(lu, b)
+    n = lu.shape[0]
+    if perm is None:  # GENP factors: identity permutation
+        perm = _index_like(device, n, lu)
+        if device:
+            import torch
+            torch.arange(n, out=perm)
+        else:
+            perm[:] = np.arange(n)
+    if b.shape[0] != n:
+        raise DimensionError("lu_solve: length mismatch")
+    nrhs = 1 if b.ndim == 1 else b.shape[1]
+    lu = _dev(lu) if device else _host(lu)
+    b = _dev(b) if device else _host(b)
+    x = _empty_like_kind(device, tuple(b.shape), b)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_gepp_solve(_ctx(), _mem(device), n, nrhs, capi.addr(lu), capi.addr(perm), capi.addr(b),
+                                    capi.addr(x), 1 if transpose else 0))
+    return x
+
+
+def lu_solve_transpose(f, c):
+    """lu_solve_transpose (lu.hpp:127-147): solves A^T x = c from A's factors
+    (GEPP or GENP); c may hold several right-hand sides as columns."""
+    return _gepp_solve(f, c, True)
+
+
+def balanced_split(n):
+    """balanced_split (block_ge.hpp:184-194): halve until scalar blocks."""
+    out, remaining = [], n
+    while remaining > 1:
+        half = remaining // 2
+        out.append(half)
+        remaining -= half
+    out.append(remaining)
+    return out
+
+
+@dataclass
+class BlockNode:
+    """BlockNode (block_ge.hpp:18-35): an internal node eliminates the first
+    pivot_size rows/columns; leaves hold their block and its GEPP factors."""
+    dim: int
+    offset: int
+    pivot_size: int = 0
+    block_matrix: object = None
+    block_lu: object = None
+    db_inv: object = None
+    b_inv_c: object = None
+    pivot_child: object = None
+    schur_child: object = None
+
+    def leaf(self):
+        return self.pivot_size == 0
+
+
+def _copy(x):
+    return x.copy() if isinstance(x, np.ndarray) else x.clone()
+
+
+class BlockFactorization:
+    """BlockFactorization (block_ge.hpp:37-83) over the flat device factors of
+    rl_block_ge_factor: the tree's blocks are copies of their regions."""
+
+    def __init__(self, factors, perm, leaf_blocks, split):
+        self.factors, self.perm, self.split = factors, perm, list(split)
+        n = factors.shape[0]
+        offs, o = [], 0
+        for i, k in enumerate(self.split):
+            offs.append((o, n - o if i + 1 == len(self.split) else k))
+            o += offs[-1][1]
+
+        def leaf(o, k):
+            f = factors[o:o + k, o:o + k]
+            return BlockNode(k, o, 0, _copy(leaf_blocks[o:o + k, o:o + k]), LuFactors(_copy(f), _copy(perm[o:o + k])))
+
+        node = None
+        for o, k in reversed(offs):
+            if node is None:
+                node = leaf(o, k)
+                continue
+            node = BlockNode(n - o, o, k, None, None, _copy(factors[o + k:, o:o + k]), _copy(factors[o:o + k, o + k:]),
+                             leaf(o, k), node)
+        self.root = node
+
+    def pivots(self):
+        """Elimination pivots in order: the leaves' U diagonals (block_ge.hpp:43-48)."""
+        f = self.factors
+        return np.diag(f).copy() if isinstance(f, np.ndarray) else f.diagonal().clone()
+
+    def reassemble(self):
+        """reassemble (block_ge.hpp:50-80): rebuild the input from the tree."""
+        def rec(node):
+            if node.leaf():
+                lu = matmul(node.block_lu.lower, node.block_lu.upper)
+                out = _copy(lu)
+                out[node.block_lu.perm] = lu  # A(perm[i], :) = (L U)(i, :)
+                return out
+            b, sc = rec(node.pivot_child), rec(node.schur_child)
+            c = matmul(b, node.b_inv_c)
+            d = matmul(node.db_inv, b)
+            k = node.pivot_size
+            out = _copy(node.db_inv.new_zeros((node.dim, node.dim)) if not isinstance(b, np.ndarray)
+                        else np.zeros((node.dim, node.dim)))
+            out[:k, :k] = b
+            out[:k, k:] = c
+            out[k:, :k] = d
+            out[k:, k:] = sc + matmul(node.db_inv, c)
+            return out
+        return rec(self.root)
+
+
+def block_ge_factor(a, split):
+    """block_ge_factor (block_ge.hpp:168-181): recursive block elimination
+    along `split` (pivot block sizes in elimination order), the reference's
+    arithmetic order throughout (leaf GEPP, strips by lu_solve /
+    lu_solve_transpose, natural-order Schur complements). Raises
+    DimensionError on a bad split, SingularPivotBlockError(offset + 1) when a
+    pivot block's smallest singular value is <= tol_pivot(n) *
+    spectral_norm_estimate(a), SingularMatrixError from a leaf's GEPP."""
+    device = _is_device(a)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionError("block_ge_factor: square input required")
+    n = a.shape[0]
+    split = [int(k) for k in split]
+    if not split or sum(split) != n:
+        raise DimensionError("block_ge_factor: split must sum to the dimension")
+    if any(k == 0 for k in split):
+        raise DimensionError("block_ge_factor: zero block size")
+    a = _dev(a) if device else _host(a)
+    factors = _empty_like_kind(device, (n, n), a)
+    leaves = _empty_like_kind(device, (n, n), a)
+    perm = _index_like(device, n, a)
+    sp = (ctypes.c_int64 * len(split))(*split)
+    pos = ctypes.c_int64(0)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_block_ge_factor(_ctx(), _mem(device), n, capi.addr(a), len(split), sp, capi.addr(factors),
+                                         capi.addr(perm), capi.addr(leaves), ctypes.byref(pos)), pos.value)
+    return BlockFactorization(factors, perm, leaves, split)
+
+
+def block_solve(f, b):
+    """block_solve (block_ge.hpp:198-201) on a block_ge_factor result."""
+    n = f.factors.shape[0]
+    if b.shape[0] != n:
+        raise DimensionError("block_solve: length mismatch")
+    device = _is_device(f.factors, b)
+    b = _dev(b) if device else _host(b)
+    x = _empty_like_kind(device, (n,), b)
+    sp = (ctypes.c_int64 * len(f.split))(*f.split)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_block_solve(_ctx(), _mem(device), n, len(f.split), sp, capi.addr(f.factors),
+                                     capi.addr(f.perm), capi.addr(b), capi.addr(x)))
+    return x
+
+
+def schur_complement(a, k):
+    """schur_complement (block_ge.hpp:202-218): E - D (B^-1 C) for the leading
+    k x k block B, B factored by gepp_factor (raises SingularMatrixError on a
+    singular leading block); the product D X on the FP64 tensor path."""
+    n = a.shape[0]
+    if a.ndim != 2 or a.shape[1] != n:
+        raise DimensionError("schur_complement: square input required")
+    if k <= 0 or k >= n:
+        raise DimensionError("schur_complement: need 0 < k < n")
+    device = _is_device(a)
+    a = _dev(a) if device else _host(a)
+    b_lu = gepp_factor(_copy(a[:k, :k]) if device else np.ascontiguousarray(a[:k, :k]))
+    c = a[:k, k:].contiguous() if device else np.ascontiguousarray(a[:k, k:])
+    x = _gepp_solve(b_lu, c, False)
+    d = a[k:, :k].contiguous() if device else np.ascontiguousarray(a[k:, :k])
+    return a[k:, k:] - matmul(d, x)
 
 
 # ---- preprocessed solve (preprocess.hpp) -------------------------------------------
