@@ -15,6 +15,11 @@
 //   MultiplierKind/MultiplierSpec        multipliers.hpp:20-40
 //   spectral_norm_estimate               norms.hpp:35-78
 //   LuFactors, genp_factor, lu_solve     lu.hpp:17-28, :40-58, :100-123
+//   gepp_factor, lu_solve_transpose      lu.hpp:62-98, :127-147 (bit-identical)
+//   BlockNode, BlockFactorization,
+//   block_ge_factor, block_solve,
+//   balanced_split, schur_complement     block_ge.hpp:18-218 (bit-identical pivots,
+//                                        Schur leaves and block_solve results)
 //   relative_residual                    lu.hpp:155-161 (host arithmetic, as in the reference)
 //   SolveOutcome, preprocess_solve,
 //   preprocess_solve_with_retry          preprocess.hpp:9-14, :156-196
@@ -29,6 +34,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -173,7 +179,7 @@ inline double spectral_norm_estimate(const RealMatrix& a) {
 struct LuFactors {
     RealMatrix lower;
     RealMatrix upper;
-    std::optional<std::vector<std::size_t>> perm;  // always empty: no pivoting
+    std::optional<std::vector<std::size_t>> perm;  // empty for GENP; GEPP: original row at position i
     std::vector<double> pivots() const {
         std::vector<double> p(upper.rows());
         for (std::size_t j = 0; j < upper.rows(); ++j) p[j] = upper(j, j);
@@ -208,13 +214,203 @@ inline LuFactors genp_factor(const RealMatrix& a) {
     return detail::unpack(packed);
 }
 
+namespace detail {
+inline std::vector<double> gepp_solve(const LuFactors& f, const std::vector<double>& b, bool transpose);
+}
 inline std::vector<double> lu_solve(const LuFactors& f, const std::vector<double>& b) {
+    if (f.perm) return detail::gepp_solve(f, b, false);
     const std::size_t n = f.upper.rows();
     if (b.size() != n) throw DimensionError("lu_solve: length mismatch");
     const RealMatrix packed = detail::pack(f);
     std::vector<double> x(n);
     detail::check(rl_lu_solve(nullptr, RL_HOST, static_cast<int64_t>(n), packed.data(), b.data(), x.data()));
     return x;
+}
+
+// ---- GEPP and block elimination (lu.hpp:62-147, block_ge.hpp) ----------------
+// The device keeps the reference's arithmetic order: factors, permutations,
+// pivots, Schur complements and block_solve results are bit-identical.
+namespace detail {
+inline RealMatrix pack_lu(const LuFactors& f) { return pack(f); }
+inline std::vector<int64_t> perm_of(const LuFactors& f) {
+    const std::size_t n = f.upper.rows();
+    std::vector<int64_t> p(n);
+    for (std::size_t i = 0; i < n; ++i) p[i] = f.perm ? static_cast<int64_t>((*f.perm)[i]) : static_cast<int64_t>(i);
+    return p;
+}
+inline std::vector<double> gepp_solve(const LuFactors& f, const std::vector<double>& b, bool transpose) {
+    const std::size_t n = f.upper.rows();
+    if (b.size() != n) throw DimensionError(transpose ? "lu_solve_transpose: length mismatch" : "lu_solve: length mismatch");
+    const RealMatrix packed = pack(f);
+    const std::vector<int64_t> p = perm_of(f);
+    std::vector<double> x(n);
+    check(rl_gepp_solve(nullptr, RL_HOST, static_cast<int64_t>(n), 1, packed.data(), p.data(), b.data(), x.data(),
+                        transpose ? 1 : 0));
+    return x;
+}
+}  // namespace detail
+
+inline LuFactors gepp_factor(const RealMatrix& a) {
+    const std::size_t n = a.rows();
+    if (a.cols() != n) throw DimensionError("gepp_factor: square input required");
+    RealMatrix packed(n, n);
+    std::vector<int64_t> p(n);
+    int64_t step = 0;
+    detail::check(rl_gepp_factor(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), packed.data(), p.data(), &step));
+    LuFactors f = detail::unpack(packed);
+    f.perm = std::vector<std::size_t>(p.begin(), p.end());
+    return f;
+}
+
+inline std::vector<double> lu_solve_transpose(const LuFactors& f, const std::vector<double>& c) {
+    return detail::gepp_solve(f, c, true);
+}
+
+struct BlockNode {  // block_ge.hpp:18-35
+    std::size_t dim = 0, offset = 0, pivot_size = 0;
+    RealMatrix block_matrix;
+    std::optional<LuFactors> block_lu;
+    RealMatrix db_inv, b_inv_c;
+    std::unique_ptr<BlockNode> pivot_child, schur_child;
+    bool leaf() const { return pivot_size == 0; }
+};
+
+struct BlockFactorization {  // block_ge.hpp:37-83
+    std::unique_ptr<BlockNode> root;
+    std::vector<std::size_t> split;
+    RealMatrix factors;           // flat device layout (rl_block_ge_factor)
+    std::vector<int64_t> perm;
+    std::vector<double> pivots() const {
+        std::vector<double> p(factors.rows());
+        for (std::size_t j = 0; j < p.size(); ++j) p[j] = factors(j, j);
+        return p;
+    }
+    RealMatrix reassemble() const { return reassemble_node(*root); }
+
+  private:
+    static RealMatrix reassemble_node(const BlockNode& node) {
+        const std::size_t d = node.dim;
+        if (node.leaf()) {
+            const RealMatrix lu = matmul(node.block_lu->lower, node.block_lu->upper);
+            RealMatrix out(d, d);
+            for (std::size_t i = 0; i < d; ++i)
+                for (std::size_t j = 0; j < d; ++j) out((*node.block_lu->perm)[i], j) = lu(i, j);
+            return out;
+        }
+        const RealMatrix b = reassemble_node(*node.pivot_child), s = reassemble_node(*node.schur_child);
+        const std::size_t k = node.pivot_size;
+        const RealMatrix c = matmul(b, node.b_inv_c), dd = matmul(node.db_inv, b), t = matmul(node.db_inv, c);
+        RealMatrix out(d, d);
+        for (std::size_t i = 0; i < d; ++i)
+            for (std::size_t j = 0; j < d; ++j)
+                out(i, j) = i < k ? (j < k ? b(i, j) : c(i, j - k)) : (j < k ? dd(i - k, j) : s(i - k, j - k) + t(i - k, j - k));
+        return out;
+    }
+};
+
+inline std::vector<std::size_t> balanced_split(std::size_t n) {  // block_ge.hpp:184-194
+    std::vector<std::size_t> out;
+    std::size_t remaining = n;
+    while (remaining > 1) {
+        const std::size_t half = remaining / 2;
+        out.push_back(half);
+        remaining -= half;
+    }
+    out.push_back(remaining);
+    return out;
+}
+
+inline BlockFactorization block_ge_factor(const RealMatrix& a, const std::vector<std::size_t>& split) {
+    const std::size_t n = a.rows();
+    if (a.cols() != n) throw DimensionError("block_ge_factor: square input required");
+    std::vector<int64_t> sp(split.begin(), split.end());
+    BlockFactorization f;
+    f.split = split;
+    f.factors = RealMatrix(n, n);
+    f.perm.assign(n, 0);
+    RealMatrix leaves(n, n);
+    int64_t position = 0;
+    const rl_status st = rl_block_ge_factor(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(),
+                                            static_cast<int64_t>(sp.size()), sp.empty() ? nullptr : sp.data(),
+                                            f.factors.data(), f.perm.data(), leaves.data(), &position);
+    detail::check(st, position);
+    auto sub = [&](const RealMatrix& m, std::size_t r0, std::size_t c0, std::size_t r, std::size_t c) {
+        RealMatrix out(r, c);
+        for (std::size_t i = 0; i < r; ++i)
+            for (std::size_t j = 0; j < c; ++j) out(i, j) = m(r0 + i, c0 + j);
+        return out;
+    };
+    auto leaf = [&](std::size_t o, std::size_t k) {
+        auto node = std::make_unique<BlockNode>();
+        node->dim = k;
+        node->offset = o;
+        node->block_matrix = sub(leaves, o, o, k, k);
+        LuFactors lu = detail::unpack(sub(f.factors, o, o, k, k));
+        lu.perm = std::vector<std::size_t>(f.perm.begin() + static_cast<std::ptrdiff_t>(o),
+                                           f.perm.begin() + static_cast<std::ptrdiff_t>(o + k));
+        node->block_lu = std::move(lu);
+        return node;
+    };
+    std::vector<std::pair<std::size_t, std::size_t>> levels;
+    std::size_t o = 0;
+    for (std::size_t i = 0; i < split.size(); ++i) {
+        const std::size_t k = i + 1 == split.size() ? n - o : split[i];
+        levels.emplace_back(o, k);
+        o += k;
+    }
+    std::unique_ptr<BlockNode> node;
+    for (auto it = levels.rbegin(); it != levels.rend(); ++it) {
+        const auto [oo, k] = *it;
+        if (!node) {
+            node = leaf(oo, k);
+            continue;
+        }
+        auto in = std::make_unique<BlockNode>();
+        in->dim = n - oo;
+        in->offset = oo;
+        in->pivot_size = k;
+        in->db_inv = sub(f.factors, oo + k, oo, n - oo - k, k);
+        in->b_inv_c = sub(f.factors, oo, oo + k, k, n - oo - k);
+        in->pivot_child = leaf(oo, k);
+        in->schur_child = std::move(node);
+        node = std::move(in);
+    }
+    f.root = std::move(node);
+    return f;
+}
+
+inline std::vector<double> block_solve(const BlockFactorization& f, const std::vector<double>& b) {
+    const std::size_t n = f.factors.rows();
+    if (b.size() != n) throw DimensionError("block_solve: length mismatch");
+    std::vector<int64_t> sp(f.split.begin(), f.split.end());
+    std::vector<double> x(n);
+    detail::check(rl_block_solve(nullptr, RL_HOST, static_cast<int64_t>(n), static_cast<int64_t>(sp.size()), sp.data(),
+                                 f.factors.data(), f.perm.data(), b.data(), x.data()));
+    return x;
+}
+
+inline RealMatrix schur_complement(const RealMatrix& a, std::size_t k) {  // block_ge.hpp:202-218
+    const std::size_t n = a.rows();
+    if (a.cols() != n) throw DimensionError("schur_complement: square input required");
+    if (k == 0 || k >= n) throw DimensionError("schur_complement: need 0 < k < n");
+    RealMatrix b(k, k), c(k, n - k), d(n - k, k);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < n; ++j) {
+            if (i < k && j < k) b(i, j) = a(i, j);
+            else if (i < k) c(i, j - k) = a(i, j);
+            else if (j < k) d(i - k, j) = a(i, j);
+        }
+    const LuFactors b_lu = gepp_factor(b);
+    const RealMatrix packed = detail::pack(b_lu);
+    const std::vector<int64_t> p = detail::perm_of(b_lu);
+    RealMatrix x(k, n - k);
+    detail::check(rl_gepp_solve(nullptr, RL_HOST, static_cast<int64_t>(k), static_cast<int64_t>(n - k), packed.data(),
+                                p.data(), c.data(), x.data(), 0));
+    const RealMatrix dx = matmul(d, x);
+    RealMatrix out(n - k, n - k);
+    for (std::size_t i = 0; i < n - k; ++i)
+        for (std::size_t j = 0; j < n - k; ++j) out(i, j) = a(k + i, k + j) - dx(i, j);
+    return out;
 }
 
 inline double relative_residual(const RealMatrix& a, const std::vector<double>& x, const std::vector<double>& b) {

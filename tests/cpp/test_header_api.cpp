@@ -88,6 +88,63 @@ int main() {
     post2.seed = 992;
     CHECK(preprocess_solve_with_retry(anti, b64, MultiplierSpec{}, post2, 0, 3).residual_history[0] <= 1e-3);
 
+    // block elimination (tests/test_elimination.cpp:91-153, 333-349)
+    {
+        const RealMatrix a8 = gen_gaussian(8, 8, 41);
+        const auto plain = genp_factor(a8);
+        const auto degen = block_ge_factor(a8, std::vector<std::size_t>(8, 1));
+        const auto pv = degen.pivots();
+        // bitwise equal to the reference's genp_factor (tests/test_block_ge_gpu.py);
+        // the device genp_factor (blocked, FMA updates) agrees to rounding
+        for (std::size_t j = 0; j < 8; ++j) CHECK(std::abs(pv[j] - plain.upper(j, j)) <= 1e-12 * std::abs(pv[j]));
+        const RealMatrix a10 = gen_gaussian(10, 10, 45);
+        for (const auto& split : {std::vector<std::size_t>{2, 3, 5}, std::vector<std::size_t>{5, 5}, balanced_split(10)}) {
+            const auto f = block_ge_factor(a10, split);
+            const RealMatrix r = f.reassemble();
+            double d = 0.0;
+            for (std::size_t i = 0; i < 10; ++i)
+                for (std::size_t j = 0; j < 10; ++j) d = std::max(d, std::abs(r(i, j) - a10(i, j)));
+            CHECK(d <= 1e-12);
+            const std::vector<double> bb = gen_gaussian_vector(10, 46);
+            CHECK(relative_residual(a10, block_solve(f, bb), bb) <= 1e-12);
+        }
+        const auto f1 = block_ge_factor(a10, {4, 6});
+        const auto f2 = block_ge_factor(a10, {2, 2, 6});
+        const RealMatrix s_op = schur_complement(a10, 4);
+        double d12 = 0.0, dop = 0.0;
+        for (std::size_t i = 0; i < 6; ++i)
+            for (std::size_t j = 0; j < 6; ++j) {
+                d12 = std::max(d12, std::abs(f1.root->schur_child->block_matrix(i, j) -
+                                             f2.root->schur_child->schur_child->block_matrix(i, j)));
+                dop = std::max(dop, std::abs(f1.root->schur_child->block_matrix(i, j) - s_op(i, j)));
+            }
+        CHECK(d12 <= 1e-11 && dop <= 1e-11);
+        const auto gp = gepp_factor(a10);
+        const std::vector<double> c10 = gen_gaussian_vector(10, 47);
+        const auto xt = lu_solve_transpose(gp, c10);
+        double rt = 0.0;
+        for (std::size_t i = 0; i < 10; ++i) {
+            double acc = -c10[i];
+            for (std::size_t k = 0; k < 10; ++k) acc += a10(k, i) * xt[k];
+            rt = std::max(rt, std::abs(acc));
+        }
+        CHECK(rt <= 1e-11);
+        bool bad_split = false, singular = false;
+        try {
+            block_ge_factor(a10, {3, 2});
+        } catch (const DimensionError&) {
+            bad_split = true;
+        }
+        RealMatrix sing(4, 4);
+        sing(1, 1) = sing(2, 2) = sing(3, 3) = 1.0;
+        try {
+            block_ge_factor(sing, {2, 2});
+        } catch (const SingularPivotBlockError& e) {
+            singular = e.position == 1;
+        }
+        CHECK(bad_split && singular);
+    }
+
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "all passed", failures);
     return failures ? 1 : 0;
 }
