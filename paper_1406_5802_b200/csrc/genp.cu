@@ -201,6 +201,10 @@ trsm_lower_unit_kernel_dyn(const double* __restrict__ l, int64_t ldl, int w, dou
 // factored diagonal block and the pivots. One launch per elimination step;
 // the trailing update A22 -= L21 U12 is one DMMA GEMM (K = 64).
 constexpr int PT = 128;  // threads per CTA
+#ifndef RL_PANEL_Q4_ROWS
+#define RL_PANEL_Q4_ROWS 2048
+#endif
+constexpr int64_t kPanelQ4Rows = RL_PANEL_Q4_ROWS;
 
 // GENP of the 64x64 block in sd (lu.hpp:47-56 order) with a rolled loop: a
 // panel kernel runs this code once per CTA, so a fully unrolled version is
@@ -353,6 +357,7 @@ __device__ __forceinline__ void mm64_rows2(const double* M, int ldm, const doubl
 //   half 1: [-Lb^-1 (L_ba La^-1), Lb^-1] in rows 64..127 (L_ba: rows c0.., the
 //           previous sub-panel's L21 columns; La^-1 from the half-0 launch)
 // so U12 of the super-panel is one K = 128 GEMM.
+template <int Q>
 __global__ void __launch_bounds__(PT)
 lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
                   double* __restrict__ piv_out, double* __restrict__ rinv_out, double* __restrict__ inv128, int half) {
@@ -436,24 +441,30 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     }
     const int64_t rest = n - c0 - kBase;
     if (b < row_ctas) {
-        const int64_t r = c0 + kBase + static_cast<int64_t>(b) * PT + tid;
-        if (r >= n) return;
-        double2* rowp = reinterpret_cast<double2*>(a + r * lda + c0);
-        double x[kBase];
+        // Q threads per row (lanes q = 0..Q-1 of a group), thread q holding
+        // columns q, q + Q, ...: the owner of column j divides, the group
+        // shares the quotient by a shuffle, each thread updates its columns.
+        // Same operations per element in the same order as Q = 1.
+        constexpr int RPC = PT / Q, NS = kBase / Q;
+        const int q = tid % Q, lane = tid & 31;
+        const int64_t r = c0 + kBase + static_cast<int64_t>(b) * RPC + tid / Q;
+        if (r >= n) return;  // whole groups leave together
+        const unsigned gm = Q == 1 ? 1u << lane : ((1u << Q) - 1u) << (lane & ~(Q - 1));
+        double* rowp = a + r * lda + c0;
+        double x[NS];
 #pragma unroll
-        for (int m = 0; m < kBase / 2; ++m) {
-            const double2 v = rowp[m];
-            x[2 * m] = v.x;
-            x[2 * m + 1] = v.y;
-        }
+        for (int s2 = 0; s2 < NS; ++s2) x[s2] = rowp[q + Q * s2];
 #pragma unroll
         for (int j = 0; j < kBase; ++j) {
-            x[j] = div_by(x[j], sp[j], sr[j]);
+            const int s = j / Q, owner = j % Q;
+            if (q == owner) x[s] = div_by(x[s], sp[j], sr[j]);
+            const double xj = Q == 1 ? x[s] : __shfl_sync(gm, x[s], (lane & ~(Q - 1)) | owner);
+            if (q > owner) x[s] = fma(-xj, sd[j][q + Q * s], x[s]);
 #pragma unroll
-            for (int k = j + 1; k < kBase; ++k) x[k] = fma(-x[j], sd[j][k], x[k]);
+            for (int s2 = s + 1; s2 < NS; ++s2) x[s2] = fma(-xj, sd[j][q + Q * s2], x[s2]);
         }
 #pragma unroll
-        for (int m = 0; m < kBase / 2; ++m) rowp[m] = make_double2(x[2 * m], x[2 * m + 1]);
+        for (int s2 = 0; s2 < NS; ++s2) rowp[q + Q * s2] = x[s2];
 #ifdef RL_PANEL_PHASES
         if (tid == 0 && b == 0) atomicExch(&g_panel_phase[2], static_cast<unsigned long long>(clock64() - t2));
 #endif
@@ -641,7 +652,9 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     static PerDeviceOnce inv_configured_once;
     {
         const rl_status cst = once_per_device(inv_configured_once, [&]() -> rl_status {
-            RL_CUDA(cudaFuncSetAttribute(lu_panel64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvFusedSmem));
+            RL_CUDA(cudaFuncSetAttribute(lu_panel64_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvFusedSmem));
+            RL_CUDA(cudaFuncSetAttribute(lu_panel64_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvFusedSmem));
+            RL_CUDA(cudaFuncSetAttribute(lu_panel64_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvFusedSmem));
             return RL_OK;
         });
         if (cst != RL_OK) return cst;
@@ -660,10 +673,19 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     // panel: factor the diagonal block and L21 = A21 U11^-1 by substitution;
     // the extra CTA fills this half of the super-panel's L11^-1
     auto panel_l = [&](cudaStream_t sm, int64_t c0) -> rl_status {
+        // late panels sit on the exposed lookahead chain with idle SMs: more
+        // threads per row shorten the L21 substitution (RL_PANEL_Q4_ROWS)
         const int64_t rest = n - c0 - kBase;
-        const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-        lu_panel64_kernel<<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0),
-                                                                  static_cast<int>((c0 / kBase) & 1));
+        const int q = rest <= kPanelQ4Rows ? 4 : (rest <= 2 * kPanelQ4Rows ? 2 : 1);
+        const int rpc = PT / q;
+        const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + rpc - 1) / rpc));
+        const int half = static_cast<int>((c0 / kBase) & 1);
+        if (q == 4)
+            lu_panel64_kernel<4><<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0), half);
+        else if (q == 2)
+            lu_panel64_kernel<2><<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0), half);
+        else
+            lu_panel64_kernel<1><<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0), half);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         return RL_OK;
     };
@@ -766,7 +788,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         auto panel_l = [&](int64_t c0) -> rl_status {
             const int64_t rest = n - c0 - kBase;
             const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-            lu_panel64_kernel<<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr, 0);
+            lu_panel64_kernel<1><<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr, 0);
             RL_CHECK_LAUNCH("lu_panel64_kernel");
             return RL_OK;
         };
@@ -818,7 +840,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
     for (; c0 + kBase <= n; c0 += kBase) {
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>((rest + PT - 1) / PT);
-        lu_panel64_kernel<<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out,
+        lu_panel64_kernel<1><<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out,
                                                                         nullptr, 0);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         if (rest > 0) {
