@@ -549,6 +549,39 @@ __device__ __forceinline__ void dit(cplx* z, double* __restrict__ y, int l, doub
     using S = Shape<L>;
     constexpr int M = N / R, groups = S::m / R;
     constexpr int64_t tstride = S::n / N;
+    if constexpr (kGlobal && N == S::m && M > 1) {
+        // pruned last pass when the first l outputs (q < ceil(l/2) <= M) all
+        // come from output r = 0 of the groups n0 < ceil(l/2): only that
+        // output, the DC term of the twiddled inputs, summed in dft_reg's order
+        const int ql = (l + 1) / 2;
+        if (ql <= M) {
+            for (int n0 = threadIdx.x; n0 < ql; n0 += S::T) {
+                cplx w[R];
+                if (twc)
+                    cached_twiddles<R>(w, twc, n0, M);
+                else
+                    base_twiddles<R>(w, tw, static_cast<int64_t>(n0) * tstride, S::n - 1);
+                cplx v[R];
+                v[0] = z[swz<L>(n0)];
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    lazy_twiddle<R>(w, r);
+                    v[r] = cmulc(z[swz<L>(n0 + r * M)], w[r]);
+                }
+#pragma unroll
+                for (int half = R / 2; half >= 1; half >>= 1)
+#pragma unroll
+                    for (int j = 0; j < half; ++j) v[j] = cadd(v[j], v[j + half]);
+                const cplx t = v[0];
+                if (2 * n0 + 1 < l) {
+                    __stcs(reinterpret_cast<double2*>(y) + n0, make_double2(t.x * scale, t.y * scale));
+                } else {
+                    y[2 * n0] = t.x * scale;
+                }
+            }
+            return;
+        }
+    }
 #pragma unroll
     for (int g0 = 0; g0 < groups; g0 += S::T) {
         const int g = g0 + threadIdx.x;

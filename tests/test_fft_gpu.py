@@ -33,7 +33,9 @@ def test_circulant_vs_oracle(cuda, orc, m, n):
 
 
 @pytest.mark.parametrize("m,k,np_,l", [(3, 48, 64, 20), (8, 1000, 1024, 256), (5, 8192, 8192, 64),
-                                       (4, 16384, 16384, 256), (7, 12000, 16384, 256), (3, 10, 12, 5)])
+                                       (4, 16384, 16384, 256), (7, 12000, 16384, 256), (3, 10, 12, 5),
+                                       (2, 8192, 8192, 77), (2, 8192, 8192, 512), (2, 8192, 8192, 513),
+                                       (2, 16384, 16384, 1)])
 def test_toeplitz_vs_oracle(cuda, orc, m, k, np_, l):
     a = orc.C.gen_gaussian(m, k, 17 + k)
     c = orc.C.gen_gaussian_vector(np_, 21)
