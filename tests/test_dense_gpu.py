@@ -31,7 +31,7 @@ def test_genp_kats(cuda):
     assert f.lower[0, 1] == 0.0
 
 
-@pytest.mark.parametrize("n", [5, 64, 65, 200, 511, 1024])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 64, 65, 127, 128, 129, 200, 511, 1024])
 def test_genp_factor_vs_oracle(cuda, orc, n):
     a = orc.C.gen_gaussian(n, n, 100 + n)
     g = orc.C.gen_gaussian(n, n, 200 + n)
