@@ -372,6 +372,16 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     cudaStream_t s = ctx->stream;
     // seeded dense multiplier: generated on the device (exact); its kernels are
     // enqueued first so that they run under the upload of A
+    // host A is uploaded in row blocks on the side stream, which waits only for
+    // this stream's earlier work (workspace reuse) — not for the generator
+    // kernels enqueued next, so block 0 lands under them
+    constexpr int kChunks = 4;
+    const bool pipelined_a = own_a && host && n >= 1024 && side_resources(ctx, kChunks) == RL_OK;
+    if (pipelined_a) {
+        cudaEvent_t start = ctx->events[kChunks - 1];
+        RL_CUDA(cudaEventRecord(start, s));
+        RL_CUDA(cudaStreamWaitEvent(ctx->hi_stream, start, 0));
+    }
     GaussJob gjob;
     const bool gen_g = kind == RL_MULT_GAUSSIAN && !post->dense;
     if (gen_g && (st = gjob.begin(ctx, n, n, post->seed, D.G, ld)) != RL_OK) return st;
@@ -387,11 +397,7 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     if (own_a) {
         // host A: uploaded in row blocks on the side stream; the product of
         // block c starts as soon as block c has landed
-        constexpr int kChunks = 4;
-        if (host && n >= 1024 && side_resources(ctx, kChunks) == RL_OK) {
-            cudaEvent_t start = ctx->events[kChunks - 1];
-            RL_CUDA(cudaEventRecord(start, s));  // workspace reuse: after this stream's earlier work
-            RL_CUDA(cudaStreamWaitEvent(ctx->hi_stream, start, 0));
+        if (pipelined_a) {
             D.a_chunks = kChunks;
             D.a_chunk_rows = (n + kChunks - 1) / kChunks;
             D.a_ready = ctx->events;

@@ -356,13 +356,35 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
             att = att_v.data();
             hv = hv_v.data();
         }
-        RL_CUDA(cudaMemcpyAsync(att, attempts, 8 * nh, cudaMemcpyDeviceToHost, s));
-        RL_CUDA(cudaStreamSynchronize(s));
-        host_polar_pairs(seed, att, nh, hv);
-        RL_CUDA(cudaMemcpyAsync(vals, hv, 16 * nh, cudaMemcpyHostToDevice, s));
-        scatter_kernel<<<static_cast<unsigned>((nh + 255) / 256), 256, 0, s>>>(pair, vals, nh, count, out,
-                                                                               Pos{rows, cols, ld});
-        RL_CHECK_LAUNCH("scatter_kernel");
+        // pipelined in chunks: the attempt lists come down (copy engine D2H),
+        // chunk c is finished on the host while chunk c-1's values go up
+        // (H2D engine) and are scattered
+        constexpr int kMaxChunks = 4;
+        const int nchunks = nh >= 4 * 65536 ? kMaxChunks : 1;
+        const int64_t cs = (nh + nchunks - 1) / nchunks;
+        cudaEvent_t ev[kMaxChunks];
+        for (int c = 0; c < nchunks; ++c) RL_CUDA(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming));
+        struct Ev {
+            cudaEvent_t* e;
+            int n;
+            ~Ev() {
+                for (int c = 0; c < n; ++c) cudaEventDestroy(e[c]);
+            }
+        } ev_guard{ev, nchunks};
+        for (int c = 0; c < nchunks; ++c) {
+            const int64_t o = c * cs, k = std::min(cs, nh - o);
+            RL_CUDA(cudaMemcpyAsync(att + o, attempts + o, 8 * k, cudaMemcpyDeviceToHost, s));
+            RL_CUDA(cudaEventRecord(ev[c], s));
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            const int64_t o = c * cs, k = std::min(cs, nh - o);
+            RL_CUDA(cudaEventSynchronize(ev[c]));
+            host_polar_pairs(seed, att + o, k, hv + 2 * o);
+            RL_CUDA(cudaMemcpyAsync(vals + 2 * o, hv + 2 * o, 16 * k, cudaMemcpyHostToDevice, s));
+            scatter_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(pair + o, vals + 2 * o, k, count, out,
+                                                                                  Pos{rows, cols, ld});
+            RL_CHECK_LAUNCH("scatter_kernel");
+        }
         // the staging buffer is reused by the next call: the copy must be done
         RL_CUDA(cudaStreamSynchronize(s));
     }

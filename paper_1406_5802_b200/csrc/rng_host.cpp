@@ -21,6 +21,9 @@
 #include <cmath>
 #include <cstdint>
 #include <thread>
+#include <mutex>
+#include <condition_variable>
+#include <functional>
 #include <vector>
 
 #include "../../include/randla_capi.h"
@@ -64,6 +67,76 @@ int thread_count() {
     return std::max(1, t);
 }
 
+// Persistent worker pool: parallel_for hands out indices to workers that
+// stay alive between calls (spawning threads per call costs ~0.3 ms, a
+// noticeable share of the device generator's host-decided tail). Every pool
+// thread joins every call; the caller drains too.
+class Pool {
+  public:
+    static Pool& get() {
+        static Pool p;
+        return p;
+    }
+    void run(int helpers, int64_t count, const std::function<void(int64_t)>& fn) {
+        std::lock_guard<std::mutex> call(call_mu_);  // one parallel_for at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            while (static_cast<int>(threads_.size()) < helpers) threads_.emplace_back([this] { loop(); });
+            fn_ = &fn;
+            count_ = count;
+            next_.store(0);
+            pending_ = static_cast<int>(threads_.size());
+            ++gen_;
+        }
+        cv_.notify_all();
+        drain();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+
+  private:
+    void drain() {
+        for (int64_t i = next_.fetch_add(1); i < count_; i = next_.fetch_add(1)) (*fn_)(i);
+    }
+    void loop() {
+        uint64_t seen = 0;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            seen = gen_ - 1;  // created for the call in progress: join it
+        }
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            drain();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> threads_;
+    const std::function<void(int64_t)>* fn_ = nullptr;
+    int64_t count_ = 0;
+    std::atomic<int64_t> next_{0};
+    int pending_ = 0;
+    uint64_t gen_ = 1;
+    bool stop_ = false;
+};
+
 template <typename F>
 void parallel_for(int64_t count, F&& fn) {
     const int workers = static_cast<int>(std::min<int64_t>(thread_count(), count));
@@ -71,14 +144,8 @@ void parallel_for(int64_t count, F&& fn) {
         for (int64_t i = 0; i < count; ++i) fn(i);
         return;
     }
-    std::atomic<int64_t> next{0};
-    std::vector<std::thread> pool;
-    pool.reserve(workers);
-    for (int w = 0; w < workers; ++w)
-        pool.emplace_back([&] {
-            for (int64_t i = next.fetch_add(1); i < count; i = next.fetch_add(1)) fn(i);
-        });
-    for (auto& t : pool) t.join();
+    const std::function<void(int64_t)> f = [&](int64_t i) { fn(i); };
+    Pool::get().run(workers - 1, count, f);
 }
 
 // Sequential generator (small matrices): exactly RngStream::next_gaussian.

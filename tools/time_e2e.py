@@ -6,6 +6,9 @@ import numpy as np
 import torch
 import paper_1406_5802_b200 as rl
 from paper_1406_5802_b200 import capi
+if os.environ.get('RANDLA_VARIANT_LIB'):  # dev A/B: a variant library from tools/build_variant.sh
+    capi.LIB_PATH = os.environ['RANDLA_VARIANT_LIB']
+    capi._lib = None
 L = capi.lib()
 n = 8192
 g = torch.empty(n, n, dtype=torch.float64, device="cuda")
