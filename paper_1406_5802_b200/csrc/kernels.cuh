@@ -79,6 +79,8 @@ struct GaussJob {
     uint64_t* attempts = nullptr;
     double* vals = nullptr;
     int64_t h_total = 0, h_hard = 0;  // host copies (pageable; valid after finish's sync)
+    int64_t nb1 = 0;                    // gen runs as blocks [0, nb1) then [nb1, nb)
+    cudaEvent_t ev1 = nullptr, ev2 = nullptr;  // after each half (with its hard-case count)
     rl_status begin(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld);
     rl_status finish(int64_t* hard_cases);
     ~GaussJob();

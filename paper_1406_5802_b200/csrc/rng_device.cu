@@ -214,10 +214,12 @@ struct Hard {
 };
 
 __global__ void __launch_bounds__(GT) gen_kernel(uint64_t state0, const int64_t* __restrict__ offsets,
-                                                 int64_t count, double* __restrict__ out, Pos pos, Hard hard) {
-    const uint64_t a0 = (static_cast<uint64_t>(blockIdx.x) * GT + threadIdx.x) * PER_THREAD;
+                                                 int64_t count, double* __restrict__ out, Pos pos, Hard hard,
+                                                 int64_t block0) {
+    const int64_t bx = block0 + blockIdx.x;
+    const uint64_t a0 = (static_cast<uint64_t>(bx) * GT + threadIdx.x) * PER_THREAD;
     const int64_t pairs = (count + 1) / 2;
-    const int64_t boff = offsets[blockIdx.x];
+    const int64_t boff = offsets[bx];
     if (boff >= pairs) return;
     unsigned mask = 0;
 #pragma unroll 4
@@ -310,12 +312,25 @@ rl_status GaussJob::begin(rl_context* c, int64_t r, int64_t cl, uint64_t sd, dou
     RL_CHECK_LAUNCH("count_kernel");
     scan_kernel<<<1, 1024, 0, s>>>(counts, nb, offsets);
     RL_CHECK_LAUNCH("scan_kernel");
-    gen_kernel<<<static_cast<unsigned>(nb), GT, 0, s>>>(state0, offsets, count, out, Pos{rows, cols, ld},
-                                                        Hard{hcount, attempts, pair, cap});
-    RL_CHECK_LAUNCH("gen_kernel");
-    // pinned readback slots: the copies stay asynchronous
+    // pinned readback slots: the copies stay asynchronous. The generator runs
+    // in two halves so the host can finish the first half's undecided
+    // attempts while the second half generates.
     RL_CUDA(cudaMemcpyAsync(ctx->host_scalars + 0, offsets + nb, 8, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+    RL_CUDA(cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming));
+    nb1 = nb / 2;
+    if (nb1 > 0) {
+        gen_kernel<<<static_cast<unsigned>(nb1), GT, 0, s>>>(state0, offsets, count, out, Pos{rows, cols, ld},
+                                                             Hard{hcount, attempts, pair, cap}, 0);
+        RL_CHECK_LAUNCH("gen_kernel");
+    }
+    RL_CUDA(cudaMemcpyAsync(ctx->host_scalars + 2, hcount, 8, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaEventRecord(ev1, s));
+    gen_kernel<<<static_cast<unsigned>(nb - nb1), GT, 0, s>>>(state0, offsets, count, out, Pos{rows, cols, ld},
+                                                              Hard{hcount, attempts, pair, cap}, nb1);
+    RL_CHECK_LAUNCH("gen_kernel");
     RL_CUDA(cudaMemcpyAsync(ctx->host_scalars + 1, hcount, 8, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaEventRecord(ev2, s));
     return RL_OK;
 }
 
@@ -325,40 +340,23 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
     if (count <= 0) return RL_OK;
     cudaStream_t s = ctx->stream;
     const int64_t pairs = (count + 1) / 2;
-    RL_CUDA(cudaStreamSynchronize(s));
-    h_total = ctx->host_scalars[0];
-    h_hard = static_cast<int64_t>(ctx->host_scalars[1]);
-    if (h_total < pairs || h_hard > cap) {
-        // astronomically unlikely: too few accepted attempts, or too many hard
-        // cases for the list; generate on the host and upload
-        std::vector<double> hg(static_cast<size_t>(count));
-        rl_gen_gaussian(rows, cols, seed, hg.data());
-        RL_CUDA(cudaMemcpy2DAsync(out, ld * 8, hg.data(), cols * 8, cols * 8, rows, cudaMemcpyHostToDevice, s));
-        RL_CUDA(cudaStreamSynchronize(s));
-        if (hard_cases) *hard_cases = -1;
-        return RL_OK;
-    }
-    const int64_t nh = h_hard;
-    if (hard_cases) *hard_cases = nh;
-    if (nh > 0) {
-        // pinned staging: attempt indices in, (u f, v f) pairs out
-        char* stage = static_cast<char*>(pinned_staging(ctx, 24 * static_cast<size_t>(nh)));
-        std::vector<uint64_t> att_v;
-        std::vector<double> hv_v;
-        uint64_t* att;
-        double* hv;
-        if (stage) {
-            att = reinterpret_cast<uint64_t*>(stage);
-            hv = reinterpret_cast<double*>(stage + 8 * nh);
-        } else {
-            att_v.resize(static_cast<size_t>(nh));
-            hv_v.resize(static_cast<size_t>(2 * nh));
-            att = att_v.data();
-            hv = hv_v.data();
+    // pinned staging for every possible hard case: attempt indices in, (u f, v f) out
+    char* stage = static_cast<char*>(pinned_staging(ctx, 24 * static_cast<size_t>(cap)));
+    uint64_t* att = stage ? reinterpret_cast<uint64_t*>(stage) : nullptr;
+    double* hv = stage ? reinterpret_cast<double*>(stage + 8 * cap) : nullptr;
+    // finish [lo, hi) of the hard list: attempts down (side stream `ds` when the
+    // main stream is still generating), host logs, values up and scattered on
+    // the main stream; in pipelined chunks
+    cudaStream_t ds = nullptr;
+    struct DsGuard {
+        cudaStream_t* p;
+        ~DsGuard() {
+            if (*p) cudaStreamDestroy(*p);
         }
-        // pipelined in chunks: the attempt lists come down (copy engine D2H),
-        // chunk c is finished on the host while chunk c-1's values go up
-        // (H2D engine) and are scattered
+    } ds_guard{&ds};
+    auto resolve = [&](int64_t lo, int64_t hi, cudaStream_t down) -> rl_status {
+        const int64_t nh = hi - lo;
+        if (nh <= 0) return RL_OK;
         constexpr int kMaxChunks = 4;
         const int nchunks = nh >= 4 * 65536 ? kMaxChunks : 1;
         const int64_t cs = (nh + nchunks - 1) / nchunks;
@@ -372,12 +370,12 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
             }
         } ev_guard{ev, nchunks};
         for (int c = 0; c < nchunks; ++c) {
-            const int64_t o = c * cs, k = std::min(cs, nh - o);
-            RL_CUDA(cudaMemcpyAsync(att + o, attempts + o, 8 * k, cudaMemcpyDeviceToHost, s));
-            RL_CUDA(cudaEventRecord(ev[c], s));
+            const int64_t o = lo + c * cs, k = std::min(cs, hi - o);
+            RL_CUDA(cudaMemcpyAsync(att + o, attempts + o, 8 * k, cudaMemcpyDeviceToHost, down));
+            RL_CUDA(cudaEventRecord(ev[c], down));
         }
         for (int c = 0; c < nchunks; ++c) {
-            const int64_t o = c * cs, k = std::min(cs, nh - o);
+            const int64_t o = lo + c * cs, k = std::min(cs, hi - o);
             RL_CUDA(cudaEventSynchronize(ev[c]));
             host_polar_pairs(seed, att + o, k, hv + 2 * o);
             RL_CUDA(cudaMemcpyAsync(vals + 2 * o, hv + 2 * o, 16 * k, cudaMemcpyHostToDevice, s));
@@ -385,14 +383,48 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
                                                                                   Pos{rows, cols, ld});
             RL_CHECK_LAUNCH("scatter_kernel");
         }
-        // the staging buffer is reused by the next call: the copy must be done
-        RL_CUDA(cudaStreamSynchronize(s));
+        return RL_OK;
+    };
+    rl_status st;
+    int64_t done = 0;
+    // first half, under the second half's generation
+    RL_CUDA(cudaEventSynchronize(ev1));
+    h_total = ctx->host_scalars[0];
+    const int64_t n1 = ctx->host_scalars[2];
+    if (stage && h_total >= pairs && n1 <= cap && n1 > 0) {
+        RL_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+        RL_CUDA(cudaStreamWaitEvent(ds, ev1, 0));
+        if ((st = resolve(0, n1, ds)) != RL_OK) return st;
+        done = n1;
     }
+    RL_CUDA(cudaEventSynchronize(ev2));
+    h_hard = static_cast<int64_t>(ctx->host_scalars[1]);
+    if (!stage || h_total < pairs || h_hard > cap) {
+        // astronomically unlikely: too few accepted attempts, or too many hard
+        // cases for the list; generate on the host and upload (after, and so
+        // over, anything already scattered)
+        std::vector<double> hg(static_cast<size_t>(count));
+        rl_gen_gaussian(rows, cols, seed, hg.data());
+        RL_CUDA(cudaMemcpy2DAsync(out, ld * 8, hg.data(), cols * 8, cols * 8, rows, cudaMemcpyHostToDevice, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+        if (hard_cases) *hard_cases = -1;
+        return RL_OK;
+    }
+    if (hard_cases) *hard_cases = h_hard;
+    // the second half's attempts also come down on the side stream: on the
+    // main stream they would queue behind the first half's uploads, which
+    // share the H2D engine with the caller's own uploads
+    if (ds) RL_CUDA(cudaStreamWaitEvent(ds, ev2, 0));
+    if ((st = resolve(done, h_hard, ds ? ds : s)) != RL_OK) return st;
+    // the staging buffer is reused by the next call: the copies must be done
+    RL_CUDA(cudaStreamSynchronize(s));
     return RL_OK;
 }
 
 GaussJob::~GaussJob() {
     if (base) cudaFreeAsync(base, ctx->stream);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
 }
 
 rl_status gen_gaussian_device(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld,
