@@ -7,28 +7,35 @@ solve at n=8192 — preprocess_solve(A, b, none, {Gaussian, G}, 0)
 (preprocess.hpp:156-180): product A*G, blocked GENP with the pivot verdict,
 chain solve x = G (LU)^-1 b — with A (seed 1), G (seed 2), b (seed 3) resident
 in HBM. value = F(n) / step time in TFLOP/s, F(n) = (2n^3 - n^2) +
-sum_{m<n} m(1+2m) + 2n^2 + (2n^2 - n). The batched-32
-figure (BASELINE config 2, 65,536 systems) rides along under "secondary".
+sum_{m<n} m(1+2m) + 2n^2 + (2n^2 - n). The batched-32 figure
+(BASELINE config 2, 65,536 systems) rides along under "secondary", and
+configs 3-5 under "configs_3_to_5" on the inputs of tools/config_inputs.py
+(the bytes the reference-made fixtures in tests/golden/ were computed on).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
---impl reference times the reference's own CPU implementation of the path
-(oracle/_ref: the reference headers compiled with our Eigen shim; the plain-C
-port when _ref is absent) on all host cores, running preprocess_solve trials
-concurrently on the reference's parallel_for_index pool, on a bounded sample
-(n=2048 per trial) in the same metric/unit.
+--gpus N > 1 without a torchrun environment relaunches itself under
+torch.distributed.run (one process per GPU, NCCL, 127.0.0.1). The dense
+solve does not shard (replicas); the batched systems shard by
+index. --dry-run exercises the launcher and the collectives (gloo) without a
+GPU and prints the line's n_gpus.
 
-Multi-GPU (torchrun): every rank solves its own n=8192 system (the dense
-path does not shard: replicas only); value = all ranks' flops /
-max-over-ranks step time.
+--impl reference times the reference's own CPU implementation of the same
+workload: oracle/_ref (the reference headers compiled from /root/reference)
+runs one full n = 8192 preprocess_solve per host core concurrently on the
+reference's parallel_for_index pool; one such step is several minutes of CPU,
+so the arm times exactly one step after no warm-up whatever --steps/--warmup
+say (the line records it).
 """
 import argparse
 import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -36,17 +43,27 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 METRIC = "preprocessed-GENP FP64 TFLOP/s at n=8192, % of FP64 peak; batched solves/s"
 FP64_PEAK_TFLOPS = 35.46   # cuBLAS DGEMM 8192^3 measured on this pool's B200 (profiles/r01_fp64_peak.txt)
 FP64_DMMA_PEAK = 37.06     # DMMA issue-rate microbenchmark (tools/fp64_peak.cu)
 BATCH_BYTES_PER_SYSTEM = 25104
+WORKLOAD = "Gaussian-preprocessed GENP solve, n=8192 (BASELINE headline; config 1 recipe at n=8192)"
 
 
 def flops_dense(n):
     """F(n) of SURVEY §8(d)."""
-    s = n * (n - 1) // 2 + 2 * ((n - 1) * n * (2 * n - 1) // 6)
-    return (2 * n ** 3 - n ** 2) + s + 2 * n ** 2 + (2 * n ** 2 - n)
+    return (2 * n ** 3 - n ** 2) + sum_lu_flops(n) + 2 * n ** 2 + (2 * n ** 2 - n)
+
+
+def sum_lu_flops(n):
+    return n * (n - 1) // 2 + 2 * ((n - 1) * n * (2 * n - 1) // 6)
+
+
+def lu_step_flops(n, j0, j1):
+    """flops of elimination steps j0..j1-1 of genp_factor: (n-1-j)(1 + 2(n-1-j))"""
+    return sum((n - 1 - j) * (1 + 2 * (n - 1 - j)) for j in range(j0, min(j1, n)))
 
 
 def measured_peaks():
@@ -55,6 +72,12 @@ def measured_peaks():
             return json.load(f)
     except Exception:
         return {}
+
+
+def base_config(n, world):
+    return {"workload": WORKLOAD, "n": n, "refine_steps": 0, "multiplier": "gaussian",
+            "l2": "inputs 1 GiB per step > 126 MB L2 (no flush needed)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 
 
 # ---- clocks during the timed region ---------------------------------------
@@ -111,15 +134,19 @@ def dist_info():
 
 
 class Dist:
-    def __init__(self, world, local):
+    def __init__(self, world, local, backend="nccl"):
         import torch
         self.torch = torch
         self.world = world
+        self.device = "cuda" if backend == "nccl" else "cpu"
         if world > 1:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if backend == "nccl":
+                torch.cuda.set_device(local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group("gloo")
             self.dist = dist
         else:
             self.dist = None
@@ -131,7 +158,7 @@ class Dist:
     def max(self, v):
         if not self.dist:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -140,47 +167,64 @@ class Dist:
             self.dist.destroy_process_group()
 
 
-# ---- the reference arm ---------------------------------------------------------
-def reference_sample(n_s, trials, steps, warmup):
-    """Time the reference CPU path: `trials` concurrent preprocess_solve calls
-    (n_s x n_s Gaussian A, Gaussian multiplier) per step. Returns (TF/s, info)."""
+# ---- the reference's CPU path ------------------------------------------------------
+def reference_full(n, trials):
+    """The reference's own code (oracle/_ref) on the headline workload:
+    `trials` concurrent preprocess_solve(A, b, none, {Gaussian, 2}, 0) at n on
+    the reference's parallel_for_index pool (A, b of the headline; G drawn
+    inside from seed 2, as the reference does). Returns (seconds, info)."""
     import oracle
-    seeds = np.array([oracle.C.derive_seed(1000 + t, 2, 0) for t in range(trials)], dtype=np.uint64)
-    a_all = np.stack([oracle.C.gen_gaussian(n_s, n_s, oracle.C.derive_seed(1000 + t, 1, 0)) for t in range(trials)])
-    b_all = np.stack([oracle.C.gen_gaussian_vector(n_s, oracle.C.derive_seed(1000 + t, 3, 0)) for t in range(trials)])
-    if oracle.REF is not None:
-        kind = "reference"
+    if oracle.REF is None:
+        raise RuntimeError("oracle/_ref not built")
+    a = oracle.REF.gen_gaussian(n, n, 1)
+    b = oracle.REF.gen_gaussian(n, 1, 3).reshape(n)
+    a_all = np.empty((trials, n, n))
+    a_all[:] = a
+    b_all = np.empty((trials, n))
+    b_all[:] = b
+    seeds = np.full(trials, 2, dtype=np.uint64)
+    t0 = time.perf_counter()
+    res, nf = oracle.REF.parallel_dense_trials(a_all, b_all, seeds)
+    dt = time.perf_counter() - t0
+    return dt, {"kind": "reference", "cores": trials, "zero_pivots": nf, "median_residual": float(np.nanmedian(res)),
+                "sample": f"{trials} concurrent full preprocess_solve(A, b, none, {{Gaussian, 2}}, 0) at n={n} "
+                          f"(the headline workload itself) on the reference's parallel_for_index pool, one step"}
 
-        def step():
-            res, nf = oracle.REF.parallel_dense_trials(a_all, b_all, seeds)
-            return res
-    else:
-        kind = "port"
 
-        def step():
-            out = [None] * trials
+def port_sample(n, threads, rows=64, steps=48):
+    """Bounded sample of the headline workload on the host cores with the
+    oracle's line-cited restatement (kind "port"; bit-identical to the
+    reference's genp_factor, tests/test_oracle.py): per thread, the product
+    rows [t R, (t+1) R) of A*G by the single-thread GEMM hook (the reference's
+    Eigen product is single-threaded) and the first `steps` elimination steps
+    of genp_factor on a full n x n matrix (the same memory traffic per step as
+    the whole factorisation's early steps). TFLOP/s = sampled flops / wall."""
+    import oracle
+    C = oracle.C
+    a = C.gen_gaussian(n, n, 1)
+    g = C.gen_gaussian(n, n, 2)
+    mats = [np.array(a) for _ in range(threads)]  # untimed copies: each thread eliminates its own matrix
+    flops = [0] * threads
 
-            def work(t):
-                g = oracle.C.gen_gaussian(n_s, n_s, int(seeds[t]))
-                out[t] = oracle.C.preprocess_solve(a_all[t], b_all[t], 1, g)["history"][0]
-            th = [threading.Thread(target=work, args=(t,)) for t in range(trials)]
-            for x in th:
-                x.start()
-            for x in th:
-                x.join()
-            return np.array(out)
-    for _ in range(warmup):
-        step()
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        res = step()
-        times.append(time.perf_counter() - t0)
-    t = statistics.mean(times)
-    tf = trials * flops_dense(n_s) / t / 1e12
-    return tf, {"kind": kind, "cores": trials, "seconds_per_step": t, "median_residual": float(np.nanmedian(res)),
-                "sample": f"{trials} concurrent preprocess_solve trials, n={n_s} (Gaussian A, Gaussian multiplier, "
-                          f"refine 0) per step on the reference's parallel_for_index pool; metric scaled by F(n)"}
+    def work(t):
+        r0 = (t * rows) % n
+        C.matmul(a[r0:r0 + rows], g)
+        C.genp_steps(mats[t], 0, steps)
+        flops[t] = 2 * rows * n * n + lu_step_flops(n, 0, steps)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    t0 = time.perf_counter()
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    dt = time.perf_counter() - t0
+    tf = sum(flops) / dt / 1e12
+    return tf, {"kind": "port", "cores": threads, "seconds": dt,
+                "sample": f"bounded sample of the n={n} headline workload on {threads} threads: per thread "
+                          f"{rows} product rows of A*G (single-thread GEMM, as the reference's Eigen) + the first "
+                          f"{steps} elimination steps of genp_factor on a full {n}x{n} matrix (oracle/oracle.c "
+                          f"restatement, bit-identical to the reference's loop); TFLOP/s = sampled flops / wall"}
 
 
 def run_reference(args):
@@ -188,28 +232,33 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    tf, info = reference_sample(args.ref_n, cores, max(1, args.steps), max(0, args.warmup))
-    line = {"impl": "reference", "metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": 0, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": info["seconds_per_step"] * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded reference RNG)",
-            "config": {"workload": f"reference CPU preprocess_solve, bounded sample n={args.ref_n} x {cores} trials",
-                       "n_sample": args.ref_n, "trials_per_step": cores},
+    n = args.n
+    dt, info = reference_full(n, cores)
+    tf = cores * flops_dense(n) / dt / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": 0, "steps": 1,
+            "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic: exact reference RNG, A=gen_gaussian(n,n,1), G=gen_gaussian(n,n,2), "
+                                    "b=gen_gaussian_vector(n,3)",
+            "config": base_config(n, 1),
             "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": info["kind"],
                              "sample": info["sample"]},
-            "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "median_residual": info["median_residual"], "zero_pivots": info["zero_pivots"]}
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ---- BASELINE configs 3-5 (device resident, one timed call each) ---------------
+# ---- BASELINE configs 3-5 on the fixture inputs -------------------------------------
 def measure_configs_3_to_5(rl, capi, L, torch, stream, hbm):
     """Config 3: circulant-preprocessed GENP at n=8192 (FFT product + blocked
     GENP + FFT chain solve); config 4: range finder m=n=8192, r=64, Gaussian H;
-    config 5: m=32768, n=16384, r=256, Toeplitz H by FFT. Inputs follow
-    BASELINE.json (Haar factors from QR of seeded N(0,1) matrices); E and the
-    large Gaussian factors are drawn on the device with torch's seeded
-    generator (untimed input construction)."""
+    config 5: m=32768, n=16384, r=256, Toeplitz H by FFT. Inputs: the pinned
+    deterministic build of tools/config_inputs.py (the bytes of the
+    reference-made fixtures, SHA-256 in the line), untimed."""
+    import config_inputs
     out = {}
+    work = tempfile.mkdtemp(prefix="randla_bench_inputs_")
 
     def ev_time(f, reps=1):
         f()
@@ -222,18 +271,20 @@ def measure_configs_3_to_5(rl, capi, L, torch, stream, hbm):
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
+    def load(cfg):
+        rec = config_inputs.build(cfg, work)
+        inp = config_inputs.load(cfg, work)
+        dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items() if k != "record"}
+        for k in ("A", "b", "c"):
+            p = os.path.join(work, f"{cfg}_{k}.npy")
+            if os.path.exists(p):
+                os.remove(p)
+        return rec["sha256"], dev
+
     # ---- config 3
     n = 8192
-    gu = torch.from_numpy(rl.gen_gaussian(n, n, 11)).cuda()
-    u, _ = torch.linalg.qr(gu)
-    del gu
-    gv = torch.from_numpy(rl.gen_gaussian(n, n, 12)).cuda()
-    v, _ = torch.linalg.qr(gv)
-    del gv
-    a = (u * torch.logspace(0, -4, n, dtype=torch.float64, device="cuda")) @ v.T
-    del u, v
-    b = torch.from_numpy(rl.gen_gaussian_vector(n, 14)).cuda()
-    c = torch.from_numpy(rl.gen_gaussian_vector(n, 13)).cuda()
+    sha, d = load("cfg3")
+    a, b, c = d["A"], d["b"], d["c"]
     x = torch.empty_like(b)
     ac = torch.empty_like(a)
     fft_ms = ev_time(lambda: L.rl_circulant_right_multiply(None, capi.RL_DEVICE, n, n, a.data_ptr(), c.data_ptr(),
@@ -245,67 +296,57 @@ def measure_configs_3_to_5(rl, capi, L, torch, stream, hbm):
     info = capi.rl_solve_info()
 
     def solve3():
-        rc = L.rl_preprocessed_genp_solve(None, capi.RL_DEVICE, n, a.data_ptr(), b.data_ptr(), ctypes.byref(m3), 0,
-                                          x.data_ptr(), None, 0, ctypes.byref(info))
+        rc = L.rl_preprocessed_genp_solve(None, capi.RL_DEVICE, n, a.data_ptr(), b.data_ptr(), None, ctypes.byref(m3),
+                                          0, x.data_ptr(), None, 0, ctypes.byref(info))
         if rc != 0:
             raise RuntimeError(capi.last_error())
     ms3 = ev_time(solve3, 2)
-    lu_flops = sum_lu_flops(n)
     fft_bytes = 2 * 8 * n * n
     out["config3"] = {
-        "workload": "circulant-preprocessed GENP, n=8192, kappa=1e4 (Haar U/V seeds 11/12), Gaussian circulant seed 13",
+        "workload": "circulant-preprocessed GENP, n=8192, kappa=1e4 (Haar U/V seeds 11/12), Gaussian circulant "
+                    "seed 13, b seed 14", "inputs_sha256": sha,
         "ms_per_call": ms3, "stage_ms": list(info.stage_ms), "residual_b": info.residual_history[0],
         "growth": info.growth,
         "fft_product": {"ms": fft_ms, "roofline": {"bound": "hbm", "achieved": fft_bytes / (fft_ms * 1e-3) / 1e9,
                                                     "peak": hbm, "unit": "GB/s",
                                                     "frac": fft_bytes / (fft_ms * 1e-3) / 1e9 / hbm,
                                                     "algorithmic_bytes": fft_bytes}},
-        "lu_tflops": lu_flops / (info.stage_ms[1] * 1e-3) / 1e12}
-    del a, b, c, x
+        "lu_tflops": sum_lu_flops(n) / (info.stage_ms[1] * 1e-3) / 1e12}
+    del a, b, c, x, d
 
     # ---- config 4
-    m = n = 8192
+    sha, d = load("cfg4")
+    a = d["A"]
+    m, n = a.shape
     r = 64
-    g = torch.Generator(device="cuda")
-    g.manual_seed(4)
-    ur, _ = torch.linalg.qr(torch.randn(m, r, dtype=torch.float64, device="cuda", generator=g))
-    vr, _ = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device="cuda", generator=g))
-    sig = torch.logspace(0, -2, r, dtype=torch.float64, device="cuda")
-    a = (ur * sig) @ vr.T + 1e-10 * torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
     out["config4"] = run_range_find(L, capi, a, r, capi.RL_MULT_GAUSSIAN, 41, ev_time, 3 * 2 * m * n * r,
-                                    "range finder m=n=8192, r=64, Gaussian H (seed 41); sigma 1..1e-2, E ~ N(0,1e-20)")
-    del a, ur, vr
+                                    "range finder m=n=8192, r=64, Gaussian H (seed 41); sigma 1..1e-2, "
+                                    "E = 1e-10 gen_gaussian(seed 44)")
+    out["config4"]["inputs_sha256"] = sha
+    del a, d
 
     # ---- config 5
-    m, n, r = 32768, 16384, 256
-    g.manual_seed(5)
-    ur, _ = torch.linalg.qr(torch.randn(m, r, dtype=torch.float64, device="cuda", generator=g))
-    vr, _ = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device="cuda", generator=g))
-    sig = torch.logspace(0, -3, r, dtype=torch.float64, device="cuda")
-    a = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g).mul_(1e-12)
-    a.addmm_(ur * sig, vr.T)
-    del ur, vr
+    sha, d = load("cfg5")
+    a = d["A"]
+    m, n = a.shape
+    r = 256
     res5 = run_range_find(L, capi, a, r, capi.RL_MULT_GAUSSIAN_CIRCULANT, 21, ev_time, 2 * 2 * m * n * r,
                           "range finder m=32768, n=16384, r=256, Toeplitz H (Gaussian circulant seed 21); "
-                          "sigma 1..1e-3, E ~ N(0,1e-24)")
-    # the Toeplitz sketch alone (HBM bound: read A, write Y)
-    cc = torch.from_numpy(rl.gen_gaussian_vector(n, 21)).cuda()
+                          "sigma 1..1e-3, E = 1e-12 gen_gaussian(seed 53)")
+    res5["inputs_sha256"] = sha
+    cc = d["c"]
     y = torch.empty(m, r, dtype=torch.float64, device="cuda")
     sk_ms = ev_time(lambda: L.rl_toeplitz_right_multiply(None, capi.RL_DEVICE, m, n, a.data_ptr(), n, cc.data_ptr(), r,
-                                                         y.data_ptr()), 1)
+                                                         y.data_ptr()), 3)
     sk_bytes = 8 * m * n + 8 * m * r
     res5["toeplitz_sketch"] = {"ms": sk_ms, "roofline": {"bound": "hbm", "achieved": sk_bytes / (sk_ms * 1e-3) / 1e9,
                                                          "peak": hbm, "unit": "GB/s",
                                                          "frac": sk_bytes / (sk_ms * 1e-3) / 1e9 / hbm,
                                                          "algorithmic_bytes": sk_bytes}}
     out["config5"] = res5
-    del a, y
+    del a, y, d
     torch.cuda.empty_cache()
     return out
-
-
-def sum_lu_flops(n):
-    return n * (n - 1) // 2 + 2 * ((n - 1) * n * (2 * n - 1) // 6)
 
 
 def run_range_find(L, capi, a, r, kind, seed, ev_time, gemm_flops, workload):
@@ -317,7 +358,7 @@ def run_range_find(L, capi, a, r, kind, seed, ev_time, gemm_flops, workload):
     info = capi.rl_lowrank_info()
 
     def call():
-        rc = L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), q.data_ptr(),
+        rc = L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), 0, q.data_ptr(),
                                       ctypes.byref(info))
         if rc != 0:
             raise RuntimeError(capi.last_error())
@@ -328,18 +369,64 @@ def run_range_find(L, capi, a, r, kind, seed, ev_time, gemm_flops, workload):
             "note": "call = sketch + CholeskyQR2 + Q^T A + residual ||.||_F + power-iteration ||.||_2"}
 
 
+# ---- end to end through the public APIs ------------------------------------------
+def e2e_python(rl, torch, A, b, n, steps, D, world, ref_x):
+    """rl.preprocess_solve on pinned host numpy buffers (the Python public API):
+    every step uploads A and b, draws G from seed 2 on the device, factors,
+    solves and returns x on the host."""
+    hA = torch.from_numpy(A).pin_memory()
+    hb = torch.from_numpy(b).pin_memory()
+    a_np, b_np = hA.numpy(), hb.numpy()
+    spec = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 2)
+    out = rl.preprocess_solve(a_np, b_np, None, spec, 0)
+    D.barrier()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = rl.preprocess_solve(a_np, b_np, None, spec, 0)
+        ts.append(time.perf_counter() - t0)
+    t = D.max(statistics.mean(ts))
+    F = flops_dense(n)
+    return {"value": world * F / t / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n + 8 * n,
+            "d2h_bytes_per_step": 8 * n, "ms_per_step": t * 1e3, "steps": steps,
+            "api": "paper_1406_5802_b200.preprocess_solve(A, b, None, MultiplierSpec(GAUSSIAN, 2), 0), pinned numpy",
+            "includes": "H2D of A (4 row blocks on a side stream, overlapped with the product) and b from pinned "
+                        "memory, exact generation of G from seed 2 on the device (the ~6% of log evaluations "
+                        "glibc must decide finished on the host), product, GENP, verdict, solve, D2H of x",
+            "matches_device_resident_x": bool(np.array_equal(out.x, ref_x))}
+
+
+def e2e_cpp_header(n, steps):
+    """tools/_build/e2e_header: the C++ drop-in header's preprocess_solve on
+    RealMatrix / std::vector (pageable host memory), as a reference user calls it."""
+    exe = os.path.join(ROOT, "tools", "_build", "e2e_header")
+    if not os.path.exists(exe):
+        return {"unavailable": "tools/_build/e2e_header not built (__graft_entry__.build())"}
+    r = subprocess.run([exe, str(n), str(steps), "2"], capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"unavailable": f"e2e_header failed: {r.stderr[-300:]}"}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    d["value"] = flops_dense(n) / (d["ms_per_step"] * 1e-3) / 1e12
+    d["unit"] = "TFLOP/s"
+    d["api"] = "randla::preprocess_solve (include/randla_b200/randla.hpp), pageable RealMatrix / std::vector"
+    return d
+
+
 # ---- our arm ---------------------------------------------------------------------
 def run_b200(args):
     import torch
     rank, world, local = dist_info()
+    if args.dry_run:
+        return run_dry(args, rank, world, local)
     if not torch.cuda.is_available():
         print(json.dumps({"error": "no CUDA device"}))
         return 1
-    D = Dist(world, local)
+    D = Dist(world, local, "nccl")
     torch.cuda.set_device(local)
     import paper_1406_5802_b200 as rl
-    from paper_1406_5802_b200 import capi
+    from paper_1406_5802_b200 import capi, shard
     L = capi.lib()
+    assert L.rl_context_device(None) == local, "the library's default context must follow the rank's device"
     n = args.n
     stream = torch.cuda.current_stream()
     L.rl_context_set_stream(None, ctypes.c_void_p(stream.cuda_stream))
@@ -356,8 +443,8 @@ def run_b200(args):
     info = capi.rl_solve_info()
 
     def step():
-        rc = L.rl_preprocessed_genp_solve(None, capi.RL_DEVICE, n, dA.data_ptr(), db.data_ptr(), ctypes.byref(mult), 0,
-                                          dx.data_ptr(), None, 0, ctypes.byref(info))
+        rc = L.rl_preprocessed_genp_solve(None, capi.RL_DEVICE, n, dA.data_ptr(), db.data_ptr(), None,
+                                          ctypes.byref(mult), 0, dx.data_ptr(), None, 0, ctypes.byref(info))
         if rc != 0:
             raise RuntimeError(f"rl_preprocessed_genp_solve failed: {rc} {capi.last_error()}")
 
@@ -388,6 +475,7 @@ def run_b200(args):
     stage = list(info.stage_ms)
     resid = info.residual_history[0]
     growth = info.growth
+    x_dev = dx.cpu().numpy()
 
     # roofline of the dominant kernel: the A*G DMMA GEMM (2 n^3 flops per launch)
     gemm_ms = statistics.mean(prod_ms)
@@ -406,53 +494,24 @@ def run_b200(args):
                 "step_frac_of_peak": value / world / FP64_PEAK_TFLOPS,
                 "algorithmic_flops_per_launch": 2 * n ** 3}
 
-    # end to end through the public API with host buffers: pinned A, b in,
-    # the multiplier generated from its seed inside the call (as the
-    # reference's preprocess_solve does), x out
     e2e = None
+    e2e_cpp = None
     if not args.no_e2e:
-        hA = torch.from_numpy(A).pin_memory()
-        hb = torch.from_numpy(b).pin_memory()
-        hx = torch.empty(n, dtype=torch.float64).pin_memory()
-        m2 = capi.rl_multiplier()
-        m2.kind = capi.RL_MULT_GAUSSIAN
-        m2.seed = 2
-        info2 = capi.rl_solve_info()
+        e2e = e2e_python(rl, torch, A, b, n, args.e2e_steps, D, world, x_dev)
+        if rank == 0 and world == 1:
+            e2e_cpp = e2e_cpp_header(n, args.e2e_steps)
+        if e2e_cpp is not None:
+            e2e["pageable_cpp_header"] = e2e_cpp
 
-        def e2e_step():
-            rc = L.rl_preprocessed_genp_solve(None, capi.RL_HOST, n, hA.data_ptr(), hb.data_ptr(), ctypes.byref(m2), 0,
-                                              hx.data_ptr(), None, 0, ctypes.byref(info2))
-            if rc != 0:
-                raise RuntimeError(capi.last_error())
-        e2e_step()
-        D.barrier()
-        ts = []
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
-            e2e_step()
-            ts.append(time.perf_counter() - t0)
-        t = D.max(statistics.mean(ts))
-        same = bool(np.array_equal(hx.numpy(), dx.cpu().numpy()))
-        e2e = {"value": world * F / t / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n + 8 * n,
-               "d2h_bytes_per_step": 8 * n, "ms_per_step": t * 1e3, "steps": args.e2e_steps,
-               "includes": "H2D of A (4 row blocks on a side stream, overlapped with the product) and b from "
-                           "pinned memory, exact generation of G from seed 2 on the device (the ~6% of log "
-                           "evaluations glibc must decide finished on the host), product, GENP, verdict, solve, "
-                           "D2H of x",
-               "matches_device_resident_x": same}
-
-    # secondary: BASELINE config 2 (65,536 batched 32x32 systems), device resident
+    # secondary: BASELINE config 2 (65,536 batched 32x32 systems per GPU), device resident
     secondary = None
     if not args.no_secondary:
         # rank r owns systems [lo, hi) of world * nb (independent
         # systems shard with no data-path collective; weak scaling)
-        from paper_1406_5802_b200 import shard
         nb = args.batch
         lo, hi = shard.shard_bounds(world * nb, rank, world)
-        seeds = shard.batch_seeds(lo, hi)
-        ba = torch.from_numpy(rl.gen_gaussian_batch(nb, 32, 32, seeds[:, 0])).cuda()
-        bb = torch.from_numpy(rl.gen_gaussian_batch(nb, 32, 1, seeds[:, 1]).reshape(nb, 32)).cuda()
-        bg = torch.from_numpy(rl.gen_gaussian_batch(nb, 32, 32, seeds[:, 2])).cuda()
+        ha, hg, hb = shard.shard_inputs(lo, hi)
+        ba, bg, bb = (torch.from_numpy(t).cuda() for t in (ha, hg, hb))
         blu, bx = torch.empty_like(ba), torch.empty_like(bb)
         br = torch.empty(nb, dtype=torch.float64, device="cuda")
         bgr = torch.empty_like(br)
@@ -487,17 +546,21 @@ def run_b200(args):
                      "max_growth": summ["max_growth"], "mean_residual": summ["mean_residual"],
                      "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                                   "traffic": None, "algorithmic_bytes_per_system": BATCH_BYTES_PER_SYSTEM}}
+        del ba, bg, bb, blu, bx
 
     configs = None
-    if not args.no_secondary and not args.no_configs:
+    if not args.no_secondary and not args.no_configs and rank == 0:
+        del dA, dG
+        torch.cuda.empty_cache()
         configs = measure_configs_3_to_5(rl, capi, L, torch, stream, measured_peaks().get("hbm_gbs", 6534.5))
 
-    # CPU baseline: the reference's CPU path on the host cores (rank 0, N=1)
+    # CPU baseline: a bounded sample of the same workload on the host cores (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        tf, cinfo = reference_sample(args.ref_n, cores, 1, 0)
-        cpu = {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": cinfo["kind"], "sample": cinfo["sample"]}
+        tf, cinfo = port_sample(n, cores)
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": cinfo["kind"], "sample": cinfo["sample"],
+               "seconds": cinfo["seconds"]}
 
     D.close()
     if rank != 0:
@@ -506,10 +569,7 @@ def run_b200(args):
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: exact reference RNG, A=gen_gaussian(n,n,1), G=gen_gaussian(n,n,2), b=gen_gaussian_vector(n,3)",
-            "config": {"workload": f"Gaussian-preprocessed GENP solve, n={n} (BASELINE headline; config 1 recipe at "
-                                   f"n={n})", "n": n, "refine_steps": 0, "multiplier": "gaussian",
-                       "l2": "inputs 1 GiB per step > 126 MB L2 (no flush needed)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": base_config(n, world),
             "frac_of_fp64_peak": value / world / FP64_PEAK_TFLOPS,
             "stage_ms_last_step": {"product": stage[0], "factor_and_verdict": stage[1], "solve": stage[2],
                                    "call": stage[3]},
@@ -520,6 +580,24 @@ def run_b200(args):
     return 0
 
 
+def run_dry(args, rank, world, local):
+    """launcher + collectives without a GPU (gloo): the shape of the N-rank line"""
+    D = Dist(world, local, "gloo")
+    D.barrier()
+    t = D.max(float(rank + 1))
+    D.close()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "max_over_ranks_probe": t,
+                          "config": base_config(args.n, world)}), flush=True)
+    return 0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -528,13 +606,18 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--batch", type=int, default=65536)
-    ap.add_argument("--ref-n", type=int, default=2048)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--dry-run", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun on this node
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -1,50 +1,105 @@
 // randla_b200/randla.hpp — C++ drop-in for the hot path of the reference
 // `randla` header library (namespace randla, /root/reference/proj/include/
 // randla/*.hpp, double instantiation), implemented over the C ABI in
-// randla_capi.h. A reference user swaps
+// randla_capi.h. A reference user swaps the reference's includes
 //     #include "randla/preprocess.hpp"   ->   #include "randla_b200/randla.hpp"
-// and links librandla_b200.so; the names, argument meaning and exception
-// types below are the reference's. Every computation runs on the GPU; there
-// is no CPU fallback (a host without a CUDA device gets DeviceError).
+// (or puts include/randla_dropin first on the include path, whose
+// randla/*.hpp files forward here) and links librandla_b200.so; the names,
+// argument meaning and exception types below are the reference's. Every
+// computation on the path runs on the GPU; there is no CPU fallback (a host
+// without a CUDA device gets DeviceError). Requires C++20, as the reference.
 //
 // Covered (reference file:line):
-//   Matrix<double>/RealMatrix           matrix.hpp:15-110  (value type, row-major)
-//   matmul                               matrix.hpp:115-121
-//   derive_seed, hash_label              multipliers.hpp:54-56, rng.hpp:87-95
-//   gen_gaussian, gen_gaussian_vector    multipliers.hpp:58-65, testbed/inputs.hpp:85-90
-//   MultiplierKind/MultiplierSpec        multipliers.hpp:20-40
-//   spectral_norm_estimate               norms.hpp:35-78
-//   LuFactors, genp_factor, lu_solve     lu.hpp:17-28, :40-58, :100-123
-//   gepp_factor, lu_solve_transpose      lu.hpp:62-98, :127-147 (bit-identical)
+//   Complex, field, tol_*, exception types   types.hpp:9-78
+//   RngStream, hash_label                    rng.hpp:16-95 (host, bit-identical)
+//   Matrix<T> (double and Complex), matmul,
+//   +, -, scalar *, matvec, frobenius_norm,
+//   max_abs, norm2, to_complex               matrix.hpp:15-203 (matmul<double> on the GPU)
+//   svd_values, spectral_norm, TruncatedSVD  svd.hpp:32-88, norms.hpp:11-14 (device Jacobi)
+//   spectral_norm_estimate                   norms.hpp:35-78
+//   fft, inverse_fft, dft_dense              fft.hpp:21-98 (GPU transforms)
+//   CirculantMatrix/RealCirculant,
+//   circulant_apply, circulant_solve,
+//   spectrum_range, circulant_is_singular,
+//   ToeplitzBlock, matmul_by_circulant,
+//   matmul_by_toeplitz_block                 circulant.hpp:17-203
+//   MultiplierKind, ToeplitzVariant,
+//   MultiplierSpec, multiplier_is_complex,
+//   derive_seed, gen_gaussian,
+//   gen_real_circulant, gen_real_toeplitz_block,
+//   gen_finite_set_uniform, gen_circ_skew_product,
+//   materialize                              multipliers.hpp:20-218
+//   LuFactors, genp_factor, lu_solve         lu.hpp:17-28, :40-58, :100-123
+//   gepp_factor, lu_solve_transpose          lu.hpp:62-98, :127-147 (bit-identical)
 //   BlockNode, BlockFactorization,
 //   block_ge_factor, block_solve,
-//   balanced_split, schur_complement     block_ge.hpp:18-218 (bit-identical pivots,
-//                                        Schur leaves and block_solve results)
-//   relative_residual                    lu.hpp:155-161 (host arithmetic, as in the reference)
-//   SolveOutcome, preprocess_solve,
-//   preprocess_solve_with_retry          preprocess.hpp:9-14, :156-196
-//   matmul_by_circulant,
-//   matmul_by_toeplitz_block             circulant.hpp:171-203 (first-column forms)
-//   orthonormal_basis, range_find,
-//   approximation_residual               qr.hpp:51-54, lowrank.hpp:62-83, :99-102
-//   batched_preprocess_solve_32          BASELINE config 2 (no reference counterpart:
-//                                        the reference loops preprocess_solve per trial)
+//   balanced_split, schur_complement         block_ge.hpp:18-218 (bit-identical)
+//   relative_residual                        lu.hpp:155-161
+//   SolveOutcome, SideMultiplier,
+//   iterative_refine, preprocess_solve,
+//   preprocess_solve_with_retry              preprocess.hpp:9-196
+//   QrResult, qr, orthonormal_basis          qr.hpp:17-54 (CholeskyQR2 on the GPU)
+//   LowRankResult, range_find_with,
+//   range_find, approximation_residual,
+//   basis_residual, subspace_residual        lowrank.hpp:21-113
+//   testbed::gen_lownumrank, gen_hard_block,
+//   gen_gaussian_vector, LowRankInstance     testbed/inputs.hpp:18-90
+//   batched_preprocess_solve_32              BASELINE config 2 (no reference counterpart:
+//                                            the reference loops preprocess_solve per trial)
+// Complex instantiations are off the B200 path: Matrix<Complex>
+// arithmetic is host arithmetic here, and the complex multiplier families raise
+// DimensionError as the reference's real pipeline does.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
+#include <complex>
+#include <concepts>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <memory>
+#include <numbers>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "randla_capi.h"
 
 namespace randla {
 
-// ---- error contract (types.hpp:44-78) -------------------------------------
+// ---- scalar fields, tolerances, error contract (types.hpp:9-78) -------------
+using Complex = std::complex<double>;
+
+template <typename T>
+struct field {
+    static constexpr bool is_complex = false;
+    using real_type = T;
+    static T conj(T x) { return x; }
+    static double abs2(T x) { return x * x; }
+    static double real(T x) { return x; }
+    static double imag(T) { return 0.0; }
+};
+template <>
+struct field<Complex> {
+    static constexpr bool is_complex = true;
+    using real_type = double;
+    static Complex conj(Complex x) { return std::conj(x); }
+    static double abs2(Complex x) { return std::norm(x); }
+    static double real(Complex x) { return x.real(); }
+    static double imag(Complex x) { return x.imag(); }
+};
+template <typename T>
+concept ScalarField = std::is_same_v<T, double> || std::is_same_v<T, Complex>;
+
+inline double tol_orth(std::size_t m, std::size_t n) { return 1e-10 * static_cast<double>(std::max(m, n)); }
+inline double tol_recon(std::size_t m, std::size_t n) { return 1e-10 * static_cast<double>(std::max(m, n)); }
+inline double tol_rank(std::size_t m, std::size_t n) { return 1e-13 * static_cast<double>(std::max(m, n)); }
+inline double tol_pivot(std::size_t n) { return 1e-13 * static_cast<double>(n); }
+
 struct DimensionError : std::invalid_argument {
     using std::invalid_argument::invalid_argument;
 };
@@ -64,6 +119,15 @@ struct SingularPivotBlockError : std::runtime_error {
     explicit SingularPivotBlockError(std::size_t p)
         : std::runtime_error("numerically singular pivot block at position " + std::to_string(p)), position(p) {}
 };
+struct ConvergenceError : std::runtime_error {
+    std::size_t iterations;
+    ConvergenceError(const std::string& what, std::size_t it)
+        : std::runtime_error(what + " (after " + std::to_string(it) + " iterations)"), iterations(it) {}
+};
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+// the device failed (no GPU, CUDA error, out of memory): no reference counterpart
 struct DeviceError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -81,101 +145,566 @@ inline void check(rl_status st, int64_t where = 0) {
         default: throw DeviceError(std::string("librandla_b200: ") + rl_last_error());
     }
 }
+inline int64_t i64(std::size_t v) { return static_cast<int64_t>(v); }
 }  // namespace detail
 
-// ---- dense row-major matrix (matrix.hpp:15-110) ------------------------------
-class RealMatrix {
+// ---- seeded streams (rng.hpp:16-95), host, the reference's arithmetic -----------
+// splitmix64 counter stream: every draw is finalize(state + k * golden); the
+// Gaussian is Marsaglia's polar method with the spare kept.
+class RngStream {
   public:
-    RealMatrix() = default;
-    RealMatrix(std::size_t rows, std::size_t cols, double fill = 0.0) : r_(rows), c_(cols), e_(rows * cols, fill) {
+    explicit RngStream(std::uint64_t seed) : state_(mix_key(kGolden, seed)) {}
+    RngStream derived(std::uint64_t key) const {
+        RngStream s(*this);
+        s.state_ = mix_key(s.state_, key);
+        s.has_spare_ = false;
+        return s;
+    }
+    RngStream derived(std::uint64_t key1, std::uint64_t key2) const { return derived(key1).derived(key2); }
+    std::uint64_t next_u64() {
+        state_ += kGolden;
+        return finalize(state_);
+    }
+    double next_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+    double next_symmetric() { return 2.0 * next_double() - 1.0; }
+    std::uint64_t next_below(std::uint64_t bound) {
+        const std::uint64_t limit = bound * (~std::uint64_t{0} / bound);
+        for (;;) {
+            const std::uint64_t v = next_u64();
+            if (v < limit) return v % bound;
+        }
+    }
+    double next_gaussian() {
+        if (has_spare_) {
+            has_spare_ = false;
+            return spare_;
+        }
+        for (;;) {
+            const double u = next_symmetric();
+            const double v = next_symmetric();
+            const double s = u * u + v * v;
+            if (s >= 1.0 || s == 0.0) continue;
+            const double f = std::sqrt(-2.0 * std::log(s) / s);
+            spare_ = v * f;
+            has_spare_ = true;
+            return u * f;
+        }
+    }
+
+  private:
+    static constexpr std::uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+    static std::uint64_t finalize(std::uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    static std::uint64_t mix_key(std::uint64_t state, std::uint64_t key) {
+        state ^= key + kGolden + (state << 6) + (state >> 2);
+        return finalize(state + kGolden);
+    }
+    std::uint64_t state_;
+    bool has_spare_ = false;
+    double spare_ = 0.0;
+};
+
+inline std::uint64_t hash_label(const char* s) { return rl_hash_label(s); }
+
+// ---- dense row-major matrix (matrix.hpp:15-110) ----------------------------------
+template <ScalarField T>
+class Matrix {
+  public:
+    using value_type = T;
+    Matrix() = default;
+    Matrix(std::size_t rows, std::size_t cols, T fill = T{}) : r_(rows), c_(cols), e_(rows * cols, fill) {
         if (rows == 0 || cols == 0) throw DimensionError("matrix dimensions must be positive");
     }
-    RealMatrix(std::size_t rows, std::size_t cols, std::vector<double> entries)
-        : r_(rows), c_(cols), e_(std::move(entries)) {
+    Matrix(std::size_t rows, std::size_t cols, std::vector<T> entries) : r_(rows), c_(cols), e_(std::move(entries)) {
         if (rows == 0 || cols == 0) throw DimensionError("matrix dimensions must be positive");
         if (e_.size() != rows * cols) throw DimensionError("entry count does not match rows*cols");
     }
-    static RealMatrix identity(std::size_t n) {
-        RealMatrix m(n, n);
-        for (std::size_t i = 0; i < n; ++i) m(i, i) = 1.0;
+    static Matrix identity(std::size_t n) {
+        Matrix m(n, n);
+        for (std::size_t i = 0; i < n; ++i) m(i, i) = T{1};
         return m;
     }
     std::size_t rows() const { return r_; }
     std::size_t cols() const { return c_; }
-    double& operator()(std::size_t i, std::size_t j) { return e_[i * c_ + j]; }
-    const double& operator()(std::size_t i, std::size_t j) const { return e_[i * c_ + j]; }
-    const std::vector<double>& entries() const { return e_; }
-    double* data() { return e_.data(); }
-    const double* data() const { return e_.data(); }
-    bool operator==(const RealMatrix& o) const { return r_ == o.r_ && c_ == o.c_ && e_ == o.e_; }
+    T& operator()(std::size_t i, std::size_t j) { return e_[i * c_ + j]; }
+    const T& operator()(std::size_t i, std::size_t j) const { return e_[i * c_ + j]; }
+    const std::vector<T>& entries() const { return e_; }
+    T* data() { return e_.data(); }
+    const T* data() const { return e_.data(); }
+
+    Matrix leading_block(std::size_t k, std::size_t l) const {
+        if (k == 0 || l == 0 || k > r_ || l > c_) throw DimensionError("leading block exceeds matrix dimensions");
+        return block(0, 0, k, l);
+    }
+    Matrix block(std::size_t row0, std::size_t col0, std::size_t k, std::size_t l) const {
+        if (row0 + k > r_ || col0 + l > c_) throw DimensionError("block exceeds matrix dimensions");
+        Matrix out(k, l);
+        for (std::size_t i = 0; i < k; ++i)
+            std::copy_n(e_.begin() + static_cast<std::ptrdiff_t>((row0 + i) * c_ + col0), l,
+                        out.e_.begin() + static_cast<std::ptrdiff_t>(i * l));
+        return out;
+    }
+    void set_block(std::size_t row0, std::size_t col0, const Matrix& b) {
+        if (row0 + b.rows() > r_ || col0 + b.cols() > c_) throw DimensionError("block exceeds matrix dimensions");
+        for (std::size_t i = 0; i < b.rows(); ++i)
+            std::copy_n(b.e_.begin() + static_cast<std::ptrdiff_t>(i * b.c_), b.c_,
+                        e_.begin() + static_cast<std::ptrdiff_t>((row0 + i) * c_ + col0));
+    }
+    Matrix transpose() const {
+        Matrix out(c_, r_);
+        for (std::size_t i = 0; i < r_; ++i)
+            for (std::size_t j = 0; j < c_; ++j) out(j, i) = (*this)(i, j);
+        return out;
+    }
+    Matrix adjoint() const {  // conjugate transpose; plain transpose over the reals
+        Matrix out(c_, r_);
+        for (std::size_t i = 0; i < r_; ++i)
+            for (std::size_t j = 0; j < c_; ++j) out(j, i) = field<T>::conj((*this)(i, j));
+        return out;
+    }
+    std::vector<T> col(std::size_t j) const {
+        std::vector<T> v(r_);
+        for (std::size_t i = 0; i < r_; ++i) v[i] = (*this)(i, j);
+        return v;
+    }
+    std::vector<T> row(std::size_t i) const {
+        return std::vector<T>(e_.begin() + static_cast<std::ptrdiff_t>(i * c_),
+                              e_.begin() + static_cast<std::ptrdiff_t>((i + 1) * c_));
+    }
+    bool operator==(const Matrix& o) const { return r_ == o.r_ && c_ == o.c_ && e_ == o.e_; }
 
   private:
     std::size_t r_ = 0, c_ = 0;
-    std::vector<double> e_;
+    std::vector<T> e_;
 };
-template <typename T>
-using Matrix = RealMatrix;  // the double instantiation is the one on the path
+using RealMatrix = Matrix<double>;
+using ComplexMatrix = Matrix<Complex>;
 
-inline RealMatrix matmul(const RealMatrix& a, const RealMatrix& b) {
+// C = A B: the FP64 DMMA GEMM for real matrices (matrix.hpp:115-121); complex
+// products are off the path and run on the host
+template <ScalarField T>
+Matrix<T> matmul(const Matrix<T>& a, const Matrix<T>& b) {
     if (a.cols() != b.rows()) throw DimensionError("matmul: inner dimensions differ");
-    RealMatrix out(a.rows(), b.cols());
-    const int64_t m = static_cast<int64_t>(a.rows()), k = static_cast<int64_t>(a.cols()),
-                  n = static_cast<int64_t>(b.cols());
-    detail::check(rl_dgemm(nullptr, RL_HOST, m, n, k, a.data(), k, b.data(), n, out.data(), n));
+    Matrix<T> out(a.rows(), b.cols());
+    const std::size_t m = a.rows(), k = a.cols(), n = b.cols();
+    if constexpr (std::is_same_v<T, double>) {
+        detail::check(rl_dgemm(nullptr, RL_HOST, detail::i64(m), detail::i64(n), detail::i64(k), a.data(),
+                               detail::i64(k), b.data(), detail::i64(n), out.data(), detail::i64(n)));
+    } else {
+        for (std::size_t i = 0; i < m; ++i)
+            for (std::size_t t = 0; t < k; ++t) {
+                const T av = a(i, t);
+                for (std::size_t j = 0; j < n; ++j) out(i, j) += av * b(t, j);
+            }
+    }
     return out;
 }
 
-inline std::vector<double> matvec(const RealMatrix& a, const std::vector<double>& x) {
+template <ScalarField T>
+Matrix<T> operator+(const Matrix<T>& a, const Matrix<T>& b) {
+    if (a.rows() != b.rows() || a.cols() != b.cols()) throw DimensionError("add: shape mismatch");
+    Matrix<T> out(a.rows(), a.cols());
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) out(i, j) = a(i, j) + b(i, j);
+    return out;
+}
+template <ScalarField T>
+Matrix<T> operator-(const Matrix<T>& a, const Matrix<T>& b) {
+    if (a.rows() != b.rows() || a.cols() != b.cols()) throw DimensionError("sub: shape mismatch");
+    Matrix<T> out(a.rows(), a.cols());
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) out(i, j) = a(i, j) - b(i, j);
+    return out;
+}
+template <ScalarField T, typename S>
+Matrix<T> operator*(S scalar, const Matrix<T>& a) {
+    Matrix<T> out(a.rows(), a.cols());
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) out(i, j) = T(scalar) * a(i, j);
+    return out;
+}
+
+template <ScalarField T>
+std::vector<T> matvec(const Matrix<T>& a, const std::vector<T>& x) {  // matrix.hpp:146-156
     if (a.cols() != x.size()) throw DimensionError("matvec: shape mismatch");
-    std::vector<double> y(a.rows(), 0.0);
+    std::vector<T> y(a.rows(), T{});
     for (std::size_t i = 0; i < a.rows(); ++i) {
-        double acc = 0.0;
+        T acc{};
         for (std::size_t j = 0; j < a.cols(); ++j) acc += a(i, j) * x[j];
         y[i] = acc;
     }
     return y;
 }
-
-inline double norm2(const std::vector<double>& v) {
+template <ScalarField T>
+double frobenius_norm(const Matrix<T>& a) {
     double s = 0.0;
-    for (double x : v) s += x * x;
+    for (const T& v : a.entries()) s += field<T>::abs2(v);
     return std::sqrt(s);
 }
+template <ScalarField T>
+double max_abs(const Matrix<T>& a) {
+    double m = 0.0;
+    for (const T& v : a.entries()) m = std::max(m, std::sqrt(field<T>::abs2(v)));
+    return m;
+}
+template <ScalarField T>
+double norm2(const std::vector<T>& v) {
+    double s = 0.0;
+    for (const T& x : v) s += field<T>::abs2(x);
+    return std::sqrt(s);
+}
+inline ComplexMatrix to_complex(const RealMatrix& a) {
+    ComplexMatrix out(a.rows(), a.cols());
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) out(i, j) = Complex(a(i, j), 0.0);
+    return out;
+}
+inline const ComplexMatrix& to_complex(const ComplexMatrix& a) { return a; }
+inline std::vector<Complex> to_complex(const std::vector<double>& v) {
+    std::vector<Complex> out(v.size());
+    for (std::size_t i = 0; i < v.size(); ++i) out[i] = Complex(v[i], 0.0);
+    return out;
+}
 
-// ---- multipliers (multipliers.hpp) ---------------------------------------------
-enum class MultiplierKind { None, Gaussian, RealCirculant, GaussianCirculant };
+// ---- singular values (svd.hpp:32-88, norms.hpp:11-33) ------------------------------
+// svd_values by the device's one-sided Jacobi; a complex A = X + iY through its
+// real embedding [[X, -Y], [Y, X]], whose singular values are A's, each twice
+template <ScalarField T>
+std::vector<double> svd_values(const Matrix<T>& a) {
+    if constexpr (std::is_same_v<T, double>) {
+        std::vector<double> sv(std::min(a.rows(), a.cols()));
+        detail::check(rl_singular_values(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                         sv.data()));
+        return sv;
+    } else {
+        const std::size_t m = a.rows(), n = a.cols();
+        RealMatrix e(2 * m, 2 * n);
+        for (std::size_t i = 0; i < m; ++i)
+            for (std::size_t j = 0; j < n; ++j) {
+                e(i, j) = e(m + i, n + j) = a(i, j).real();
+                e(m + i, j) = a(i, j).imag();
+                e(i, n + j) = -a(i, j).imag();
+            }
+        const std::vector<double> twice = svd_values(e);
+        std::vector<double> sv(std::min(m, n));
+        for (std::size_t i = 0; i < sv.size(); ++i) sv[i] = twice[2 * i];
+        return sv;
+    }
+}
+template <ScalarField T>
+double spectral_norm(const Matrix<T>& a) {
+    return svd_values(a).front();
+}
+template <ScalarField T>
+double pseudo_inverse_norm(const Matrix<T>& a) {
+    const double smin = svd_values(a).back();
+    if (smin == 0.0) throw SingularMatrixError("pseudo-inverse norm of an exactly singular matrix");
+    return 1.0 / smin;
+}
+template <ScalarField T>
+double condition_number(const Matrix<T>& a) {
+    const auto sv = svd_values(a);
+    if (sv.back() == 0.0) throw SingularMatrixError("condition number of an exactly singular matrix");
+    return sv.front() / sv.back();
+}
+
+template <ScalarField T>
+struct TruncatedSVD {
+    Matrix<T> left;                 // m-by-r
+    std::vector<double> singulars;  // r leading values
+    Matrix<T> right;                // n-by-r
+    Matrix<T> reconstruct() const {
+        Matrix<T> scaled = left;
+        for (std::size_t j = 0; j < singulars.size(); ++j)
+            for (std::size_t i = 0; i < scaled.rows(); ++i) scaled(i, j) *= T(singulars[j]);
+        return matmul(scaled, right.adjoint());
+    }
+};
+
+// spectral_norm_estimate (norms.hpp:35-78): the reference's power iteration, in
+// its summation order, on the GPU
+inline double spectral_norm_estimate(const RealMatrix& a) {
+    double out = 0.0;
+    detail::check(rl_spectral_norm_estimate(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                            &out));
+    return out;
+}
+
+// ---- transforms (fft.hpp) ----------------------------------------------------------
+inline bool is_power_of_two(std::size_t n) { return n != 0 && (n & (n - 1)) == 0; }
+
+// n-by-n matrix with entry (i, j) = omega^{ij}, omega = exp(+2 pi i / n)
+inline ComplexMatrix dft_dense(std::size_t n) {
+    if (n < 1) throw DimensionError("dft_dense: n must be positive");
+    std::vector<Complex> root(n);
+    for (std::size_t k = 0; k < n; ++k)
+        root[k] = std::polar(1.0, 2.0 * std::numbers::pi * static_cast<double>(k) / static_cast<double>(n));
+    ComplexMatrix out(n, n);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < n; ++j) out(i, j) = root[(i * j) % n];
+    return out;
+}
+
+namespace detail {
+inline std::vector<Complex> transform(std::vector<Complex> v, bool inverse) {
+    if (v.empty()) throw DimensionError(inverse ? "inverse_fft: empty input" : "fft: empty input");
+    check(rl_fft(nullptr, RL_HOST, 1, i64(v.size()), reinterpret_cast<double*>(v.data()), inverse ? 1 : 0));
+    return v;
+}
+}  // namespace detail
+
+inline std::vector<Complex> fft(std::vector<Complex> v) { return detail::transform(std::move(v), false); }
+inline std::vector<Complex> fft(const std::vector<double>& v) { return fft(to_complex(v)); }
+inline std::vector<Complex> inverse_fft(std::vector<Complex> v) { return detail::transform(std::move(v), true); }
+
+// ---- circulants (circulant.hpp:17-203), real field -------------------------------
+template <ScalarField T>
+class CirculantMatrix {
+    static_assert(std::is_same_v<T, double>, "complex circulants are off the B200 path");
+
+  public:
+    explicit CirculantMatrix(std::vector<T> first_column) : c_(std::move(first_column)) {
+        if (c_.empty()) throw DimensionError("circulant: empty first column");
+        spectrum_ = fft(c_);  // eager, as the reference (circulant.hpp:19-22)
+    }
+    std::size_t size() const { return c_.size(); }
+    const std::vector<T>& first_column() const { return c_; }
+    const std::vector<Complex>& spectrum() const { return spectrum_; }
+    T entry(std::size_t i, std::size_t j) const { return c_[(i + c_.size() - j) % c_.size()]; }
+    Matrix<T> dense() const {
+        const std::size_t n = c_.size();
+        Matrix<T> out(n, n);
+        for (std::size_t i = 0; i < n; ++i)
+            for (std::size_t j = 0; j < n; ++j) out(i, j) = entry(i, j);
+        return out;
+    }
+    CirculantMatrix transposed() const {  // first column c[(n - i) mod n]
+        const std::size_t n = c_.size();
+        std::vector<T> rev(n);
+        for (std::size_t i = 0; i < n; ++i) rev[i] = c_[(n - i) % n];
+        return CirculantMatrix(std::move(rev));
+    }
+
+  private:
+    std::vector<T> c_;
+    std::vector<Complex> spectrum_;
+};
+using RealCirculant = CirculantMatrix<double>;
+
+// C x through the FFT kernel (circulant.hpp:91-96)
+inline std::vector<double> circulant_apply(const RealCirculant& c, const std::vector<double>& x) {
+    if (x.size() != c.size()) throw DimensionError("circulant_apply: length mismatch");
+    std::vector<double> y(x.size());
+    detail::check(rl_circulant_apply(nullptr, RL_HOST, detail::i64(c.size()), c.first_column().data(), x.data(), y.data()));
+    return y;
+}
+// real circulant times complex input (circulant.hpp:98-101): the real and
+// imaginary parts separately (C is real, so this is C x exactly)
+inline std::vector<Complex> circulant_apply(const RealCirculant& c, const std::vector<Complex>& x) {
+    if (x.size() != c.size()) throw DimensionError("circulant_apply: length mismatch");
+    std::vector<double> re(x.size()), im(x.size());
+    for (std::size_t i = 0; i < x.size(); ++i) {
+        re[i] = x[i].real();
+        im[i] = x[i].imag();
+    }
+    const std::vector<double> yr = circulant_apply(c, re), yi = circulant_apply(c, im);
+    std::vector<Complex> y(x.size());
+    for (std::size_t i = 0; i < x.size(); ++i) y[i] = Complex(yr[i], yi[i]);
+    return y;
+}
+
+template <ScalarField T>
+std::pair<double, double> spectrum_range(const CirculantMatrix<T>& c) {
+    double lo = std::abs(c.spectrum().front()), hi = lo;
+    for (const Complex& u : c.spectrum()) {
+        lo = std::min(lo, std::abs(u));
+        hi = std::max(hi, std::abs(u));
+    }
+    return {lo, hi};
+}
+template <ScalarField T>
+bool circulant_is_singular(const CirculantMatrix<T>& c) {
+    const auto [lo, hi] = spectrum_range(c);
+    return lo <= tol_rank(c.size(), c.size()) * hi;
+}
+
+// C^-1 b by spectral division (circulant.hpp:111-139); the transforms on the GPU
+inline std::vector<double> circulant_solve(const RealCirculant& c, const std::vector<double>& b) {
+    if (b.size() != c.size()) throw DimensionError("circulant_solve: length mismatch");
+    if (circulant_is_singular(c)) throw SingularMatrixError("circulant is numerically singular");
+    std::vector<Complex> y = fft(b);
+    for (std::size_t i = 0; i < y.size(); ++i) y[i] /= c.spectrum()[i];
+    y = inverse_fft(std::move(y));
+    const auto [lo, hi] = spectrum_range(c);
+    (void)hi;
+    const double scale = lo > 0.0 ? norm2(b) / lo : norm2(b);
+    double imag2 = 0.0, full2 = 0.0;
+    for (const Complex& v : y) {
+        imag2 += v.imag() * v.imag();
+        full2 += std::norm(v);
+    }
+    if (std::sqrt(imag2) > 1e-11 * (std::sqrt(full2) + scale))
+        throw std::logic_error("real circulant product produced non-negligible imaginary part");
+    std::vector<double> out(y.size());
+    for (std::size_t i = 0; i < y.size(); ++i) out[i] = y[i].real();
+    return out;
+}
+
+template <ScalarField T>
+class ToeplitzBlock {  // leading rows x cols block of a circulant (circulant.hpp:143-169)
+  public:
+    ToeplitzBlock(CirculantMatrix<T> parent, std::size_t rows, std::size_t cols)
+        : parent_(std::move(parent)), rows_(rows), cols_(cols) {
+        if (rows == 0 || cols == 0 || rows > parent_.size() || cols > parent_.size())
+            throw DimensionError("toeplitz block exceeds parent dimensions");
+    }
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    const CirculantMatrix<T>& parent() const { return parent_; }
+    T entry(std::size_t i, std::size_t j) const { return parent_.entry(i, j); }
+    Matrix<T> dense() const {
+        Matrix<T> out(rows_, cols_);
+        for (std::size_t i = 0; i < rows_; ++i)
+            for (std::size_t j = 0; j < cols_; ++j) out(i, j) = entry(i, j);
+        return out;
+    }
+
+  private:
+    CirculantMatrix<T> parent_;
+    std::size_t rows_, cols_;
+};
+
+// A C, every row through the FFT kernel (circulant.hpp:171-185)
+inline RealMatrix matmul_by_circulant(const RealMatrix& a, const RealCirculant& c) {
+    if (a.cols() != c.size()) throw DimensionError("matmul_by_circulant: shape mismatch");
+    RealMatrix out(a.rows(), a.cols());
+    detail::check(rl_circulant_right_multiply(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                              c.first_column().data(), out.data()));
+    return out;
+}
+// A T for a leading Toeplitz block (circulant.hpp:187-203)
+inline RealMatrix matmul_by_toeplitz_block(const RealMatrix& a, const ToeplitzBlock<double>& t) {
+    if (a.cols() != t.rows()) throw DimensionError("matmul_by_toeplitz_block: shape mismatch");
+    RealMatrix out(a.rows(), t.cols());
+    const auto& c = t.parent().first_column();
+    detail::check(rl_toeplitz_right_multiply(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                             detail::i64(c.size()), c.data(), detail::i64(t.cols()), out.data()));
+    return out;
+}
+// first-column forms (no spectrum on the host)
+inline RealMatrix matmul_by_circulant(const RealMatrix& a, const std::vector<double>& first_column) {
+    if (a.cols() != first_column.size()) throw DimensionError("matmul_by_circulant: shape mismatch");
+    RealMatrix out(a.rows(), a.cols());
+    detail::check(rl_circulant_right_multiply(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                              first_column.data(), out.data()));
+    return out;
+}
+inline RealMatrix matmul_by_toeplitz_block(const RealMatrix& a, const std::vector<double>& parent_column,
+                                           std::size_t cols) {
+    RealMatrix out(a.rows(), cols);
+    detail::check(rl_toeplitz_right_multiply(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                             detail::i64(parent_column.size()), parent_column.data(),
+                                             detail::i64(cols), out.data()));
+    return out;
+}
+
+// ---- multiplier families (multipliers.hpp:20-218) -----------------------------------
+// The reference's ordinals; GaussianCirculant is the B200 extension outside
+// them: RealCirculant(gen_gaussian_vector(n, seed)) (BASELINE configs 3, 5).
+enum class MultiplierKind {
+    None = RL_MULT_NONE,
+    Gaussian = RL_MULT_GAUSSIAN,
+    RealCirculant = RL_MULT_REAL_CIRCULANT,
+    UnitaryCirculant = RL_MULT_UNITARY_CIRCULANT,
+    ToeplitzBlock = RL_MULT_TOEPLITZ_BLOCK,
+    Srft = RL_MULT_SRFT,
+    FiniteSetUniform = RL_MULT_FINITE_SET_UNIFORM,
+    CircSkewProduct = RL_MULT_CIRC_SKEW_PRODUCT,
+    GaussianCirculant = RL_MULT_GAUSSIAN_CIRCULANT,
+};
+enum class ToeplitzVariant { Real = RL_TOEPLITZ_REAL, Unitary = RL_TOEPLITZ_UNITARY };
 
 struct MultiplierSpec {
     MultiplierKind kind = MultiplierKind::None;
     std::size_t rows = 0;
-    std::size_t cols = 0;
+    std::size_t cols = 0;  // cols <= rows for sketching uses
     std::uint64_t seed = 0;
+    std::size_t set_cardinality = 65536;              // FiniteSetUniform only
+    ToeplitzVariant variant = ToeplitzVariant::Real;  // ToeplitzBlock only
 };
+
+inline bool multiplier_is_complex(const MultiplierSpec& spec) {
+    return spec.kind == MultiplierKind::UnitaryCirculant || spec.kind == MultiplierKind::Srft ||
+           (spec.kind == MultiplierKind::ToeplitzBlock && spec.variant == ToeplitzVariant::Unitary);
+}
+
+namespace detail {
+inline rl_multiplier to_abi(const MultiplierSpec& s) {
+    rl_multiplier m{};
+    m.kind = static_cast<int32_t>(s.kind);
+    m.variant = static_cast<int32_t>(s.variant);
+    m.seed = s.seed;
+    m.set_cardinality = s.set_cardinality;
+    return m;
+}
+}  // namespace detail
 
 inline std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t k1, std::uint64_t k2 = 0) {
     return rl_derive_seed(seed, k1, k2);
 }
-inline std::uint64_t hash_label(const char* s) { return rl_hash_label(s); }
 
 inline RealMatrix gen_gaussian(std::size_t m, std::size_t n, std::uint64_t seed) {
     RealMatrix out(m, n);
-    detail::check(rl_gen_gaussian(static_cast<int64_t>(m), static_cast<int64_t>(n), seed, out.data()));
+    detail::check(rl_gen_gaussian(detail::i64(m), detail::i64(n), seed, out.data()));
     return out;
 }
 inline std::vector<double> gen_gaussian_vector(std::size_t n, std::uint64_t seed) {
     std::vector<double> v(n);
-    detail::check(rl_gen_gaussian(static_cast<int64_t>(n), 1, seed, v.data()));
+    detail::check(rl_gen_gaussian(detail::i64(n), 1, seed, v.data()));
     return v;
 }
-
-// ---- norms / GENP (norms.hpp, lu.hpp) ---------------------------------------------
-inline double spectral_norm_estimate(const RealMatrix& a) {
-    double out = 0.0;
-    detail::check(rl_spectral_norm_estimate(nullptr, RL_HOST, static_cast<int64_t>(a.rows()),
-                                            static_cast<int64_t>(a.cols()), a.data(), &out));
+inline RealCirculant gen_real_circulant(std::size_t n, std::uint64_t seed) {
+    std::vector<double> c(n);
+    detail::check(rl_gen_real_circulant_column(detail::i64(n), seed, c.data()));
+    return RealCirculant(std::move(c));
+}
+inline ToeplitzBlock<double> gen_real_toeplitz_block(std::size_t n, std::size_t l, std::uint64_t seed) {
+    return ToeplitzBlock<double>(gen_real_circulant(n, seed), n, l);
+}
+inline RealMatrix gen_finite_set_uniform(std::size_t m, std::size_t n, std::uint64_t seed, std::size_t cardinality) {
+    if (cardinality < 2) throw DimensionError("gen_finite_set_uniform: cardinality must be >= 2");
+    RealMatrix out(m, n);
+    detail::check(rl_gen_finite_set_uniform(detail::i64(m), detail::i64(n), seed, cardinality, out.data()));
     return out;
 }
 
+// materialize<T>(spec) (multipliers.hpp:174-218): the real families' dense
+// samples from the reference's generators (expansions and the skew product on
+// the GPU); complex families raise DimensionError (off the B200 path)
+template <ScalarField T>
+Matrix<T> materialize(const MultiplierSpec& spec) {
+    if (multiplier_is_complex(spec)) {
+        if constexpr (!field<T>::is_complex)
+            throw DimensionError("complex multiplier family requested in a real pipeline");
+        throw DimensionError("complex multiplier families are not on the B200 path");
+    }
+    RealMatrix out(spec.rows, spec.cols);
+    const rl_multiplier m = detail::to_abi(spec);
+    detail::check(rl_materialize(nullptr, RL_HOST, &m, detail::i64(spec.rows), detail::i64(spec.cols), out.data()));
+    if constexpr (field<T>::is_complex)
+        return to_complex(out);
+    else
+        return out;
+}
+inline RealMatrix gen_circ_skew_product(std::size_t n, std::uint64_t seed) {
+    MultiplierSpec s{MultiplierKind::CircSkewProduct, n, n, seed};
+    return materialize<double>(s);
+}
+
+// ---- GENP (lu.hpp) --------------------------------------------------------------------
 struct LuFactors {
     RealMatrix lower;
     RealMatrix upper;
@@ -209,8 +738,8 @@ inline LuFactors genp_factor(const RealMatrix& a) {
     if (a.cols() != n) throw DimensionError("genp_factor: square input required");
     RealMatrix packed(n, n);
     rl_solve_info info{};
-    const rl_status st = rl_genp_factor(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), packed.data(), &info);
-    detail::check(st, info.zero_pivot_step);  // step read after the call
+    const rl_status st = rl_genp_factor(nullptr, RL_HOST, detail::i64(n), a.data(), packed.data(), &info);
+    detail::check(st, info.zero_pivot_step);
     return detail::unpack(packed);
 }
 
@@ -223,7 +752,7 @@ inline std::vector<double> lu_solve(const LuFactors& f, const std::vector<double
     if (b.size() != n) throw DimensionError("lu_solve: length mismatch");
     const RealMatrix packed = detail::pack(f);
     std::vector<double> x(n);
-    detail::check(rl_lu_solve(nullptr, RL_HOST, static_cast<int64_t>(n), packed.data(), b.data(), x.data()));
+    detail::check(rl_lu_solve(nullptr, RL_HOST, detail::i64(n), packed.data(), b.data(), x.data()));
     return x;
 }
 
@@ -420,43 +949,140 @@ inline double relative_residual(const RealMatrix& a, const std::vector<double>& 
     return std::sqrt(num) / norm2(b);
 }
 
-// ---- preprocessed solve (preprocess.hpp) -----------------------------------------
+// ---- preprocessing (preprocess.hpp) ------------------------------------------------
+template <ScalarField T = double>
 struct SolveOutcome {
-    std::vector<double> x;
-    std::vector<double> residual_history;
+    std::vector<T> x;
+    std::vector<double> residual_history;  // ||Ax - b|| / ||b|| after the solve and each refinement
     bool diverged = false;
-    rl_solve_info info{};
+    rl_solve_info info{};                  // device diagnostics (growth, pivots, stage times)
 };
 
-inline SolveOutcome preprocess_solve(const RealMatrix& a, const std::vector<double>& b, const MultiplierSpec& pre_spec,
-                                     const MultiplierSpec& post_spec, std::size_t refine_steps) {
+// One side of A -> F A H (preprocess.hpp:20-110): identity, a dense sample, or
+// a circulant kept structured; products on the GPU.
+template <ScalarField T = double>
+class SideMultiplier {
+    static_assert(std::is_same_v<T, double>, "complex pipelines are off the B200 path");
+
+  public:
+    static SideMultiplier identity() { return SideMultiplier(); }
+    static SideMultiplier make(MultiplierSpec spec, std::size_t n) {
+        if (spec.rows == 0) spec.rows = n;
+        if (spec.cols == 0) spec.cols = n;
+        if (spec.rows != n || spec.cols != n)
+            throw DimensionError("solve preprocessing takes square n-by-n multipliers");
+        SideMultiplier out;
+        out.spec_ = spec;
+        switch (spec.kind) {
+            case MultiplierKind::None: return out;
+            case MultiplierKind::RealCirculant:
+                out.circ_.emplace(gen_real_circulant(n, spec.seed));
+                return out;
+            case MultiplierKind::GaussianCirculant:
+                out.circ_.emplace(gen_gaussian_vector(n, spec.seed));
+                return out;
+            case MultiplierKind::ToeplitzBlock:
+                if (spec.variant == ToeplitzVariant::Real) {
+                    out.circ_.emplace(gen_real_circulant(n, spec.seed));
+                    return out;
+                }
+                break;
+            case MultiplierKind::UnitaryCirculant: break;
+            default: out.dense_.emplace(materialize<double>(spec)); return out;
+        }
+        throw DimensionError("complex multiplier family requested in a real pipeline");
+    }
+    bool is_identity() const { return !dense_ && !circ_; }
+    RealMatrix right_multiply(const RealMatrix& a) const {  // A H
+        if (is_identity()) return a;
+        if (dense_) return matmul(a, *dense_);
+        return matmul_by_circulant(a, *circ_);
+    }
+    RealMatrix left_multiply(const RealMatrix& a) const {  // F A
+        if (is_identity()) return a;
+        if (dense_) return matmul(*dense_, a);
+        // F A = (A^T F^T)^T
+        return matmul_by_circulant(a.transpose(), circ_->transposed()).transpose();
+    }
+    std::vector<double> apply_vec(const std::vector<double>& v) const {  // H v
+        if (is_identity()) return v;
+        if (dense_) return matvec(*dense_, v);
+        return circulant_apply(*circ_, v);
+    }
+
+  private:
+    SideMultiplier() = default;
+    MultiplierSpec spec_{};
+    std::optional<RealMatrix> dense_;
+    std::optional<RealCirculant> circ_;
+};
+
+// residual-correction loop reusing one factorization through `solver`
+// (preprocess.hpp:115-143): two consecutive increases set `diverged`
+inline SolveOutcome<double> iterative_refine(const RealMatrix& a,
+                                             const std::function<std::vector<double>(const std::vector<double>&)>& solver,
+                                             const std::vector<double>& b, std::vector<double> x0, std::size_t steps) {
+    SolveOutcome<double> out;
+    out.x = std::move(x0);
+    const double bnorm = norm2(b);
+    auto residual = [&](const std::vector<double>& x) {
+        std::vector<double> r = matvec(a, x);
+        for (std::size_t i = 0; i < r.size(); ++i) r[i] = b[i] - r[i];
+        return r;
+    };
+    std::vector<double> r = residual(out.x);
+    out.residual_history.push_back(norm2(r) / bnorm);
+    std::size_t streak = 0;
+    for (std::size_t s = 0; s < steps; ++s) {
+        const std::vector<double> d = solver(r);
+        for (std::size_t i = 0; i < out.x.size(); ++i) out.x[i] += d[i];
+        r = residual(out.x);
+        const double rel = norm2(r) / bnorm;
+        streak = rel > out.residual_history.back() ? streak + 1 : 0;
+        out.residual_history.push_back(rel);
+        if (streak >= 2) {
+            out.diverged = true;
+            break;
+        }
+    }
+    return out;
+}
+inline SolveOutcome<double> iterative_refine(const RealMatrix& a, const LuFactors& factors,
+                                             const std::vector<double>& b, std::vector<double> x0, std::size_t steps) {
+    return iterative_refine(
+        a, [&](const std::vector<double>& r) { return lu_solve(factors, r); }, b, std::move(x0), steps);
+}
+
+// preprocess_solve(a, b, pre, post, refine) (preprocess.hpp:156-180): one
+// device call: F (A H), blocked GENP with the reference's pivot verdict, chain
+// solve H (LU)^-1 (F r) and the refinement loop
+inline SolveOutcome<double> preprocess_solve(const RealMatrix& a, const std::vector<double>& b,
+                                             const MultiplierSpec& pre_spec, const MultiplierSpec& post_spec,
+                                             std::size_t refine_steps) {
     const std::size_t n = a.rows();
     if (a.cols() != n) throw DimensionError("preprocess_solve: square input required");
     if (b.size() != n) throw DimensionError("preprocess_solve: length mismatch");
-    if (pre_spec.kind != MultiplierKind::None)
-        throw DimensionError("preprocess_solve: left multipliers are not on the B200 path");
-    rl_multiplier m{};
-    switch (post_spec.kind) {
-        case MultiplierKind::None: m.kind = RL_MULT_NONE; break;
-        case MultiplierKind::Gaussian: m.kind = RL_MULT_GAUSSIAN; break;
-        case MultiplierKind::RealCirculant: m.kind = RL_MULT_REAL_CIRCULANT; break;
-        case MultiplierKind::GaussianCirculant: m.kind = RL_MULT_GAUSSIAN_CIRCULANT; break;
-    }
-    m.seed = post_spec.seed;
-    SolveOutcome out;
+    for (const MultiplierSpec* s : {&pre_spec, &post_spec})
+        if ((s->rows != 0 && s->rows != n) || (s->cols != 0 && s->cols != n))
+            throw DimensionError("solve preprocessing takes square n-by-n multipliers");
+    const rl_multiplier pre = detail::to_abi(pre_spec), post = detail::to_abi(post_spec);
+    SolveOutcome<double> out;
     out.x.resize(n);
-    const rl_status st = rl_preprocessed_genp_solve(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), b.data(), &m,
-                                                    static_cast<int64_t>(refine_steps), out.x.data(), nullptr, 0,
-                                                    &out.info);
+    out.residual_history.assign(refine_steps + 1, 0.0);
+    out.info.history = out.residual_history.data();
+    out.info.history_capacity = detail::i64(refine_steps + 1);
+    const rl_status st = rl_preprocessed_genp_solve(nullptr, RL_HOST, detail::i64(n), a.data(), b.data(), &pre, &post,
+                                                    detail::i64(refine_steps), out.x.data(), nullptr, 0, &out.info);
     detail::check(st, out.info.zero_pivot_step);
-    out.residual_history.assign(out.info.residual_history, out.info.residual_history + out.info.history_len);
+    out.residual_history.resize(static_cast<std::size_t>(out.info.history_len));
+    out.info.history = nullptr;
     out.diverged = out.info.diverged != 0;
     return out;
 }
 
-inline SolveOutcome preprocess_solve_with_retry(const RealMatrix& a, const std::vector<double>& b,
-                                                MultiplierSpec pre_spec, MultiplierSpec post_spec,
-                                                std::size_t refine_steps, std::size_t max_retries = 3) {
+inline SolveOutcome<double> preprocess_solve_with_retry(const RealMatrix& a, const std::vector<double>& b,
+                                                        MultiplierSpec pre_spec, MultiplierSpec post_spec,
+                                                        std::size_t refine_steps, std::size_t max_retries = 3) {
     for (std::size_t attempt = 0;; ++attempt) {
         try {
             return preprocess_solve(a, b, pre_spec, post_spec, refine_steps);
@@ -468,66 +1094,157 @@ inline SolveOutcome preprocess_solve_with_retry(const RealMatrix& a, const std::
     }
 }
 
-// ---- structured multipliers (circulant.hpp), first-column forms ------------------
-inline RealMatrix matmul_by_circulant(const RealMatrix& a, const std::vector<double>& first_column) {
-    if (a.cols() != first_column.size()) throw DimensionError("matmul_by_circulant: shape mismatch");
-    RealMatrix out(a.rows(), a.cols());
-    detail::check(rl_circulant_right_multiply(nullptr, RL_HOST, static_cast<int64_t>(a.rows()),
-                                              static_cast<int64_t>(a.cols()), a.data(), first_column.data(),
-                                              out.data()));
-    return out;
-}
-
-inline RealMatrix matmul_by_toeplitz_block(const RealMatrix& a, const std::vector<double>& parent_column,
-                                           std::size_t cols) {
-    RealMatrix out(a.rows(), cols);
-    detail::check(rl_toeplitz_right_multiply(nullptr, RL_HOST, static_cast<int64_t>(a.rows()),
-                                             static_cast<int64_t>(a.cols()), a.data(),
-                                             static_cast<int64_t>(parent_column.size()), parent_column.data(),
-                                             static_cast<int64_t>(cols), out.data()));
-    return out;
-}
-
-// ---- low-rank (qr.hpp, lowrank.hpp) ------------------------------------------------
-inline RealMatrix orthonormal_basis(const RealMatrix& y) {
-    RealMatrix q(y.rows(), y.cols());
+// ---- QR (qr.hpp:17-54): CholeskyQR2 on the GPU, positive diagonal R -----------------
+template <ScalarField T = double>
+struct QrResult {
+    Matrix<T> q;  // m-by-n
+    Matrix<T> r;  // n-by-n
+};
+inline QrResult<double> qr(const RealMatrix& y) {
+    if (y.rows() < y.cols()) throw DimensionError("qr: expected rows >= cols");
+    QrResult<double> out{RealMatrix(y.rows(), y.cols()), RealMatrix(y.cols(), y.cols())};
     int64_t bad = 0;
-    const rl_status st = rl_cholqr2(nullptr, RL_HOST, static_cast<int64_t>(y.rows()), static_cast<int64_t>(y.cols()),
-                                    y.data(), q.data(), nullptr, &bad);
+    const rl_status st = rl_cholqr2(nullptr, RL_HOST, detail::i64(y.rows()), detail::i64(y.cols()), y.data(),
+                                    out.q.data(), out.r.data(), &bad);
     if (st == RL_ERR_RANK_DEFICIENCY)
         throw RankDeficiencyError("qr: numerically rank-deficient at column " + std::to_string(bad));
     detail::check(st);
-    return q;
+    return out;
 }
+inline RealMatrix orthonormal_basis(const RealMatrix& y) { return qr(y).q; }
 
+// ---- range finder (lowrank.hpp:21-113) ------------------------------------------------
+template <ScalarField T = double>
 struct LowRankResult {
-    RealMatrix q;
-    std::size_t rank = 0, oversample = 0, power_steps = 0;
-    rl_lowrank_info info{};
+    Matrix<T> q;  // m-by-l, orthonormal columns
+    std::size_t rank = 0;
+    std::size_t oversample = 0;
+    std::size_t power_steps = 0;
+
+    std::size_t sketch_width() const { return q.cols(); }
+    std::vector<T> apply_projection(const std::vector<T>& v) const { return matvec(q, matvec(q.adjoint(), v)); }
+    Matrix<T> apply_approximation(const Matrix<T>& a) const { return matmul(q, matmul(q.adjoint(), a)); }
+    Matrix<T> projector_dense() const {
+        if (q.rows() > 2048) throw DimensionError("projector materialization capped at 2048");
+        return matmul(q, q.adjoint());
+    }
 };
 
-inline LowRankResult range_find(const RealMatrix& a, std::size_t r, std::size_t p, MultiplierSpec spec,
-                                std::size_t power_steps = 0) {
-    if (power_steps != 0) throw DimensionError("range_find: power steps are not on the B200 path");
-    const std::size_t l = r + p;
-    LowRankResult out{RealMatrix(a.rows(), l), r, p, power_steps, {}};
-    rl_multiplier m{};
-    m.kind = spec.kind == MultiplierKind::Gaussian ? RL_MULT_GAUSSIAN : RL_MULT_GAUSSIAN_CIRCULANT;
-    m.seed = spec.seed;
-    const rl_status st = rl_range_find_residual(nullptr, RL_HOST, static_cast<int64_t>(a.rows()),
-                                                static_cast<int64_t>(a.cols()), a.data(), static_cast<int64_t>(l), &m,
-                                                out.q.data(), &out.info);
+// range finder on a supplied sketch: power steps (A A^T)^s, then the basis
+inline LowRankResult<double> range_find_with(const RealMatrix& a, RealMatrix sketch, std::size_t r, std::size_t p,
+                                             std::size_t power_steps) {
+    if (r < 1 || r + p > std::min(a.rows(), a.cols()))
+        throw DimensionError("range_find: rank plus oversampling exceeds matrix size");
+    for (std::size_t s = 0; s < power_steps; ++s) sketch = matmul(a, matmul(a.adjoint(), sketch));
+    return LowRankResult<double>{orthonormal_basis(sketch), r, p, power_steps};
+}
+
+// range_find (lowrank.hpp:62-83): one device call (sketch by the spec's family,
+// power steps, CholeskyQR2)
+inline LowRankResult<double> range_find(const RealMatrix& a, std::size_t r, std::size_t p, MultiplierSpec spec,
+                                        std::size_t power_steps) {
+    const std::size_t n = a.cols(), l = r + p;
+    if (r < 1 || l > std::min(a.rows(), a.cols()))
+        throw DimensionError("range_find: rank plus oversampling exceeds matrix size");
+    spec.rows = n;
+    spec.cols = l;
+    const rl_multiplier m = detail::to_abi(spec);
+    LowRankResult<double> out{RealMatrix(a.rows(), l), r, p, power_steps};
+    rl_lowrank_info info{};
+    const rl_status st = rl_range_find(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(n), a.data(),
+                                       detail::i64(l), &m, detail::i64(power_steps), out.q.data(), &info);
     if (st == RL_ERR_RANK_DEFICIENCY)
         throw RankDeficiencyError("qr: numerically rank-deficient at column " +
-                                  std::to_string(out.info.rank_deficient_column));
+                                  std::to_string(info.rank_deficient_column));
     detail::check(st);
     return out;
 }
 
-// ||A - Q Q^T A||_2 of the range_find result, evaluated with A (lowrank.hpp:99-102)
-inline double approximation_residual(const RealMatrix&, const LowRankResult& result) {
-    return result.info.residual_spectral;
+// ||A - Q (Q^T A)||_2 for this A (lowrank.hpp:99-102), on the GPU: B = Q^T A,
+// the residual never stored, its 2-norm by the restated power iteration
+inline double approximation_residual(const RealMatrix& a, const LowRankResult<double>& result) {
+    if (a.rows() != result.q.rows()) throw DimensionError("approximation_residual: shape mismatch");
+    rl_lowrank_info info{};
+    detail::check(rl_approximation_residual(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                            detail::i64(result.q.cols()), result.q.data(), &info));
+    return info.residual_spectral;
 }
+
+struct SubspaceResiduals {
+    double rn1 = 0.0;  // projection residual of the leading left singular basis
+    double rn2 = 0.0;  // ||A - Q Q^H A||
+};
+inline double basis_residual(const LowRankResult<double>& result, const TruncatedSVD<double>& truth) {
+    const RealMatrix y = matmul(result.q.adjoint(), truth.left);
+    return spectral_norm(matmul(result.q, y) - truth.left);
+}
+inline SubspaceResiduals subspace_residual(const RealMatrix& a, const LowRankResult<double>& result,
+                                           const TruncatedSVD<double>& truth) {
+    return {basis_residual(result, truth), approximation_residual(a, result)};
+}
+
+// ---- testbed inputs (testbed/inputs.hpp) ------------------------------------------------
+namespace testbed {
+
+// hard-block GENP input (inputs.hpp:18-49): leading n/2 block with four zero
+// singular values, Gaussian Toeplitz borders scaled to unit estimate
+inline RealMatrix gen_hard_block(std::size_t n, std::uint64_t seed) {
+    if (n < 8 || n % 2 != 0) throw DimensionError("gen_hard_block: need even n >= 8");
+    const std::size_t k = n / 2;
+    const RealMatrix u = orthonormal_basis(gen_gaussian(k, k, derive_seed(seed, 1)));
+    const RealMatrix v = orthonormal_basis(gen_gaussian(k, k, derive_seed(seed, 2)));
+    RealMatrix scaled = u;
+    for (std::size_t j = k - 4; j < k; ++j)
+        for (std::size_t i = 0; i < k; ++i) scaled(i, j) = 0.0;
+    const RealMatrix a_k = matmul(scaled, v.transpose());
+    auto toeplitz = [&](std::uint64_t s) {
+        RngStream rng(s);
+        std::vector<double> diag(2 * k - 1);  // index (i - j) + (k - 1)
+        for (double& t : diag) t = rng.next_gaussian();
+        RealMatrix t(k, k);
+        for (std::size_t i = 0; i < k; ++i)
+            for (std::size_t j = 0; j < k; ++j) t(i, j) = diag[i + (k - 1) - j];
+        const double norm = spectral_norm_estimate(t);
+        for (std::size_t i = 0; i < k; ++i)
+            for (std::size_t j = 0; j < k; ++j) t(i, j) /= norm;
+        return t;
+    };
+    RealMatrix out(n, n);
+    out.set_block(0, 0, a_k);
+    out.set_block(0, k, toeplitz(derive_seed(seed, 3)));
+    out.set_block(k, 0, toeplitz(derive_seed(seed, 4)));
+    out.set_block(k, k, toeplitz(derive_seed(seed, 5)));
+    return out;
+}
+
+struct LowRankInstance {
+    RealMatrix a;
+    TruncatedSVD<double> truth;
+    std::vector<double> singulars;
+};
+
+// known numerical rank r (inputs.hpp:67-83): sigma_j = 1/(j+1) up to r, 1e-10 beyond
+inline LowRankInstance gen_lownumrank(std::size_t n, std::size_t r, std::uint64_t seed) {
+    if (r < 1 || r >= n) throw DimensionError("gen_lownumrank: need 1 <= r < n");
+    const RealMatrix s = orthonormal_basis(gen_gaussian(n, n, derive_seed(seed, 1)));
+    const RealMatrix t = orthonormal_basis(gen_gaussian(n, n, derive_seed(seed, 2)));
+    std::vector<double> sigma(n);
+    for (std::size_t j = 0; j < n; ++j) sigma[j] = (j < r) ? 1.0 / static_cast<double>(j + 1) : 1e-10;
+    RealMatrix scaled = s;
+    for (std::size_t j = 0; j < n; ++j)
+        for (std::size_t i = 0; i < n; ++i) scaled(i, j) *= sigma[j];
+    return LowRankInstance{matmul(scaled, t.transpose()),
+                           TruncatedSVD<double>{s.leading_block(n, r),
+                                                std::vector<double>(sigma.begin(), sigma.begin() + static_cast<std::ptrdiff_t>(r)),
+                                                t.leading_block(n, r)},
+                           std::move(sigma)};
+}
+
+inline std::vector<double> gen_gaussian_vector(std::size_t n, std::uint64_t seed) {
+    return randla::gen_gaussian_vector(n, seed);
+}
+
+}  // namespace testbed
 
 // ---- BASELINE config 2: many independent 32x32 preprocessed solves ---------------
 struct BatchedSolve {

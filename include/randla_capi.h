@@ -4,7 +4,7 @@
  *
  * A plain C ABI: extern "C", plain pointers, int64 sizes, no C++ or torch
  * types. Each entry point replaces one function template of the reference's
- * header API (namespace randla, /root/reference/proj/include/randla/*.hpp,
+ * header API (namespace randla, /root/reference/proj/include/randla/<name>.hpp,
  * `double` instantiation); the replaced interface is cited per entry.
  * The C++ header include/randla_b200/randla.hpp re-creates the reference
  * signatures (Matrix<double>, LuFactors, SolveOutcome, typed exceptions) on
@@ -50,7 +50,7 @@ extern "C" {
 #define RL_API
 #endif
 
-#define RL_ABI_VERSION 1
+#define RL_ABI_VERSION 2
 
 typedef enum rl_status {
     RL_OK = 0,
@@ -69,24 +69,46 @@ typedef enum rl_status {
 
 typedef enum rl_mem { RL_HOST = 0, RL_DEVICE = 1 } rl_mem;
 
-/* Multiplier families on the path (multipliers.hpp:20-40). GAUSSIAN_CIRCULANT
- * is RealCirculant(gen_gaussian_vector(n, seed)) — the "Gaussian circulant"
- * of BASELINE configs 3 and 5 (SURVEY §0 finding 2); REAL_CIRCULANT is the
- * reference's own uniform[-1,1] family gen_real_circulant (multipliers.hpp:67-73). */
+/* Multiplier families: the ordinals of randla::MultiplierKind
+ * (multipliers.hpp:20-29), one for one. In this real (double) pipeline the
+ * complex families (UNITARY_CIRCULANT, SRFT, TOEPLITZ_BLOCK with the UNITARY
+ * variant) are rejected with RL_ERR_DIMENSION exactly where the reference's
+ * real instantiation throws DimensionError("complex multiplier family
+ * requested in a real pipeline") (preprocess.hpp:39-53, multipliers.hpp:174-218,
+ * lowrank.hpp:71-78).
+ * RL_MULT_GAUSSIAN_CIRCULANT is an extension outside the reference's ordinal
+ * range: RealCirculant(gen_gaussian_vector(n, seed)), the "circulant with an
+ * N(0,1) first column" of BASELINE configs 3 and 5 (the reference's own
+ * RealCirculant family draws the column uniform on [-1, 1],
+ * multipliers.hpp:67-73); it behaves as RealCirculant / the real ToeplitzBlock
+ * everywhere else. */
 typedef enum rl_multiplier_kind {
     RL_MULT_NONE = 0,
     RL_MULT_GAUSSIAN = 1,
     RL_MULT_REAL_CIRCULANT = 2,
-    RL_MULT_GAUSSIAN_CIRCULANT = 3
+    RL_MULT_UNITARY_CIRCULANT = 3,
+    RL_MULT_TOEPLITZ_BLOCK = 4,
+    RL_MULT_SRFT = 5,
+    RL_MULT_FINITE_SET_UNIFORM = 6,
+    RL_MULT_CIRC_SKEW_PRODUCT = 7,
+    RL_MULT_GAUSSIAN_CIRCULANT = 100
 } rl_multiplier_kind;
 
-/* A multiplier: drawn from `seed` by the reference's generator
- * (MultiplierSpec, multipliers.hpp:33-40), or supplied explicitly: `dense`
- * (n x n, row-major) for GAUSSIAN, `column` (first column, length n) for the
- * circulant kinds. Explicit buffers live in the call's rl_mem space. */
+/* randla::ToeplitzVariant (multipliers.hpp:31) */
+typedef enum rl_toeplitz_variant { RL_TOEPLITZ_REAL = 0, RL_TOEPLITZ_UNITARY = 1 } rl_toeplitz_variant;
+
+/* A multiplier spec (randla::MultiplierSpec, multipliers.hpp:33-40; rows and
+ * cols come from the call: n x n for preprocessing, n x l for sketching).
+ * Drawn from `seed` by the reference's generator, or supplied explicitly:
+ * `dense` (rows x cols, row-major) for the dense kinds, `column` (first
+ * column of the circulant, length n) for the circulant kinds. Explicit buffers
+ * live in the call's rl_mem space. set_cardinality 0 means the reference's
+ * default 65536. */
 typedef struct rl_multiplier {
-    int32_t kind; /* rl_multiplier_kind */
+    int32_t kind;             /* rl_multiplier_kind */
+    int32_t variant;          /* rl_toeplitz_variant (TOEPLITZ_BLOCK only) */
     uint64_t seed;
+    uint64_t set_cardinality; /* FINITE_SET_UNIFORM only */
     const double* dense;
     const double* column;
 } rl_multiplier;
@@ -112,6 +134,10 @@ typedef struct rl_solve_info {
     double pivot_tolerance;      /* tol_pivot(n) * norm used for the verdict (upper bound when lazy) */
     double stage_ms[4];          /* device time (CUDA events on the context stream): product A*H,
                                     factor + verdict, chain solve + refinement, whole call */
+    /* in: optional caller buffer for the whole residual history (refine_steps + 1 entries;
+       residual_history above keeps the first 8). Required when refine_steps > 7. */
+    double* history;
+    int64_t history_capacity;
 } rl_solve_info;
 
 /* Per-batch summary of rl_batched_genp_solve_32. */
@@ -139,6 +165,10 @@ RL_API rl_status rl_synchronize(rl_context* ctx);
 RL_API int64_t rl_kernel_launches(void);
 /* number of host threads used by the exact multiplier generator (0 = all cores) */
 RL_API void rl_set_host_threads(int threads);
+/* the CUDA device a context (NULL: the calling thread's default context, which
+ * is the one for the thread's current device, cudaGetDevice) runs on; -1 when
+ * there is no device */
+RL_API int rl_context_device(rl_context* ctx);
 
 /* ---- seeded multipliers (host, bit-exact to the reference) ----------- */
 /* derive_seed (multipliers.hpp:54-56) */
@@ -159,12 +189,27 @@ RL_API rl_status rl_gen_gaussian_device(rl_context* ctx, int64_t m, int64_t n, u
                                         int64_t* hard_cases);
 /* gen_real_circulant first column (multipliers.hpp:67-73) */
 RL_API rl_status rl_gen_real_circulant_column(int64_t n, uint64_t seed, double* out);
+/* gen_finite_set_uniform(m, n, seed, cardinality) (multipliers.hpp:142-154):
+ * entries uniform over {-floor(card/2), ..., ceil(card/2) - 1}, next_below
+ * rejection sampling (rng.hpp:46-53); RL_ERR_DIMENSION for cardinality < 2 */
+RL_API rl_status rl_gen_finite_set_uniform(int64_t m, int64_t n, uint64_t seed, uint64_t cardinality, double* out);
+/* materialize(spec) of a real family with rows x cols (multipliers.hpp:174-218)
+ * into out (row-major, ld = cols): the dense multiplier the reference would
+ * build. Host or device output per `mem`; circulant and skew-product families
+ * are expanded on the device. */
+RL_API rl_status rl_materialize(rl_context* ctx, rl_mem mem, const rl_multiplier* spec, int64_t rows, int64_t cols,
+                                double* out);
 
 /* ---- dense products ---------------------------------------------------- */
 /* C = A B (m x k times k x n, row-major, leading dimensions in elements);
  * replaces matmul (matrix.hpp:115-121). FP64 DMMA tiles. */
 RL_API rl_status rl_dgemm(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, int64_t k, const double* a,
                           int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
+/* svd_values (svd.hpp:76-88): the min(m, n) singular values of a (m x n),
+ * non-increasing, by one-sided Jacobi on the device (the reference calls
+ * Eigen's JacobiSVD / BDCSVD: equal up to rounding). One CTA: meant for the
+ * small matrices the reference's checks use, not for the hot path. */
+RL_API rl_status rl_singular_values(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a, double* out);
 /* spectral_norm_estimate (norms.hpp:35-78) */
 RL_API rl_status rl_spectral_norm_estimate(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
                                            double* out);
@@ -207,14 +252,17 @@ RL_API rl_status rl_block_ge_factor(rl_context* ctx, rl_mem mem, int64_t n, cons
 RL_API rl_status rl_block_solve(rl_context* ctx, rl_mem mem, int64_t n, int64_t nsplit, const int64_t* split,
                                const double* factors, const int64_t* perm, const double* b, double* x);
 
-/* preprocess_solve(a, b, none, post, refine_steps) (preprocess.hpp:156-180):
- * product = A*H (dense GEMM or circulant FFT), GENP, chain solve
- * x = H (LU)^-1 b, refinement. lu_out (n x n, nullable) receives the packed
- * factors of the product. want_norm_a != 0 also evaluates
+/* preprocess_solve(a, b, pre, post, refine_steps) (preprocess.hpp:156-180):
+ * product = F (A H) with F = SideMultiplier::make(pre), H = make(post)
+ * (preprocess.hpp:27-60: dense kinds by the DMMA GEMM, circulant kinds
+ * structured through the FFT kernel), GENP, chain solve x = H (LU)^-1 (F b),
+ * refinement. pre / post NULL = None. lu_out (n x n, nullable) receives the
+ * packed factors of the product. want_norm_a != 0 also evaluates
  * spectral_norm_estimate(A) for info->residual_rel_a. */
 RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* a,
-                                            const double* b, const rl_multiplier* post, int64_t refine_steps,
-                                            double* x, double* lu_out, int32_t want_norm_a, rl_solve_info* info);
+                                            const double* b, const rl_multiplier* pre, const rl_multiplier* post,
+                                            int64_t refine_steps, double* x, double* lu_out, int32_t want_norm_a,
+                                            rl_solve_info* info);
 
 /* BASELINE config 2: `batch` independent 32x32 systems, each
  * preprocess_solve(A_i, b_i, none, {Gaussian, G_i}, 0). a, g: batch x 32 x 32;
@@ -233,17 +281,26 @@ RL_API rl_status rl_circulant_right_multiply(rl_context* ctx, rl_mem mem, int64_
  * A m x k, c parent column length np >= k, out m x l */
 RL_API rl_status rl_toeplitz_right_multiply(rl_context* ctx, rl_mem mem, int64_t m, int64_t k, const double* a,
                                             int64_t np, const double* c, int64_t l, double* out);
+/* circulant_apply(C(c), x) (circulant.hpp:91-96): y = C x for real c, x, with
+ * the reference's imaginary-part check (RL_ERR_LOGIC, circulant.hpp:57-66) */
+RL_API rl_status rl_circulant_apply(rl_context* ctx, rl_mem mem, int64_t n, const double* c, const double* x,
+                                    double* y);
+/* fft / inverse_fft (fft.hpp:76-98) on `count` complex vectors of length n,
+ * in place, interleaved (re, im) doubles: forward multiplies by
+ * Omega = (omega^{jk}), omega = exp(+2 pi i / n) — the reference's sign —
+ * inverse by Omega^-1 = Omega^H / n. Power-of-two lengths run a radix FFT,
+ * other lengths the dense O(n^2) transform as the reference does. */
+RL_API rl_status rl_fft(rl_context* ctx, rl_mem mem, int64_t count, int64_t n, double* z, int32_t inverse);
 
 /* ---- low-rank ----------------------------------------------------------- */
 /* orthonormal_basis (qr.hpp:51-54) by CholeskyQR2: q (m x l) with positive
  * diag R; RL_ERR_RANK_DEFICIENCY (info column) per qr.hpp:33-38. r nullable. */
 RL_API rl_status rl_cholqr2(rl_context* ctx, rl_mem mem, int64_t m, int64_t l, const double* y, double* q,
                             double* r, int64_t* bad_column);
-/* range_find + approximation residual (lowrank.hpp:62-83, :99-102):
- * Y = A H (H: n x l Gaussian(seed) or Toeplitz block of a Gaussian circulant
- * of parent length n), Q = orthonormal_basis(Y), residual R = A - Q (Q^T A).
- * Outputs: q (m x l, nullable), frobenius = ||R||_F, spectral = ||R||_2 by
- * the restated power iteration (norms.hpp:52-77). */
+/* Low-rank outcome: the residual R = A - Q (Q^T A) (lowrank.hpp:35-37) in
+ * Frobenius and spectral norm (||R||_2 by the restated power iteration of
+ * norms.hpp:52-77 on the implicit operator R), the 1-based rank-deficient
+ * column of qr (qr.hpp:33-38), 0 = none. */
 typedef struct rl_lowrank_info {
     double residual_frobenius;
     double residual_spectral;
@@ -251,8 +308,23 @@ typedef struct rl_lowrank_info {
     int32_t power_iterations;
     int32_t reserved;
 } rl_lowrank_info;
+/* range_find(a, r, p, spec, power_steps) (lowrank.hpp:62-83) with l = r + p:
+ * the sketch Y = A H for H = the spec's n x l multiplier (ToeplitzBlock
+ * through the FFT, everything else materialized and multiplied by the DMMA
+ * GEMM, as the reference does), power_steps alternating products
+ * Y <- A (A^T Y) (lowrank.hpp:51-57), Q = orthonormal_basis(Y) (CholeskyQR2,
+ * qr.hpp:51-54) into q (m x l). */
+RL_API rl_status rl_range_find(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a, int64_t l,
+                               const rl_multiplier* h, int64_t power_steps, double* q, rl_lowrank_info* info);
+/* approximation_residual(a, result) (lowrank.hpp:99-102) for a given A (m x n)
+ * and basis Q (m x l): residual norms of R = A - Q (Q^T A) into info. */
+RL_API rl_status rl_approximation_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                           int64_t l, const double* q, rl_lowrank_info* info);
+/* range_find followed by approximation_residual on the same resident A (one
+ * call, one upload of A): the BASELINE config 4/5 pipeline. q nullable. */
 RL_API rl_status rl_range_find_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
-                                        int64_t l, const rl_multiplier* h, double* q, rl_lowrank_info* info);
+                                        int64_t l, const rl_multiplier* h, int64_t power_steps, double* q,
+                                        rl_lowrank_info* info);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,7 @@ class _C:
         self._normest = s("or_spectral_norm_estimate", ctypes.c_double, [i64, i64, _dp])
         self._genp = s("or_genp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p, _dp])
         self._solve = s("or_lu_solve", None, [i64, _dp, _dp, _dp])
+        self._gsteps = s("or_genp_steps", None, [i64, _dp, i64, i64])
         self._fft = s("or_fft", ctypes.c_int, [i64, _dp])
         self._ifft = s("or_inverse_fft", ctypes.c_int, [i64, _dp])
         self._capply = s("or_circulant_apply", ctypes.c_int, [i64, _dp, _dp, _dp])
@@ -132,6 +133,11 @@ class _C:
         x = np.empty_like(b)
         self._solve(lu.shape[0], ptr(lu), ptr(b), ptr(x))
         return x
+
+    def genp_steps(self, lu, j0, j1):
+        """elimination steps j0..j1-1 of genp_factor, in place (lu C-contiguous)"""
+        assert lu.flags.c_contiguous and lu.dtype == np.float64
+        self._gsteps(lu.shape[0], ptr(lu), j0, j1)
 
     def fft(self, z, inverse=False):
         w = np.ascontiguousarray(np.asarray(z, dtype=np.complex128)).copy()
@@ -211,6 +217,8 @@ class _Ref:
         self._golden = s("ref_golden_draws", None, [ctypes.c_char_p, u64, i64, _dp, _dp])
         self._gen = s("ref_gen_gaussian", None, [i64, i64, u64, _dp])
         self._genc = s("ref_gen_real_circulant_column", None, [i64, u64, _dp])
+        self._genf = s("ref_gen_finite_set_uniform", None, [i64, i64, u64, u64, _dp])
+        self._genk = s("ref_gen_circ_skew_product", None, [i64, u64, _dp])
         self._matmul = s("ref_matmul", ctypes.c_int, [i64, i64, i64, _dp, _dp, _dp])
         self._normest = s("ref_spectral_norm_estimate", ctypes.c_double, [i64, i64, _dp])
         self._genp = s("ref_genp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p])
@@ -222,6 +230,12 @@ class _Ref:
         self._mtoep = s("ref_matmul_by_toeplitz_block", ctypes.c_int, [i64, i64, _dp, i64, _dp, i64, _dp])
         self._pre = s("ref_preprocess_solve", ctypes.c_int,
                       [i64, _dp, _dp, ctypes.c_int, u64, i64, _dp, _dp, _i32p, _i64p])
+        self._pre2 = s("ref_preprocess_solve_spec", ctypes.c_int,
+                       [i64, _dp, _dp, ctypes.c_int, ctypes.c_int, u64, ctypes.c_int, ctypes.c_int, u64, u64, i64,
+                        _dp, _dp, _i32p, _i64p])
+        self._sketch = s("ref_range_sketch", ctypes.c_int,
+                         [i64, i64, _dp, i64, ctypes.c_int, ctypes.c_int, u64, u64, i64, _dp])
+        self._mat = s("ref_materialize", ctypes.c_int, [ctypes.c_int, ctypes.c_int, u64, u64, i64, i64, _dp])
         self._batch = s("ref_batched_config2", i64, [i64, u64, i64, i64, _dp, _dp])
         self._trials = s("ref_parallel_dense_trials", i64, [i64, i64, _dp, _dp, _u64p, _dp])
         self._gepp = s("ref_gepp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p])
@@ -281,6 +295,16 @@ class _Ref:
     def gen_real_circulant_column(self, n, seed):
         out = np.empty(n)
         self._genc(n, seed, ptr(out))
+        return out
+
+    def gen_finite_set_uniform(self, m, n, seed, card):
+        out = np.empty((m, n))
+        self._genf(m, n, seed, card, ptr(out))
+        return out
+
+    def gen_circ_skew_product(self, n, seed):
+        out = np.empty((n, n))
+        self._genk(n, seed, ptr(out))
         return out
 
     def matmul(self, a, b):
@@ -355,6 +379,33 @@ class _Ref:
         zs = np.zeros(1, np.int64)
         st = self._pre(n, ptr(a), ptr(b), post_kind, seed, refine, ptr(x), ptr(hist), ctypes.byref(div), ptr(zs))
         return dict(x=x, history=hist, diverged=bool(div.value), status=st, zero_step=int(zs[0]))
+
+    def preprocess_solve_spec(self, a, b, pre=(0, 0, 0), post=(0, 0, 0), refine=0, card=65536):
+        """preprocess_solve with MultiplierSpecs given as (kind, variant, seed),
+        kinds = the reference's MultiplierKind ordinals"""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        n = a.shape[0]
+        x = np.empty(n)
+        hist = np.empty(refine + 1)
+        div = ctypes.c_int(0)
+        zs = np.zeros(1, np.int64)
+        st = self._pre2(n, ptr(a), ptr(b), pre[0], pre[1], pre[2], post[0], post[1], post[2], card, refine, ptr(x),
+                        ptr(hist), ctypes.byref(div), ptr(zs))
+        return dict(x=x, history=hist, diverged=bool(div.value), status=st, zero_step=int(zs[0]))
+
+    def range_sketch(self, a, l, kind, seed, variant=0, power_steps=0, card=65536):
+        """range_find's sketch (lowrank.hpp:51-81) -> (Y, status)"""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        m, n = a.shape
+        y = np.empty((m, l))
+        st = self._sketch(m, n, ptr(a), l, kind, variant, seed, card, power_steps, ptr(y))
+        return y, st
+
+    def materialize(self, kind, rows, cols, seed, variant=0, card=65536):
+        out = np.empty((rows, cols))
+        st = self._mat(kind, variant, seed, card, rows, cols, ptr(out))
+        return out, st
 
     def batched_config2(self, count, base=7, i0=0, dim=32):
         x = np.empty((count, dim))

@@ -257,6 +257,21 @@ int or_genp_factor(int64_t n, const double* a, double* lu, int64_t* zero_step, d
     return OR_OK;
 }
 
+/* elimination steps j0..j1-1 of genp_factor's loop (lu.hpp:47-56), in place on
+ * the n x n matrix `lu` (no verdict): the bounded sample of the full-size GENP
+ * workload that bench.py's cpu_baseline times (the same arithmetic and memory
+ * traffic per step as or_genp_factor) */
+void or_genp_steps(int64_t n, double* lu, int64_t j0, int64_t j1) {
+    for (int64_t j = j0; j < j1 && j < n; ++j) {
+        const double piv = lu[j * n + j];
+        for (int64_t i = j + 1; i < n; ++i) {
+            const double l = lu[i * n + j] / piv;
+            lu[i * n + j] = l;
+            for (int64_t k = j + 1; k < n; ++k) lu[i * n + k] = lu[i * n + k] - l * lu[j * n + k];
+        }
+    }
+}
+
 /* lu.hpp:100-123 (no permutation) */
 void or_lu_solve(int64_t n, const double* lu, const double* b, double* x) {
     if (x != b) memcpy(x, b, sizeof(double) * n);

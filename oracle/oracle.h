@@ -63,6 +63,7 @@ double or_spectral_norm_estimate(int64_t m, int64_t n, const double* a);
 /* packed LU: strict lower = L (unit diag implicit), upper incl. diag = U.
  * Returns OR_OK or OR_ZERO_PIVOT with *zero_step = 1-based step. */
 int or_genp_factor(int64_t n, const double* a, double* lu, int64_t* zero_step, double* tol_out);
+void or_genp_steps(int64_t n, double* lu, int64_t j0, int64_t j1);
 void or_lu_solve(int64_t n, const double* lu, const double* b, double* x);
 double or_relative_residual(int64_t n, const double* a, const double* x, const double* b);
 

@@ -16,6 +16,7 @@
 #include "randla/block_ge.hpp"
 #include "randla/circulant.hpp"
 #include "randla/fft.hpp"
+#include "randla/lowrank.hpp"
 #include "randla/lu.hpp"
 #include "randla/multipliers.hpp"
 #include "randla/norms.hpp"
@@ -98,6 +99,18 @@ void ref_golden_draws(const char* label, uint64_t seed, int64_t trials, double* 
 void ref_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out) {
     const RealMatrix g = gen_gaussian(static_cast<std::size_t>(m), static_cast<std::size_t>(n), seed);
     std::memcpy(out, g.data(), sizeof(double) * m * n);
+}
+
+void ref_gen_finite_set_uniform(int64_t m, int64_t n, uint64_t seed, uint64_t card, double* out) {
+    const RealMatrix g = gen_finite_set_uniform(static_cast<std::size_t>(m), static_cast<std::size_t>(n), seed,
+                                                static_cast<std::size_t>(card));
+    std::memcpy(out, g.data(), sizeof(double) * m * n);
+}
+
+// gen_circ_skew_product (multipliers.hpp:164-172), through the shim's GEMM hook
+void ref_gen_circ_skew_product(int64_t n, uint64_t seed, double* out) {
+    const RealMatrix g = gen_circ_skew_product(static_cast<std::size_t>(n), seed);
+    std::memcpy(out, g.data(), sizeof(double) * n * n);
 }
 
 void ref_gen_real_circulant_column(int64_t n, uint64_t seed, double* out) {
@@ -215,6 +228,75 @@ int ref_preprocess_solve(int64_t n, const double* a, const double* b, int post_k
             *diverged = out.diverged ? 1 : 0;
         },
         zero_step);
+}
+
+// preprocess_solve(a, b, pre, post, refine) with full MultiplierSpecs
+// (kinds are the reference's MultiplierKind ordinals, multipliers.hpp:20-29)
+int ref_preprocess_solve_spec(int64_t n, const double* a, const double* b, int pre_kind, int pre_variant,
+                              uint64_t pre_seed, int post_kind, int post_variant, uint64_t post_seed, uint64_t card,
+                              int64_t refine, double* x, double* history, int* diverged, int64_t* zero_step) {
+    *zero_step = 0;
+    return guarded(
+        [&] {
+            MultiplierSpec pre, post;
+            pre.kind = static_cast<MultiplierKind>(pre_kind);
+            pre.variant = static_cast<ToeplitzVariant>(pre_variant);
+            pre.seed = pre_seed;
+            pre.set_cardinality = static_cast<std::size_t>(card);
+            post.kind = static_cast<MultiplierKind>(post_kind);
+            post.variant = static_cast<ToeplitzVariant>(post_variant);
+            post.seed = post_seed;
+            post.set_cardinality = static_cast<std::size_t>(card);
+            const SolveOutcome<double> out =
+                preprocess_solve(wrap(n, n, a), std::vector<double>(b, b + n), pre, post, static_cast<std::size_t>(refine));
+            std::memcpy(x, out.x.data(), sizeof(double) * n);
+            for (int64_t s = 0; s <= refine; ++s)
+                history[s] = s < static_cast<int64_t>(out.residual_history.size()) ? out.residual_history[s] : NAN;
+            *diverged = out.diverged ? 1 : 0;
+        },
+        zero_step);
+}
+
+// the sketch of range_find(a, l, 0, spec, power_steps) (lowrank.hpp:51-81): the
+// reference's own multiplier materialization / Toeplitz FFT product and power
+// alternation, before its qr (which needs Eigen's Householder QR; the tests
+// finish with the restated QR)
+int ref_range_sketch(int64_t m, int64_t n, const double* a, int64_t l, int kind, int variant, uint64_t seed,
+                     uint64_t card, int64_t power_steps, double* y) {
+    return guarded([&] {
+        MultiplierSpec spec;
+        spec.kind = static_cast<MultiplierKind>(kind);
+        spec.variant = static_cast<ToeplitzVariant>(variant);
+        spec.seed = seed;
+        spec.set_cardinality = static_cast<std::size_t>(card);
+        spec.rows = static_cast<std::size_t>(n);
+        spec.cols = static_cast<std::size_t>(l);
+        const RealMatrix am = wrap(m, n, a);
+        RealMatrix sketch(1, 1);
+        if (spec.kind == MultiplierKind::ToeplitzBlock) {
+            if (spec.variant != ToeplitzVariant::Real) throw DimensionError("complex multiplier family requested in a real pipeline");
+            sketch = matmul_by_toeplitz_block(am, gen_real_toeplitz_block(spec.rows, spec.cols, spec.seed));
+        } else {
+            sketch = matmul(am, materialize<double>(spec));
+        }
+        for (int64_t s = 0; s < power_steps; ++s) sketch = matmul(am, matmul(am.adjoint(), sketch));
+        std::memcpy(y, sketch.data(), sizeof(double) * m * l);
+    });
+}
+
+// materialize<double>(spec) (multipliers.hpp:174-218)
+int ref_materialize(int kind, int variant, uint64_t seed, uint64_t card, int64_t rows, int64_t cols, double* out) {
+    return guarded([&] {
+        MultiplierSpec spec;
+        spec.kind = static_cast<MultiplierKind>(kind);
+        spec.variant = static_cast<ToeplitzVariant>(variant);
+        spec.seed = seed;
+        spec.set_cardinality = static_cast<std::size_t>(card);
+        spec.rows = static_cast<std::size_t>(rows);
+        spec.cols = static_cast<std::size_t>(cols);
+        const RealMatrix g = materialize<double>(spec);
+        std::memcpy(out, g.data(), sizeof(double) * rows * cols);
+    });
 }
 
 // BASELINE config 2 with the reference's own trial pool

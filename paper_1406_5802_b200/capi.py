@@ -28,10 +28,19 @@ RL_ERR_UNSUPPORTED = 14
 RL_HOST = 0
 RL_DEVICE = 1
 
+# randla::MultiplierKind ordinals (multipliers.hpp:20-29) + one extension
 RL_MULT_NONE = 0
 RL_MULT_GAUSSIAN = 1
 RL_MULT_REAL_CIRCULANT = 2
-RL_MULT_GAUSSIAN_CIRCULANT = 3
+RL_MULT_UNITARY_CIRCULANT = 3
+RL_MULT_TOEPLITZ_BLOCK = 4
+RL_MULT_SRFT = 5
+RL_MULT_FINITE_SET_UNIFORM = 6
+RL_MULT_CIRC_SKEW_PRODUCT = 7
+RL_MULT_GAUSSIAN_CIRCULANT = 100
+
+RL_TOEPLITZ_REAL = 0
+RL_TOEPLITZ_UNITARY = 1
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -44,7 +53,8 @@ i32 = ctypes.c_int32
 
 
 class rl_multiplier(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("seed", ctypes.c_uint64), ("dense", _vp), ("column", _vp)]
+    _fields_ = [("kind", ctypes.c_int32), ("variant", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("set_cardinality", ctypes.c_uint64), ("dense", _vp), ("column", _vp)]
 
 
 class rl_solve_info(ctypes.Structure):
@@ -55,11 +65,16 @@ class rl_solve_info(ctypes.Structure):
                 ("max_abs_u", ctypes.c_double), ("norm_floor", ctypes.c_double),
                 ("norm_frobenius", ctypes.c_double), ("norm_estimate", ctypes.c_double),
                 ("norm_estimate_evaluated", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("pivot_tolerance", ctypes.c_double), ("stage_ms", ctypes.c_double * 4)]
+                ("pivot_tolerance", ctypes.c_double), ("stage_ms", ctypes.c_double * 4),
+                ("history", _dp), ("history_capacity", ctypes.c_int64)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("residual_history", "reserved", "stage_ms")}
-        d["residual_history"] = list(self.residual_history)[: self.history_len]
+        skip = ("residual_history", "reserved", "stage_ms", "history", "history_capacity")
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in skip}
+        if self.history and self.history_capacity >= self.history_len:
+            d["residual_history"] = [self.history[i] for i in range(self.history_len)]
+        else:
+            d["residual_history"] = list(self.residual_history)[: min(self.history_len, 8)]
         d["stage_ms"] = list(self.stage_ms)
         return d
 
@@ -87,14 +102,18 @@ SIGNATURES = {
     "rl_synchronize": (ctypes.c_int, [_vp]),
     "rl_kernel_launches": (ctypes.c_int64, []),
     "rl_set_host_threads": (None, [ctypes.c_int]),
+    "rl_context_device": (ctypes.c_int, [_vp]),
     "rl_derive_seed": (u64, [u64, u64, u64]),
     "rl_hash_label": (u64, [ctypes.c_char_p]),
     "rl_gen_gaussian": (ctypes.c_int, [i64, i64, u64, _vp]),
     "rl_gen_gaussian_batch": (ctypes.c_int, [i64, i64, i64, _vp, _vp]),
     "rl_gen_gaussian_device": (ctypes.c_int, [_vp, i64, i64, u64, _vp, i64, ctypes.POINTER(i64)]),
     "rl_gen_real_circulant_column": (ctypes.c_int, [i64, u64, _vp]),
+    "rl_gen_finite_set_uniform": (ctypes.c_int, [i64, i64, u64, u64, _vp]),
+    "rl_materialize": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(rl_multiplier), i64, i64, _vp]),
     "rl_dgemm": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, i64, _vp, i64, _vp, i64, _vp, i64]),
     "rl_spectral_norm_estimate": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _dp]),
+    "rl_singular_values": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp]),
     "rl_genp_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, ctypes.POINTER(rl_solve_info)]),
     "rl_lu_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
     "rl_gepp_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp, _vp]),
@@ -102,14 +121,21 @@ SIGNATURES = {
     "rl_block_ge_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, i64, _vp, _vp, _vp, _vp, _vp]),
     "rl_block_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp, _vp, _vp, _vp]),
     "rl_preprocessed_genp_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, ctypes.POINTER(rl_multiplier),
-                                                  i64, _vp, _vp, i32, ctypes.POINTER(rl_solve_info)]),
+                                                  ctypes.POINTER(rl_multiplier), i64, _vp, _vp, i32,
+                                                  ctypes.POINTER(rl_solve_info)]),
     "rl_batched_genp_solve_32": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                                 ctypes.POINTER(rl_batch_summary)]),
     "rl_circulant_right_multiply": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp, _vp]),
     "rl_toeplitz_right_multiply": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, _vp, i64, _vp]),
+    "rl_circulant_apply": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
+    "rl_fft": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i32]),
     "rl_cholqr2": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp, _vp, _i64p]),
+    "rl_range_find": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, ctypes.POINTER(rl_multiplier), i64,
+                                     _vp, ctypes.POINTER(rl_lowrank_info)]),
+    "rl_approximation_residual": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, _vp,
+                                                 ctypes.POINTER(rl_lowrank_info)]),
     "rl_range_find_residual": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, ctypes.POINTER(rl_multiplier),
-                                              _vp, ctypes.POINTER(rl_lowrank_info)]),
+                                              i64, _vp, ctypes.POINTER(rl_lowrank_info)]),
 }
 
 

@@ -160,7 +160,8 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
 }
 
 // Main-kernel shared memory: only P (then its LU) and a few vectors per warp
-// (9,472 B): 5 CTAs x 4 warps = 20 resident warps per SM. G never touches
+// (9,472 B): the kernel is built for 4 CTAs x 4 warps = 16 resident warps per SM
+// (__launch_bounds__ below; 20 warps spilled). G never touches
 // shared memory: its B fragments go from global straight into registers, and
 // the two late passes that need A and G again (x = G y, r = b - A x) re-read
 // them from L2 with evict-first loads.

@@ -25,6 +25,7 @@
 // uses them.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "device_common.cuh"
@@ -202,20 +203,21 @@ __global__ void row_update_kernel(double* __restrict__ y, const double* __restri
     y[i] = acc;
 }
 
-// Singular values of a (n x n, ld) by one-sided Jacobi on its columns, one
-// CTA: the columns are copied transposed into w (n x n, contiguous rows), n/2
-// disjoint pairs per round (round-robin order), one warp per pair; sweeps
-// until no pair is rotated. sv (n) receives the column norms (unsorted).
+// Singular values of a (m x n, ld, m >= n) by one-sided Jacobi on its
+// columns, one CTA: the columns are copied transposed into w (n rows of
+// length m), n/2 disjoint pairs per round (round-robin order), one warp per
+// pair; sweeps until no pair is rotated. sv (n) receives the column norms
+// (unsorted).
 constexpr int JT = 512;
-__global__ void __launch_bounds__(JT) jacobi_sv_kernel(const double* __restrict__ a, int64_t ld, int n,
+__global__ void __launch_bounds__(JT) jacobi_sv_kernel(const double* __restrict__ a, int64_t ld, int m, int n,
                                                         double* __restrict__ w, int* __restrict__ order,
                                                         double* __restrict__ sv) {
     __shared__ int s_rot;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int np = n + (n & 1);  // with a dummy column when n is odd
-    for (int64_t e = tid; e < static_cast<int64_t>(n) * n; e += JT) {
+    for (int64_t e = tid; e < static_cast<int64_t>(m) * n; e += JT) {
         const int i = static_cast<int>(e / n), p = static_cast<int>(e % n);
-        w[static_cast<int64_t>(p) * n + i] = a[i * ld + p];
+        w[static_cast<int64_t>(p) * m + i] = a[i * ld + p];
     }
     for (int i = tid; i < np; i += JT) order[i] = i;
     __syncthreads();
@@ -233,10 +235,10 @@ __global__ void __launch_bounds__(JT) jacobi_sv_kernel(const double* __restrict_
                     p = q;
                     q = t;
                 }
-                double* wp = w + static_cast<int64_t>(p) * n;
-                double* wq = w + static_cast<int64_t>(q) * n;
+                double* wp = w + static_cast<int64_t>(p) * m;
+                double* wq = w + static_cast<int64_t>(q) * m;
                 double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = lane; i < n; i += 32) {
+                for (int i = lane; i < m; i += 32) {
                     al = fma(wp[i], wp[i], al);
                     be = fma(wq[i], wq[i], be);
                     ga = fma(wp[i], wq[i], ga);
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(JT) jacobi_sv_kernel(const double* __restrict_
                     const double zeta = (be - al) / (2.0 * ga);
                     const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-                    for (int i = lane; i < n; i += 32) {
+                    for (int i = lane; i < m; i += 32) {
                         const double xp = wp[i], xq = wq[i];
                         wp[i] = cs * xp - sn * xq;
                         wq[i] = sn * xp + cs * xq;
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(JT) jacobi_sv_kernel(const double* __restrict_
     }
     for (int p = warp; p < n; p += JT / 32) {
         double s = 0.0;
-        for (int i = lane; i < n; i += 32) s = fma(w[static_cast<int64_t>(p) * n + i], w[static_cast<int64_t>(p) * n + i], s);
+        for (int i = lane; i < m; i += 32) s = fma(w[static_cast<int64_t>(p) * m + i], w[static_cast<int64_t>(p) * m + i], s);
         s = warp_sum(s);
         if (lane == 0) sv[p] = sqrt(s);
     }
@@ -343,7 +345,7 @@ rl_status min_singular_value(rl_context* ctx, int64_t k, const double* blk, int6
     if ((st = dev_alloc(bs, ctx->stream, static_cast<size_t>(k), &sv)) != RL_OK) return st;
     if ((st = dev_alloc(bo, ctx->stream, static_cast<size_t>(2 * (k + 1)), &order)) != RL_OK) return st;
     if ((st = dev_alloc(bm, ctx->stream, 1, &mn)) != RL_OK) return st;
-    jacobi_sv_kernel<<<1, JT, 0, ctx->stream>>>(blk, ld, static_cast<int>(k), w, order, sv);
+    jacobi_sv_kernel<<<1, JT, 0, ctx->stream>>>(blk, ld, static_cast<int>(k), static_cast<int>(k), w, order, sv);
     RL_CHECK_LAUNCH("jacobi_sv_kernel");
     min_kernel<<<1, 256, 0, ctx->stream>>>(sv, static_cast<int>(k), mn);
     RL_CHECK_LAUNCH("min_kernel");
@@ -588,5 +590,46 @@ extern "C" RL_API rl_status rl_block_solve(rl_context* ctx, rl_mem mem, int64_t 
     RL_CUDA(cudaMemcpyAsync(xs, t, n * 8, cudaMemcpyDeviceToDevice, s));
     if (mem == RL_HOST) RL_CUDA(cudaMemcpyAsync(x, xs, n * 8, cudaMemcpyDeviceToHost, s));
     RL_CUDA(cudaStreamSynchronize(s));
+    return RL_OK;
+}
+
+// svd_values (svd.hpp:76-88): the min(m, n) singular values, non-increasing,
+// by the one-sided Jacobi kernel (on a^T when m < n: same values)
+extern "C" RL_API rl_status rl_singular_values(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                               double* out) {
+    if (m <= 0 || n <= 0) return set_error(RL_ERR_DIMENSION, "svd_values: empty matrix");
+    if (!a || !out) return set_error(RL_ERR_INVALID_ARGUMENT, "svd_values: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    const int64_t r = std::min(m, n), c = std::max(m, n);  // operate on the tall orientation (c x r)
+    double *da = nullptr, *w = nullptr, *sv = nullptr, *tall = nullptr;
+    int* order = nullptr;
+    DevBuf ba, bw, bs, bo, bt;
+    if ((st = dev_alloc(ba, s, static_cast<size_t>(m * n), &da)) != RL_OK) return st;
+    if ((st = dev_alloc(bt, s, static_cast<size_t>(m * n), &tall)) != RL_OK) return st;
+    if ((st = dev_alloc(bw, s, static_cast<size_t>(m * n), &w)) != RL_OK) return st;
+    if ((st = dev_alloc(bs, s, static_cast<size_t>(r), &sv)) != RL_OK) return st;
+    if ((st = dev_alloc(bo, s, static_cast<size_t>(2 * (r + 1)), &order)) != RL_OK) return st;
+    RL_CUDA(cudaMemcpyAsync(da, a, m * n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    const double* src = da;
+    if (m < n) {
+        if ((st = transpose_device(ctx, da, n, m, n, tall, m)) != RL_OK) return st;
+        src = tall;
+    }
+    jacobi_sv_kernel<<<1, JT, 0, s>>>(src, r, static_cast<int>(c), static_cast<int>(r), w, order, sv);
+    RL_CHECK_LAUNCH("jacobi_sv_kernel");
+    std::vector<double> h(static_cast<size_t>(r));
+    RL_CUDA(cudaMemcpyAsync(h.data(), sv, r * 8, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaStreamSynchronize(s));
+    std::sort(h.begin(), h.end(), [](double x, double y) { return x > y; });
+    if (host) {
+        std::memcpy(out, h.data(), r * 8);
+    } else {
+        RL_CUDA(cudaMemcpyAsync(out, h.data(), r * 8, cudaMemcpyHostToDevice, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+    }
     return RL_OK;
 }

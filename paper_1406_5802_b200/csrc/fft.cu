@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -901,6 +902,87 @@ rl_status circulant_dense(rl_context* ctx, const double* c, int64_t np, int64_t 
 bool circulant_fft_ok(int64_t np) { return is_pow2(np) && np <= 2 * MAXN; }
 }  // namespace rl
 
+// ---- standalone complex transforms: fft / inverse_fft (fft.hpp:76-98) -------
+namespace rl {
+namespace {
+
+// position of natural-order frequency k in the digit-reversed output of
+// forward_fft (the DIF pass with radix R leaves frequencies = r (mod R) in
+// subarray r of length N / R, recursively)
+__device__ __forceinline__ int dif_position(int k, int n) {
+    int radix[8];
+    const int passes = plan(n, radix);
+    int pos = 0, N = n;
+    for (int p = 0; p < passes; ++p) {
+        const int R = radix[p];
+        N /= R;
+        pos += (k % R) * N;
+        k /= R;
+    }
+    return pos;
+}
+
+// one vector of n <= MAXN points per CTA, resident in shared memory
+__global__ void __launch_bounds__(FT) cfft_kernel(cplx* __restrict__ z, int n, const cplx* __restrict__ tw, int inverse) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* s = reinterpret_cast<cplx*>(smem_raw);
+    cplx* v = z + static_cast<int64_t>(blockIdx.x) * n;
+    if (inverse) {  // the DIT passes consume the digit-reversed order
+        for (int k = threadIdx.x; k < n; k += blockDim.x) s[dif_position(k, n)] = v[k];
+        __syncthreads();
+        inverse_fft(s, n, tw, n, 1.0 / static_cast<double>(n));
+        for (int k = threadIdx.x; k < n; k += blockDim.x) v[k] = s[k];
+    } else {
+        for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = v[k];
+        __syncthreads();
+        forward_fft(s, n, tw, n);
+        for (int k = threadIdx.x; k < n; k += blockDim.x) v[k] = s[dif_position(k, n)];
+    }
+}
+
+// longer power-of-two vectors: radix-2 Stockham passes through global memory
+// (natural order in and out); pass span ns = 1, 2, 4, ..., n/2
+__global__ void stockham_pass_kernel(const cplx* __restrict__ x, cplx* __restrict__ y, int64_t n, int64_t count,
+                                     int64_t ns, const cplx* __restrict__ tw, int inverse, double scale) {
+    const int64_t half = n / 2;
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= count * half) return;
+    const int64_t v = idx / half, j = idx % half;
+    const cplx* xv = x + v * n;
+    cplx* yv = y + v * n;
+    const int64_t k = j % ns;
+    const cplx w = tw[k * (n / (2 * ns))];  // exp(+2 pi i k / (2 ns))
+    const cplx a = xv[j];
+    const cplx b = inverse ? cmulc(xv[j + half], w) : cmul(xv[j + half], w);
+    const int64_t d = (j / ns) * ns * 2 + k;
+    const cplx p = cadd(a, b), q = csub(a, b);
+    yv[d] = {p.x * scale, p.y * scale};
+    yv[d + ns] = {q.x * scale, q.y * scale};
+}
+
+// other lengths: the dense transform the reference falls back to
+// (dft_dense_apply, fft.hpp:59-72), one output entry per thread
+__global__ void dft_dense_kernel(const cplx* __restrict__ x, cplx* __restrict__ y, int64_t n, int64_t count,
+                                 const cplx* __restrict__ tw, int inverse) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= count * n) return;
+    const int64_t v = idx / n, i = idx % n;
+    const cplx* xv = x + v * n;
+    cplx acc = {0.0, 0.0};
+    int64_t t = 0;  // (i j) mod n
+    for (int64_t j = 0; j < n; ++j) {
+        const cplx r = tw[t];
+        acc = cadd(acc, inverse ? cmulc(xv[j], r) : cmul(xv[j], r));
+        t += i;
+        if (t >= n) t -= n;
+    }
+    const double sc = inverse ? 1.0 / static_cast<double>(n) : 1.0;
+    y[idx] = {acc.x * sc, acc.y * sc};
+}
+
+}  // namespace
+}  // namespace rl
+
 // ---- C ABI -----------------------------------------------------------------
 namespace {
 using namespace rl;
@@ -964,4 +1046,108 @@ extern "C" RL_API rl_status rl_toeplitz_right_multiply(rl_context* ctx, rl_mem m
                                                        const double* a, int64_t np, const double* c, int64_t l,
                                                        double* out) {
     return right_multiply(ctx, mem, m, k, a, np, c, l, out);
+}
+
+extern "C" RL_API rl_status rl_fft(rl_context* ctx, rl_mem mem, int64_t count, int64_t n, double* z, int32_t inverse) {
+    if (n <= 0 || count < 0) return set_error(RL_ERR_DIMENSION, inverse ? "inverse_fft: empty input" : "fft: empty input");
+    if (count == 0) return RL_OK;
+    if (!z) return set_error(RL_ERR_INVALID_ARGUMENT, "fft: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    const int64_t bytes = count * n * 16;
+    cplx* dz = reinterpret_cast<cplx*>(z);
+    cplx* work = nullptr;
+    const bool pow2 = is_pow2(n);
+    const bool small = pow2 && n <= MAXN;
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        if (host) dz = ar.take<cplx>(count * n);
+        if (!small) work = ar.take<cplx>(count * n);
+    });
+    if (!ok) return RL_ERR_OUT_OF_MEMORY;
+    if (host) RL_CUDA(cudaMemcpyAsync(dz, z, bytes, cudaMemcpyHostToDevice, s));
+    cplx* tw = nullptr;
+    if ((st = twiddles(ctx, n, &tw)) != RL_OK) return st;
+    if (small) {
+        static PerDeviceOnce configured_once;
+        st = once_per_device(configured_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(cfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAXN * 16));
+            return RL_OK;
+        });
+        if (st != RL_OK) return st;
+        cfft_kernel<<<static_cast<unsigned>(count), FT, static_cast<int>(n) * 16, s>>>(dz, static_cast<int>(n), tw,
+                                                                                        inverse ? 1 : 0);
+        RL_CHECK_LAUNCH("cfft_kernel");
+    } else if (pow2) {
+        const int64_t threads = count * (n / 2);
+        cplx *src = dz, *dst = work;
+        for (int64_t ns = 1; ns < n; ns *= 2) {
+            const double scale = (inverse && ns * 2 == n) ? 1.0 / static_cast<double>(n) : 1.0;
+            stockham_pass_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(src, dst, n, count, ns,
+                                                                                            tw, inverse ? 1 : 0, scale);
+            RL_CHECK_LAUNCH("stockham_pass_kernel");
+            std::swap(src, dst);
+        }
+        if (src != dz) RL_CUDA(cudaMemcpyAsync(dz, src, bytes, cudaMemcpyDeviceToDevice, s));
+    } else {
+        dft_dense_kernel<<<static_cast<unsigned>((count * n + 255) / 256), 256, 0, s>>>(dz, work, n, count, tw,
+                                                                                        inverse ? 1 : 0);
+        RL_CHECK_LAUNCH("dft_dense_kernel");
+        RL_CUDA(cudaMemcpyAsync(dz, work, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    if (host) {
+        RL_CUDA(cudaMemcpyAsync(z, dz, bytes, cudaMemcpyDeviceToHost, s));
+        RL_CUDA(cudaStreamSynchronize(s));
+    }
+    return RL_OK;
+}
+
+// circulant_apply(C(c), x) (circulant.hpp:91-96): y^T = x^T C^T, one row
+// through the circulant kernel with the transposed circulant's column
+// (circulant.hpp:40-45); the dense expansion and a GEMV when the FFT kernel
+// does not cover n. The transform of a real row is real by construction
+// (r2c), so strip_imag's logic_error cannot arise (nor does it for real
+// input in the reference).
+extern "C" RL_API rl_status rl_circulant_apply(rl_context* ctx, rl_mem mem, int64_t n, const double* c,
+                                               const double* x, double* y) {
+    if (n <= 0) return set_error(RL_ERR_DIMENSION, "circulant_apply: length mismatch");
+    if (!c || !x || !y) return set_error(RL_ERR_INVALID_ARGUMENT, "circulant_apply: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    std::vector<double> col(static_cast<size_t>(n)), colt(static_cast<size_t>(n));
+    if (host)
+        std::memcpy(col.data(), c, n * 8);
+    else
+        RL_CUDA(cudaMemcpy(col.data(), c, n * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) colt[i] = col[(n - i) % n];
+    const bool fft_path = circulant_fft_ok(n);
+    const int64_t ld = (n + 1) & ~int64_t(1);
+    double *dct = nullptr, *dx = nullptr, *dy = nullptr, *dense = nullptr;
+    void* spec = nullptr;
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        dct = ar.take<double>(n);
+        dx = ar.take<double>(n);
+        dy = ar.take<double>(n);
+        if (fft_path)
+            spec = ar.take<char>(n * 16);
+        else
+            dense = ar.take<double>(n * ld);
+    });
+    if (!ok) return RL_ERR_OUT_OF_MEMORY;
+    RL_CUDA(cudaMemcpyAsync(dct, (fft_path ? colt : col).data(), n * 8, cudaMemcpyHostToDevice, s));
+    RL_CUDA(cudaMemcpyAsync(dx, x, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    if (fft_path) {
+        st = circulant_rows(ctx, 1, n, dx, n, n, dct, n, dy, n, spec);
+    } else {
+        if ((st = circulant_dense(ctx, dct, n, n, n, dense, ld)) == RL_OK) st = gemv(ctx, n, n, dense, ld, dx, dy, nullptr);
+    }
+    if (st != RL_OK) return st;
+    RL_CUDA(cudaMemcpyAsync(y, dy, n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    RL_CUDA(cudaStreamSynchronize(s));  // col / colt are locals
+    return RL_OK;
 }

@@ -3,16 +3,17 @@
 // Mathematically genp_factor (lu.hpp:40-58): natural pivot order, no row
 // exchanges. Any recursive block factorization with unpivoted leaves "turns
 // into GENP up to the order", so the L and U here are the
-// reference's up to rounding. Structure (recursive, right-looking):
+// reference's up to rounding. Structure (right-looking, see genp_inplace):
 //
-//   rec(c0, w):  factor columns [c0, c0+w) of the trailing rows [c0, n)
-//     w <= kBase:  panel_diag_kernel   — w x w diagonal block, one CTA in smem
-//                  panel_rows_kernel   — L21 = A21 U11^-1, one row per thread
-//     else:        rec(c0, w1); U12 = L11^-1 A12 (trsm); A22 -= L21 U12 (DMMA
-//                  GEMM, kernels.cuh); rec(c0+w1, w-w1)
-//
-// so nearly all 2n^3/3 flops run in large GEMMs (K = n/2, n/4, ...). The
-// unit-lower TRSM is recursive the same way down to a 64-row base kernel.
+//   n >= 256:  128-column super-panels (genp_super128) with a one-super-panel
+//              lookahead on a high-priority stream; each super-panel is two
+//              fused 64-column panel launches (lu_panel64_kernel: diagonal
+//              block in registers, L21 rows, and the 128x128 L11^-1 built by an
+//              extra CTA), U12 = L11^-1 A12 as one K = 128 DMMA GEMM, and the
+//              trailing update A22 -= L21 U12 as one K = 128 DMMA GEMM
+//              (kernels.cuh);
+//   n <  256:  64-column panels with the same kernels (lookahead at n >= 192);
+//   the ragged last block (< 64 columns): panel_diag_kernel + panel_rows_kernel_dyn.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -24,7 +25,7 @@
 namespace rl {
 namespace {
 
-constexpr int kBase = 64;  // base panel width / base TRSM size
+constexpr int kBase = 64;  // panel width
 
 // ---- w x w diagonal block (w <= 64): GENP in shared memory --------------
 __global__ void __launch_bounds__(256)
@@ -52,47 +53,6 @@ panel_diag_kernel(double* __restrict__ a, int64_t lda, int w, double* __restrict
     }
 }
 
-// ---- 64 x 64 diagonal block, register-resident: thread i owns row i; the
-// pivot row is broadcast through a double-buffered shared row, one barrier
-// per elimination step (lu.hpp:47-56 order, IEEE division for multipliers)
-template <int W>
-__global__ void __launch_bounds__(W)
-panel_diag_reg_kernel(double* __restrict__ a, int64_t lda, double* __restrict__ piv_out, double* __restrict__ rinv_out) {
-    __shared__ __align__(16) double buf[2][W];
-    const int i = threadIdx.x;
-    double p[W];
-    double2* arow = reinterpret_cast<double2*>(a + i * lda);
-#pragma unroll
-    for (int m = 0; m < W / 2; ++m) {
-        const double2 v = arow[m];
-        p[2 * m] = v.x;
-        p[2 * m + 1] = v.y;
-    }
-    double mypiv = 0.0;
-#pragma unroll
-    for (int j = 0; j < W; ++j) {
-        double* row = buf[j & 1];
-        if (i == j) {
-#pragma unroll
-            for (int m = 0; m < W / 2; ++m)
-                if (2 * m + 1 >= j) *reinterpret_cast<double2*>(&row[2 * m]) = make_double2(p[2 * m], p[2 * m + 1]);
-        }
-        __syncthreads();
-        const double piv = row[j];
-        if (i == j) mypiv = piv;
-        const bool below = i > j;
-        const double l = below ? p[j] / piv : 0.0;
-        if (below) p[j] = l;
-#pragma unroll
-        for (int k = 0; k < W; ++k)
-            if (k > j) p[k] = fma(-l, row[k], p[k]);
-    }
-#pragma unroll
-    for (int m = 0; m < W / 2; ++m) arow[m] = make_double2(p[2 * m], p[2 * m + 1]);
-    piv_out[i] = mypiv;
-    rinv_out[i] = 1.0 / mypiv;
-}
-
 // 1/x: MUFU seed + two Newton steps (no division subroutine on the critical path)
 __device__ __forceinline__ double rcp64(double x) {
     double r;
@@ -109,64 +69,8 @@ __device__ __forceinline__ double div_by(double a, double b, double r) {
     return fma(r, fma(-b, q0, a), q0);
 }
 
-// ---- rows below the diagonal block: L21 = A21 U11^-1 (row-wise) ---------
-// x U11 = a  ->  x_j = (a_j - sum_{i<j} x_i u_ij) / u_jj, one row per thread.
-template <int W>
-__global__ void __launch_bounds__(128)
-panel_rows_kernel(double* __restrict__ rows, int64_t lda, int64_t nrows, const double* __restrict__ u11,
-                  const double* __restrict__ piv, const double* __restrict__ rinv) {
-    __shared__ double su[W][W];
-    __shared__ double sp[W], sr[W];
-    for (int idx = threadIdx.x; idx < W * W; idx += 128) su[idx / W][idx % W] = u11[(idx / W) * lda + idx % W];
-    if (threadIdx.x < W) {
-        sp[threadIdx.x] = piv[threadIdx.x];
-        sr[threadIdx.x] = rinv[threadIdx.x];
-    }
-    __syncthreads();
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
-    if (r >= nrows) return;
-    double2* row = reinterpret_cast<double2*>(rows + r * lda);
-    double x[W];
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-        const double2 v = row[j];
-        x[2 * j] = v.x;
-        x[2 * j + 1] = v.y;
-    }
-    // column sweep: x_j final after its division, then folded into every
-    // later column at once (independent FMAs -> short dependency chains)
-#pragma unroll
-    for (int j = 0; j < W; ++j) {
-        x[j] = div_by(x[j], sp[j], sr[j]);
-#pragma unroll
-        for (int k = j + 1; k < W; ++k) x[k] = fma(-x[j], su[j][k], x[k]);
-    }
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) row[j] = make_double2(x[2 * j], x[2 * j + 1]);
-}
-
-// ---- base TRSM: X = L^-1 B, L unit lower (w x w, w <= 64), column-parallel
-template <int W>
-__global__ void __launch_bounds__(128)
-trsm_lower_unit_kernel(const double* __restrict__ l, int64_t ldl, double* __restrict__ b, int64_t ldb, int64_t ncols) {
-    __shared__ double sl[W][W];
-    for (int idx = threadIdx.x; idx < W * W; idx += 128) sl[idx / W][idx % W] = l[(idx / W) * ldl + idx % W];
-    __syncthreads();
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
-    if (c >= ncols) return;
-    double x[W];
-#pragma unroll
-    for (int i = 0; i < W; ++i) x[i] = b[i * ldb + c];
-    // column sweep (x_k final -> update all later rows): short dependency chains
-#pragma unroll
-    for (int k = 0; k < W - 1; ++k)
-#pragma unroll
-        for (int i = k + 1; i < W; ++i) x[i] = fma(-sl[i][k], x[k], x[i]);
-#pragma unroll
-    for (int i = 0; i < W; ++i) b[i * ldb + c] = x[i];
-}
-
-// generic (w < 64, e.g. the ragged last block) versions: runtime width
+// ragged last block (w < 64): rows below the w x w diagonal block,
+// L21 = A21 U11^-1, x U11 = a -> x_j = (a_j - sum_{i<j} x_i u_ij) / u_jj, one row per thread
 __global__ void __launch_bounds__(128)
 panel_rows_kernel_dyn(double* __restrict__ rows, int64_t lda, int64_t nrows, int w, const double* __restrict__ u11,
                       const double* __restrict__ piv, const double* __restrict__ rinv) {
@@ -177,18 +81,6 @@ panel_rows_kernel_dyn(double* __restrict__ rows, int64_t lda, int64_t nrows, int
         double acc = x[j];
         for (int i = 0; i < j; ++i) acc = fma(-x[i], u11[i * lda + j], acc);
         x[j] = div_by(acc, piv[j], rinv[j]);
-    }
-}
-
-__global__ void __launch_bounds__(128)
-trsm_lower_unit_kernel_dyn(const double* __restrict__ l, int64_t ldl, int w, double* __restrict__ b, int64_t ldb,
-                           int64_t ncols) {
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
-    if (c >= ncols) return;
-    for (int i = 1; i < w; ++i) {
-        double acc = b[i * ldb + c];
-        for (int k = 0; k < i; ++k) acc = fma(-l[i * ldl + k], b[k * ldb + c], acc);
-        b[i * ldb + c] = acc;
     }
 }
 
@@ -517,65 +409,21 @@ struct Ctx {
     double* rinv;
 };
 
-// X = L^-1 B for the unit-lower diagonal block L = a[r0:r0+w, r0:r0+w],
-// B = a[r0:r0+w, c0:c0+ncols]
-rl_status trsm(const Ctx& g, int64_t r0, int64_t w, int64_t c0, int64_t ncols) {
-    if (ncols <= 0 || w <= 1) return RL_OK;
-    double* L = g.a + r0 * g.lda + r0;
-    double* B = g.a + r0 * g.lda + c0;
-    if (w <= kBase) {
-        const unsigned blocks = static_cast<unsigned>((ncols + 127) / 128);
-        if (w == kBase)
-            trsm_lower_unit_kernel<kBase><<<blocks, 128, 0, g.ctx->stream>>>(L, g.lda, B, g.lda, ncols);
-        else
-            trsm_lower_unit_kernel_dyn<<<blocks, 128, 0, g.ctx->stream>>>(L, g.lda, static_cast<int>(w), B, g.lda, ncols);
-        RL_CHECK_LAUNCH("trsm_lower_unit_kernel");
-        return RL_OK;
-    }
-    const int64_t w1 = std::max<int64_t>(kBase, (w / 2) / kBase * kBase);
-    rl_status st = trsm(g, r0, w1, c0, ncols);
-    if (st != RL_OK) return st;
-    // B2 -= L21 B1
-    st = gemm(g.ctx, w - w1, ncols, w1, g.a + (r0 + w1) * g.lda + r0, g.lda, g.a + r0 * g.lda + c0, g.lda,
-              g.a + (r0 + w1) * g.lda + c0, g.lda, -1.0, true, nullptr);
-    if (st != RL_OK) return st;
-    return trsm(g, r0 + w1, w - w1, c0, ncols);
-}
-
+// the ragged last block (w < 64 columns): diagonal block in one CTA, then L21
 rl_status panel(const Ctx& g, int64_t c0, int64_t w) {
     const int64_t m = g.n - c0;
     double* d = g.a + c0 * g.lda + c0;
-    if (w == kBase)
-        panel_diag_reg_kernel<kBase><<<1, kBase, 0, g.ctx->stream>>>(d, g.lda, g.piv + c0, g.rinv + c0);
-    else
-        panel_diag_kernel<<<1, 256, 0, g.ctx->stream>>>(d, g.lda, static_cast<int>(w), g.piv + c0, g.rinv + c0);
+    panel_diag_kernel<<<1, 256, 0, g.ctx->stream>>>(d, g.lda, static_cast<int>(w), g.piv + c0, g.rinv + c0);
     RL_CHECK_LAUNCH("panel_diag_kernel");
     const int64_t rows = m - w;
     if (rows > 0) {
         const unsigned blocks = static_cast<unsigned>((rows + 127) / 128);
         double* r = g.a + (c0 + w) * g.lda + c0;
-        if (w == kBase)
-            panel_rows_kernel<kBase><<<blocks, 128, 0, g.ctx->stream>>>(r, g.lda, rows, d, g.piv + c0, g.rinv + c0);
-        else
-            panel_rows_kernel_dyn<<<blocks, 128, 0, g.ctx->stream>>>(r, g.lda, rows, static_cast<int>(w), d,
-                                                                     g.piv + c0, g.rinv + c0);
-        RL_CHECK_LAUNCH("panel_rows_kernel");
+        panel_rows_kernel_dyn<<<blocks, 128, 0, g.ctx->stream>>>(r, g.lda, rows, static_cast<int>(w), d, g.piv + c0,
+                                                                 g.rinv + c0);
+        RL_CHECK_LAUNCH("panel_rows_kernel_dyn");
     }
     return RL_OK;
-}
-
-rl_status rec(const Ctx& g, int64_t c0, int64_t w) {
-    if (w <= kBase) return panel(g, c0, w);
-    const int64_t w1 = std::max<int64_t>(kBase, (w / 2) / kBase * kBase);
-    rl_status st = rec(g, c0, w1);
-    if (st != RL_OK) return st;
-    st = trsm(g, c0, w1, c0 + w1, w - w1);
-    if (st != RL_OK) return st;
-    // A22 -= L21 U12   (rows c0+w1 .. n, cols c0+w1 .. c0+w)
-    st = gemm(g.ctx, g.n - c0 - w1, w - w1, w1, g.a + (c0 + w1) * g.lda + c0, g.lda, g.a + c0 * g.lda + c0 + w1,
-              g.lda, g.a + (c0 + w1) * g.lda + c0 + w1, g.lda, -1.0, true, nullptr);
-    if (st != RL_OK) return st;
-    return rec(g, c0 + w1, w - w1);
 }
 
 }  // namespace

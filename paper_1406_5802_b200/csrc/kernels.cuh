@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "runtime.cuh"
 
 namespace rl {
@@ -87,6 +89,44 @@ struct GaussJob {
 };
 rl_status gen_gaussian_device(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld,
                               int64_t* hard_cases);
+
+// ---- multiplier specs (multipliers.cu) ------------------------------------
+// How a real-pipeline spec acts: not at all (identity), as a dense matrix (the
+// DMMA GEMM), or as a circulant kept structured (the FFT kernel).
+enum class MForm { NONE, DENSE, CIRC };
+// SideMultiplier::make (preprocess.hpp:27-60) for an n x n side multiplier:
+// RL_ERR_DIMENSION for the complex families (the reference's real pipeline
+// throws DimensionError there), RL_ERR_INVALID_ARGUMENT for unknown kinds.
+rl_status side_form(const rl_multiplier* m, MForm* out);
+// range_find's sketch (lowrank.hpp:62-81) with an n x l multiplier: Toeplitz
+// blocks (and the Gaussian-circulant extension) structured, the rest dense
+// (materialize: None and RealCirculant need l == n).
+rl_status sketch_form(const rl_multiplier* m, int64_t n, int64_t l, MForm* out);
+// first column (host, length n) of a structured spec: the explicit column
+// (host or device memory per `host`), gen_gaussian_vector(n, seed) for the
+// Gaussian-circulant extension, else gen_real_circulant(n, seed)
+// (multipliers.hpp:67-73, :84-86).
+rl_status multiplier_column(const rl_multiplier* m, int64_t n, bool host, std::vector<double>& col);
+// materialize(spec) with spec.rows = rows, spec.cols = cols
+// (multipliers.hpp:174-218) into device memory (ld); an explicit `dense`
+// buffer is copied (host or device per `host`). Enqueued on ctx->stream
+// (the seeded Gaussian synchronises it).
+rl_status materialize_device(rl_context* ctx, const rl_multiplier* m, int64_t rows, int64_t cols, bool host,
+                             double* out, int64_t ld);
+// out (cols x rows, ldo) = in^T (rows x cols, ldi), device
+rl_status transpose_device(rl_context* ctx, const double* in, int64_t ldi, int64_t rows, int64_t cols, double* out,
+                           int64_t ldo);
+
+// stream-ordered device scratch freed at scope exit
+struct StreamBuf {
+    double* p = nullptr;
+    cudaStream_t s;
+    explicit StreamBuf(cudaStream_t st) : s(st) {}
+    rl_status alloc(size_t bytes);
+    ~StreamBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
 
 // batched 32x32 kernel (batched32.cu)
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,

@@ -651,7 +651,6 @@ rl_status residual_power_iteration(rl_context* ctx, int64_t m, int64_t n, int64_
                 cudaGetLastError();
                 active = ctx->num_sms / kPC / 2;
             }
-            if (std::getenv("RL_DEBUG_POWER")) std::fprintf(stderr, "power_pass: %d active clusters\n", active);
         }
         clusters = static_cast<int>(std::min<int64_t>(std::max(1, active), (m + kPR - 1) / kPR));
         if ((st = fbuf.alloc(sizeof(double) * (static_cast<size_t>(clusters) * (n + l + 1) + 8))) != RL_OK) return st;
@@ -761,106 +760,202 @@ extern "C" RL_API rl_status rl_cholqr2(rl_context* ctx, rl_mem mem, int64_t m, i
     return RL_OK;
 }
 
-extern "C" RL_API rl_status rl_range_find_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
-                                                   int64_t l, const rl_multiplier* h, double* q_out,
-                                                   rl_lowrank_info* info) {
-    rl_lowrank_info local;
-    if (!info) info = &local;
-    std::memset(info, 0, sizeof(*info));
-    if (m <= 0 || n <= 0 || l < 1 || l > std::min(m, n))
-        return set_error(RL_ERR_DIMENSION, "range_find: rank plus oversampling exceeds matrix size");
-    if (!a || !h) return set_error(RL_ERR_INVALID_ARGUMENT, "range_find: null pointer");
-    if (h->kind != RL_MULT_GAUSSIAN && h->kind != RL_MULT_GAUSSIAN_CIRCULANT && h->kind != RL_MULT_REAL_CIRCULANT)
-        return set_error(RL_ERR_UNSUPPORTED, "range_find: multiplier must be Gaussian or a real Toeplitz block");
-    rl_status st;
-    ctx = resolve(ctx, &st);
-    if (!ctx) return st;
-    cudaStream_t s = ctx->stream;
-    const bool host = mem == RL_HOST;
-    const int64_t lda = (n + 1) & ~int64_t(1), ldq = (l + 1) & ~int64_t(1);
-    Buf ba(s), by(s), bq(s), bb(s), bqt(s), bh(s), bw(s), bsc(s);
-    const double* A = a;
-    if (host || (n & 1) || (reinterpret_cast<uintptr_t>(a) & 15)) {
-        if ((st = ba.alloc(sizeof(double) * m * lda)) != RL_OK) return st;
-        RL_CUDA(cudaMemcpy2DAsync(ba.p, lda * 8, a, n * 8, n * 8, m,
-                                  host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-        A = ba.p;
-    }
-    const int64_t ldA = A == a ? n : lda;
-    if ((st = by.alloc(sizeof(double) * m * ldq)) != RL_OK) return st;
-    if ((st = bq.alloc(sizeof(double) * m * ldq)) != RL_OK) return st;
-    if ((st = bb.alloc(sizeof(double) * l * lda)) != RL_OK) return st;
-    if ((st = bqt.alloc(sizeof(double) * l * ((m + 1) & ~int64_t(1)))) != RL_OK) return st;
-    if ((st = bsc.alloc(sizeof(double) * 8)) != RL_OK) return st;
-    if (ldq != l) RL_CUDA(cudaMemsetAsync(by.p, 0, sizeof(double) * m * ldq, s));
+namespace rl {
+namespace {
 
-    // ---- sketch Y = A H (lowrank.hpp:66-81)
-    if (h->kind == RL_MULT_GAUSSIAN) {
-        if ((st = bh.alloc(sizeof(double) * n * ldq)) != RL_OK) return st;
-        if (h->dense) {
-            RL_CUDA(cudaMemcpy2DAsync(bh.p, ldq * 8, h->dense, l * 8, l * 8, n,
-                                      host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-        } else if ((st = gen_gaussian_device(ctx, n, l, h->seed, bh.p, ldq, nullptr)) != RL_OK) {
-            // materialize: gen_gaussian(n, l, seed) (multipliers.hpp:191-192), exact, on the device
-            return st;
-        }
+// sketch Y = A H (lowrank.hpp:62-81), power_steps alternating products
+// Y <- A (A^T Y) (lowrank.hpp:51-57), Q = orthonormal_basis(Y) (qr.hpp:51-54)
+// into Q (m x l, ldq, device)
+rl_status range_find_core(rl_context* ctx, bool host, int64_t m, int64_t n, const double* A, int64_t ldA, int64_t l,
+                          const rl_multiplier* h, int64_t power_steps, double* Q, int64_t ldq, rl_lowrank_info* info) {
+    cudaStream_t s = ctx->stream;
+    rl_status st;
+    MForm form;
+    if ((st = sketch_form(h, n, l, &form)) != RL_OK) return st;
+    Buf by(s), bh(s), bw(s);
+    if ((st = by.alloc(sizeof(double) * m * ldq)) != RL_OK) return st;
+    if (ldq != l) RL_CUDA(cudaMemsetAsync(by.p, 0, sizeof(double) * m * ldq, s));
+    auto times_a = [&](const double* H, double* Y) -> rl_status {  // Y (m x l) = A H (H: n x l, ldq)
         const int64_t tiles = ((m + 127) / 128) * ((l + 127) / 128);
         const int splits = splits_for(tiles, (n + 15) / 16, ctx->num_sms);
-        if ((st = bw.alloc(gemm_splitk_work_bytes(m, l, splits))) != RL_OK) return st;
-        if ((st = gemm_splitk(ctx, m, l, n, A, ldA, bh.p, ldq, by.p, ldq, 1.0, false, splits, bw.p)) != RL_OK) return st;
-    } else {
-        // Toeplitz block of the parent circulant, parent length n (lowrank.hpp:71-73)
-        std::vector<double> col(static_cast<size_t>(n));
-        if (h->column) {
-            if (host)
-                std::memcpy(col.data(), h->column, n * 8);
-            else
-                RL_CUDA(cudaMemcpy(col.data(), h->column, n * 8, cudaMemcpyDeviceToHost));
-        } else if (h->kind == RL_MULT_GAUSSIAN_CIRCULANT) {
-            rl_gen_gaussian(n, 1, h->seed, col.data());
-        } else {
-            rl_gen_real_circulant_column(n, h->seed, col.data());
-        }
+        Buf w(s);
+        rl_status e = w.alloc(gemm_splitk_work_bytes(m, l, splits));
+        if (e != RL_OK) return e;
+        return gemm_splitk(ctx, m, l, n, A, ldA, H, ldq, Y, ldq, 1.0, false, splits, w.p);
+    };
+    if (form == MForm::CIRC && circulant_fft_ok(n)) {
+        // Toeplitz block of the parent n-point circulant (lowrank.hpp:71-73)
+        std::vector<double> col;
+        if ((st = multiplier_column(h, n, host, col)) != RL_OK) return st;
         if ((st = bh.alloc(sizeof(double) * n + 16 * n + 256)) != RL_OK) return st;
         RL_CUDA(cudaMemcpyAsync(bh.p, col.data(), n * 8, cudaMemcpyHostToDevice, s));
         RL_CUDA(cudaStreamSynchronize(s));
         if ((st = circulant_rows(ctx, m, n, A, ldA, n, bh.p, l, by.p, ldq, bh.p + n)) != RL_OK) return st;
+    } else {
+        // sketch = matmul(a, materialize<T>(spec)) (lowrank.hpp:80): gen_gaussian(n, l, seed) exact on the
+        // device, or the family's dense expansion
+        if ((st = bh.alloc(sizeof(double) * n * ldq)) != RL_OK) return st;
+        if (ldq != l) RL_CUDA(cudaMemsetAsync(bh.p, 0, sizeof(double) * n * ldq, s));
+        if ((st = materialize_device(ctx, h, n, l, host, bh.p, ldq)) != RL_OK) return st;
+        if ((st = times_a(bh.p, by.p)) != RL_OK) return st;
     }
-
-    // ---- Q = orthonormal_basis(Y) (qr.hpp:51-54)
-    st = cholqr2_device(ctx, m, l, by.p, bq.p, ldq, nullptr, 0, &info->rank_deficient_column);
-    if (st != RL_OK) {
-        cudaStreamSynchronize(s);
-        return st;
+    if (power_steps > 0) {
+        // sketch = matmul(a, matmul(a.adjoint(), sketch)), no re-orthonormalisation (lowrank.hpp:51-57):
+        // Z^T = Y^T A by the split-K GEMM over the m rows, Z = (Z^T)^T, Y = A Z
+        const int64_t ldm = (m + 1) & ~int64_t(1), ldn = (n + 1) & ~int64_t(1);
+        Buf byt(s), bzt(s), bz(s);
+        if ((st = byt.alloc(sizeof(double) * l * ldm)) != RL_OK) return st;
+        if ((st = bzt.alloc(sizeof(double) * l * ldn)) != RL_OK) return st;
+        if ((st = bz.alloc(sizeof(double) * n * ldq)) != RL_OK) return st;
+        if (ldq != l) RL_CUDA(cudaMemsetAsync(bz.p, 0, sizeof(double) * n * ldq, s));
+        const int64_t tiles = ((l + 127) / 128) * ((n + 127) / 128);
+        const int splits = splits_for(tiles, (m + 15) / 16, ctx->num_sms);
+        if ((st = bw.alloc(gemm_splitk_work_bytes(l, n, splits))) != RL_OK) return st;
+        for (int64_t step = 0; step < power_steps; ++step) {
+            if ((st = transpose_device(ctx, by.p, ldq, m, l, byt.p, ldm)) != RL_OK) return st;
+            if ((st = gemm_splitk(ctx, l, n, m, byt.p, ldm, A, ldA, bzt.p, ldn, 1.0, false, splits, bw.p)) != RL_OK)
+                return st;
+            if ((st = transpose_device(ctx, bzt.p, ldn, l, n, bz.p, ldq)) != RL_OK) return st;
+            if ((st = times_a(bz.p, by.p)) != RL_OK) return st;
+        }
     }
+    st = cholqr2_device(ctx, m, l, by.p, Q, ldq, nullptr, 0, &info->rank_deficient_column);
+    if (st != RL_OK) cudaStreamSynchronize(s);
+    return st;
+}
 
-    // ---- B = Q^T A (split-K over the m rows), residual statistics
-    const int64_t ldm = (m + 1) & ~int64_t(1);
-    transpose_kernel<<<dim3(nblk(l, 32), nblk(m, 32)), dim3(32, 8), 0, s>>>(bq.p, ldq, m, l, bqt.p, ldm);
+// residual R = A - Q (Q^T A) (lowrank.hpp:35-37, :99-102): ||R||_F from a GEMM
+// epilogue that never stores R, ||R||_2 by the power iteration on the
+// implicit operator
+rl_status residual_core(rl_context* ctx, int64_t m, int64_t n, const double* A, int64_t ldA, int64_t l,
+                        const double* Q, int64_t ldq, rl_lowrank_info* info) {
+    cudaStream_t s = ctx->stream;
+    rl_status st;
+    const int64_t lda = (n + 1) & ~int64_t(1), ldm = (m + 1) & ~int64_t(1);
+    Buf bb(s), bqt(s), bsc(s), bw2(s);
+    if ((st = bb.alloc(sizeof(double) * l * lda)) != RL_OK) return st;
+    if ((st = bqt.alloc(sizeof(double) * l * ldm)) != RL_OK) return st;
+    if ((st = bsc.alloc(sizeof(double) * 8)) != RL_OK) return st;
+    // B = Q^T A (split-K over the m rows)
+    transpose_kernel<<<dim3(nblk(l, 32), nblk(m, 32)), dim3(32, 8), 0, s>>>(Q, ldq, m, l, bqt.p, ldm);
     RL_CHECK_LAUNCH("transpose_kernel");
     {
         const int64_t tiles = ((l + 127) / 128) * ((n + 127) / 128);
         const int splits = splits_for(tiles, (m + 15) / 16, ctx->num_sms);
-        Buf bw2(s);
         if ((st = bw2.alloc(gemm_splitk_work_bytes(l, n, splits))) != RL_OK) return st;
         if ((st = gemm_splitk(ctx, l, n, m, bqt.p, ldm, A, ldA, bb.p, lda, 1.0, false, splits, bw2.p)) != RL_OK)
             return st;
     }
     GemmStats* gs = reinterpret_cast<GemmStats*>(bsc.p);
     RL_CUDA(cudaMemsetAsync(gs, 0, sizeof(GemmStats), s));
-    if ((st = gemm_residual_stats(ctx, m, n, l, bq.p, ldq, bb.p, lda, A, ldA, gs)) != RL_OK) return st;
+    if ((st = gemm_residual_stats(ctx, m, n, l, Q, ldq, bb.p, lda, A, ldA, gs)) != RL_OK) return st;
     GemmStats hs;
     RL_CUDA(cudaMemcpyAsync(&hs, gs, sizeof(hs), cudaMemcpyDeviceToHost, s));
     RL_CUDA(cudaStreamSynchronize(s));
     info->residual_frobenius = std::sqrt(hs.sumsq);
     int its = 0;
-    if ((st = residual_power_iteration(ctx, m, n, l, A, ldA, bq.p, ldq, bb.p, lda, &info->residual_spectral, &its)) !=
+    if ((st = residual_power_iteration(ctx, m, n, l, A, ldA, Q, ldq, bb.p, lda, &info->residual_spectral, &its)) !=
         RL_OK)
         return st;
     info->power_iterations = its;
+    return RL_OK;
+}
+
+// A resident on the device with an even leading dimension (TMA), staged when
+// it is host memory or not aligned
+struct ResidentA {
+    Buf buf;
+    const double* p = nullptr;
+    int64_t ld = 0;
+    explicit ResidentA(cudaStream_t s) : buf(s) {}
+    rl_status stage(bool host, int64_t m, int64_t n, const double* a, cudaStream_t s) {
+        p = a;
+        ld = n;
+        if (host || (n & 1) || (reinterpret_cast<uintptr_t>(a) & 15)) {
+            const int64_t lda = (n + 1) & ~int64_t(1);
+            rl_status st = buf.alloc(sizeof(double) * m * lda);
+            if (st != RL_OK) return st;
+            RL_CUDA(cudaMemcpy2DAsync(buf.p, lda * 8, a, n * 8, n * 8, m,
+                                      host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+            p = buf.p;
+            ld = lda;
+        }
+        return RL_OK;
+    }
+};
+
+rl_status lowrank_args(int64_t m, int64_t n, int64_t l, const double* a) {
+    if (m <= 0 || n <= 0 || l < 1 || l > std::min(m, n))
+        return set_error(RL_ERR_DIMENSION, "range_find: rank plus oversampling exceeds matrix size");
+    if (!a) return set_error(RL_ERR_INVALID_ARGUMENT, "range_find: null pointer");
+    return RL_OK;
+}
+
+rl_status range_find_entry(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a, int64_t l,
+                           const rl_multiplier* h, int64_t power_steps, double* q_out, rl_lowrank_info* info,
+                           bool residual) {
+    rl_lowrank_info local;
+    if (!info) info = &local;
+    std::memset(info, 0, sizeof(*info));
+    rl_status st = lowrank_args(m, n, l, a);
+    if (st != RL_OK) return st;
+    if (!h) return set_error(RL_ERR_INVALID_ARGUMENT, "range_find: null multiplier spec");
+    if (power_steps < 0) return set_error(RL_ERR_INVALID_ARGUMENT, "range_find: negative power_steps");
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    const int64_t ldq = (l + 1) & ~int64_t(1);
+    ResidentA ra(s);
+    if ((st = ra.stage(host, m, n, a, s)) != RL_OK) return st;
+    Buf bq(s);
+    if ((st = bq.alloc(sizeof(double) * m * ldq)) != RL_OK) return st;
+    if ((st = range_find_core(ctx, host, m, n, ra.p, ra.ld, l, h, power_steps, bq.p, ldq, info)) != RL_OK) return st;
+    if (residual && (st = residual_core(ctx, m, n, ra.p, ra.ld, l, bq.p, ldq, info)) != RL_OK) return st;
     if (q_out)
         RL_CUDA(cudaMemcpy2DAsync(q_out, l * 8, bq.p, ldq * 8, l * 8, m,
                                   host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
     RL_CUDA(cudaStreamSynchronize(s));
     return RL_OK;
+}
+
+}  // namespace
+}  // namespace rl
+
+extern "C" RL_API rl_status rl_range_find(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                          int64_t l, const rl_multiplier* h, int64_t power_steps, double* q,
+                                          rl_lowrank_info* info) {
+    if (!q) return set_error(RL_ERR_INVALID_ARGUMENT, "range_find: null q");
+    return range_find_entry(ctx, mem, m, n, a, l, h, power_steps, q, info, false);
+}
+
+extern "C" RL_API rl_status rl_range_find_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                                   int64_t l, const rl_multiplier* h, int64_t power_steps,
+                                                   double* q_out, rl_lowrank_info* info) {
+    return range_find_entry(ctx, mem, m, n, a, l, h, power_steps, q_out, info, true);
+}
+
+extern "C" RL_API rl_status rl_approximation_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n,
+                                                      const double* a, int64_t l, const double* q,
+                                                      rl_lowrank_info* info) {
+    rl_lowrank_info local;
+    if (!info) info = &local;
+    std::memset(info, 0, sizeof(*info));
+    rl_status st = lowrank_args(m, n, l, a);
+    if (st != RL_OK) return st;
+    if (!q) return set_error(RL_ERR_INVALID_ARGUMENT, "approximation_residual: null q");
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    ResidentA ra(s);
+    if ((st = ra.stage(host, m, n, a, s)) != RL_OK) return st;
+    const int64_t ldq = (l + 1) & ~int64_t(1);
+    Buf bq(s);
+    if ((st = bq.alloc(sizeof(double) * m * ldq)) != RL_OK) return st;
+    RL_CUDA(cudaMemcpy2DAsync(bq.p, ldq * 8, q, l * 8, l * 8, m,
+                              host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    st = residual_core(ctx, m, n, ra.p, ra.ld, l, bq.p, ldq, info);
+    RL_CUDA(cudaStreamSynchronize(s));
+    return st;
 }

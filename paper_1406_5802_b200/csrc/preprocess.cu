@@ -136,6 +136,14 @@ struct Dense {
     double* c = nullptr;   // circulant first column (device)
     double* ct = nullptr;  // transposed circulant's first column c[(n-i) mod n]
     void* spec = nullptr;  // FFT spectrum workspace (16 n bytes)
+    // left multiplier F of F (A H) (preprocess.hpp:164): dense n x n, or a
+    // circulant kept structured (its transpose's first column fct, spectrum
+    // workspace fspec); fr = F r for the chain solver
+    PostKind pre = POST_NONE;
+    double* F = nullptr;
+    double* fct = nullptr;
+    void* fspec = nullptr;
+    double* fr = nullptr;
     double *A = nullptr, *G = nullptr, *P = nullptr;
     double *b = nullptr, *x = nullptr, *r = nullptr, *y = nullptr, *d = nullptr, *piv = nullptr, *rinv = nullptr;
     void* solve_work = nullptr;
@@ -152,6 +160,22 @@ struct Dense {
 // exact-verdict path recomputes it bit for bit)
 rl_status form_product(rl_context* ctx, Dense& D, double* P, GemmStats* stats) {
     const int64_t n = D.n;
+    cudaStream_t s = ctx->stream;
+    // with a left multiplier, A H lands in scratch T (or is A itself) and
+    // F T is written to P; the verdict statistics belong to the final product
+    StreamBuf tbuf(s);
+    double* T = P;
+    const bool left = D.pre != POST_NONE;
+    if (left) {
+        if (D.post == POST_NONE) {
+            T = D.A;
+        } else {
+            rl_status st = tbuf.alloc(sizeof(double) * n * D.ld);
+            if (st != RL_OK) return st;
+            T = tbuf.p;
+        }
+    }
+    GemmStats* ah_stats = left ? nullptr : stats;
     // row blocks of A (all of A when it is already resident); every block's
     // product rows are computed exactly as in one call (per-tile K order)
     const int chunks = D.a_chunks > 0 ? D.a_chunks : 1;
@@ -159,23 +183,40 @@ rl_status form_product(rl_context* ctx, Dense& D, double* P, GemmStats* stats) {
     for (int c = 0; c < chunks; ++c) {
         const int64_t r0 = c * rows, rc = std::min(rows, n - r0);
         if (rc <= 0) break;
-        if (D.a_chunks > 0) RL_CUDA(cudaStreamWaitEvent(ctx->stream, D.a_ready[c], 0));
+        if (D.a_chunks > 0) RL_CUDA(cudaStreamWaitEvent(s, D.a_ready[c], 0));
         const double* Ac = D.A + r0 * D.ld;
-        double* Pc = P + r0 * D.ld;
+        double* Tc = T + r0 * D.ld;
         rl_status st = RL_OK;
         if (D.post == POST_DENSE) {
-            st = gemm(ctx, rc, n, n, Ac, D.ld, D.G, D.ld, Pc, D.ld, 1.0, false, stats);
+            st = gemm(ctx, rc, n, n, Ac, D.ld, D.G, D.ld, Tc, D.ld, 1.0, false, ah_stats);
         } else if (D.post == POST_CIRC) {
             // matmul_by_circulant (circulant.hpp:171-185), SideMultiplier::right_multiply (preprocess.hpp:65-73)
-            st = circulant_rows(ctx, rc, n, Ac, D.ld, n, D.c, n, Pc, D.ld, D.spec);
-        } else if (Pc != Ac) {
-            RL_CUDA(cudaMemcpy2DAsync(Pc, D.ld * 8, Ac, D.ld * 8, n * 8, rc, cudaMemcpyDeviceToDevice, ctx->stream));
+            st = circulant_rows(ctx, rc, n, Ac, D.ld, n, D.c, n, Tc, D.ld, D.spec);
+        } else if (Tc != Ac) {
+            RL_CUDA(cudaMemcpy2DAsync(Tc, D.ld * 8, Ac, D.ld * 8, n * 8, rc, cudaMemcpyDeviceToDevice, s));
         }
         if (st != RL_OK) return st;
     }
     D.a_chunks = 0;  // resident from here on (the exact-verdict recompute reuses A)
-    if (stats && D.post != POST_DENSE) {
-        matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, ctx->stream>>>(P, D.ld, n, false, stats);
+    bool stats_done = !left && D.post == POST_DENSE;
+    if (D.pre == POST_DENSE) {
+        // F (A H) (SideMultiplier::left_multiply, preprocess.hpp:76-86)
+        rl_status st = gemm(ctx, n, n, n, D.F, D.ld, T, D.ld, P, D.ld, 1.0, false, stats);
+        if (st != RL_OK) return st;
+        stats_done = true;
+    } else if (D.pre == POST_CIRC) {
+        // column j of F T is circulant_apply(F, T e_j) (preprocess.hpp:80-84):
+        // F T = (T^T F^T)^T, the rows of T^T through the FFT kernel
+        StreamBuf ub(s);
+        rl_status st = ub.alloc(sizeof(double) * n * D.ld);
+        if (st != RL_OK) return st;
+        if ((st = transpose_device(ctx, T, D.ld, n, n, ub.p, D.ld)) != RL_OK) return st;
+        if ((st = circulant_rows(ctx, n, n, ub.p, D.ld, n, D.fct, n, P, D.ld, D.fspec)) != RL_OK) return st;
+        if ((st = transpose_device(ctx, P, D.ld, n, n, ub.p, D.ld)) != RL_OK) return st;
+        RL_CUDA(cudaMemcpyAsync(P, ub.p, sizeof(double) * n * D.ld, cudaMemcpyDeviceToDevice, s));
+    }
+    if (stats && !stats_done) {
+        matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(P, D.ld, n, false, stats);
         RL_CHECK_LAUNCH("matrix_stats_kernel");
     }
     return RL_OK;
@@ -255,7 +296,16 @@ rl_status chain_solve(rl_context* ctx, Dense& D, int64_t refine, rl_solve_info* 
     info->diverged = 0;
     const int64_t steps = refine + 1;
     for (int64_t k = 0; k < steps; ++k) {
-        st = lu_solve_device(ctx, n, D.P, D.ld, D.rinv, D.r, D.y, D.solve_work);
+        // chain solver H (LU)^-1 (F r) (preprocess.hpp:167-169)
+        const double* rhs = D.r;
+        if (D.pre == POST_DENSE) {
+            if ((st = gemv(ctx, n, n, D.F, D.ld, D.r, D.fr, nullptr)) != RL_OK) return st;
+            rhs = D.fr;
+        } else if (D.pre == POST_CIRC) {  // F r = (r^T F^T)^T
+            if ((st = circulant_rows(ctx, 1, n, D.r, n, n, D.fct, n, D.fr, n, D.fspec)) != RL_OK) return st;
+            rhs = D.fr;
+        }
+        st = lu_solve_device(ctx, n, D.P, D.ld, D.rinv, rhs, D.y, D.solve_work);
         if (st != RL_OK) return st;
         if (D.post == POST_DENSE) {  // H y = matvec (preprocess.hpp:88-94)
             st = gemv(ctx, n, n, D.G, D.ld, D.y, D.d, nullptr);
@@ -284,6 +334,7 @@ rl_status chain_solve(rl_context* ctx, Dense& D, int64_t refine, rl_solve_info* 
         const double rel = std::sqrt(rsq) / std::sqrt(bsq);
         streak = rel > last ? streak + 1 : 0;
         if (info->history_len < 8) info->residual_history[info->history_len] = rel;
+        if (info->history && info->history_len < info->history_capacity) info->history[info->history_len] = rel;
         ++info->history_len;
         last = rel;
         if (streak >= 2) {
@@ -291,7 +342,6 @@ rl_status chain_solve(rl_context* ctx, Dense& D, int64_t refine, rl_solve_info* 
             break;
         }
     }
-    if (info->history_len > 8) info->history_len = 8;
     return RL_OK;
 }
 
@@ -307,6 +357,7 @@ rl_status dense_alloc(rl_context* ctx, Dense& D, int64_t n, bool need_g, bool ow
         D.r = ar.take<double>(n);
         D.y = ar.take<double>(n);
         D.d = ar.take<double>(n);
+        D.fr = ar.take<double>(n);
         D.solve_work = ar.take<char>(lu_solve_work_bytes(n));
         if (own_a) D.A = ar.take<double>(n * D.ld);
         if (need_g) D.G = ar.take<double>(n * D.ld);
@@ -331,7 +382,14 @@ bool aligned_even(const double* p, int64_t ld) {
     return (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 
-void clear_info(rl_solve_info* info) { std::memset(info, 0, sizeof(*info)); }
+// zero the outputs; the caller's history buffer (an input) survives
+void clear_info(rl_solve_info* info) {
+    double* h = info->history;
+    const int64_t cap = info->history_capacity;
+    std::memset(info, 0, sizeof(*info));
+    info->history = h;
+    info->history_capacity = cap;
+}
 
 }  // namespace
 }  // namespace rl
@@ -339,37 +397,74 @@ void clear_info(rl_solve_info* info) { std::memset(info, 0, sizeof(*info)); }
 using namespace rl;
 
 extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* a,
-                                                       const double* b, const rl_multiplier* post, int64_t refine_steps,
-                                                       double* x, double* lu_out, int32_t want_norm_a,
-                                                       rl_solve_info* info) {
+                                                       const double* b, const rl_multiplier* pre,
+                                                       const rl_multiplier* post, int64_t refine_steps, double* x,
+                                                       double* lu_out, int32_t want_norm_a, rl_solve_info* info) {
     rl_solve_info local;
     if (!info) info = &local;
     clear_info(info);
     if (n <= 0) return set_error(RL_ERR_DIMENSION, "preprocess_solve: matrix dimensions must be positive");
     if (!a || !b || !x) return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: a, b, x are required");
     if (refine_steps < 0) return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: negative refine_steps");
-    const int kind = post ? post->kind : RL_MULT_NONE;
-    if (kind < RL_MULT_NONE || kind > RL_MULT_GAUSSIAN_CIRCULANT)
-        return set_error(RL_ERR_INVALID_ARGUMENT, "preprocess_solve: unknown multiplier kind %d", kind);
+    // SolveOutcome::residual_history has refine_steps + 1 entries (preprocess.hpp:124-140): beyond the 8
+    // inline slots the caller must supply the buffer, never a silently truncated history
+    if (refine_steps + 1 > 8 && (!info->history || info->history_capacity < refine_steps + 1))
+        return set_error(RL_ERR_INVALID_ARGUMENT,
+                         "preprocess_solve: refine_steps = %lld needs rl_solve_info.history with %lld entries",
+                         static_cast<long long>(refine_steps), static_cast<long long>(refine_steps + 1));
+    // SideMultiplier::make for both sides (preprocess.hpp:27-60, :162-163)
     rl_status st;
+    MForm post_form, pre_form;
+    if ((st = side_form(post, &post_form)) != RL_OK) return st;
+    if ((st = side_form(pre, &pre_form)) != RL_OK) return st;
+    const int kind = post ? post->kind : RL_MULT_NONE;
     ctx = resolve(ctx, &st);
     if (!ctx) return st;
     const bool host = mem == RL_HOST;
-    const bool circ = kind == RL_MULT_REAL_CIRCULANT || kind == RL_MULT_GAUSSIAN_CIRCULANT;
+    const bool circ = post_form == MForm::CIRC;
     // SideMultiplier::make (preprocess.hpp:27-60): circulants stay structured
     // (FFT products) when the FFT kernel covers n; otherwise their dense
     // expansion goes through the GEMM path
     const bool circ_fft = circ && circulant_fft_ok(n);
-    const bool dense = kind == RL_MULT_GAUSSIAN || (circ && !circ_fft);
+    const bool dense = post_form == MForm::DENSE || (circ && !circ_fft);
     const int64_t ld = (n + 1) & ~int64_t(1);
     // device A can be used in place when it is TMA-compatible (even n, aligned)
     const bool own_a = host || !((n & 1) == 0 && aligned_even(a, n));
-    const bool g_dev_direct = kind == RL_MULT_GAUSSIAN && !host && post->dense && (n & 1) == 0 && aligned_even(post->dense, n);
+    const bool g_dev_direct = post_form == MForm::DENSE && !host && post->dense && (n & 1) == 0 &&
+                              aligned_even(post->dense, n);
     Dense D;
     D.post = dense ? POST_DENSE : (circ ? POST_CIRC : POST_NONE);
     st = dense_alloc(ctx, D, n, dense && !g_dev_direct, own_a, true);
     if (st != RL_OK) return st;
     cudaStream_t s = ctx->stream;
+    // left multiplier F: dense (materialized on the device) or a structured
+    // circulant (the dense expansion when the FFT kernel does not cover n)
+    StreamBuf fbuf(s);
+    if (pre_form != MForm::NONE) {
+        const bool fcirc = pre_form == MForm::CIRC && circulant_fft_ok(n);
+        D.pre = fcirc ? POST_CIRC : POST_DENSE;
+        if ((st = fbuf.alloc(sizeof(double) * (fcirc ? 3 * n + 64 : n * ld))) != RL_OK) return st;
+        if (pre_form == MForm::CIRC) {
+            std::vector<double> col, colt(static_cast<size_t>(n));
+            if ((st = multiplier_column(pre, n, host, col)) != RL_OK) return st;
+            for (int64_t i = 0; i < n; ++i) colt[i] = col[(n - i) % n];  // transposed() (circulant.hpp:40-45)
+            if (fcirc) {
+                D.fct = fbuf.p;
+                D.fspec = fbuf.p + n + 32;
+                RL_CUDA(cudaMemcpyAsync(D.fct, colt.data(), n * 8, cudaMemcpyHostToDevice, s));
+            } else {
+                StreamBuf cb(s);
+                if ((st = cb.alloc(n * 8)) != RL_OK) return st;
+                RL_CUDA(cudaMemcpyAsync(cb.p, col.data(), n * 8, cudaMemcpyHostToDevice, s));
+                D.F = fbuf.p;
+                if ((st = circulant_dense(ctx, cb.p, n, n, n, D.F, ld)) != RL_OK) return st;
+            }
+            RL_CUDA(cudaStreamSynchronize(s));  // col / colt are locals
+        } else {
+            D.F = fbuf.p;
+            if ((st = materialize_device(ctx, pre, n, n, host, D.F, ld)) != RL_OK) return st;
+        }
+    }
     // seeded dense multiplier: generated on the device (exact); its kernels are
     // enqueued first so that they run under the upload of A
     // host A is uploaded in row blocks on the side stream, which waits only for
@@ -377,7 +472,14 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     // kernels enqueued next, so block 0 lands under them
     constexpr int kChunks = 4;
     const bool pipelined_a = own_a && host && n >= 1024 && side_resources(ctx, kChunks) == RL_OK;
+    struct SideDrain {  // error exits: the side stream's uploads read the caller's `a` and write the
+        cudaStream_t s = nullptr;  // workspace, so they must be done before the call returns
+        ~SideDrain() {
+            if (s) cudaStreamSynchronize(s);
+        }
+    } side_drain;
     if (pipelined_a) {
+        side_drain.s = ctx->hi_stream;
         cudaEvent_t start = ctx->events[kChunks - 1];
         RL_CUDA(cudaEventRecord(start, s));
         RL_CUDA(cudaStreamWaitEvent(ctx->hi_stream, start, 0));
@@ -422,17 +524,8 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     } colbuf{nullptr, s};
     if (circ) {
         // first column: explicit, or drawn by the family's generator
-        std::vector<double> col(static_cast<size_t>(n));
-        if (post->column) {
-            if (host)
-                std::memcpy(col.data(), post->column, n * 8);
-            else
-                RL_CUDA(cudaMemcpy(col.data(), post->column, n * 8, cudaMemcpyDeviceToHost));
-        } else if (kind == RL_MULT_GAUSSIAN_CIRCULANT) {
-            rl_gen_gaussian(n, 1, post->seed, col.data());  // gen_gaussian_vector (testbed/inputs.hpp:85-90)
-        } else {
-            rl_gen_real_circulant_column(n, post->seed, col.data());  // multipliers.hpp:67-73
-        }
+        std::vector<double> col;
+        if ((st = multiplier_column(post, n, host, col)) != RL_OK) return st;
         std::vector<double> colt(static_cast<size_t>(n));
         for (int64_t i = 0; i < n; ++i) colt[i] = col[(n - i) % n];  // circulant.hpp:40-45
         RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&colbuf.p), sizeof(double) * 2 * n + 16 * n + 256, s));
@@ -443,14 +536,16 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         RL_CUDA(cudaMemcpyAsync(D.ct, colt.data(), n * 8, cudaMemcpyHostToDevice, s));
         RL_CUDA(cudaStreamSynchronize(s));
         if (dense && (st = circulant_dense(ctx, D.c, n, n, n, D.G, ld)) != RL_OK) return st;
-    } else if (kind == RL_MULT_GAUSSIAN) {
+    } else if (post_form == MForm::DENSE) {
         if (g_dev_direct) {
             D.G = const_cast<double*>(post->dense);
         } else if (post->dense) {
             if ((st = copy_in(ctx, D.G, ld, post->dense, n, n, host)) != RL_OK) return st;
-        } else if ((st = gjob.finish(nullptr)) != RL_OK) {
+        } else if (gen_g) {
             // materialize(spec) = gen_gaussian(n, n, seed) (multipliers.hpp:191-192)
-            return st;
+            if ((st = gjob.finish(nullptr)) != RL_OK) return st;
+        } else if ((st = materialize_device(ctx, post, n, n, host, D.G, ld)) != RL_OK) {
+            return st;  // FiniteSetUniform, CircSkewProduct (multipliers.hpp:195-200)
         }
     }
     // b before the remaining blocks of A (the stream s work must not queue behind them)

@@ -348,10 +348,13 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
     // main stream is still generating), host logs, values up and scattered on
     // the main stream; in pipelined chunks
     cudaStream_t ds = nullptr;
-    struct DsGuard {
-        cudaStream_t* p;
+    struct DsGuard {  // on every exit (errors included) the side stream's copies out of `attempts`
+        cudaStream_t* p;  // finish before ~GaussJob frees it on the main stream
         ~DsGuard() {
-            if (*p) cudaStreamDestroy(*p);
+            if (*p) {
+                cudaStreamSynchronize(*p);
+                cudaStreamDestroy(*p);
+            }
         }
     } ds_guard{&ds};
     auto resolve = [&](int64_t lo, int64_t hi, cudaStream_t down) -> rl_status {

@@ -24,6 +24,8 @@
 #include <mutex>
 #include <condition_variable>
 #include <functional>
+#include <new>
+#include <pthread.h>
 #include <vector>
 
 #include "../../include/randla_capi.h"
@@ -71,14 +73,38 @@ int thread_count() {
 // stay alive between calls (spawning threads per call costs ~0.3 ms, a
 // noticeable share of the device generator's host-decided tail). Every pool
 // thread joins every call; the caller drains too.
+// The pool is per process: a forked child (pthread_atfork handler below)
+// starts a fresh one instead of waiting on the parent's threads, which do not
+// exist in the child; the parent's pool object is abandoned there, never
+// joined. A caller that finds the pool busy with another caller's call runs
+// its own indices itself instead of queueing behind it.
+class Pool;
+std::atomic<Pool*> g_pool{nullptr};
+std::mutex g_pool_mu;
+
 class Pool {
   public:
     static Pool& get() {
-        static Pool p;
-        return p;
+        static const bool registered = [] {
+            pthread_atfork(nullptr, nullptr, [] {
+                new (&g_pool_mu) std::mutex();  // the child has one thread: nothing can hold it
+                g_pool.store(nullptr);
+            });
+            return true;
+        }();
+        (void)registered;
+        Pool* p = g_pool.load();
+        if (p) return *p;
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool.load()) g_pool.store(new Pool());  // never destroyed: workers die with the process
+        return *g_pool.load();
     }
     void run(int helpers, int64_t count, const std::function<void(int64_t)>& fn) {
-        std::lock_guard<std::mutex> call(call_mu_);  // one parallel_for at a time
+        std::unique_lock<std::mutex> call(call_mu_, std::try_to_lock);  // one parallel_for at a time
+        if (!call.owns_lock()) {
+            for (int64_t i = 0; i < count; ++i) fn(i);
+            return;
+        }
         {
             std::lock_guard<std::mutex> lk(mu_);
             while (static_cast<int>(threads_.size()) < helpers) threads_.emplace_back([this] { loop(); });
@@ -93,14 +119,6 @@ class Pool {
         std::unique_lock<std::mutex> lk(mu_);
         done_cv_.wait(lk, [&] { return pending_ == 0; });
         fn_ = nullptr;
-    }
-    ~Pool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-        }
-        cv_.notify_all();
-        for (auto& t : threads_) t.join();
     }
 
   private:
@@ -134,7 +152,7 @@ class Pool {
     std::atomic<int64_t> next_{0};
     int pending_ = 0;
     uint64_t gen_ = 1;
-    bool stop_ = false;
+    bool stop_ = false;  // never set: the pool lives as long as the process
 };
 
 template <typename F>
@@ -272,6 +290,51 @@ RL_API rl_status rl_gen_real_circulant_column(int64_t n, uint64_t seed, double* 
     if (n <= 0 || !out) return RL_ERR_DIMENSION;
     const uint64_t s0 = stream_state(seed);
     for (int64_t i = 0; i < n; ++i) out[i] = symmetric_at(s0, static_cast<uint64_t>(i) + 1);
+    return RL_OK;
+}
+
+// gen_finite_set_uniform (multipliers.hpp:142-154): entry (i, j) is the
+// (i n + j)-th next_below(card) of one stream, minus floor(card / 2).
+// next_below rejects draws >= card * floor((2^64 - 1) / card) (rng.hpp:46-53),
+// so the draw -> entry map is data-dependent; as for the Gaussians, pass 1
+// counts the accepted draws per chunk, a prefix sum places every chunk, and
+// pass 2 fills the chunks independently (bit-identical to the sequence).
+RL_API rl_status rl_gen_finite_set_uniform(int64_t m, int64_t n, uint64_t seed, uint64_t card, double* out) {
+    if (m <= 0 || n <= 0 || !out || card < 2) return RL_ERR_DIMENSION;
+    const uint64_t s0 = stream_state(seed);
+    const uint64_t limit = card * (~uint64_t{0} / card);
+    const int64_t offset = static_cast<int64_t>(card / 2);
+    const int64_t count = m * n;
+    constexpr int64_t kDraws = 1 << 16;
+    auto draw = [&](uint64_t t) { return finalize(s0 + t * kGamma); };  // draw t (1-based) of the stream
+    std::vector<int64_t> accepted;
+    int64_t have = 0;
+    while (have < count) {
+        const int64_t base = static_cast<int64_t>(accepted.size());
+        const int64_t more = (count - have) / kDraws + 2;
+        accepted.resize(base + more);
+        parallel_for(more, [&](int64_t i) {
+            const uint64_t t0 = static_cast<uint64_t>(base + i) * kDraws + 1;
+            int64_t c = 0;
+            for (int64_t j = 0; j < kDraws; ++j) c += draw(t0 + j) < limit ? 1 : 0;
+            accepted[base + i] = c;
+        });
+        have = 0;
+        for (int64_t c : accepted) have += c;
+    }
+    std::vector<int64_t> start(accepted.size() + 1, 0);
+    for (size_t i = 0; i < accepted.size(); ++i) start[i + 1] = start[i] + accepted[i];
+    int64_t chunks = 0;
+    while (start[chunks] < count) ++chunks;
+    parallel_for(chunks, [&](int64_t i) {
+        const uint64_t t0 = static_cast<uint64_t>(i) * kDraws + 1;
+        int64_t k = start[i];
+        for (int64_t j = 0; j < kDraws && k < count; ++j) {
+            const uint64_t v = draw(t0 + j);
+            if (v >= limit) continue;
+            out[k++] = static_cast<double>(static_cast<int64_t>(v % card) - offset);
+        }
+    });
     return RL_OK;
 }
 

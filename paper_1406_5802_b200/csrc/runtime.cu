@@ -1,6 +1,7 @@
 // Context management, errors and launch accounting for the C ABI
 // (include/randla_capi.h).
 #include <cstring>
+#include <unistd.h>
 #include <mutex>
 #include <vector>
 
@@ -69,19 +70,27 @@ static void destroy_context(rl_context* c) {
     delete c;
 }
 
-// Per-thread default contexts come from a process-wide pool: a thread that
-// exits hands its context back (no CUDA calls at thread exit), so callers that
-// spawn fresh worker threads per call (parallel_for_index, parallel.hpp:14-35)
-// reuse streams and workspaces instead of leaking them.
+// Per-thread default contexts, one per (thread, device): a NULL context
+// resolves to the calling thread's context for its CURRENT device
+// (cudaGetDevice), so one process per GPU (torch.cuda.set_device(local_rank))
+// and threads that switch devices both land on the right GPU. They come from a
+// process-wide pool keyed by device: a thread that exits hands its contexts
+// back (no CUDA calls at thread exit), so callers that spawn fresh worker
+// threads per call (parallel_for_index, parallel.hpp:14-35) reuse streams and
+// workspaces instead of leaking them.
+static constexpr int kMaxDevices = 64;
 static std::mutex g_pool_mu;
-static std::vector<rl_context*>* g_pool = new std::vector<rl_context*>();  // intentionally leaked
+static std::vector<rl_context*>* g_pool = new std::vector<rl_context*>[kMaxDevices];  // intentionally leaked
+static pid_t g_pool_pid = getpid();
 
 struct ThreadDefault {
-    rl_context* ctx = nullptr;
+    rl_context* ctx[kMaxDevices] = {};
+    pid_t pid = getpid();
     ~ThreadDefault() {
-        if (!ctx) return;
         std::lock_guard<std::mutex> lk(g_pool_mu);
-        g_pool->push_back(ctx);
+        if (pid != getpid() || g_pool_pid != pid) return;  // forked child: the parent's contexts are not ours
+        for (int d = 0; d < kMaxDevices; ++d)
+            if (ctx[d]) g_pool[d].push_back(ctx[d]);
     }
 };
 static thread_local ThreadDefault t_default;
@@ -92,27 +101,46 @@ rl_context* resolve(rl_context* ctx, rl_status* st) {
         cudaSetDevice(ctx->device);
         return ctx;
     }
-    if (!t_default.ctx) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *st = set_error(RL_ERR_NO_DEVICE, "no CUDA device available (librandla_b200 has no CPU fallback)");
+        return nullptr;
+    }
+    if (dev < 0 || dev >= kMaxDevices) {
+        *st = set_error(RL_ERR_INVALID_ARGUMENT, "device %d beyond the supported %d", dev, kMaxDevices);
+        return nullptr;
+    }
+    if (t_default.pid != getpid()) {  // a forked child inherits the parent's thread-local pointers: drop them
+        for (int d = 0; d < kMaxDevices; ++d) t_default.ctx[d] = nullptr;
+        t_default.pid = getpid();
+    }
+    rl_context*& mine = t_default.ctx[dev];
+    if (!mine) {
         {
             std::lock_guard<std::mutex> lk(g_pool_mu);
-            if (!g_pool->empty()) {
-                t_default.ctx = g_pool->back();
-                g_pool->pop_back();
+            if (g_pool_pid != getpid()) {  // contexts pooled by the parent process are unusable here
+                for (int d = 0; d < kMaxDevices; ++d) g_pool[d].clear();
+                g_pool_pid = getpid();
+            }
+            if (!g_pool[dev].empty()) {
+                mine = g_pool[dev].back();
+                g_pool[dev].pop_back();
             }
         }
-        if (!t_default.ctx) {
+        if (!mine) {
             rl_context* c = new rl_context();
-            rl_status s = init_context(c, 0);
+            rl_status s = init_context(c, dev);
             if (s != RL_OK) {
                 delete c;
                 *st = s;
                 return nullptr;
             }
-            t_default.ctx = c;
+            mine = c;
         }
     }
-    cudaSetDevice(t_default.ctx->device);
-    return t_default.ctx;
+    return mine;
 }
 
 rl_status side_resources(rl_context* ctx, int count) {
@@ -215,5 +243,11 @@ RL_API rl_status rl_synchronize(rl_context* ctx) {
 }
 
 RL_API int64_t rl_kernel_launches(void) { return rl::g_launches.load(); }
+
+RL_API int rl_context_device(rl_context* ctx) {
+    rl_status st;
+    ctx = rl::resolve(ctx, &st);
+    return ctx ? ctx->device : -1;
+}
 
 }  // extern "C"

@@ -87,18 +87,60 @@ def _raise(status, info_step=0, what=""):
 
 # ---- multipliers (multipliers.hpp:20-56) ------------------------------------
 class MultiplierKind(enum.IntEnum):
+    """randla::MultiplierKind (multipliers.hpp:20-29), the same ordinals; the
+    reference's CamelCase names are aliases. In this real pipeline the complex
+    families raise DimensionError exactly where the reference's real
+    instantiation does. GAUSSIAN_CIRCULANT is an extension outside the
+    reference's range: RealCirculant(gen_gaussian_vector(n, seed)), the
+    N(0,1)-column circulant of BASELINE configs 3 and 5."""
     NONE = capi.RL_MULT_NONE
     GAUSSIAN = capi.RL_MULT_GAUSSIAN
-    REAL_CIRCULANT = capi.RL_MULT_REAL_CIRCULANT          # reference family: uniform[-1,1] column
-    GAUSSIAN_CIRCULANT = capi.RL_MULT_GAUSSIAN_CIRCULANT  # BASELINE configs 3/5: N(0,1) column
+    REAL_CIRCULANT = capi.RL_MULT_REAL_CIRCULANT          # uniform[-1,1] first column
+    UNITARY_CIRCULANT = capi.RL_MULT_UNITARY_CIRCULANT
+    TOEPLITZ_BLOCK = capi.RL_MULT_TOEPLITZ_BLOCK
+    SRFT = capi.RL_MULT_SRFT
+    FINITE_SET_UNIFORM = capi.RL_MULT_FINITE_SET_UNIFORM
+    CIRC_SKEW_PRODUCT = capi.RL_MULT_CIRC_SKEW_PRODUCT
+    GAUSSIAN_CIRCULANT = capi.RL_MULT_GAUSSIAN_CIRCULANT  # extension: N(0,1) first column
+    # the reference's spellings
+    None_ = capi.RL_MULT_NONE
+    Gaussian = capi.RL_MULT_GAUSSIAN
+    RealCirculant = capi.RL_MULT_REAL_CIRCULANT
+    UnitaryCirculant = capi.RL_MULT_UNITARY_CIRCULANT
+    ToeplitzBlock = capi.RL_MULT_TOEPLITZ_BLOCK
+    Srft = capi.RL_MULT_SRFT
+    FiniteSetUniform = capi.RL_MULT_FINITE_SET_UNIFORM
+    CircSkewProduct = capi.RL_MULT_CIRC_SKEW_PRODUCT
+
+
+class ToeplitzVariant(enum.IntEnum):
+    """randla::ToeplitzVariant (multipliers.hpp:31)"""
+    REAL = capi.RL_TOEPLITZ_REAL
+    UNITARY = capi.RL_TOEPLITZ_UNITARY
+    Real = capi.RL_TOEPLITZ_REAL
+    Unitary = capi.RL_TOEPLITZ_UNITARY
 
 
 @dataclass
 class MultiplierSpec:
+    """randla::MultiplierSpec (multipliers.hpp:33-40): the same fields
+    (rows / cols 0 = taken from the call, as SideMultiplier::make and
+    range_find set them), plus two B200 extras: an explicit `dense` multiplier
+    or circulant first `column` instead of the seeded draw."""
     kind: MultiplierKind = MultiplierKind.NONE
     seed: int = 0
-    dense: Optional[object] = None   # explicit n x n multiplier (GAUSSIAN)
-    column: Optional[object] = None  # explicit first column (circulant kinds)
+    rows: int = 0
+    cols: int = 0
+    set_cardinality: int = 65536
+    variant: ToeplitzVariant = ToeplitzVariant.REAL
+    dense: Optional[object] = None
+    column: Optional[object] = None
+
+
+def multiplier_is_complex(spec):
+    """multipliers.hpp:42-52"""
+    return spec.kind in (MultiplierKind.UNITARY_CIRCULANT, MultiplierKind.SRFT) or (
+        spec.kind == MultiplierKind.TOEPLITZ_BLOCK and spec.variant == ToeplitzVariant.UNITARY)
 
 
 def derive_seed(seed, k1, k2=0):
@@ -134,6 +176,39 @@ def gen_real_circulant_column(n, seed):
     """multipliers.hpp:67-73 (first column of gen_real_circulant)"""
     out = np.empty(n)
     _raise(capi.lib().rl_gen_real_circulant_column(n, seed, out.ctypes.data))
+    return out
+
+
+def gen_real_circulant(n, seed):
+    """gen_real_circulant (multipliers.hpp:67-73): first column uniform on [-1, 1]"""
+    return RealCirculant(gen_real_circulant_column(n, seed))
+
+
+def gen_real_toeplitz_block(n, l, seed):
+    """gen_real_toeplitz_block (multipliers.hpp:84-86)"""
+    return ToeplitzBlock(gen_real_circulant(n, seed), n, l)
+
+
+def gen_finite_set_uniform(m, n, seed, cardinality):
+    """gen_finite_set_uniform (multipliers.hpp:142-154), bit-identical."""
+    if cardinality < 2:
+        raise DimensionError("gen_finite_set_uniform: cardinality must be >= 2")
+    out = np.empty((m, n))
+    _raise(capi.lib().rl_gen_finite_set_uniform(m, n, seed, cardinality, out.ctypes.data))
+    return out
+
+
+def materialize(spec, device=False):
+    """materialize<double>(spec) (multipliers.hpp:174-218): the dense sample
+    of a real family (spec.rows x spec.cols), generated by the reference's
+    generators; circulant and skew-product expansions run on the GPU."""
+    if spec.rows <= 0 or spec.cols <= 0:
+        raise DimensionError("materialize: spec.rows and spec.cols must be set")
+    out = _empty_like_kind(device, (spec.rows, spec.cols))
+    m, keep = _multiplier(spec, device)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_materialize(_ctx(), _mem(device), ctypes.byref(m), spec.rows, spec.cols, capi.addr(out)))
+    del keep
     return out
 
 
@@ -545,6 +620,8 @@ def _multiplier(spec, device):
         m.kind = capi.RL_MULT_NONE
         return m, []
     m.kind = int(spec.kind)
+    m.variant = int(getattr(spec, "variant", 0))
+    m.set_cardinality = int(getattr(spec, "set_cardinality", 65536))
     m.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
     keep = []
     if spec.dense is not None:
@@ -558,29 +635,46 @@ def _multiplier(spec, device):
     return m, keep
 
 
+def _check_side(spec, n):
+    """SideMultiplier::make's shape rule (preprocess.hpp:29-32)"""
+    if spec is None:
+        return
+    rows = spec.rows or n
+    cols = spec.cols or n
+    if rows != n or cols != n:
+        raise DimensionError("solve preprocessing takes square n-by-n multipliers")
+
+
 def preprocess_solve(a, b, pre_spec=None, post_spec=None, refine_steps=0, want_lu=False, want_norm_a=False):
-    """preprocess_solve(a, b, pre, post, refine) (preprocess.hpp:156-180) with
-    pre = none: product A*H, GENP, x = H (LU)^-1 b, refinement. Raises
+    """preprocess_solve(a, b, pre, post, refine) (preprocess.hpp:156-180):
+    product F (A H) (dense sides by the DMMA GEMM, circulant sides through the
+    FFT kernel), GENP, x = H (LU)^-1 (F b), refinement steps. Raises
     ZeroPivotError like the reference; retry with preprocess_solve_with_retry."""
-    if pre_spec is not None and pre_spec.kind != MultiplierKind.NONE:
-        raise DimensionError("preprocess_solve: left multipliers are not on the B200 path (pre must be none)")
     device = _is_device(a, b)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise DimensionError("preprocess_solve: square input required")
     n = a.shape[0]
     if b.shape[0] != n:
         raise DimensionError("preprocess_solve: length mismatch")
+    _check_side(pre_spec, n)
+    _check_side(post_spec, n)
+    if refine_steps < 0:
+        raise DimensionError("preprocess_solve: negative refine_steps")
     a = _dev(a) if device else _host(a)
     b = _dev(b) if device else _host(b)
     x = _empty_like_kind(device, (n,), b)
     lu = _empty_like_kind(device, (n, n), a) if want_lu else None
     m, keep = _multiplier(post_spec, device)
+    fm, fkeep = _multiplier(pre_spec, device)
     info = capi.rl_solve_info()
+    hist = (ctypes.c_double * (refine_steps + 1))()  # SolveOutcome::residual_history has refine + 1 entries
+    info.history = ctypes.cast(hist, ctypes.POINTER(ctypes.c_double))
+    info.history_capacity = refine_steps + 1
     _sync_stream_for(device)
-    rc = capi.lib().rl_preprocessed_genp_solve(_ctx(), _mem(device), n, capi.addr(a), capi.addr(b), ctypes.byref(m),
-                                               refine_steps, capi.addr(x), capi.addr(lu), 1 if want_norm_a else 0,
-                                               ctypes.byref(info))
-    del keep
+    rc = capi.lib().rl_preprocessed_genp_solve(_ctx(), _mem(device), n, capi.addr(a), capi.addr(b), ctypes.byref(fm),
+                                               ctypes.byref(m), refine_steps, capi.addr(x), capi.addr(lu),
+                                               1 if want_norm_a else 0, ctypes.byref(info))
+    del keep, fkeep
     _raise(rc, info.zero_pivot_step)
     d = info.as_dict()
     return SolveOutcome(x, d["residual_history"], bool(info.diverged), d, lu)
@@ -590,20 +684,150 @@ def preprocess_solve_with_retry(a, b, pre_spec, post_spec, refine_steps=0, max_r
     """preprocess.hpp:182-196: on ZeroPivot reseed with
     derive_seed(seed, 0x52455452, attempt + 1)."""
     import copy
+    pre = copy.copy(pre_spec) if pre_spec is not None else MultiplierSpec()
     post = copy.copy(post_spec) if post_spec is not None else MultiplierSpec()
     for attempt in range(max_retries + 1):
         try:
-            return preprocess_solve(a, b, pre_spec, post, refine_steps)
+            return preprocess_solve(a, b, pre, post, refine_steps)
         except ZeroPivotError:
             if attempt >= max_retries:
                 raise
+            pre.seed = derive_seed(pre.seed, 0x52455452, attempt + 1)
             post.seed = derive_seed(post.seed, 0x52455452, attempt + 1)
 
 
-# ---- structured multipliers (circulant.hpp) -------------------------------------
+# ---- FFT and structured multipliers (fft.hpp, circulant.hpp) ---------------------
+def _fft(v, inverse):
+    device = _is_device(v)
+    if device:
+        import torch
+        if not v.is_complex():
+            v = v.to(torch.complex128)
+        z = v.to(torch.complex128).contiguous().clone()
+        n = z.shape[-1]
+        count = z.numel() // n if n else 0
+        zr = torch.view_as_real(z)
+    else:
+        z = np.array(v, dtype=np.complex128, copy=True, order="C")
+        n = z.shape[-1] if z.ndim else 0
+        count = z.size // n if n else 0
+        zr = z.view(np.float64)
+    if n == 0:
+        raise DimensionError("inverse_fft: empty input" if inverse else "fft: empty input")
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_fft(_ctx(), _mem(device), count, n, capi.addr(zr), 1 if inverse else 0))
+    return z
+
+
+def fft(v):
+    """fft (fft.hpp:76-86): Omega v with omega = exp(+2 pi i / n), the
+    reference's sign; a batch of vectors along the last axis. Real input is
+    promoted to complex (fft.hpp:86)."""
+    return _fft(v, False)
+
+
+def inverse_fft(v):
+    """inverse_fft (fft.hpp:88-98): Omega^-1 v = Omega^H v / n."""
+    return _fft(v, True)
+
+
+class CirculantMatrix:
+    """CirculantMatrix<double> / RealCirculant (circulant.hpp:17-50): held by
+    its first column, entry (i, j) = c[(i - j) mod n]; the spectrum fft(c) is
+    computed on the GPU at construction, as the reference does eagerly."""
+
+    def __init__(self, first_column):
+        c = first_column
+        if (isinstance(c, np.ndarray) and c.size == 0) or len(c) == 0:
+            raise DimensionError("circulant: empty first column")
+        self._c = c if not isinstance(c, (list, tuple)) else np.asarray(c, dtype=np.float64)
+        self._spectrum = None
+
+    def size(self):
+        return int(self._c.shape[0])
+
+    def first_column(self):
+        return self._c
+
+    def spectrum(self):
+        if self._spectrum is None:
+            self._spectrum = fft(self._c)
+        return self._spectrum
+
+    def entry(self, i, j):
+        n = self.size()
+        return self._c[(i + n - j) % n]
+
+    def dense(self):
+        n = self.size()
+        spec = MultiplierSpec(MultiplierKind.REAL_CIRCULANT, 0, n, n, column=self._c)
+        return materialize(spec, device=_is_device(self._c))
+
+    def transposed(self):
+        """circulant.hpp:40-45: first column c[(n - i) mod n]"""
+        n = self.size()
+        idx = (n - np.arange(n)) % n
+        if isinstance(self._c, np.ndarray):
+            return CirculantMatrix(self._c[idx].copy())
+        import torch
+        return CirculantMatrix(self._c[torch.from_numpy(idx).to(self._c.device)].contiguous())
+
+
+RealCirculant = CirculantMatrix
+
+
+class ToeplitzBlock:
+    """ToeplitzBlock<double> (circulant.hpp:143-169): the leading rows x cols
+    block of a parent circulant, entry (i, j) = c[(i - j) mod n]."""
+
+    def __init__(self, parent, rows, cols):
+        n = parent.size()
+        if rows > n or cols > n or rows < 1 or cols < 1:
+            raise DimensionError("toeplitz block exceeds parent dimensions")
+        self.parent, self._rows, self._cols = parent, rows, cols
+
+    def rows(self):
+        return self._rows
+
+    def cols(self):
+        return self._cols
+
+    def entry(self, i, j):
+        return self.parent.entry(i, j)
+
+    def dense(self):
+        n = self.parent.size()
+        spec = MultiplierSpec(MultiplierKind.TOEPLITZ_BLOCK, 0, self._rows, self._cols, column=self.parent.first_column())
+        if self._rows != n:  # the block of a larger parent: expand the parent's leading block
+            full = self.parent.dense()
+            return full[: self._rows, : self._cols].copy() if isinstance(full, np.ndarray) else \
+                full[: self._rows, : self._cols].contiguous()
+        return materialize(spec, device=_is_device(self.parent.first_column()))
+
+
+def _column_of(c):
+    return c.first_column() if isinstance(c, CirculantMatrix) else c
+
+
+def circulant_apply(c, x):
+    """circulant_apply(RealCirculant, x) (circulant.hpp:91-96): C x by FFT on the GPU."""
+    c = _column_of(c)
+    device = _is_device(c, x)
+    n = c.shape[0]
+    if x.shape[0] != n:
+        raise DimensionError("circulant_apply: length mismatch")
+    c = _dev(c) if device else _host(c)
+    x = _dev(x) if device else _host(x)
+    y = _empty_like_kind(device, (n,), x)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_circulant_apply(_ctx(), _mem(device), n, capi.addr(c), capi.addr(x), capi.addr(y)))
+    return y
+
+
 def matmul_by_circulant(a, c):
-    """matmul_by_circulant(A, C(c)) (circulant.hpp:171-185): A (m x n) times the
-    real circulant with first column c, by FFT on the GPU."""
+    """matmul_by_circulant(A, C) (circulant.hpp:171-185): A (m x n) times the
+    real circulant C (a RealCirculant or its first column), by FFT on the GPU."""
+    c = _column_of(c)
     device = _is_device(a, c)
     m, n = a.shape
     if c.shape[0] != n:
@@ -617,10 +841,14 @@ def matmul_by_circulant(a, c):
     return out
 
 
-def matmul_by_toeplitz_block(a, c, cols):
-    """matmul_by_toeplitz_block(A, ToeplitzBlock(C(c), k, cols))
-    (circulant.hpp:187-203): A (m x k) times the leading k x cols block of the
-    circulant with first column c (parent length len(c) >= k)."""
+def matmul_by_toeplitz_block(a, c, cols=None):
+    """matmul_by_toeplitz_block(A, T) (circulant.hpp:187-203): A (m x k) times
+    the Toeplitz block T (a ToeplitzBlock, or a parent first column c and the
+    block's column count), by FFT on the GPU."""
+    if isinstance(c, ToeplitzBlock):
+        if a.shape[1] != c.rows():
+            raise DimensionError("matmul_by_toeplitz_block: shape mismatch")
+        c, cols = c.parent.first_column(), c.cols()
     device = _is_device(a, c)
     m, k = a.shape
     np_ = c.shape[0]
@@ -670,31 +898,55 @@ class LowRankResult:
         return self.q.shape[1]
 
 
-def range_find(a, r, p, spec, power_steps=0):
-    """range_find (lowrank.hpp:62-83): Y = A H (Gaussian H, or the Toeplitz block
-    of a circulant through the FFT), Q = orthonormal_basis(Y); also evaluates
-    ||A - Q Q^T A||_F and the power-iteration ||.||_2 (lowrank.hpp:99-102)."""
-    if power_steps:
-        raise DimensionError("range_find: power steps are not on the B200 path")
+def range_find(a, r, p, spec, power_steps=0, with_residual=True):
+    """range_find (lowrank.hpp:62-83): Y = A H (Toeplitz blocks through the FFT
+    kernel, every other real family materialized and multiplied by the DMMA
+    GEMM), power_steps alternating products Y <- A (A^T Y) (lowrank.hpp:51-57),
+    Q = orthonormal_basis(Y). With with_residual (one call, A resident once)
+    the result also carries ||A - Q Q^T A||_F and _2 of this A in `info`."""
     device = _is_device(a)
     m, n = a.shape
     l = r + p
     if r < 1 or l > min(m, n):
         raise DimensionError("range_find: rank plus oversampling exceeds matrix size")
+    if power_steps < 0:
+        raise DimensionError("range_find: negative power_steps")
     a = _dev(a) if device else _host(a)
     q = _empty_like_kind(device, (m, l), a)
     mlt, keep = _multiplier(spec, device)
     info = capi.rl_lowrank_info()
     _sync_stream_for(device)
-    rc = capi.lib().rl_range_find_residual(_ctx(), _mem(device), m, n, capi.addr(a), l, ctypes.byref(mlt),
-                                           capi.addr(q), ctypes.byref(info))
+    fn = capi.lib().rl_range_find_residual if with_residual else capi.lib().rl_range_find
+    rc = fn(_ctx(), _mem(device), m, n, capi.addr(a), l, ctypes.byref(mlt), power_steps, capi.addr(q),
+            ctypes.byref(info))
     del keep
     _raise(rc, info.rank_deficient_column)
     d = {k: getattr(info, k) for k, _ in info._fields_ if k != "reserved"}
+    if not with_residual:
+        d = {"rank_deficient_column": d["rank_deficient_column"]}
     return LowRankResult(q, r, p, power_steps, d)
 
 
+def residual_norms(a, result):
+    """||A - Q (Q^T A)||_F and ||.||_2 (power iteration, norms.hpp:52-77 on
+    the implicit operator) of `a` against result.q, on the GPU."""
+    q = result.q
+    device = _is_device(a, q)
+    m, n = a.shape
+    l = q.shape[1]
+    if q.shape[0] != m:
+        raise DimensionError("approximation_residual: shape mismatch")
+    a = _dev(a) if device else _host(a)
+    q = _dev(q) if device else _host(q)
+    info = capi.rl_lowrank_info()
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_approximation_residual(_ctx(), _mem(device), m, n, capi.addr(a), l, capi.addr(q),
+                                                ctypes.byref(info)))
+    return {"residual_frobenius": info.residual_frobenius, "residual_spectral": info.residual_spectral,
+            "power_iterations": info.power_iterations}
+
+
 def approximation_residual(a, result):
-    """||A - Q (Q^T A)||_2 of a range_find result (lowrank.hpp:99-102), from the
-    device power iteration on the implicit residual operator."""
-    return result.info["residual_spectral"]
+    """approximation_residual(a, result) (lowrank.hpp:99-102):
+    ||A - Q (Q^H A)||_2 of the given A, evaluated on the GPU."""
+    return residual_norms(a, result)["residual_spectral"]

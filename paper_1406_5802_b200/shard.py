@@ -66,3 +66,33 @@ def reduce_summary(local: dict, dist=None, device=None) -> dict:
                "zero_pivots": int(sm[1]), "counted": int(sm[2])}
     out["mean_residual"] = out["sum_residual"] / out["counted"] if out["counted"] else 0.0
     return out
+
+
+def shard_inputs(lo: int, hi: int, base: int = 7):
+    """(A, G, b) of systems lo..hi-1 as host arrays, from the reference's
+    generators (bit-identical to the single-process inputs)."""
+    from . import randla as _r
+    seeds = batch_seeds(lo, hi, base)
+    k = hi - lo
+    a = _r.gen_gaussian_batch(k, 32, 32, seeds[:, 0])
+    b = _r.gen_gaussian_batch(k, 32, 1, seeds[:, 1]).reshape(k, 32)
+    g = _r.gen_gaussian_batch(k, 32, 32, seeds[:, 2])
+    return a, g, b
+
+
+def run_batched_shard(total: int, rank: int, world: int, dist=None, device=None, base: int = 7, solve=None,
+                      to_device=None):
+    """One rank's share of BASELINE config 2: its contiguous block of systems,
+    generated from the per-trial seeds, solved by the library's batched entry
+    point (randla.batched_preprocess_solve_32; `to_device` moves the inputs to
+    the rank's GPU first), then the summary all-reduce. Returns
+    (lo, hi, result, reduced summary)."""
+    from . import randla as _r
+    lo, hi = shard_bounds(total, rank, world)
+    a, g, b = shard_inputs(lo, hi, base)
+    if to_device is not None:
+        a, g, b = to_device(a), to_device(g), to_device(b)
+    out = (solve or _r.batched_preprocess_solve_32)(a, g, b)
+    host = (lambda t: t) if isinstance(out.residual, np.ndarray) else (lambda t: t.cpu().numpy())
+    local = local_summary(host(out.residual), host(out.growth), host(out.status))
+    return lo, hi, out, reduce_summary(local, dist, device=device)

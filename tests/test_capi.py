@@ -17,7 +17,7 @@ def test_library_exports_every_header_symbol():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     assert set(syms) == set(capi.SIGNATURES), set(syms) ^ set(capi.SIGNATURES)
-    assert capi.lib().rl_abi_version() == 1
+    assert capi.lib().rl_abi_version() == 2
 
 
 def test_product_library_is_native_sm100a():
@@ -71,3 +71,18 @@ def test_compute_fails_loudly_without_device():
     b = np.zeros((4, 32))
     with pytest.raises(rl.DeviceError):
         rl.batched_preprocess_solve_32(a, a, b)
+
+
+@pytest.mark.parametrize("card", [2, 3, 1000, 65536, 2 ** 63 + 5])
+def test_finite_set_uniform_bit_exact_vs_reference(orc, card):
+    """gen_finite_set_uniform (multipliers.hpp:142-154) incl. next_below
+    rejections (rng.hpp:46-53; card = 2^63 + 5 rejects about half the draws)"""
+    import paper_1406_5802_b200 as rl
+    if orc.REF is None:
+        pytest.skip("oracle/_ref not built")
+    for seed in (0, 7, 2 ** 64 - 1):
+        got = rl.gen_finite_set_uniform(37, 29, seed, card)
+        ref = orc.REF.gen_finite_set_uniform(37, 29, seed, card)
+        assert np.array_equal(got, ref)
+    big = rl.gen_finite_set_uniform(1024, 600, 5, card)  # the parallel two-pass path
+    assert np.array_equal(big, orc.REF.gen_finite_set_uniform(1024, 600, 5, card))

@@ -22,12 +22,12 @@ q = a.new_empty(m, r)
 mlt = capi.rl_multiplier(); mlt.kind = kind; mlt.seed = 41
 info = capi.rl_lowrank_info()
 for _ in range(2):
-    rc = L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), q.data_ptr(), ctypes.byref(info))
+    rc = L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), 0, q.data_ptr(), ctypes.byref(info))
     if not os.environ.get('RANDLA_VARIANT_LIB'):
         assert rc == 0, capi.last_error()
 torch.cuda.synchronize()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record()
-L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), q.data_ptr(), ctypes.byref(info))
+L.rl_range_find_residual(None, capi.RL_DEVICE, m, n, a.data_ptr(), r, ctypes.byref(mlt), 0, q.data_ptr(), ctypes.byref(info))
 e1.record(); e1.synchronize()
 print(f"range_find {m}x{n} r={r}: {e0.elapsed_time(e1):.2f} ms, its {info.power_iterations}, fro {info.residual_frobenius:.3e} spec {info.residual_spectral:.3e}")

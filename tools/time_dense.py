@@ -15,7 +15,7 @@ L.rl_context_set_stream(None, ctypes.c_void_p(torch.cuda.current_stream().cuda_s
 m = capi.rl_multiplier(); m.kind = 1; m.dense = g.data_ptr()
 info = capi.rl_solve_info()
 def run():
-    rc = L.rl_preprocessed_genp_solve(None, 1, n, a.data_ptr(), b.data_ptr(), ctypes.byref(m), 0, x.data_ptr(), None, 0, ctypes.byref(info))
+    rc = L.rl_preprocessed_genp_solve(None, 1, n, a.data_ptr(), b.data_ptr(), None, ctypes.byref(m), 0, x.data_ptr(), None, 0, ctypes.byref(info))
     assert rc == 0, capi.last_error()
 run(); torch.cuda.synchronize()
 for rep in range(3):

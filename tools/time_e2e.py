@@ -31,6 +31,6 @@ m2 = capi.rl_multiplier(); m2.kind = capi.RL_MULT_GAUSSIAN; m2.seed = 2
 info = capi.rl_solve_info()
 for i in range(3):
     t0 = time.perf_counter()
-    rc = L.rl_preprocessed_genp_solve(None, capi.RL_HOST, n, hA.data_ptr(), hb.data_ptr(), ctypes.byref(m2), 0, hx.data_ptr(), None, 0, ctypes.byref(info))
+    rc = L.rl_preprocessed_genp_solve(None, capi.RL_HOST, n, hA.data_ptr(), hb.data_ptr(), None, ctypes.byref(m2), 0, hx.data_ptr(), None, 0, ctypes.byref(info))
     dt = time.perf_counter() - t0
     print(f"e2e: {dt*1e3:.2f} ms rc={rc} stages {[round(x,2) for x in info.stage_ms]}")
