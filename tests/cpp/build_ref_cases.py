@@ -56,8 +56,10 @@ def build(verbose=False):
         return []
     os.makedirs(OUT, exist_ok=True)
     built = []
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="randla_ref_cases_")  # the assembled source never lands in the tree
     for name, (rel, ranges) in CASES.items():
-        src = os.path.join(OUT, name + ".cpp")
+        src = os.path.join(tmp, name + ".cpp")
         with open(src, "w") as f:
             f.write(assemble(rel, ranges))
         exe = os.path.join(OUT, name)
@@ -68,6 +70,8 @@ def build(verbose=False):
         if r.returncode != 0:
             raise RuntimeError(f"reference cases {name} do not compile against the drop-in:\n{r.stderr[-4000:]}")
         built.append(exe)
+        os.remove(src)
+    os.rmdir(tmp)
     return built
 
 
