@@ -9,8 +9,9 @@
 // (mma.sync .f64, SASS DMMA.8x8x4), measured at 37.0 TF/s on this B200
 // against 36.4 for DFMA and 35.5 for cuBLAS DGEMM (profiles/r01_fp64_peak.txt).
 //
-// Tiling: 128x128 CTA tile, k-slabs of 16, 8 warps of 64x32 (32 DMMA per
-// k=4 step, 128 accumulator registers per lane). Operands arrive by TMA
+// Tiling: 128x64 CTA tiles, k-slabs of 16, 8 warps of 32x32, two CTAs per SM
+// (the C prologue / epilogue of one overlaps the other's main loop); a
+// 128x128 one-CTA tile for the split-K partial products. Operands arrive by TMA
 // (cp.async.bulk.tensor.2d, 128-byte swizzle) into a 4-stage shared-memory
 // ring guarded by mbarriers; one thread issues the copies. CTAs are rastered
 // in groups of 8 tile-rows so concurrently resident CTAs share A and B panels
@@ -334,11 +335,14 @@ rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm: accumulate supports alpha = +1 or -1");
     if (M > (int64_t(1) << 30) || N > (int64_t(1) << 30) || K > (int64_t(1) << 30))
         return set_error(RL_ERR_DIMENSION, "gemm: dimension too large");
-    // short K (Schur updates): the two-CTAs-per-SM configuration; problems
-    // that would not fill the SMs with it: 64x32 tiles
-    const bool small = K <= 256;
+    // the two-CTAs-per-SM 128x64 configuration: one CTA's prologue / epilogue
+    // (the C tile) overlaps the other's MMA main loop. Measured on this pool
+    // (tools/gemm_update_bench.cu): 35.5 TF/s at 8192^3 against 34.2 for the
+    // one-CTA 128x128 tile, and 32.2 against 27.3 for the K = 128 Schur update.
+    // Problems that would not fill the SMs with it: 64x32 tiles.
+    const bool small = true;
     const int64_t small_tiles = ((M + 127) / 128) * ((N + 63) / 64);
-    const bool tiny = small && small_tiles < ctx->num_sms;
+    const bool tiny = small_tiles < ctx->num_sms;
 #define RL_GEMM_DISPATCH(AC, ST)                                                                                   \
     return tiny    ? run_cfg<TinyCfg, AC, ST, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0)  \
            : small ? run_cfg<SmallCfg, AC, ST, true>(ctx, M, N, K, A, lda, B, ldb, C, ldc, alpha, stats, 1, 0, 0) \
@@ -357,7 +361,7 @@ rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, 
     if (M <= 0 || N <= 0) return RL_OK;
     if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
         return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_residual_stats: misaligned operands");
-    const bool small = K <= 256;
+    const bool small = true;  // as gemm(): the two-CTAs-per-SM tile wins at every K measured
     return small ? run_cfg<SmallCfg, true, true, false>(ctx, M, N, K, A, lda, B, ldb, const_cast<double*>(C), ldc, -1.0,
                                                         stats, 1, 0, 0)
                  : run_cfg<BigCfg, true, true, false>(ctx, M, N, K, A, lda, B, ldb, const_cast<double*>(C), ldc, -1.0,

@@ -77,35 +77,41 @@ def test_mean_residual_known_rank_ensemble(cuda):
 
 @pytest.mark.parametrize("kind", ["gaussian", "toeplitz"])
 def test_range_find_residual_vs_oracle(cuda, orc, kind):
-    """Y, Q and the residual against the oracle's Householder path on the same
-    inputs; ||R||_2 against numpy's SVD of the oracle's residual."""
+    """Y, Q and the residual norms against the reference on the same inputs:
+    the sketch by the reference's own code, Q by the restated Householder QR
+    with qr.hpp:33-45's phases, ||R||_F of the explicit residual, and ||R||_2
+    by the reference's own spectral_norm_estimate (norms.hpp:35-78) run on the
+    explicit residual -- the device runs the same power iteration (start
+    vector, stopping rule) on the implicit operator. Bars: the north star's
+    1e-9 relative for both norms (measured agreement ~1e-12 .. 1e-10, see
+    DESIGN.md §2)."""
     m = n = 1024
     r = 32
-    rng = np.random.default_rng(4)
-    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
-    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
-    sig = np.logspace(0, -2, r)
-    a = (u * sig) @ v.T + 1e-10 * rng.standard_normal((m, n))
+    u = orc.C.gen_gaussian(m, r, 61)
+    v = orc.C.gen_gaussian(n, r, 62)
+    u, _ = np.linalg.qr(u)
+    v, _ = np.linalg.qr(v)
+    a = (u * np.logspace(0, -2, r)) @ v.T + 1e-10 * orc.C.gen_gaussian(m, n, 63)
     if kind == "gaussian":
         spec = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 77)
-        y_ref = orc.C.matmul(a, orc.C.gen_gaussian(n, r, 77))
+        y_ref, st = orc.REF.range_sketch(a, r, int(rl.MultiplierKind.GAUSSIAN), 77)
     else:
         spec = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN_CIRCULANT, 21)
-        y_ref, st = orc.C.matmul_by_toeplitz_block(a, orc.C.gen_gaussian_vector(n, 21), r)
-        assert st == 0
+        y_ref, st = orc.REF.matmul_by_toeplitz_block(a, orc.C.gen_gaussian_vector(n, 21), r)
+    assert st == 0
     res = rl.range_find(a, r, 0, spec)
     q_ref, _, st, _ = orc.C.qr(y_ref)
     assert st == 0
-    # same subspace: compare projectors through Q^T Q_ref (sign-free)
-    assert np.abs(np.abs(np.linalg.svd(res.q.T @ q_ref, compute_uv=False)) - 1).max() < 1e-6
+    kap = np.linalg.cond(y_ref)
+    assert np.abs(res.q - q_ref).max() <= 1e-13 * kap * np.sqrt(m)
     resid_ref = a - q_ref @ (q_ref.T @ a)
-    s_ref = np.linalg.svd(resid_ref, compute_uv=False)
-    floor = 2.2e-16 * np.linalg.norm(a, 2) / s_ref[0]  # rounding floor of the comparison (SURVEY finding 9)
-    assert abs(res.info["residual_frobenius"] / np.linalg.norm(resid_ref) - 1) <= max(1e-6, 100 * floor)
-    # power iteration: a lower bound of sigma_1 converging to it
-    rel = abs(res.info["residual_spectral"] / s_ref[0] - 1)
-    print(kind, "sigma1", s_ref[0], "est", res.info["residual_spectral"], "rel", rel, "its", res.info["power_iterations"])
-    assert rel <= 0.05
+    fro_ref = np.linalg.norm(resid_ref)
+    est_ref = orc.REF.spectral_norm_estimate(resid_ref)
+    e_fro = abs(res.info["residual_frobenius"] / fro_ref - 1)
+    e_spec = abs(res.info["residual_spectral"] / est_ref - 1)
+    print(kind, "fro", e_fro, "spec vs reference estimate", e_spec, "its", res.info["power_iterations"])
+    assert e_fro <= 1e-9
+    assert e_spec <= 1e-9
 
 
 @pytest.mark.parametrize("m,n,r", [(1000, 998, 17), (2050, 4100, 40), (3001, 640, 64), (513, 9000, 8)])
