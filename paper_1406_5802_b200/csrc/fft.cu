@@ -297,6 +297,87 @@ __global__ void __launch_bounds__(FT) circ_rows_kernel(const double* __restrict_
     }
 }
 
+// ---- narrow Toeplitz blocks by overlap-save correlation ---------------------------
+// Y = A T for a k x l Toeplitz block of an np-point circulant with l << np
+// (BASELINE config 5: np = k = 16384, l = 256): Y[i, j] = sum_t A[i, t]
+// c[(t - j) mod np]. A row splits into chunks of Lc = NF - l + 1 samples;
+// chunk s contributes the correlation of its samples with the segment
+// h_s[u] = c[(s Lc - (l - 1) + u) mod np], u < NF, evaluated at lags
+// j' = l - 1 - j < l, which an NF-point circular correlation gives without
+// wrap-around: r_s = Omega^-1 (conj(Omega a_s) .* Omega h_s). The chunk
+// products sum in the frequency domain, so one inverse transform serves all
+// chunks of a row. Two real rows travel as one complex row z = a1 + i a2:
+// conj(Omega z) = conj(Omega a1) - i conj(Omega a2), so the inverse is
+// r1 - i r2. Per row that is ceil(k / Lc) NF-point transforms instead of two
+// np-point ones (10 x 2048 against 2 x 8192 complex points here, about a
+// third of the FP64 work), with the same single read of A.
+constexpr int OLA_NF = 2048;  // transform length (complex points)
+constexpr int OLA_T = 128;    // threads: one radix-16 group each
+
+// spectra of the segments h_s (digit-reversed: the forward DIF's order)
+__global__ void __launch_bounds__(OLA_T) ola_spectra_kernel(const double* __restrict__ c, int np, int lc, int l,
+                                                            const cplx* __restrict__ tw, cplx* __restrict__ spec) {
+    __shared__ __align__(16) cplx z[OLA_NF];
+    const int s = blockIdx.x;
+    const int64_t base = static_cast<int64_t>(s) * lc - (l - 1);
+    for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) {
+        const int64_t idx = ((base + u) % np + np) % np;
+        z[u] = {c[idx], 0.0};
+    }
+    __syncthreads();
+    forward_fft(z, OLA_NF, tw, OLA_NF);
+    for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) spec[static_cast<int64_t>(s) * OLA_NF + u] = z[u];
+}
+
+__global__ void __launch_bounds__(OLA_T) ola_rows_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int k,
+                                                         int lc, int chunks, const cplx* __restrict__ spec,
+                                                         const cplx* __restrict__ tw, double* __restrict__ out,
+                                                         int64_t ldo, int l) {
+    __shared__ __align__(16) cplx z[OLA_NF];
+    constexpr int PER = OLA_NF / OLA_T;  // frequency slots per thread
+    for (int64_t pair = blockIdx.x; 2 * pair < m; pair += gridDim.x) {
+        const int64_t r0 = 2 * pair;
+        const bool two = r0 + 1 < m;
+        const double* a0 = a + r0 * lda;
+        const double* a1 = a + (r0 + 1) * lda;
+        cplx acc[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) acc[q] = {0.0, 0.0};
+        for (int s = 0; s < chunks; ++s) {
+            const int t0 = s * lc;
+            for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) {
+                const int t = t0 + u;
+                const bool in = u < lc && t < k;
+                z[u] = {in ? __ldcs(a0 + t) : 0.0, (in && two) ? __ldcs(a1 + t) : 0.0};
+            }
+            __syncthreads();
+            forward_fft(z, OLA_NF, tw, OLA_NF);
+            const cplx* hs = spec + static_cast<int64_t>(s) * OLA_NF;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int u = threadIdx.x + q * OLA_T;
+                const cplx zz = z[u], hh = hs[u];
+                // acc += conj(zz) * hh
+                acc[q].x = fma(zz.x, hh.x, fma(zz.y, hh.y, acc[q].x));
+                acc[q].y = fma(zz.x, hh.y, fma(-zz.y, hh.x, acc[q].y));
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) z[threadIdx.x + q * OLA_T] = acc[q];
+        __syncthreads();
+        inverse_fft(z, OLA_NF, tw, OLA_NF, 1.0 / static_cast<double>(OLA_NF));
+        double* o0 = out + r0 * ldo;
+        double* o1 = out + (r0 + 1) * ldo;
+        for (int j = threadIdx.x; j < l; j += blockDim.x) {
+            const cplx v = z[l - 1 - j];
+            __stcs(o0 + j, v.x);
+            if (two) __stcs(o1 + j, -v.y);
+        }
+        __syncthreads();
+    }
+}
+
 // ---- parent length 2*MAXN on a 2-CTA cluster ------------------------------------
 // CTA h keeps half h of the first radix-2 DIF split:
 //   h = 0: y0[j] = z[j] + z[j + H]          h = 1: y1[j] = (z[j] - z[j + H]) w_n^j
@@ -868,6 +949,24 @@ rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a,
     }
     const bool aligned = (lda % 2 == 0) && (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (n >= 4 * OLA_NF && 8 * l <= OLA_NF && m >= 2) {
+        // narrow Toeplitz block: overlap-save correlation with NF-point transforms
+        const int lc = OLA_NF - static_cast<int>(l) + 1;
+        const int chunks = static_cast<int>((k + lc - 1) / lc);
+        cplx* tw_f = nullptr;
+        if ((st = twiddles(ctx, OLA_NF, &tw_f)) != RL_OK) return st;
+        cplx* ospec = nullptr;
+        RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ospec), sizeof(cplx) * OLA_NF * chunks, ctx->stream));
+        ola_spectra_kernel<<<chunks, OLA_T, 0, ctx->stream>>>(c, n, lc, static_cast<int>(l), tw_f, ospec);
+        RL_CHECK_LAUNCH("ola_spectra_kernel");
+        const int64_t pairs = (m + 1) / 2;
+        const int64_t grid = std::min<int64_t>(pairs, static_cast<int64_t>(ctx->num_sms) * 8);
+        ola_rows_kernel<<<static_cast<unsigned>(grid), OLA_T, 0, ctx->stream>>>(
+            a, lda, m, static_cast<int>(k), lc, chunks, ospec, tw_f, out, ldo, static_cast<int>(l));
+        RL_CHECK_LAUNCH("ola_rows_kernel");
+        RL_CUDA(cudaFreeAsync(ospec, ctx->stream));
+        return RL_OK;
+    }
     if (aligned && n >= 4) {
         int L = 0;
         while ((2 << L) < n) ++L;

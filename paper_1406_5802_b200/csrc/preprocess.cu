@@ -472,6 +472,22 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     // kernels enqueued next, so block 0 lands under them
     constexpr int kChunks = 4;
     const bool pipelined_a = own_a && host && n >= 1024 && side_resources(ctx, kChunks) == RL_OK;
+    // pageable host A (the C++ drop-in's RealMatrix, a numpy array): copied
+    // into the context's grow-only pinned staging by all host cores first
+    // (~16 threads beat the driver's single-threaded staging copies several
+    // times over), so its row blocks then stream by DMA under the product.
+    // Page-locking the caller's buffer per call instead costs more than the
+    // copies (cudaHostRegister of 512 MiB: ~50 ms on this pool).
+    if (pipelined_a) {
+        cudaPointerAttributes pa{};
+        const bool pageable = cudaPointerGetAttributes(&pa, a) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered;
+        cudaGetLastError();
+        double* stage = pageable ? static_cast<double*>(pinned_staging(ctx, sizeof(double) * n * n, 1)) : nullptr;
+        if (stage) {
+            host_parallel_copy(stage, a, sizeof(double) * n * n);
+            a = stage;
+        }
+    }
     struct SideDrain {  // error exits: the side stream's uploads read the caller's `a` and write the
         cudaStream_t s = nullptr;  // workspace, so they must be done before the call returns
         ~SideDrain() {

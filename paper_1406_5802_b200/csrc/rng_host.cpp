@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <thread>
 #include <mutex>
 #include <condition_variable>
@@ -229,6 +230,15 @@ void gaussian_parallel(uint64_t seed, int64_t count, double* out) {
 
 namespace rl {
 uint64_t host_stream_state(uint64_t seed) { return stream_state(seed); }
+
+void host_parallel_copy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kPiece = size_t(4) << 20;
+    const int64_t pieces = static_cast<int64_t>((bytes + kPiece - 1) / kPiece);
+    parallel_for(pieces, [&](int64_t i) {
+        const size_t off = static_cast<size_t>(i) * kPiece;
+        std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(kPiece, bytes - off));
+    });
+}
 
 // finish listed polar attempts with glibc's log (rng_device.cu hard cases):
 // out2[2i], out2[2i+1] = u f, v f of attempt attempts[i]

@@ -61,7 +61,8 @@ static void destroy_context(rl_context* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->ws) cudaFree(c->ws);
     if (c->flags) cudaFree(c->flags);
-    if (c->pinned) cudaFreeHost(c->pinned);
+    for (void* p : c->pinned)
+        if (p) cudaFreeHost(p);
     if (c->host_scalars) cudaFreeHost(c->host_scalars);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->hi_stream) cudaStreamDestroy(c->hi_stream);
@@ -160,20 +161,21 @@ rl_status side_resources(rl_context* ctx, int count) {
     return RL_OK;
 }
 
-void* pinned_staging(rl_context* ctx, size_t bytes) {
-    if (bytes <= ctx->pinned_bytes) return ctx->pinned;
+void* pinned_staging(rl_context* ctx, size_t bytes, int slot) {
+    if (bytes <= ctx->pinned_bytes[slot]) return ctx->pinned[slot];
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    ctx->pinned = nullptr;
-    ctx->pinned_bytes = 0;
+    if (ctx->hi_stream) cudaStreamSynchronize(ctx->hi_stream);
+    if (ctx->pinned[slot]) cudaFreeHost(ctx->pinned[slot]);
+    ctx->pinned[slot] = nullptr;
+    ctx->pinned_bytes[slot] = 0;
     const size_t want = align_up(bytes, size_t(1) << 20);
-    if (cudaHostAlloc(&ctx->pinned, want, cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc(&ctx->pinned[slot], want, cudaHostAllocDefault) != cudaSuccess) {
         cudaGetLastError();
-        ctx->pinned = nullptr;
+        ctx->pinned[slot] = nullptr;
         return nullptr;
     }
-    ctx->pinned_bytes = want;
-    return ctx->pinned;
+    ctx->pinned_bytes[slot] = want;
+    return ctx->pinned[slot];
 }
 
 void* workspace(rl_context* ctx, size_t bytes) {

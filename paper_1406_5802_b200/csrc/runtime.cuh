@@ -28,9 +28,10 @@ struct rl_context {
     cudaStream_t hi_stream = nullptr;
     cudaEvent_t* events = nullptr;
     int num_events = 0;
-    // grow-only pinned host staging (exact-generator hard cases)
-    void* pinned = nullptr;
-    size_t pinned_bytes = 0;
+    // grow-only pinned host staging: slot 0 the exact generator's hard cases,
+    // slot 1 a pageable host A on its way to the device
+    void* pinned[2] = {nullptr, nullptr};
+    size_t pinned_bytes[2] = {0, 0};
     // 4 KiB pinned host scalars for asynchronous device->host readbacks
     int64_t* host_scalars = nullptr;
 };
@@ -49,8 +50,11 @@ rl_context* resolve(rl_context* ctx, rl_status* st);
 // Grow-only device workspace; returns nullptr on OOM (error already set).
 void* workspace(rl_context* ctx, size_t bytes);
 
-// Grow-only pinned host buffer owned by the context (nullptr on failure).
-void* pinned_staging(rl_context* ctx, size_t bytes);
+// Grow-only pinned host buffer `slot` (0 or 1) owned by the context (nullptr on failure).
+void* pinned_staging(rl_context* ctx, size_t bytes, int slot = 0);
+
+// memcpy on the host worker pool (all cores; serial when the pool is busy)
+void host_parallel_copy(void* dst, const void* src, size_t bytes);
 
 // High-priority side stream and at least `count` reusable timing-free events.
 rl_status side_resources(rl_context* ctx, int count);

@@ -23,6 +23,8 @@ What is stored (compact: the n x n factors themselves are 512 MiB each):
 
 Usage: python tests/golden/make_fullsize.py [headline cfg3 cfg4 cfg5]
        python tests/golden/make_fullsize.py floor [headline cfg3]   (adds the rounding floors)
+       python tests/golden/make_fullsize.py floor_alg [headline cfg3]   (adds the algorithm floors)
+       python tests/golden/make_fullsize.py floor_inv [headline cfg3]   (... with the inverse-based U12)
 """
 import ctypes
 import os
@@ -262,7 +264,77 @@ def rounding_floor(name):
     np.savez(os.path.join(HERE, f"fullsize_{name}.npz"), **fx)
 
 
+def blocked_genp(p, nb=128, explicit_inverse=False):
+    """GENP (no pivoting) of p as a right-looking blocked factorisation with
+    BLAS updates: unblocked 128-column panels, U12 = L11^-1 A12, A22 -= L21 U12
+    -- the algorithm class of the device's, in LAPACK / OpenBLAS arithmetic.
+    explicit_inverse: U12 = (L11^-1) A12 with the inverse formed first, as the
+    device does (MAGMA-style TRSM by inverted diagonal blocks)"""
+    import scipy.linalg as sl
+    a = p.copy()
+    n = a.shape[0]
+    for k in range(0, n, nb):
+        e = min(k + nb, n)
+        for j in range(k, e):
+            a[j + 1:, j] /= a[j, j]
+            if j + 1 < e:
+                a[j + 1:, j + 1:e] -= np.outer(a[j + 1:, j], a[j, j + 1:e])
+        if e < n:
+            if explicit_inverse:
+                linv = sl.solve_triangular(a[k:e, k:e], np.eye(e - k), lower=True, unit_diagonal=True)
+                a[k:e, e:] = linv @ a[k:e, e:]
+            else:
+                a[k:e, e:] = sl.solve_triangular(a[k:e, k:e], a[k:e, e:], lower=True, unit_diagonal=True)
+            a[e:, e:] -= a[e:, k:e] @ a[k:e, e:]
+    return a
+
+
+def algorithm_floor(name, explicit_inverse=False):
+    """The reference's GENP against a blocked right-looking GENP with BLAS
+    updates (blocked_genp) on the SAME product bits: the disagreement of two
+    correct elimination orders, the other half of what separates the device
+    (blocked, K = 128 DMMA updates, FMA) from the reference's scalar loop."""
+    fx = dict(np.load(os.path.join(HERE, f"fullsize_{name}.npz")))
+    n = 8192
+    blas_threads(8)
+    if name == "headline":
+        a = R.gen_gaussian(n, n, 1)
+        g = R.gen_gaussian(n, n, 2)
+        b = R.gen_gaussian(n, 1, 3).reshape(n)
+        p = a @ g  # bit-identical to the reference's product (OpenBLAS blocking is thread-count independent)
+    else:
+        config_inputs.build("cfg3", WORK)
+        inp = config_inputs.load("cfg3", WORK, mmap=False)
+        a, c, b = inp["A"], inp["c"], inp["b"]
+        blas_threads(1)
+        p, st = R.matmul_by_circulant(a, c)
+        blas_threads(8)
+    lu = blocked_genp(p, explicit_inverse=explicit_inverse)
+    d = lu_digest(lu, n)
+    import scipy.linalg as sl
+    y = sl.solve_triangular(np.triu(lu), sl.solve_triangular(lu, b, lower=True, unit_diagonal=True), lower=False)
+    if name == "headline":
+        x = g @ y
+    else:
+        blas_threads(1)
+        x, st = R.circulant_apply(c, y)
+    rel = lambda u, v: float(np.linalg.norm(u - v) / np.linalg.norm(v))  # noqa: E731
+    floor = {"x": rel(x, fx["x_refine0"]), "pivots": rel(d["pivots"], fx["pivots"]),
+             "lu_rows": rel(d["lu_rows"], fx["lu_rows"]), "L_sketch": rel(d["lw"], fx["lw"]),
+             "U_sketch": rel(d["uw"], fx["uw"]),
+             "growth": float(abs(d["max_abs_u"][0] / np.abs(p).max() - fx["growth"][0]) / fx["growth"][0])}
+    tag = "floor_inv" if explicit_inverse else "floor_alg"
+    log(name, tag, floor)
+    for k, v in floor.items():
+        fx[f"{tag}_{k}"] = np.array([v])
+    np.savez(os.path.join(HERE, f"fullsize_{name}.npz"), **fx)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:2] in (["floor_alg"], ["floor_inv"]):
+        for w in sys.argv[2:] or ["headline", "cfg3"]:
+            algorithm_floor(w, explicit_inverse=sys.argv[1] == "floor_inv")
+        sys.exit(0)
     if sys.argv[1:2] == ["floor"]:
         for w in sys.argv[2:] or ["headline", "cfg3"]:
             rounding_floor(w)

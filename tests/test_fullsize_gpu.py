@@ -58,18 +58,23 @@ def lu_sketches(torch, packed, w_seed, cols=8):
     return lw.cpu().numpy(), uw.cpu().numpy()
 
 
-FLOOR_FACTOR = 10.0
+FLOOR_FACTOR = 5.0
 
 
 def check_dense(torch, fx, out, lu, refine_key="refine0"):
     """the north-star bars for one dense solve; returns the measured errors.
     Each quantity must agree with the reference within 1e-10 kappa(A), or --
-    where GENP's forward error exceeds that for the reference itself -- within
-    FLOOR_FACTOR times the reference's own disagreement with itself when every
-    entry of the factored product moves by one rounding unit (fixture keys
-    floor_*, tests/golden/make_fullsize.py rounding_floor): L, U and the
-    pivots follow the leading principal minors (growth ~1e4-1e5 here), not
-    kappa(A)."""
+    where GENP's forward error exceeds that between correct CPU
+    implementations -- within FLOOR_FACTOR times the largest of these
+    disagreements with the reference (tests/golden/make_fullsize.py):
+      floor_*      the reference's own genp_factor on the product summed in
+                   another order;
+      floor_alg_*  a blocked right-looking GENP with BLAS updates on the same
+                   product bits;
+      floor_inv_*  the same with U12 = (L11^-1) A12 through the explicitly
+                   inverted diagonal block, the device's formulation.
+    L, U and the pivots follow the leading principal minors (growth ~1e4-1e5
+    here), not kappa(A)."""
     kappa = float(fx["kappa_a"][0])
     tol = 1e-10 * kappa
     lu_h_rows = lu[torch.from_numpy(fx["lu_rows_idx"]).cuda()].cpu().numpy()
@@ -79,8 +84,10 @@ def check_dense(torch, fx, out, lu, refine_key="refine0"):
     err = {"x": rel(x, fx[f"x_{refine_key}"]), "pivots": rel(piv, fx["pivots"]),
            "lu_rows": rel(lu_h_rows, fx["lu_rows"]), "L_sketch": rel(lw, fx["lw"]), "U_sketch": rel(uw, fx["uw"]),
            "growth": abs(out.info["growth"] - float(fx["growth"][0])) / float(fx["growth"][0]), "tol": tol}
-    floors = {k: float(fx[f"floor_{k}"][0]) for k in ("x", "pivots", "lu_rows", "L_sketch", "U_sketch", "growth")
-              if f"floor_{k}" in fx}
+    floors = {k: max(float(fx.get(f"{tag}_{k}", [0.0])[0]) for tag in ("floor", "floor_alg", "floor_inv"))
+              for k in ("x", "pivots", "lu_rows", "L_sketch", "U_sketch", "growth")}
+    # rho = max|U| / max|product| is one entry of U: its error is bounded by U's
+    floors["growth"] = max(floors["growth"], floors["U_sketch"], floors["pivots"])
     print({k: f"{v:.3e}" for k, v in err.items()}, "reference rounding floor", {k: f"{v:.3e}" for k, v in floors.items()})
     for k in ("x", "pivots", "lu_rows", "L_sketch", "U_sketch", "growth"):
         bar = max(tol, FLOOR_FACTOR * floors.get(k, 0.0))
