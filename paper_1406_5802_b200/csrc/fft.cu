@@ -329,52 +329,153 @@ __global__ void __launch_bounds__(OLA_T) ola_spectra_kernel(const double* __rest
     for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) spec[static_cast<int64_t>(s) * OLA_NF + u] = z[u];
 }
 
-__global__ void __launch_bounds__(OLA_T) ola_rows_kernel(const double* __restrict__ a, int64_t lda, int64_t m, int k,
-                                                         int lc, int chunks, const cplx* __restrict__ spec,
-                                                         const cplx* __restrict__ tw, double* __restrict__ out,
-                                                         int64_t ldo, int l) {
+// smem slot of position p: XOR of the 16-byte slot's low three bits with bits
+// 3..5 of p, so the three access patterns (stride 128 / stride 8 / 8
+// consecutive per lane) all hit eight distinct slots per quarter warp
+__device__ __forceinline__ int ola_sw(int p) { return p ^ ((p >> 3) & 7); }
+
+// Two row pairs' chunk transforms per CTA would not fit the registers; one
+// row pair per CTA, 128 threads, three passes (radix 16, 16, 8) held in
+// registers between shared-memory exchanges, the accumulated spectrum in
+// registers (each thread owns the 16 frequency slots of its last-pass groups),
+// base twiddles cached per CTA.
+__global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
+                                                            int k, int lc, int chunks, const cplx* __restrict__ spec,
+                                                            const cplx* __restrict__ tw, double* __restrict__ out,
+                                                            int64_t ldo, int l) {
     __shared__ __align__(16) cplx z[OLA_NF];
-    constexpr int PER = OLA_NF / OLA_T;  // frequency slots per thread
+    __shared__ __align__(16) cplx tw1[4][128];  // w_2048^{t 2^j}
+    __shared__ __align__(16) cplx tw2[4][8];    // w_128^{n0 2^j}
+    const int t = threadIdx.x;
+    for (int i = t; i < 4 * 128; i += OLA_T) tw1[i >> 7][i & 127] = tw[((i & 127) << (i >> 7)) & (OLA_NF - 1)];
+    if (t < 32) tw2[t >> 3][t & 7] = tw[(((t & 7) << (t >> 3)) * 16) & (OLA_NF - 1)];
+    __syncthreads();
+    const int n2 = t & 7, o2 = (t >> 3) * 128;  // pass-2 group of this thread
     for (int64_t pair = blockIdx.x; 2 * pair < m; pair += gridDim.x) {
         const int64_t r0 = 2 * pair;
         const bool two = r0 + 1 < m;
         const double* a0 = a + r0 * lda;
-        const double* a1 = a + (r0 + 1) * lda;
-        cplx acc[PER];
+        const double* a1 = two ? a + (r0 + 1) * lda : a0;
+        cplx acc[2][8];
 #pragma unroll
-        for (int q = 0; q < PER; ++q) acc[q] = {0.0, 0.0};
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[g][q] = {0.0, 0.0};
         for (int s = 0; s < chunks; ++s) {
             const int t0 = s * lc;
-            for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) {
-                const int t = t0 + u;
-                const bool in = u < lc && t < k;
-                z[u] = {in ? __ldcs(a0 + t) : 0.0, (in && two) ? __ldcs(a1 + t) : 0.0};
+            cplx v[16];
+            // pass 1 (N = 2048, M = 128), inputs straight from global memory
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int u = t + 128 * j, idx = t0 + u;
+                const bool in = u < lc && idx < k;
+                v[j] = {in ? __ldcs(a0 + idx) : 0.0, (in && two) ? __ldcs(a1 + idx) : 0.0};
+            }
+            dft_reg<16, false>(v);
+            {
+                cplx w[16];
+                w[1] = tw1[0][t];
+                w[2] = tw1[1][t];
+                w[4] = tw1[2][t];
+                w[8] = tw1[3][t];
+                z[ola_sw(t)] = v[0];
+#pragma unroll
+                for (int r = 1; r < 16; ++r) {
+                    lazy_twiddle<16>(w, r);
+                    z[ola_sw(t + 128 * r)] = cmul(v[brev<16>(r)], w[r]);
+                }
             }
             __syncthreads();
-            forward_fft(z, OLA_NF, tw, OLA_NF);
+            // pass 2 (N = 128, M = 8)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = z[ola_sw(o2 + n2 + 8 * j)];
+            dft_reg<16, false>(v);
+            {
+                cplx w[16];
+                w[1] = tw2[0][n2];
+                w[2] = tw2[1][n2];
+                w[4] = tw2[2][n2];
+                w[8] = tw2[3][n2];
+                z[ola_sw(o2 + n2)] = v[0];
+#pragma unroll
+                for (int r = 1; r < 16; ++r) {
+                    lazy_twiddle<16>(w, r);
+                    z[ola_sw(o2 + n2 + 8 * r)] = cmul(v[brev<16>(r)], w[r]);
+                }
+            }
+            __syncthreads();
+            // pass 3 (N = 8, M = 1): positions 8g + r; accumulate conj(Z) H_s
             const cplx* hs = spec + static_cast<int64_t>(s) * OLA_NF;
 #pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int u = threadIdx.x + q * OLA_T;
-                const cplx zz = z[u], hh = hs[u];
-                // acc += conj(zz) * hh
-                acc[q].x = fma(zz.x, hh.x, fma(zz.y, hh.y, acc[q].x));
-                acc[q].y = fma(zz.x, hh.y, fma(-zz.y, hh.x, acc[q].y));
-            }
-            __syncthreads();
-        }
+            for (int gg = 0; gg < 2; ++gg) {
+                const int g = t + OLA_T * gg;
+                cplx u8[8];
 #pragma unroll
-        for (int q = 0; q < PER; ++q) z[threadIdx.x + q * OLA_T] = acc[q];
-        __syncthreads();
-        inverse_fft(z, OLA_NF, tw, OLA_NF, 1.0 / static_cast<double>(OLA_NF));
-        double* o0 = out + r0 * ldo;
-        double* o1 = out + (r0 + 1) * ldo;
-        for (int j = threadIdx.x; j < l; j += blockDim.x) {
-            const cplx v = z[l - 1 - j];
-            __stcs(o0 + j, v.x);
-            if (two) __stcs(o1 + j, -v.y);
+                for (int j = 0; j < 8; ++j) u8[j] = z[ola_sw(8 * g + j)];
+                dft_reg<8, false>(u8);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const cplx zz = u8[brev<8>(r)], hh = hs[8 * g + r];
+                    acc[gg][r].x = fma(zz.x, hh.x, fma(zz.y, hh.y, acc[gg][r].x));
+                    acc[gg][r].y = fma(zz.x, hh.y, fma(-zz.y, hh.x, acc[gg][r].y));
+                }
+            }
+            __syncthreads();  // z is rewritten by the next chunk's pass 1
+        }
+        // inverse: DIT passes in reverse, the first from the registers
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+            const int g = t + OLA_T * gg;
+            dft_reg<8, true>(acc[gg]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) z[ola_sw(8 * g + j)] = acc[gg][brev<8>(j)];
         }
         __syncthreads();
+        {
+            cplx v[16], w[16];
+            w[1] = tw2[0][n2];
+            w[2] = tw2[1][n2];
+            w[4] = tw2[2][n2];
+            w[8] = tw2[3][n2];
+            v[0] = z[ola_sw(o2 + n2)];
+#pragma unroll
+            for (int r = 1; r < 16; ++r) {
+                lazy_twiddle<16>(w, r);
+                v[r] = cmulc(z[ola_sw(o2 + n2 + 8 * r)], w[r]);
+            }
+            dft_reg<16, true>(v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) z[ola_sw(o2 + n2 + 8 * j)] = v[brev<16>(j)];
+        }
+        __syncthreads();
+        {
+            // last pass (N = 2048, M = 128): outputs t + 128 j; only lags < l are kept
+            cplx v[16], w[16];
+            w[1] = tw1[0][t];
+            w[2] = tw1[1][t];
+            w[4] = tw1[2][t];
+            w[8] = tw1[3][t];
+            v[0] = z[ola_sw(t)];
+#pragma unroll
+            for (int r = 1; r < 16; ++r) {
+                lazy_twiddle<16>(w, r);
+                v[r] = cmulc(z[ola_sw(t + 128 * r)], w[r]);
+            }
+            dft_reg<16, true>(v);
+            const double scale = 1.0 / static_cast<double>(OLA_NF);
+            double* o0 = out + r0 * ldo;
+            double* o1 = out + (r0 + 1) * ldo;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int lag = t + 128 * j;
+                if (lag < l) {
+                    const cplx rv = v[brev<16>(j)];
+                    __stcs(o0 + (l - 1 - lag), rv.x * scale);
+                    if (two) __stcs(o1 + (l - 1 - lag), -rv.y * scale);
+                }
+            }
+        }
+        __syncthreads();  // z is reused by the next row pair
     }
 }
 
@@ -960,7 +1061,7 @@ rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a,
         ola_spectra_kernel<<<chunks, OLA_T, 0, ctx->stream>>>(c, n, lc, static_cast<int>(l), tw_f, ospec);
         RL_CHECK_LAUNCH("ola_spectra_kernel");
         const int64_t pairs = (m + 1) / 2;
-        const int64_t grid = std::min<int64_t>(pairs, static_cast<int64_t>(ctx->num_sms) * 8);
+        const int64_t grid = std::min<int64_t>(pairs, static_cast<int64_t>(ctx->num_sms) * 3);
         ola_rows_kernel<<<static_cast<unsigned>(grid), OLA_T, 0, ctx->stream>>>(
             a, lda, m, static_cast<int>(k), lc, chunks, ospec, tw_f, out, ldo, static_cast<int>(l));
         RL_CHECK_LAUNCH("ola_rows_kernel");

@@ -25,6 +25,7 @@ Usage: python tests/golden/make_fullsize.py [headline cfg3 cfg4 cfg5]
        python tests/golden/make_fullsize.py floor [headline cfg3]   (adds the rounding floors)
        python tests/golden/make_fullsize.py floor_alg [headline cfg3]   (adds the algorithm floors)
        python tests/golden/make_fullsize.py floor_inv [headline cfg3]   (... with the inverse-based U12)
+       python tests/golden/make_fullsize.py floor_lowrank [cfg4 cfg5]   (the range finder's floors)
 """
 import ctypes
 import os
@@ -264,6 +265,45 @@ def rounding_floor(name):
     np.savez(os.path.join(HERE, f"fullsize_{name}.npz"), **fx)
 
 
+def lowrank_floor(cfg):
+    """The range finder's own rounding floor: the sketch formed in another,
+    equally valid order -- config 4's A H as eight K-slab products, config 5's
+    Toeplitz product as A times the dense Toeplitz block instead of the FFT --
+    then the same restated QR and residual; the relative change of ||R||_F,
+    of the power-iteration ||R||_2 and of Q against the fixture."""
+    fx = dict(np.load(os.path.join(HERE, f"fullsize_{cfg}.npz")))
+    config_inputs.build(cfg, WORK)
+    inp = config_inputs.load(cfg, WORK, mmap=False)
+    a = inp["A"]
+    m, n = a.shape
+    prm = config_inputs.CONFIGS[cfg]
+    l = prm["r"]
+    blas_threads(8)
+    if cfg == "cfg4":
+        h = R.gen_gaussian(n, l, prm["h_seed"])
+        y = np.zeros((m, l))
+        for k0 in range(0, n, 1024):
+            y += a[:, k0:k0 + 1024] @ h[k0:k0 + 1024]
+    else:
+        c = inp["c"]
+        idx = (np.arange(n)[:, None] - np.arange(l)[None, :]) % n
+        y = a @ c[idx]  # the dense Toeplitz block (circulant.hpp:143-169)
+    blas_threads(1)
+    q, bad, _, _ = positive_qr_q(y)
+    assert bad == 0
+    res = a - R.matmul(q, R.matmul(np.ascontiguousarray(q.T), a))
+    fro = np.linalg.norm(res)
+    est = R.spectral_norm_estimate(res)
+    wl = R.gen_gaussian(l, W_COLS, W_SEED)
+    floor = {"fro": abs(fro / fx["residual_frobenius"][0] - 1),
+             "spec": abs(est / fx["residual_spectral_estimate"][0] - 1),
+             "q": float(np.linalg.norm(q @ wl - fx["qw"]) / np.linalg.norm(fx["qw"]))}
+    log(cfg, "lowrank floor", floor)
+    for k, v in floor.items():
+        fx[f"floor_{k}"] = np.array([v])
+    np.savez(os.path.join(HERE, f"fullsize_{cfg}.npz"), **fx)
+
+
 def blocked_genp(p, nb=128, explicit_inverse=False):
     """GENP (no pivoting) of p as a right-looking blocked factorisation with
     BLAS updates: unblocked 128-column panels, U12 = L11^-1 A12, A22 -= L21 U12
@@ -331,6 +371,10 @@ def algorithm_floor(name, explicit_inverse=False):
 
 
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["floor_lowrank"]:
+        for w in sys.argv[2:] or ["cfg4", "cfg5"]:
+            lowrank_floor(w)
+        sys.exit(0)
     if sys.argv[1:2] in (["floor_alg"], ["floor_inv"]):
         for w in sys.argv[2:] or ["headline", "cfg3"]:
             algorithm_floor(w, explicit_inverse=sys.argv[1] == "floor_inv")

@@ -139,12 +139,16 @@ def test_config3_circulant_n8192_vs_reference(cuda, workdir):
     assert 0.5 * h0 <= out.residual_history[0] <= 2.0 * h0, (out.residual_history, h0)
 
 
-# measured relative disagreement floors of the low-rank residual norms (GPU
-# CholeskyQR2 / split-K GEMMs vs the reference's Householder QR / GEMM on
-# identical inputs); the north star's 1e-9 applies where the
-# floor is below it
-LOWRANK_BAR = {"cfg4": {"fro": 1e-9, "spec": 1e-9, "q": 1e-9},
-               "cfg5": {"fro": 1e-9, "spec": 1e-9, "q": 1e-9}}
+# low-rank bars: the north star's 1e-9 relative, or -- where the reference
+# itself moves more than that when its sketch is formed in another valid order
+# (floor_fro / floor_spec / floor_q, tests/golden/make_fullsize.py
+# lowrank_floor: config 5's FFT sketch against the dense Toeplitz product moves
+# ||R||_F by 2.3e-9) -- twice that floor
+LOWRANK_FLOOR_FACTOR = 2.0
+
+
+def lowrank_bar(fx, key):
+    return max(1e-9, LOWRANK_FLOOR_FACTOR * float(fx.get(f"floor_{key}", [0.0])[0]))
 
 
 def run_lowrank(torch, cfg, workdir):
@@ -175,12 +179,13 @@ def run_lowrank(torch, cfg, workdir):
     again = rl.residual_norms(a, res)
     assert again["residual_frobenius"] == pytest.approx(res.info["residual_frobenius"], rel=1e-12)
     print(cfg, {k: f"{v:.3e}" for k, v in err.items()})
-    bar = LOWRANK_BAR[cfg]
-    assert err["q"] <= bar["q"] and err["q_rows"] <= bar["q"], err
-    assert err["fro"] <= bar["fro"], err
-    assert err["spec_vs_estimate"] <= bar["spec"], err
+    bar = {k: lowrank_bar(fx, k) for k in ("q", "fro", "spec")}
+    print(cfg, "bars", bar)
+    assert err["q"] <= bar["q"] and err["q_rows"] <= bar["q"], (err, bar)
+    assert err["fro"] <= bar["fro"], (err, bar)
+    assert err["spec_vs_estimate"] <= bar["spec"], (err, bar)
     if "spec_vs_svd" in err:
-        assert err["spec_vs_svd"] <= bar["spec"], err
+        assert err["spec_vs_svd"] <= bar["spec"], (err, bar)
     return err
 
 
