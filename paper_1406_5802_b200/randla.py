@@ -325,6 +325,24 @@ def matmul(a, b):
     return c
 
 
+def svd_values(a):
+    """svd_values (svd.hpp:76-88): the min(m, n) singular values, non-increasing,
+    by the device's one-sided Jacobi (small matrices: one CTA)."""
+    device = _is_device(a)
+    a = _dev(a) if device else _host(a)
+    m, n = a.shape
+    out = np.empty(min(m, n))
+    if device:
+        a = a.cpu().numpy()
+    _raise(capi.lib().rl_singular_values(_ctx(), capi.RL_HOST, m, n, capi.addr(_host(a)), capi.addr(out)))
+    return out
+
+
+def spectral_norm(a):
+    """spectral_norm (norms.hpp:11-14) = svd_values(a)[0]"""
+    return float(svd_values(a)[0])
+
+
 def spectral_norm_estimate(a):
     """spectral_norm_estimate (norms.hpp:35-78), evaluated on the GPU in the
     reference's summation order (bit-identical for a given matrix)."""
@@ -925,6 +943,15 @@ def range_find(a, r, p, spec, power_steps=0, with_residual=True):
     if not with_residual:
         d = {"rank_deficient_column": d["rank_deficient_column"]}
     return LowRankResult(q, r, p, power_steps, d)
+
+
+def basis_residual(result, truth_left):
+    """basis_residual (lowrank.hpp:88-93): ||Q (Q^H S_r) - S_r||_2 for the
+    leading left singular basis S_r, products and norm on the GPU."""
+    q = result.q
+    y = matmul(np.ascontiguousarray(np.asarray(q).T) if isinstance(q, np.ndarray) else q.T.contiguous(), truth_left)
+    d = matmul(q, y) - truth_left
+    return spectral_norm(d)
 
 
 def residual_norms(a, result):

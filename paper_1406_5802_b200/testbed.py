@@ -1,19 +1,31 @@
-"""Trial engine for the paper's preprocessed-GENP experiments on the B200 path
-(SURVEY.md §8(f), rank 2): the reference's testbed (testbed/experiment.hpp,
-testbed/presets.hpp, testbed/inputs.hpp) restated over this package's
-device-backed API, so the Monte-Carlo tables run their solves on the GPU.
+"""Trial engine for the paper's experiments on the B200 path (SURVEY.md §8(f),
+rank 2): the reference's testbed (testbed/experiment.hpp, testbed/presets.hpp,
+testbed/inputs.hpp) restated over this package's device-backed API, so the
+Monte-Carlo tables run their solves and sketches on the GPU.
 
     run_experiment            experiment.hpp:30-69 (per-trial derived seeds,
-                              failed trials counted, order-independent report)
+                              failed trials counted, order-independent report;
+                              trials run concurrently on a worker pool as the
+                              reference's parallel_for_index does -- each
+                              worker thread gets its own device context and
+                              stream, so small trials overlap on the GPU)
     summarize                 stats.hpp:19-34
     gen_hard_block            inputs.hpp:18-49 (orthonormal_basis = CholeskyQR2,
                               which yields the same positive-diagonal Q as the
                               reference's Householder QR up to rounding)
+    gen_lownumrank            inputs.hpp:67-83
+    error_bounds_from_parts   lowrank.hpp:132-170 (the bound columns)
     run_hardblock_preprocessed  presets.hpp:90-119
-    PRESETS                   table3 (Gaussian) and table4 (real circulant)
-                              with the reference's checks (presets.hpp:219-240)
+    run_lowrank_preset        presets.hpp:121-179
+    PRESETS                   table2 (GEPP baseline), table3 (Gaussian),
+                              table4 (real circulant), table6 / table7
+                              (Gaussian sketch: rn1 / rn2), table8 / table10
+                              (real Toeplitz sketch: rn2 / rn1), table13
+                              (inverse-norm ratio), with the reference's checks
+                              (presets.hpp:194-420)
 
-Complex families (table5, table5a) are outside this path.
+Out of this path: the complex families (table5, table5a, table9, table11,
+table14) and the a-posteriori estimator (table12).
 """
 from __future__ import annotations
 
@@ -24,6 +36,10 @@ from typing import Callable, List, Optional
 import numpy as np
 
 from . import randla as rl
+
+
+# concurrent trial workers (each its own per-thread device context / stream)
+WORKERS = 8
 
 
 @dataclass
@@ -85,12 +101,22 @@ def run_experiment(label: str, trials: int, seed: int, metric_names: List[str],
     if trials < 1:
         raise rl.DimensionError("run_experiment: trials must be >= 1")
     key = rl.hash_label(label)
-    slots = []
-    for t in range(trials):
+    slots = [None] * trials
+
+    def one(t):
         try:
-            slots.append(run_trial(rl.derive_seed(seed, key, t), t))
+            slots[t] = run_trial(rl.derive_seed(seed, key, t), t)
         except rl.RandlaError:  # the reference catches std::runtime_error (types.hpp errors)
-            slots.append(None)
+            slots[t] = None
+
+    workers = min(trials, WORKERS)
+    if workers <= 1:
+        for t in range(trials):
+            one(t)
+    else:  # parallel_for_index (parallel.hpp:14-35): results land in per-trial slots
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            list(ex.map(one, range(trials)))
     rep = ExperimentReport(label=label, trials=trials, seed=seed, multiplier=multiplier, refine_steps=refine_steps,
                            dimension=dimension)
     cols = [[] for _ in metric_names]
@@ -165,6 +191,126 @@ def run_hardblock_preprocessed(label: str, post_kind: rl.MultiplierKind, seed: i
     return out
 
 
+def lowrank_dims(full: bool) -> List[int]:
+    """presets.hpp:39-41"""
+    return [64, 128, 256, 512] if full else [64, 128]
+
+
+def format_multiplier_token(spec) -> str:
+    """multipliers.hpp:222-236"""
+    k = rl.MultiplierKind(spec.kind)
+    if k == rl.MultiplierKind.TOEPLITZ_BLOCK:
+        return "toeplitz:variant=real" if spec.variant == rl.ToeplitzVariant.REAL else "toeplitz:variant=unitary"
+    if k == rl.MultiplierKind.FINITE_SET_UNIFORM:
+        return f"finite:card={spec.set_cardinality}"
+    return {rl.MultiplierKind.NONE: "none", rl.MultiplierKind.GAUSSIAN: "gaussian",
+            rl.MultiplierKind.REAL_CIRCULANT: "circulant", rl.MultiplierKind.UNITARY_CIRCULANT: "unitary-circulant",
+            rl.MultiplierKind.SRFT: "srft", rl.MultiplierKind.CIRC_SKEW_PRODUCT: "circskew",
+            rl.MultiplierKind.GAUSSIAN_CIRCULANT: "gaussian-circulant"}.get(k, "none")
+
+
+@dataclass
+class LowRankInstance:
+    """inputs.hpp:60-65: the matrix and its construction's truncated factors"""
+    a: np.ndarray
+    left: np.ndarray      # truth.left (n x r)
+    singulars: np.ndarray  # all n sigma_j
+    right: np.ndarray     # truth.right (n x r)
+
+
+def gen_lownumrank(n: int, r: int, seed: int) -> LowRankInstance:
+    """inputs.hpp:67-83: sigma_j = 1/(j+1) up to r, 1e-10 beyond, between the
+    orthonormal bases of two seeded Gaussians (CholeskyQR2 on the GPU)."""
+    if r < 1 or r >= n:
+        raise rl.DimensionError("gen_lownumrank: need 1 <= r < n")
+    s = np.array(rl.orthonormal_basis(rl.gen_gaussian(n, n, rl.derive_seed(seed, 1))))
+    t = np.array(rl.orthonormal_basis(rl.gen_gaussian(n, n, rl.derive_seed(seed, 2))))
+    sigma = np.array([1.0 / (j + 1) if j < r else 1e-10 for j in range(n)])
+    a = np.array(rl.matmul(s * sigma, np.ascontiguousarray(t.T)))
+    return LowRankInstance(a, np.ascontiguousarray(s[:, :r]), sigma, np.ascontiguousarray(t[:, :r]))
+
+
+@dataclass
+class BoundReport:
+    delta_plus: float = 0.0
+    delta_plus_prime: float = 0.0
+    sigma_r: float = 0.0
+    sigma_r1: float = 0.0
+    h_frobenius: float = 0.0
+    t_h_inv_norm: float = 0.0
+
+
+def error_bounds_from_parts(t_r, singulars, h, r) -> BoundReport:
+    """lowrank.hpp:132-170 (the deterministic part): delta_plus =
+    sqrt(2) ||H||_F ||(T_r^H H)^+|| sigma_{r+1} / sigma_r, delta_plus_prime =
+    sigma_{r+1} + 2 delta_plus ||A||; T_r^H H and its singular values on the GPU."""
+    if r < 1 or r > len(singulars):
+        raise rl.DimensionError("error_bounds: rank out of range")
+    rep = BoundReport(sigma_r=float(singulars[r - 1]), sigma_r1=float(singulars[r]) if r < len(singulars) else 0.0,
+                      h_frobenius=float(np.linalg.norm(h)))
+    gsv = rl.svd_values(rl.matmul(np.ascontiguousarray(t_r.T), h))
+    if not gsv[-1] > 0.0:
+        raise rl.SingularMatrixError("unlucky multiplier: T_r^H H is singular, the bound is undefined")
+    rep.t_h_inv_norm = 1.0 / gsv[-1]
+    rep.delta_plus = math.sqrt(2.0) * rep.h_frobenius * rep.t_h_inv_norm * rep.sigma_r1 / rep.sigma_r
+    rep.delta_plus_prime = rep.sigma_r1 + 2.0 * rep.delta_plus * float(singulars[0])
+    return rep
+
+
+def run_lowrank_preset(label: str, spec_base, basis_metric: bool, seed: int, trials: int, full: bool,
+                       r: int = 8, dims: Optional[List[int]] = None) -> List[ExperimentReport]:
+    """presets.hpp:121-179: zero-oversampling range finder on the known-rank
+    inputs; rn1 (basis) or rn2 (approximation) and its ratio to the bound."""
+    import copy
+    out = []
+    for n in (dims if dims is not None else lowrank_dims(full)):
+        def trial(ts, _t, n=n):
+            inst = gen_lownumrank(n, r, rl.derive_seed(ts, 1))
+            spec = copy.copy(spec_base)
+            spec.seed = rl.derive_seed(ts, 2)
+            spec.rows, spec.cols = n, r
+            result = rl.range_find(inst.a, r, 0, spec, 0, with_residual=False)
+            rep = error_bounds_from_parts(inst.right, inst.singulars, rl.materialize(spec), r)
+            if basis_metric:
+                rn, bound = rl.basis_residual(result, inst.left), rep.delta_plus
+            else:
+                rn, bound = rl.approximation_residual(inst.a, result), rep.delta_plus_prime
+            return [rn, rn / bound]
+
+        names = ["rn1", "ratio_rn1"] if basis_metric else ["rn2", "ratio_rn2"]
+        out.append(run_experiment(f"{label}/n={n}", trials, seed, names, trial, format_multiplier_token(spec_base),
+                                  0, n))
+    return out
+
+
+def run_gepp_baseline(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
+    """presets.hpp:201-217 (table2): pivoted elimination on the hard-block inputs"""
+    out = []
+    for n in (dims if dims is not None else solve_dims(full)):
+        def trial(ts, _t, n=n):
+            a = gen_hard_block(n, rl.derive_seed(ts, 1))
+            b = rl.gen_gaussian_vector(n, rl.derive_seed(ts, 2))
+            x = rl.lu_solve(rl.gepp_factor(a), b)  # solve_gepp (lu.hpp:150-153)
+            return [float(np.linalg.norm(a @ x - b) / np.linalg.norm(b))]  # relative_residual (lu.hpp:155-161)
+        out.append(run_experiment(f"table2/n={n}", trials, seed, ["residual"], trial, "none", 0, n))
+    return out
+
+
+def run_inverse_norm_ratio(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
+    """presets.hpp:379-406 (table13): ||(T_r^T H)^+|| against ||(H_rr)^+||"""
+    out = []
+    for n in (dims if dims is not None else lowrank_dims(full)):
+        def trial(ts, _t, n=n):
+            r = 8
+            inst = gen_lownumrank(n, r, rl.derive_seed(ts, 1))
+            h = rl.gen_gaussian(n, r, rl.derive_seed(ts, 2))
+            num = 1.0 / rl.svd_values(rl.matmul(np.ascontiguousarray(inst.right.T), h))[-1]
+            den = 1.0 / rl.svd_values(np.ascontiguousarray(h[:r, :r]))[-1]
+            return [num / den]
+        out.append(run_experiment(f"table13/n={n}", trials, seed, ["inv_norm_ratio"], trial, "gaussian", 0, n))
+    return out
+
+
 @dataclass
 class CheckResult:
     description: str
@@ -191,7 +337,25 @@ def check_stat(reports, dim, column, use_max, threshold) -> CheckResult:
     return c
 
 
+def check_fraction(reports, dim, column, threshold, quota) -> CheckResult:
+    """presets.hpp:74-86: value <= threshold in >= quota of the trials (failed
+    trials count against the quota)"""
+    c = CheckResult(f"{column} <= {threshold:.3g} in >= {100 * quota:.3g}% of trials at n={dim}")
+    r = _report_at(reports, dim)
+    if r is None:
+        return c
+    hits = sum(1 for v in r.column(column).values if v <= threshold)
+    c.passed = hits / r.trials >= quota
+    return c
+
+
+_G = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN)
+_TR = rl.MultiplierSpec(rl.MultiplierKind.TOEPLITZ_BLOCK, variant=rl.ToeplitzVariant.REAL)
+
 PRESETS = {
+    # presets.hpp:201-217
+    "table2": (lambda seed, trials, full, dims=None: run_gepp_baseline(seed, trials, full, dims),
+               lambda rs: [check_stat(rs, 64, "residual", False, 1e-11)]),
     # presets.hpp:219-233
     "table3": (lambda seed, trials, full, dims=None: run_hardblock_preprocessed(
                    "table3", rl.MultiplierKind.GAUSSIAN, seed, trials, full, 1, dims),
@@ -203,6 +367,26 @@ PRESETS = {
     "table4": (lambda seed, trials, full, dims=None: run_hardblock_preprocessed(
                    "table4", rl.MultiplierKind.REAL_CIRCULANT, seed, trials, full, 1, dims),
                lambda rs: [check_stat(rs, 64, "residual_iter0", False, 1e-8)]),
+    # presets.hpp:293-300
+    "table6": (lambda seed, trials, full, dims=None: run_lowrank_preset("table6", _G, True, seed, trials, full,
+                                                                         dims=dims),
+               lambda rs: [check_fraction(rs, 64, "ratio_rn1", 1.01, 0.99)]),
+    # presets.hpp:302-311
+    "table7": (lambda seed, trials, full, dims=None: run_lowrank_preset("table7", _G, False, seed, trials, full,
+                                                                         dims=dims),
+               lambda rs: [check_stat(rs, 64, "rn2", False, 1e-6), check_stat(rs, 64, "ratio_rn2", False, 0.1),
+                           check_fraction(rs, 64, "ratio_rn2", 1.0, 0.99)]),
+    # presets.hpp:313-320
+    "table8": (lambda seed, trials, full, dims=None: run_lowrank_preset("table8", _TR, False, seed, trials, full,
+                                                                         dims=dims),
+               lambda rs: [check_stat(rs, 64, "rn2", False, 1e-6), check_fraction(rs, 64, "ratio_rn2", 1.0, 0.99)]),
+    # presets.hpp:324-333
+    "table10": (lambda seed, trials, full, dims=None: run_lowrank_preset("table10", _TR, True, seed, trials, full,
+                                                                          dims=dims),
+                lambda rs: [check_fraction(rs, 64, "ratio_rn1", 1.01, 0.99)]),
+    # presets.hpp:379-406 (no checks in the reference)
+    "table13": (lambda seed, trials, full, dims=None: run_inverse_norm_ratio(seed, trials, full, dims),
+                lambda rs: []),
 }
 
 

@@ -56,3 +56,42 @@ def test_table3_and_table4_presets_pass_reference_checks(cuda, orc):
     ref = orc.C.preprocess_solve(a, b, 1, g, refine=1)
     dev = rep[0].column("residual_iter0").values[0], rep[0].column("residual_iter1").values[0]
     assert 0.1 < dev[0] / ref["history"][0] < 10 and dev[1] < 1e-12 and ref["history"][1] < 1e-12
+
+
+def test_gepp_baseline_and_lowrank_presets_pass_reference_checks(cuda):
+    """table2 (GEPP baseline), table6 / table7 (Gaussian sketch), table8 /
+    table10 (real Toeplitz sketch), table13 with the reference's checks
+    (presets.hpp:201-406), trials running concurrently on the worker pool"""
+    for name, trials in (("table2", 8), ("table6", 100), ("table7", 100), ("table8", 100), ("table10", 100),
+                         ("table13", 8)):
+        reports, checks = testbed.run_preset(name, 7, trials, dims=[64])
+        assert all(c.passed for c in checks), (name, [(c.description, c.passed) for c in checks])
+        assert all(r.failures == 0 for r in reports), name
+        assert reports[0].trials == trials
+
+
+def test_concurrent_trials_equal_sequential(cuda):
+    """order- and concurrency-independent reports (experiment.hpp:13-17)"""
+    w = testbed.WORKERS
+    try:
+        testbed.WORKERS = 1
+        seq, _ = testbed.run_preset("table7", 3, 12, dims=[64])
+        testbed.WORKERS = 6
+        par, _ = testbed.run_preset("table7", 3, 12, dims=[64])
+    finally:
+        testbed.WORKERS = w
+    assert seq[0].column("rn2").values == par[0].column("rn2").values
+
+
+def test_lowrank_bounds_vs_reference_formula(cuda, orc):
+    """error_bounds_from_parts (lowrank.hpp:132-170) against numpy on the same parts"""
+    inst = testbed.gen_lownumrank(64, 8, 5)
+    h = rl.gen_gaussian(64, 8, 6)
+    rep = testbed.error_bounds_from_parts(inst.right, inst.singulars, h, 8)
+    gsv = np.linalg.svd(inst.right.T @ h, compute_uv=False)
+    dp = np.sqrt(2) * np.linalg.norm(h) / gsv[-1] * inst.singulars[8] / inst.singulars[7]
+    assert rep.delta_plus == pytest.approx(dp, rel=1e-10)
+    assert rep.delta_plus_prime == pytest.approx(inst.singulars[8] + 2 * dp * inst.singulars[0], rel=1e-10)
+    # the instance: sigma_j = 1/(j+1) up to r, 1e-10 beyond, between orthonormal factors
+    s = np.linalg.svd(inst.a, compute_uv=False)
+    assert np.allclose(s[:8], 1.0 / np.arange(1, 9), rtol=1e-12) and np.allclose(s[8:], 1e-10, rtol=1e-4)
