@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <vector>
 
 #include "runtime.cuh"
@@ -84,7 +85,13 @@ struct GaussJob {
     int64_t nb1 = 0;                    // gen runs as blocks [0, nb1) then [nb1, nb)
     cudaEvent_t ev1 = nullptr, ev2 = nullptr;  // after each half (with its hard-case count)
     rl_status begin(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld);
-    rl_status finish(int64_t* hard_cases);
+    // first_rows_ready (optional) runs once rows [0, k) of the output are final
+    // in stream order on ctx->stream (the first half's undecided attempts
+    // scattered), while the host still finishes the second half's: work it
+    // enqueues on ctx->stream that reads only those rows overlaps that host
+    // work. The second half is then scattered on a side stream that
+    // ctx->stream waits for.
+    rl_status finish(int64_t* hard_cases, const std::function<rl_status(int64_t)>& first_rows_ready = nullptr);
     ~GaussJob();
 };
 rl_status gen_gaussian_device(rl_context* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out, int64_t ld,

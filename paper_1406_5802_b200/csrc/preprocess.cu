@@ -153,6 +153,14 @@ struct Dense {
     int a_chunks = 0;
     int64_t a_chunk_rows = 0;
     cudaEvent_t* a_ready = nullptr;
+    // A G split at K = k_split (a multiple of the GEMM's k-tile): columns
+    // [0, k_split) of A times rows [0, k_split) of G first, then the rest
+    // accumulated. A DMMA tile accumulates its k-steps in order in FP64 and C
+    // round-trips exactly, so the sum is the unsplit product bit for bit. Used
+    // when a seeded G is generated on the device: its first rows are final
+    // while the host still finishes the rest (GaussJob::finish).
+    int64_t k_split = 0;
+    int part1_blocks = 0;  // row blocks whose first K-part is already enqueued
 };
 
 // P = A G (or A), blocked GENP in place, growth, verdict (lu.hpp:44-49).
@@ -187,7 +195,13 @@ rl_status form_product(rl_context* ctx, Dense& D, double* P, GemmStats* stats) {
         const double* Ac = D.A + r0 * D.ld;
         double* Tc = T + r0 * D.ld;
         rl_status st = RL_OK;
-        if (D.post == POST_DENSE) {
+        if (D.post == POST_DENSE && D.k_split > 0) {
+            const int64_t k1 = D.k_split;
+            if (!(c < D.part1_blocks && Tc == D.P + r0 * D.ld))
+                st = gemm(ctx, rc, n, k1, Ac, D.ld, D.G, D.ld, Tc, D.ld, 1.0, false, nullptr);
+            if (st == RL_OK)
+                st = gemm(ctx, rc, n, n - k1, Ac + k1, D.ld, D.G + k1 * D.ld, D.ld, Tc, D.ld, 1.0, true, ah_stats);
+        } else if (D.post == POST_DENSE) {
             st = gemm(ctx, rc, n, n, Ac, D.ld, D.G, D.ld, Tc, D.ld, 1.0, false, ah_stats);
         } else if (D.post == POST_CIRC) {
             // matmul_by_circulant (circulant.hpp:171-185), SideMultiplier::right_multiply (preprocess.hpp:65-73)
@@ -219,6 +233,25 @@ rl_status form_product(rl_context* ctx, Dense& D, double* P, GemmStats* stats) {
         matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(P, D.ld, n, false, stats);
         RL_CHECK_LAUNCH("matrix_stats_kernel");
     }
+    return RL_OK;
+}
+
+// the first K-part of P = A G (columns [0, k_split) of A, rows of G already
+// final) for the row blocks [0, blocks) already uploaded; form_product adds
+// the rest
+rl_status form_product_part1(rl_context* ctx, Dense& D, int blocks) {
+    const int64_t n = D.n;
+    const int chunks = D.a_chunks > 0 ? std::min(blocks, D.a_chunks) : 1;
+    const int64_t rows = D.a_chunks > 0 ? D.a_chunk_rows : n;
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t r0 = c * rows, rc = std::min(rows, n - r0);
+        if (rc <= 0) break;
+        if (D.a_chunks > 0) RL_CUDA(cudaStreamWaitEvent(ctx->stream, D.a_ready[c], 0));
+        const rl_status st = gemm(ctx, rc, n, D.k_split, D.A + r0 * D.ld, D.ld, D.G, D.ld, D.P + r0 * D.ld, D.ld, 1.0,
+                                  false, nullptr);
+        if (st != RL_OK) return st;
+    }
+    D.part1_blocks = chunks;
     return RL_OK;
 }
 
@@ -470,7 +503,10 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
     // host A is uploaded in row blocks on the side stream, which waits only for
     // this stream's earlier work (workspace reuse) — not for the generator
     // kernels enqueued next, so block 0 lands under them
-    constexpr int kChunks = 4;
+#ifndef RL_A_CHUNKS
+#define RL_A_CHUNKS 8
+#endif
+    constexpr int kChunks = RL_A_CHUNKS;  // row blocks of a host A (the first is exposed before the product)
     const bool pipelined_a = own_a && host && n >= 1024 && side_resources(ctx, kChunks) == RL_OK;
     // pageable host A (the C++ drop-in's RealMatrix, a numpy array): copied
     // into the context's grow-only pinned staging by all host cores first
@@ -500,6 +536,9 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         RL_CUDA(cudaEventRecord(start, s));
         RL_CUDA(cudaStreamWaitEvent(ctx->hi_stream, start, 0));
     }
+    // b first: a small copy on the main stream must not queue behind the
+    // side stream's row blocks of A on the copy engine
+    RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
     GaussJob gjob;
     const bool gen_g = kind == RL_MULT_GAUSSIAN && !post->dense;
     if (gen_g && (st = gjob.begin(ctx, n, n, post->seed, D.G, ld)) != RL_OK) return st;
@@ -558,14 +597,22 @@ extern "C" RL_API rl_status rl_preprocessed_genp_solve(rl_context* ctx, rl_mem m
         } else if (post->dense) {
             if ((st = copy_in(ctx, D.G, ld, post->dense, n, n, host)) != RL_OK) return st;
         } else if (gen_g) {
-            // materialize(spec) = gen_gaussian(n, n, seed) (multipliers.hpp:191-192)
-            if ((st = gjob.finish(nullptr)) != RL_OK) return st;
+            // materialize(spec) = gen_gaussian(n, n, seed) (multipliers.hpp:191-192).
+            // Once G's first rows are final, the first K-part of A G starts
+            // under the host's work on the rest of G
+            // (for the row blocks of A already issued: the rest of A follows
+            // G's last values on the copy engine, as below)
+            auto first_rows = [&](int64_t rows1) -> rl_status {
+                const int64_t k1 = rows1 / 16 * 16;
+                if (k1 < 512 || D.pre != POST_NONE) return RL_OK;
+                D.k_split = k1;
+                return form_product_part1(ctx, D, D.a_chunks > 0 ? a_issued : 1);
+            };
+            if ((st = gjob.finish(nullptr, first_rows)) != RL_OK) return st;
         } else if ((st = materialize_device(ctx, post, n, n, host, D.G, ld)) != RL_OK) {
             return st;  // FiniteSetUniform, CircSkewProduct (multipliers.hpp:195-200)
         }
     }
-    // b before the remaining blocks of A (the stream s work must not queue behind them)
-    RL_CUDA(cudaMemcpyAsync(D.b, b, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
     for (; a_issued > 0 && a_issued < D.a_chunks; ++a_issued)
         if ((st = upload_a_block(a_issued)) != RL_OK) return st;
     StageTimer timer(s);

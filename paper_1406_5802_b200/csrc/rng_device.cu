@@ -316,6 +316,7 @@ rl_status GaussJob::begin(rl_context* c, int64_t r, int64_t cl, uint64_t sd, dou
     // in two halves so the host can finish the first half's undecided
     // attempts while the second half generates.
     RL_CUDA(cudaMemcpyAsync(ctx->host_scalars + 0, offsets + nb, 8, cudaMemcpyDeviceToHost, s));
+    RL_CUDA(cudaMemcpyAsync(ctx->host_scalars + 3, offsets + nb / 2, 8, cudaMemcpyDeviceToHost, s));
     RL_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
     RL_CUDA(cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming));
     nb1 = nb / 2;
@@ -336,7 +337,7 @@ rl_status GaussJob::begin(rl_context* c, int64_t r, int64_t cl, uint64_t sd, dou
 
 // Phase 2: wait for the counts, finish the undecided attempts with glibc on
 // the host and scatter them (synchronises the context stream).
-rl_status GaussJob::finish(int64_t* hard_cases) {
+rl_status GaussJob::finish(int64_t* hard_cases, const std::function<rl_status(int64_t)>& first_rows_ready) {
     if (count <= 0) return RL_OK;
     cudaStream_t s = ctx->stream;
     const int64_t pairs = (count + 1) / 2;
@@ -357,7 +358,7 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
             }
         }
     } ds_guard{&ds};
-    auto resolve = [&](int64_t lo, int64_t hi, cudaStream_t down) -> rl_status {
+    auto resolve = [&](int64_t lo, int64_t hi, cudaStream_t down, cudaStream_t up) -> rl_status {
         const int64_t nh = hi - lo;
         if (nh <= 0) return RL_OK;
         constexpr int kMaxChunks = 4;
@@ -381,9 +382,9 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
             const int64_t o = lo + c * cs, k = std::min(cs, hi - o);
             RL_CUDA(cudaEventSynchronize(ev[c]));
             host_polar_pairs(seed, att + o, k, hv + 2 * o);
-            RL_CUDA(cudaMemcpyAsync(vals + 2 * o, hv + 2 * o, 16 * k, cudaMemcpyHostToDevice, s));
-            scatter_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, s>>>(pair + o, vals + 2 * o, k, count, out,
-                                                                                  Pos{rows, cols, ld});
+            RL_CUDA(cudaMemcpyAsync(vals + 2 * o, hv + 2 * o, 16 * k, cudaMemcpyHostToDevice, up));
+            scatter_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, up>>>(pair + o, vals + 2 * o, k, count,
+                                                                                   out, Pos{rows, cols, ld});
             RL_CHECK_LAUNCH("scatter_kernel");
         }
         return RL_OK;
@@ -397,8 +398,18 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
     if (stage && h_total >= pairs && n1 <= cap && n1 > 0) {
         RL_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
         RL_CUDA(cudaStreamWaitEvent(ds, ev1, 0));
-        if ((st = resolve(0, n1, ds)) != RL_OK) return st;
+        if ((st = resolve(0, n1, ds, s)) != RL_OK) return st;
         done = n1;
+    }
+    // rows [0, rows1) hold only first-half values, final in stream order now
+    bool overlapped = false;
+    if (first_rows_ready && stage && h_total >= pairs && n1 <= cap) {
+        const int64_t half_vals = 2 * static_cast<int64_t>(ctx->host_scalars[3]);
+        const int64_t rows1 = std::min<int64_t>(rows, half_vals / cols);
+        if (rows1 > 0) {
+            if ((st = first_rows_ready(rows1)) != RL_OK) return st;
+            overlapped = true;
+        }
     }
     RL_CUDA(cudaEventSynchronize(ev2));
     h_hard = static_cast<int64_t>(ctx->host_scalars[1]);
@@ -417,8 +428,37 @@ rl_status GaussJob::finish(int64_t* hard_cases) {
     // the second half's attempts also come down on the side stream: on the
     // main stream they would queue behind the first half's uploads, which
     // share the H2D engine with the caller's own uploads
+    if (overlapped && !ds) RL_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+    if (overlapped) {
+        // the main stream's GEMM fills every SM: the second half's scatter
+        // must be scheduled ahead of its remaining CTAs, or it (and the host,
+        // which waits for its copies) waits for the whole GEMM
+        int lo_p = 0, hi_p = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p);
+        cudaStream_t hs = nullptr;
+        RL_CUDA(cudaStreamCreateWithPriority(&hs, cudaStreamNonBlocking, hi_p));
+        RL_CUDA(cudaStreamWaitEvent(hs, ev2, 0));
+        cudaStreamSynchronize(ds);  // ds only ever held the first half's attempt downloads
+        cudaStreamDestroy(ds);
+        ds = hs;
+    }
     if (ds) RL_CUDA(cudaStreamWaitEvent(ds, ev2, 0));
-    if ((st = resolve(done, h_hard, ds ? ds : s)) != RL_OK) return st;
+    // the second half's values go up and scatter on the side stream when the
+    // main stream already runs work queued by first_rows_ready (only the
+    // rows >= rows1 they touch are not read by it), else on the main stream
+    cudaStream_t up = overlapped ? ds : s;
+    if ((st = resolve(done, h_hard, ds ? ds : s, up)) != RL_OK) return st;
+    if (overlapped) {
+        cudaEvent_t e_done;
+        RL_CUDA(cudaEventCreateWithFlags(&e_done, cudaEventDisableTiming));
+        RL_CUDA(cudaEventRecord(e_done, ds));
+        RL_CUDA(cudaStreamWaitEvent(s, e_done, 0));
+        // the staging buffer is reused by the next call: its copies must be done
+        const cudaError_t e = cudaEventSynchronize(e_done);
+        cudaEventDestroy(e_done);
+        RL_CUDA(e);
+        return RL_OK;
+    }
     // the staging buffer is reused by the next call: the copies must be done
     RL_CUDA(cudaStreamSynchronize(s));
     return RL_OK;
