@@ -406,6 +406,13 @@ __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __rest
             __syncthreads();
             // pass 3 (N = 8, M = 1): positions 8g + r; accumulate conj(Z) H_s
             const cplx* hs = spec + static_cast<int64_t>(s) * OLA_NF;
+            // the segment spectrum's slots of both groups first: their L2
+            // latency runs under the shared-memory reads and the DFTs
+            cplx hq[2][8];
+#pragma unroll
+            for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+                for (int r = 0; r < 8; ++r) hq[gg][r] = hs[8 * (t + OLA_T * gg) + r];
 #pragma unroll
             for (int gg = 0; gg < 2; ++gg) {
                 const int g = t + OLA_T * gg;
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __rest
                 dft_reg<8, false>(u8);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    const cplx zz = u8[brev<8>(r)], hh = hs[8 * g + r];
+                    const cplx zz = u8[brev<8>(r)], hh = hq[gg][r];
                     acc[gg][r].x = fma(zz.x, hh.x, fma(zz.y, hh.y, acc[gg][r].x));
                     acc[gg][r].y = fma(zz.x, hh.y, fma(-zz.y, hh.x, acc[gg][r].y));
                 }
