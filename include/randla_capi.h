@@ -326,6 +326,68 @@ RL_API rl_status rl_range_find_residual(rl_context* ctx, rl_mem mem, int64_t m, 
                                         int64_t l, const rl_multiplier* h, int64_t power_steps, double* q,
                                         rl_lowrank_info* info);
 
+/* ---- the complex field (Matrix<Complex>) -----------
+ * Complex arrays are interleaved (re, im) doubles, row-major — the layout of
+ * std::complex<double>. Multiplier specs take every MultiplierKind: the
+ * complex families (UNITARY_CIRCULANT, TOEPLITZ_BLOCK with RL_TOEPLITZ_UNITARY,
+ * SRFT) are drawn from `seed` by the reference's recipes
+ * (multipliers.hpp:75-138); explicit `dense` / `column` buffers are real. */
+
+/* preprocess_solve<Complex>(a, b, pre, post, refine_steps) (preprocess.hpp:156-180,
+ * SideMultiplier<Complex>::make :27-60): circulant kinds (real or unitary,
+ * either Toeplitz variant) stay structured through the FFT, the others are
+ * dense (SRFT complex). a, lu_out: n x n; b, x: n (all complex). info as for
+ * rl_preprocessed_genp_solve (moduli for growth and pivots; stage_ms unset). */
+RL_API rl_status rl_zpreprocessed_genp_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* a,
+                                             const double* b, const rl_multiplier* pre, const rl_multiplier* post,
+                                             int64_t refine_steps, double* x, double* lu_out, rl_solve_info* info);
+/* range_find<Complex>(a, r, p, spec, power_steps) (lowrank.hpp:51-83) with
+ * l = r + p, then approximation_residual on the same A (lowrank.hpp:99-102):
+ * a m x n complex, q m x l complex (nullable). Q has orthonormal columns and
+ * positive real R diagonal (qr.hpp:33-45). */
+RL_API rl_status rl_zrange_find_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                         int64_t l, const rl_multiplier* h, int64_t power_steps, double* q,
+                                         rl_lowrank_info* info);
+/* residual norms of A - Q Q^H A for a given complex A (m x n) and Q (m x l) */
+RL_API rl_status rl_zapproximation_residual(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a,
+                                            int64_t l, const double* q, rl_lowrank_info* info);
+/* materialize<Complex>(spec) (multipliers.hpp:174-218): out rows x cols complex */
+RL_API rl_status rl_zmaterialize(rl_context* ctx, rl_mem mem, const rl_multiplier* spec, int64_t rows, int64_t cols,
+                                 double* out);
+/* first column of gen_unitary_circulant(n, seed) (multipliers.hpp:75-82),
+ * inverse_fft of the unit spectrum: n complex */
+RL_API rl_status rl_gen_unitary_circulant(rl_context* ctx, rl_mem mem, int64_t n, uint64_t seed, double* column);
+/* srft_columns(n, l, seed) (multipliers.hpp:132-138): l sorted indices (host) */
+RL_API rl_status rl_srft_columns(int64_t n, int64_t l, uint64_t seed, int64_t* out);
+/* svd_values of a complex m x n matrix (svd.hpp:76-88), non-increasing */
+RL_API rl_status rl_zsingular_values(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a, double* out);
+/* srft_sketch_check (lowrank.hpp:200-261) on a real m x n `a` */
+typedef struct rl_srft_check {
+    double residual;      /* ||(I - P_Y) A|| (spectral_norm_estimate) */
+    double bound;         /* sqrt(1 + 7 n / l) sigma_{r+1} */
+    int64_t sketch_width; /* l */
+    int32_t clamped;      /* the prescribed width reached n and was cut back */
+    int32_t reserved;
+} rl_srft_check;
+/* variant 0 = SketchVariant::Srft, 1 = CirculantPermutation; known_sigma_r1 < 0
+ * (or NaN) evaluates svd_values(a)[r] */
+RL_API rl_status rl_srft_sketch_check(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, const double* a, int64_t r,
+                                      uint64_t seed, int32_t variant, double known_sigma_r1, rl_srft_check* out);
+/* matmul_by_circulant / matmul_by_toeplitz_block (circulant.hpp:171-203) over
+ * the complex field: A (m x k) times the leading k x l block of the np-point
+ * circulant with complex first column c (length np), out m x l */
+RL_API rl_status rl_zcirculant_right_multiply(rl_context* ctx, rl_mem mem, int64_t m, int64_t k, const double* a,
+                                              int64_t np, const double* c, int64_t l, double* out);
+/* circulant_apply(C(c), x) (circulant.hpp:81-98), complex c, x, y (length n) */
+RL_API rl_status rl_zcirculant_apply(rl_context* ctx, rl_mem mem, int64_t n, const double* c, const double* x,
+                                     double* y);
+/* matmul<Complex> (matrix.hpp:115-121): c (m x n) = a (m x k) b (k x n) */
+RL_API rl_status rl_zgemm(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, int64_t k, const double* a,
+                          const double* b, double* c);
+/* the unit roots polar(1, 2 pi k / n), k < n (fft.hpp:21-30, multipliers.hpp:98-100),
+ * rounded as the reference's host code: n complex (host) */
+RL_API rl_status rl_unit_roots(int64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

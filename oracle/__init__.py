@@ -241,6 +241,19 @@ class _Ref:
         self._gepp = s("ref_gepp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p])
         self._gepp_solve = s("ref_gepp_solve", ctypes.c_int, [i64, _dp, _dp, _dp, ctypes.c_int])
         self._block_ge = s("ref_block_ge", ctypes.c_int, [i64, _dp, i64, _i64p, _dp, _dp, _dp, _dp, _dp, _i64p])
+        # the complex field (interleaved buffers)
+        self._zgenp = s("ref_zgenp_factor", ctypes.c_int, [i64, _dp, _dp, _i64p])
+        self._zpre = s("ref_zpreprocess_solve_spec", ctypes.c_int,
+                       [i64, _dp, _dp, ctypes.c_int, ctypes.c_int, u64, ctypes.c_int, ctypes.c_int, u64, u64, i64,
+                        _dp, _dp, _i32p, _i64p])
+        self._zmat = s("ref_zmaterialize", ctypes.c_int, [ctypes.c_int, ctypes.c_int, u64, u64, i64, i64, _dp])
+        self._zsketch = s("ref_zrange_sketch", ctypes.c_int,
+                          [i64, i64, _dp, i64, ctypes.c_int, ctypes.c_int, u64, u64, i64, _dp])
+        self._ucirc = s("ref_gen_unitary_circulant", None, [i64, u64, _dp])
+        self._srftc = s("ref_srft_columns", None, [i64, i64, u64, _i64p])
+        self._srftm = s("ref_srft_matrix", ctypes.c_int, [i64, i64, u64, ctypes.c_int, _dp])
+        self._znormest = s("ref_zspectral_norm_estimate", ctypes.c_double, [i64, i64, _dp])
+        self._dft = s("ref_dft_dense", ctypes.c_int, [i64, _dp])
 
     # status codes of the ref_* entry points (ref_capi.cpp)
     DIM, ZERO_PIVOT, SINGULAR_BLOCK, SINGULAR = 1, 2, 3, 6
@@ -406,6 +419,68 @@ class _Ref:
         out = np.empty((rows, cols))
         st = self._mat(kind, variant, seed, card, rows, cols, ptr(out))
         return out, st
+
+    # ---- complex field (numpy complex128 in and out) ----
+    @staticmethod
+    def _z(a):
+        return np.ascontiguousarray(a, dtype=np.complex128)
+
+    def zgenp_factor(self, a):
+        a = self._z(a)
+        n = a.shape[0]
+        lu = np.empty((n, n), np.complex128)
+        zs = np.zeros(1, np.int64)
+        st = self._zgenp(n, ptr(a.view(np.float64)), ptr(lu.view(np.float64)), ptr(zs))
+        return lu, st, int(zs[0])
+
+    def zpreprocess_solve_spec(self, a, b, pre=(0, 0, 0), post=(0, 0, 0), refine=0, card=65536):
+        a, b = self._z(a), self._z(b)
+        n = a.shape[0]
+        x = np.empty(n, np.complex128)
+        hist = np.empty(refine + 1)
+        div = ctypes.c_int(0)
+        zs = np.zeros(1, np.int64)
+        st = self._zpre(n, ptr(a.view(np.float64)), ptr(b.view(np.float64)), pre[0], pre[1], pre[2], post[0],
+                        post[1], post[2], card, refine, ptr(x.view(np.float64)), ptr(hist), ctypes.byref(div), ptr(zs))
+        return dict(x=x, history=hist, diverged=bool(div.value), status=st, zero_step=int(zs[0]))
+
+    def zmaterialize(self, kind, rows, cols, seed, variant=0, card=65536):
+        out = np.empty((rows, cols), np.complex128)
+        st = self._zmat(kind, variant, seed, card, rows, cols, ptr(out.view(np.float64)))
+        return out, st
+
+    def zrange_sketch(self, a, l, kind, seed, variant=0, power_steps=0, card=65536):
+        a = self._z(a)
+        m, n = a.shape
+        y = np.empty((m, l), np.complex128)
+        st = self._zsketch(m, n, ptr(a.view(np.float64)), l, kind, variant, seed, card, power_steps,
+                           ptr(y.view(np.float64)))
+        return y, st
+
+    def gen_unitary_circulant(self, n, seed):
+        out = np.empty(n, np.complex128)
+        self._ucirc(n, seed, ptr(out.view(np.float64)))
+        return out
+
+    def srft_columns(self, n, l, seed):
+        out = np.empty(l, np.int64)
+        self._srftc(n, l, seed, ptr(out))
+        return out
+
+    def srft_matrix(self, n, l, seed, variant=0):
+        out = np.empty((n, l), np.complex128)
+        st = self._srftm(n, l, seed, variant, ptr(out.view(np.float64)))
+        return out, st
+
+    def zspectral_norm_estimate(self, a):
+        a = self._z(a)
+        return float(self._znormest(a.shape[0], a.shape[1], ptr(a.view(np.float64))))
+
+    def dft_dense(self, n):
+        out = np.empty((n, n), np.complex128)
+        st = self._dft(n, ptr(out.view(np.float64)))
+        assert st == 0
+        return out
 
     def batched_config2(self, count, base=7, i0=0, dim=32):
         x = np.empty((count, dim))

@@ -50,6 +50,11 @@ RealMatrix wrap(int64_t m, int64_t n, const double* p) {
     return RealMatrix(static_cast<std::size_t>(m), static_cast<std::size_t>(n), std::vector<double>(p, p + m * n));
 }
 
+ComplexMatrix wrapz(int64_t m, int64_t n, const double* p) {
+    const Complex* c = reinterpret_cast<const Complex*>(p);
+    return ComplexMatrix(static_cast<std::size_t>(m), static_cast<std::size_t>(n), std::vector<Complex>(c, c + m * n));
+}
+
 template <typename F>
 int guarded(F&& f, int64_t* step = nullptr) {
     try {
@@ -400,4 +405,133 @@ int ref_block_ge(int64_t n, const double* a, int64_t nsplit, const int64_t* spli
         },
         position);
 }
+// ---- the complex field (Matrix<Complex>): interleaved (re, im) buffers ----
+
+// genp_factor<Complex> (lu.hpp:40-58), packed L\U
+int ref_zgenp_factor(int64_t n, const double* a, double* lu, int64_t* zero_step) {
+    *zero_step = 0;
+    return guarded(
+        [&] {
+            const LuFactors<Complex> f = genp_factor(wrapz(n, n, a));
+            Complex* out = reinterpret_cast<Complex*>(lu);
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t j = 0; j < n; ++j)
+                    out[i * n + j] = (j < i) ? f.lower(static_cast<std::size_t>(i), static_cast<std::size_t>(j))
+                                             : f.upper(static_cast<std::size_t>(i), static_cast<std::size_t>(j));
+        },
+        zero_step);
+}
+
+// preprocess_solve<Complex>(a, b, pre, post, refine) (preprocess.hpp:156-180)
+int ref_zpreprocess_solve_spec(int64_t n, const double* a, const double* b, int pre_kind, int pre_variant,
+                               uint64_t pre_seed, int post_kind, int post_variant, uint64_t post_seed, uint64_t card,
+                               int64_t refine, double* x, double* history, int* diverged, int64_t* zero_step) {
+    *zero_step = 0;
+    return guarded(
+        [&] {
+            MultiplierSpec pre, post;
+            pre.kind = static_cast<MultiplierKind>(pre_kind);
+            pre.variant = static_cast<ToeplitzVariant>(pre_variant);
+            pre.seed = pre_seed;
+            pre.set_cardinality = static_cast<std::size_t>(card);
+            post.kind = static_cast<MultiplierKind>(post_kind);
+            post.variant = static_cast<ToeplitzVariant>(post_variant);
+            post.seed = post_seed;
+            post.set_cardinality = static_cast<std::size_t>(card);
+            const Complex* bz = reinterpret_cast<const Complex*>(b);
+            const SolveOutcome<Complex> out = preprocess_solve(wrapz(n, n, a), std::vector<Complex>(bz, bz + n), pre,
+                                                               post, static_cast<std::size_t>(refine));
+            std::memcpy(x, out.x.data(), sizeof(Complex) * n);
+            for (int64_t s = 0; s <= refine; ++s)
+                history[s] = s < static_cast<int64_t>(out.residual_history.size()) ? out.residual_history[s] : NAN;
+            *diverged = out.diverged ? 1 : 0;
+        },
+        zero_step);
+}
+
+// materialize<Complex>(spec) (multipliers.hpp:174-218)
+int ref_zmaterialize(int kind, int variant, uint64_t seed, uint64_t card, int64_t rows, int64_t cols, double* out) {
+    return guarded([&] {
+        MultiplierSpec spec;
+        spec.kind = static_cast<MultiplierKind>(kind);
+        spec.variant = static_cast<ToeplitzVariant>(variant);
+        spec.seed = seed;
+        spec.set_cardinality = static_cast<std::size_t>(card);
+        spec.rows = static_cast<std::size_t>(rows);
+        spec.cols = static_cast<std::size_t>(cols);
+        const ComplexMatrix g = materialize<Complex>(spec);
+        std::memcpy(out, g.data(), sizeof(Complex) * rows * cols);
+    });
+}
+
+// the sketch of range_find<Complex> (lowrank.hpp:51-81) before its qr
+int ref_zrange_sketch(int64_t m, int64_t n, const double* a, int64_t l, int kind, int variant, uint64_t seed,
+                      uint64_t card, int64_t power_steps, double* y) {
+    return guarded([&] {
+        MultiplierSpec spec;
+        spec.kind = static_cast<MultiplierKind>(kind);
+        spec.variant = static_cast<ToeplitzVariant>(variant);
+        spec.seed = seed;
+        spec.set_cardinality = static_cast<std::size_t>(card);
+        spec.rows = static_cast<std::size_t>(n);
+        spec.cols = static_cast<std::size_t>(l);
+        const ComplexMatrix am = wrapz(m, n, a);
+        ComplexMatrix sketch(1, 1);
+        if (spec.kind == MultiplierKind::ToeplitzBlock) {
+            if (spec.variant == ToeplitzVariant::Real)
+                sketch = matmul_by_toeplitz_block(am, gen_real_toeplitz_block(spec.rows, spec.cols, spec.seed));
+            else
+                sketch = matmul_by_toeplitz_block(am, gen_unitary_toeplitz_block(spec.rows, spec.cols, spec.seed));
+        } else {
+            sketch = matmul(am, materialize<Complex>(spec));
+        }
+        for (int64_t s = 0; s < power_steps; ++s) sketch = matmul(am, matmul(am.adjoint(), sketch));
+        std::memcpy(y, sketch.data(), sizeof(Complex) * m * l);
+    });
+}
+
+// first column of gen_unitary_circulant (multipliers.hpp:75-82)
+void ref_gen_unitary_circulant(int64_t n, uint64_t seed, double* out) {
+    const ComplexCirculant c = gen_unitary_circulant(static_cast<std::size_t>(n), seed);
+    std::memcpy(out, c.first_column().data(), sizeof(Complex) * n);
+}
+
+// srft_columns (multipliers.hpp:132-138)
+void ref_srft_columns(int64_t n, int64_t l, uint64_t seed, int64_t* out) {
+    const auto cols = srft_columns(static_cast<std::size_t>(n), static_cast<std::size_t>(l), seed);
+    for (int64_t j = 0; j < l; ++j) out[j] = static_cast<int64_t>(cols[j]);
+}
+
+// the sketching matrix of srft_sketch_check (lowrank.hpp:235-246) for a given
+// width l: gen_srft, or the same columns of the unitary circulant drawn from
+// the same phases (restated from those lines with the reference's functions)
+int ref_srft_matrix(int64_t n, int64_t l, uint64_t seed, int variant, double* out) {
+    return guarded([&] {
+        const std::size_t nn = static_cast<std::size_t>(n), ll = static_cast<std::size_t>(l);
+        ComplexMatrix s(1, 1);
+        if (variant == 0) {
+            s = gen_srft(nn, ll, seed);
+        } else {
+            const ComplexCirculant circ = gen_unitary_circulant(nn, seed);
+            const auto cols = srft_columns(nn, ll, seed);
+            s = ComplexMatrix(nn, ll);
+            for (std::size_t i = 0; i < nn; ++i)
+                for (std::size_t j = 0; j < ll; ++j) s(i, j) = circ.entry(i, cols[j]);
+        }
+        std::memcpy(out, s.data(), sizeof(Complex) * n * l);
+    });
+}
+
+double ref_zspectral_norm_estimate(int64_t m, int64_t n, const double* a) {
+    return spectral_norm_estimate(wrapz(m, n, a));
+}
+
+// gen_dft_input (testbed/inputs.hpp:52-55) = dft_dense(n) (fft.hpp:21-30)
+int ref_dft_dense(int64_t n, double* out) {
+    return guarded([&] {
+        const ComplexMatrix d = dft_dense(static_cast<std::size_t>(n));
+        std::memcpy(out, d.data(), sizeof(Complex) * n * n);
+    });
+}
+
 }  // extern "C"

@@ -91,6 +91,11 @@ class rl_lowrank_info(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
+class rl_srft_check(ctypes.Structure):
+    _fields_ = [("residual", ctypes.c_double), ("bound", ctypes.c_double), ("sketch_width", ctypes.c_int64),
+                ("clamped", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 # name -> (restype, argtypes); every symbol include/randla_capi.h declares
 SIGNATURES = {
     "rl_abi_version": (ctypes.c_int, []),
@@ -136,6 +141,25 @@ SIGNATURES = {
                                                  ctypes.POINTER(rl_lowrank_info)]),
     "rl_range_find_residual": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, ctypes.POINTER(rl_multiplier),
                                               i64, _vp, ctypes.POINTER(rl_lowrank_info)]),
+    # the complex field
+    "rl_zpreprocessed_genp_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, ctypes.POINTER(rl_multiplier),
+                                                   ctypes.POINTER(rl_multiplier), i64, _vp, _vp,
+                                                   ctypes.POINTER(rl_solve_info)]),
+    "rl_zrange_find_residual": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64,
+                                               ctypes.POINTER(rl_multiplier), i64, _vp,
+                                               ctypes.POINTER(rl_lowrank_info)]),
+    "rl_zapproximation_residual": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, _vp,
+                                                  ctypes.POINTER(rl_lowrank_info)]),
+    "rl_zmaterialize": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(rl_multiplier), i64, i64, _vp]),
+    "rl_gen_unitary_circulant": (ctypes.c_int, [_vp, ctypes.c_int, i64, u64, _vp]),
+    "rl_srft_columns": (ctypes.c_int, [i64, i64, u64, _vp]),
+    "rl_zsingular_values": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp]),
+    "rl_srft_sketch_check": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, u64, i32, ctypes.c_double,
+                                            ctypes.POINTER(rl_srft_check)]),
+    "rl_unit_roots": (ctypes.c_int, [i64, _vp]),
+    "rl_zcirculant_right_multiply": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, _vp, i64, _vp]),
+    "rl_zcirculant_apply": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
+    "rl_zgemm": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, i64, _vp, _vp, _vp]),
 }
 
 

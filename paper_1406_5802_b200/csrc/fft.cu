@@ -1255,26 +1255,20 @@ extern "C" RL_API rl_status rl_toeplitz_right_multiply(rl_context* ctx, rl_mem m
     return right_multiply(ctx, mem, m, k, a, np, c, l, out);
 }
 
-extern "C" RL_API rl_status rl_fft(rl_context* ctx, rl_mem mem, int64_t count, int64_t n, double* z, int32_t inverse) {
-    if (n <= 0 || count < 0) return set_error(RL_ERR_DIMENSION, inverse ? "inverse_fft: empty input" : "fft: empty input");
-    if (count == 0) return RL_OK;
-    if (!z) return set_error(RL_ERR_INVALID_ARGUMENT, "fft: null pointer");
-    rl_status st;
-    ctx = resolve(ctx, &st);
-    if (!ctx) return st;
+namespace rl {
+// batched complex transform of `count` contiguous rows of n points, in place
+// on the device (fft.hpp:76-98, +1 sign forward, 1/n on the inverse); `work`
+// (count * n complex) is needed unless n is a power of two <= MAXN.
+size_t cfft_work_bytes(int64_t count, int64_t n) { return is_pow2(n) && n <= MAXN ? 0 : size_t(count) * n * 16; }
+rl_status cfft_device(rl_context* ctx, int64_t count, int64_t n, double* z, bool inverse, double* work_ptr) {
+    if (count <= 0) return RL_OK;
     cudaStream_t s = ctx->stream;
-    const bool host = mem == RL_HOST;
-    const int64_t bytes = count * n * 16;
     cplx* dz = reinterpret_cast<cplx*>(z);
-    cplx* work = nullptr;
+    cplx* work = reinterpret_cast<cplx*>(work_ptr);
     const bool pow2 = is_pow2(n);
     const bool small = pow2 && n <= MAXN;
-    bool ok = with_arena(ctx, [&](Arena& ar) {
-        if (host) dz = ar.take<cplx>(count * n);
-        if (!small) work = ar.take<cplx>(count * n);
-    });
-    if (!ok) return RL_ERR_OUT_OF_MEMORY;
-    if (host) RL_CUDA(cudaMemcpyAsync(dz, z, bytes, cudaMemcpyHostToDevice, s));
+    if (!small && !work) return set_error(RL_ERR_INVALID_ARGUMENT, "fft: work buffer required for n = %lld", (long long)n);
+    rl_status st;
     cplx* tw = nullptr;
     if ((st = twiddles(ctx, n, &tw)) != RL_OK) return st;
     if (small) {
@@ -1297,13 +1291,37 @@ extern "C" RL_API rl_status rl_fft(rl_context* ctx, rl_mem mem, int64_t count, i
             RL_CHECK_LAUNCH("stockham_pass_kernel");
             std::swap(src, dst);
         }
-        if (src != dz) RL_CUDA(cudaMemcpyAsync(dz, src, bytes, cudaMemcpyDeviceToDevice, s));
+        if (src != dz) RL_CUDA(cudaMemcpyAsync(dz, src, count * n * 16, cudaMemcpyDeviceToDevice, s));
     } else {
         dft_dense_kernel<<<static_cast<unsigned>((count * n + 255) / 256), 256, 0, s>>>(dz, work, n, count, tw,
                                                                                         inverse ? 1 : 0);
         RL_CHECK_LAUNCH("dft_dense_kernel");
-        RL_CUDA(cudaMemcpyAsync(dz, work, bytes, cudaMemcpyDeviceToDevice, s));
+        RL_CUDA(cudaMemcpyAsync(dz, work, count * n * 16, cudaMemcpyDeviceToDevice, s));
     }
+    return RL_OK;
+}
+}  // namespace rl
+
+extern "C" RL_API rl_status rl_fft(rl_context* ctx, rl_mem mem, int64_t count, int64_t n, double* z, int32_t inverse) {
+    if (n <= 0 || count < 0) return set_error(RL_ERR_DIMENSION, inverse ? "inverse_fft: empty input" : "fft: empty input");
+    if (count == 0) return RL_OK;
+    if (!z) return set_error(RL_ERR_INVALID_ARGUMENT, "fft: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    const int64_t bytes = count * n * 16;
+    double* dz = z;
+    double* work = nullptr;
+    const size_t wb = cfft_work_bytes(count, n);
+    bool ok = with_arena(ctx, [&](Arena& ar) {
+        if (host) dz = ar.take<double>(2 * count * n);
+        if (wb) work = ar.take<double>(2 * count * n);
+    });
+    if (!ok) return RL_ERR_OUT_OF_MEMORY;
+    if (host) RL_CUDA(cudaMemcpyAsync(dz, z, bytes, cudaMemcpyHostToDevice, s));
+    if ((st = cfft_device(ctx, count, n, dz, inverse != 0, work)) != RL_OK) return st;
     if (host) {
         RL_CUDA(cudaMemcpyAsync(z, dz, bytes, cudaMemcpyDeviceToHost, s));
         RL_CUDA(cudaStreamSynchronize(s));

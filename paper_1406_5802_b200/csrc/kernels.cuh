@@ -63,6 +63,13 @@ rl_status spectral_norm_estimate_device(rl_context* ctx, int64_t m, int64_t n, c
 rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a, int64_t lda, int64_t np,
                          const double* c, int64_t l, double* out, int64_t ldo, void* spec_ws);
 
+// batched complex transform of `count` contiguous n-point rows (interleaved
+// re/im), in place on the device, the reference's +1 sign forward and 1/n on
+// the inverse (fft.hpp:76-98); `work` (>= cfft_work_bytes) unless n is a
+// power of two <= 8192
+size_t cfft_work_bytes(int64_t count, int64_t n);
+rl_status cfft_device(rl_context* ctx, int64_t count, int64_t n, double* z, bool inverse, double* work);
+
 // dense expansion of the leading k x l block of the np-point circulant (device)
 rl_status circulant_dense(rl_context* ctx, const double* c, int64_t np, int64_t k, int64_t l, double* h, int64_t ldh);
 // whether circulant_rows handles parent length np
@@ -134,6 +141,23 @@ struct StreamBuf {
         if (p) cudaFreeAsync(p, s);
     }
 };
+
+// ---- low-rank building blocks (lowrank.cu) --------------------------------
+// orthonormal_basis (qr.hpp:51-54) by CholeskyQR2 (shifted CholeskyQR3 on
+// breakdown): Q (m x l, ldq) from Y (m x l, ldq), R (l x l, ldr, nullable).
+// Options for callers that run it on a real embedding of a complex Y:
+// rank_m / rank_l replace (m, l) in tol_rank, reported columns are divided
+// by column_group, unchecked skips the verdict (orthonormal_basis_unchecked).
+struct CholqrOpts {
+    int64_t rank_m = 0, rank_l = 0;
+    int64_t column_group = 1;
+    bool unchecked = false;
+};
+rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y, double* q, int64_t ldq, double* r,
+                         int64_t ldr, int64_t* bad_column, const CholqrOpts* opts = nullptr);
+// ||A - Q (Q^T A)||_F and ||.||_2 (power iteration) into info (lowrank.hpp:99-102)
+rl_status residual_core(rl_context* ctx, int64_t m, int64_t n, const double* A, int64_t ldA, int64_t l,
+                        const double* Q, int64_t ldq, rl_lowrank_info* info);
 
 // batched 32x32 kernel (batched32.cu)
 rl_status launch_batched_genp32(rl_context* ctx, int64_t batch, const double* a, const double* g, const double* b,

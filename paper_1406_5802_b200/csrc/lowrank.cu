@@ -241,6 +241,18 @@ __global__ void diag_min_kernel(const double* __restrict__ r, int64_t ld, int l,
     *first_le = first;
 }
 
+// max |W - I| over an l x l Gram matrix (bit pattern of a non-negative double)
+__global__ void gram_deviation_kernel(const double* __restrict__ w, int64_t ld, int l,
+                                      unsigned long long* __restrict__ out) {
+    double mx = 0.0;
+    for (int64_t idx = threadIdx.x; idx < static_cast<int64_t>(l) * l; idx += blockDim.x) {
+        const int64_t i = idx / l, j = idx - i * l;
+        mx = fmax(mx, fabs(w[i * ld + j] - (i == j ? 1.0 : 0.0)));
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(mx)));
+}
+
 int splits_for(int64_t tiles, int64_t ktiles, int sms) {
     const int64_t want = (2 * sms + tiles - 1) / tiles;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, ktiles / 4)));
@@ -330,7 +342,9 @@ rl_status gram(rl_context* ctx, int64_t m, int64_t l, const double* y, int64_t l
 // CholeskyQR2 (shifted CholeskyQR3 on breakdown) of Y (m x l, ld = ldq) into
 // Q (m x l, ld = ldq) and R (l x l, ld = ldr, nullable). Returns the rank verdict.
 rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y, double* q, int64_t ldq, double* r,
-                         int64_t ldr, int64_t* bad_column) {
+                         int64_t ldr, int64_t* bad_column, const CholqrOpts* opts) {
+    const CholqrOpts dflt;
+    if (!opts) opts = &dflt;
     cudaStream_t s = ctx->stream;
     *bad_column = 0;
     const int64_t ldl = (l + 1) & ~int64_t(1), ldm = (m + 1) & ~int64_t(1);
@@ -361,9 +375,18 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
     int npass = 0;
     // one CholeskyQR pass: out = in R^-1 with in^T in (+ shift I) = R^T R;
     // Racc <- R Racc. Returns the Cholesky breakdown step (0 = none).
-    auto pass = [&](const double* in, double* out, bool shift, int* fail) -> rl_status {
+    // deviation of the pass's Gram from I (the orthogonality of its input),
+    // measured when `dev` is given
+    unsigned long long* dev_bits = reinterpret_cast<unsigned long long*>(sc + 10);
+    auto pass = [&](const double* in, double* out, bool shift, int* fail, double* dev = nullptr) -> rl_status {
         rl_status e = gram(ctx, m, l, in, ldq, W, ldl, byt.p, ldm, bsplit.p, splits);
         if (e != RL_OK) return e;
+        if (dev) {
+            RL_CUDA(cudaMemsetAsync(dev_bits, 0, 8, s));
+            gram_deviation_kernel<<<1, 256, 0, s>>>(W, ldl, static_cast<int>(l), dev_bits);
+            RL_CHECK_LAUNCH("gram_deviation_kernel");
+            RL_CUDA(cudaMemcpyAsync(dev, dev_bits, 8, cudaMemcpyDeviceToHost, s));
+        }
         if (shift) {
             // shifted CholeskyQR3: s = 11 (m l + l (l + 1)) u ||Y||_F^2
             const double sh = 11.0 * (static_cast<double>(m) * l + static_cast<double>(l) * (l + 1)) *
@@ -388,7 +411,15 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
     int fail = 0;
     if ((st = pass(y, bq1.p, false, &fail)) != RL_OK) return st;
     if (!fail) {
-        if ((st = pass(bq1.p, q, false, &fail)) != RL_OK) return st;
+        // CholeskyQR2; when the first pass left Q1 far from orthonormal
+        // (kappa(Y) near u^-1/2: the Gram of Q1 is off I by more than 1e-4),
+        // a third pass restores orthogonality to rounding level
+        double dev1 = 0.0;
+        if ((st = pass(bq1.p, q, false, &fail, &dev1)) != RL_OK) return st;
+        if (!fail && dev1 > 1e-4) {
+            if ((st = pass(q, bq2.p, false, &fail)) != RL_OK) return st;
+            RL_CUDA(cudaMemcpy2DAsync(q, ldq * 8, bq2.p, ldq * 8, l * 8, m, cudaMemcpyDeviceToDevice, s));
+        }
     } else {
         npass = 0;  // breakdown: shifted CholeskyQR3
         if ((st = pass(y, bq1.p, true, &fail)) != RL_OK) return st;
@@ -396,11 +427,17 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
         if (!fail && (st = pass(bq2.p, q, false, &fail)) != RL_OK) return st;
     }
     if (fail) {
-        *bad_column = fail;
-        return set_error(RL_ERR_RANK_DEFICIENCY, "qr: numerically rank-deficient at column %d", fail);
+        *bad_column = (fail + opts->column_group - 1) / opts->column_group;
+        return set_error(RL_ERR_RANK_DEFICIENCY, "qr: numerically rank-deficient at column %lld",
+                         static_cast<long long>(*bad_column));
+    }
+    if (opts->unchecked) {  // orthonormal_basis_unchecked (qr.hpp:58-76): no rank verdict
+        if (r) RL_CUDA(cudaMemcpy2DAsync(r, ldr * 8, Racc, ldl * 8, l * 8, l, cudaMemcpyDeviceToDevice, s));
+        return RL_OK;
     }
     // rank verdict (qr.hpp:33-38): |r_jj| <= tol_rank(m, l) * spectral_norm_estimate(Y)
-    const double tol_rank = 1e-13 * static_cast<double>(std::max(m, l));
+    const double tol_rank = 1e-13 * static_cast<double>(std::max(opts->rank_m ? opts->rank_m : m,
+                                                                 opts->rank_l ? opts->rank_l : l));
     int* first_d = flags + 1;
     diag_min_kernel<<<1, 32, 0, s>>>(Racc, ldl, static_cast<int>(l), tol_rank * std::sqrt(ysq) * (1.0 + 1e-10), sc + 1,
                                      first_d);
@@ -416,8 +453,9 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
         RL_CUDA(cudaMemcpyAsync(&first, first_d, sizeof(int), cudaMemcpyDeviceToHost, s));
         RL_CUDA(cudaStreamSynchronize(s));
         if (first) {
-            *bad_column = first;
-            return set_error(RL_ERR_RANK_DEFICIENCY, "qr: numerically rank-deficient at column %d", first);
+            *bad_column = (first + opts->column_group - 1) / opts->column_group;
+            return set_error(RL_ERR_RANK_DEFICIENCY, "qr: numerically rank-deficient at column %lld",
+                             static_cast<long long>(*bad_column));
         }
     }
     if (r) RL_CUDA(cudaMemcpy2DAsync(r, ldr * 8, Racc, ldl * 8, l * 8, l, cudaMemcpyDeviceToDevice, s));
@@ -824,6 +862,8 @@ rl_status range_find_core(rl_context* ctx, bool host, int64_t m, int64_t n, cons
     return st;
 }
 
+}  // namespace
+
 // residual R = A - Q (Q^T A) (lowrank.hpp:35-37, :99-102): ||R||_F from a GEMM
 // epilogue that never stores R, ||R||_2 by the power iteration on the
 // implicit operator
@@ -860,6 +900,8 @@ rl_status residual_core(rl_context* ctx, int64_t m, int64_t n, const double* A, 
     info->power_iterations = its;
     return RL_OK;
 }
+
+namespace {
 
 // A resident on the device with an even leading dimension (TMA), staged when
 // it is host memory or not aligned

@@ -27,6 +27,7 @@
 #include <functional>
 #include <new>
 #include <pthread.h>
+#include <complex>
 #include <vector>
 
 #include "../../include/randla_capi.h"
@@ -231,6 +232,75 @@ void gaussian_parallel(uint64_t seed, int64_t count, double* out) {
 namespace rl {
 uint64_t host_stream_state(uint64_t seed) { return stream_state(seed); }
 
+// ---- complex families' host draws (multipliers.hpp:75-138), sequential on
+// one stream and rounded exactly as the reference (glibc cos/sin through
+// std::polar, no FMA contraction) ------------------------------------------
+namespace {
+constexpr double kTwoPi = 2.0 * 3.141592653589793;  // 2.0 * std::numbers::pi
+struct SeqStream {  // RngStream::next_u64 / next_double / next_below (rng.hpp:30-53)
+    uint64_t s0, t = 0;
+    explicit SeqStream(uint64_t seed) : s0(stream_state(seed)) {}
+    uint64_t next_u64() { return finalize(s0 + (++t) * kGamma); }
+    double next_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+    uint64_t next_below(uint64_t bound) {
+        const uint64_t limit = bound * ((~uint64_t{0}) / bound);
+        uint64_t v;
+        do {
+            v = next_u64();
+        } while (v >= limit);
+        return v % bound;
+    }
+};
+// sample_without_replacement (multipliers.hpp:112-121)
+void sample_columns(SeqStream& rng, int64_t n, int64_t l, int64_t* out) {
+    std::vector<int64_t> pool(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) pool[i] = i;
+    for (int64_t i = 0; i < l; ++i) {
+        const int64_t j = i + static_cast<int64_t>(rng.next_below(static_cast<uint64_t>(n - i)));
+        std::swap(pool[i], pool[j]);
+    }
+    std::sort(pool.begin(), pool.begin() + l);
+    std::copy(pool.begin(), pool.begin() + l, out);
+}
+}  // namespace
+
+// spectrum of gen_unitary_circulant (multipliers.hpp:77-82): u_j =
+// polar(1, 2 pi phi_j), phi_j = next_double draws 1..n; u2 interleaved
+void host_unit_spectrum(uint64_t seed, int64_t n, double* u2) {
+    SeqStream rng(seed);
+    for (int64_t j = 0; j < n; ++j) {
+        const std::complex<double> u = std::polar(1.0, kTwoPi * rng.next_double());
+        u2[2 * j] = u.real();
+        u2[2 * j + 1] = u.imag();
+    }
+}
+
+// srft_columns (multipliers.hpp:132-138)
+void host_srft_columns(uint64_t seed, int64_t n, int64_t l, int64_t* cols) {
+    SeqStream rng(seed);
+    for (int64_t i = 0; i < n; ++i) rng.next_double();
+    sample_columns(rng, n, l, cols);
+}
+
+// the parts of gen_srft(n, l, seed) (multipliers.hpp:94-130): d_i = sqrt(n/l)
+// polar(1, 2 pi phi_i), root_k = polar(1, 2 pi k / n), the sampled columns;
+// entry (i, j) = d_i * root[(i cols_j) mod n]
+void host_srft_parts(uint64_t seed, int64_t n, int64_t l, double* d2, double* root2, int64_t* cols) {
+    SeqStream rng(seed);
+    std::vector<double> phases(static_cast<size_t>(n));
+    for (double& p : phases) p = rng.next_double();
+    sample_columns(rng, n, l, cols);
+    const double scale = std::sqrt(static_cast<double>(n) / static_cast<double>(l));
+    for (int64_t i = 0; i < n; ++i) {
+        const std::complex<double> d = scale * std::polar(1.0, kTwoPi * phases[i]);
+        d2[2 * i] = d.real();
+        d2[2 * i + 1] = d.imag();
+        const std::complex<double> r = std::polar(1.0, kTwoPi * static_cast<double>(i) / static_cast<double>(n));
+        root2[2 * i] = r.real();
+        root2[2 * i + 1] = r.imag();
+    }
+}
+
 void host_parallel_copy(void* dst, const void* src, size_t bytes) {
     constexpr size_t kPiece = size_t(4) << 20;
     const int64_t pieces = static_cast<int64_t>((bytes + kPiece - 1) / kPiece);
@@ -276,6 +346,18 @@ RL_API uint64_t rl_hash_label(const char* s) {
         h *= 1099511628211ull;
     }
     return h;
+}
+
+// polar(1, 2 pi k / n) for k < n (fft.hpp:21-30, multipliers.hpp:98-100)
+RL_API rl_status rl_unit_roots(int64_t n, double* out) {
+    if (n <= 0 || !out) return RL_ERR_DIMENSION;
+    for (int64_t k = 0; k < n; ++k) {
+        const std::complex<double> r = std::polar(1.0, 2.0 * 3.141592653589793 * static_cast<double>(k) /
+                                                           static_cast<double>(n));
+        out[2 * k] = r.real();
+        out[2 * k + 1] = r.imag();
+    }
+    return RL_OK;
 }
 
 RL_API rl_status rl_gen_gaussian(int64_t m, int64_t n, uint64_t seed, double* out) {

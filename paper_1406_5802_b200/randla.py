@@ -204,6 +204,8 @@ def materialize(spec, device=False):
     generators; circulant and skew-product expansions run on the GPU."""
     if spec.rows <= 0 or spec.cols <= 0:
         raise DimensionError("materialize: spec.rows and spec.cols must be set")
+    if multiplier_is_complex(spec):
+        raise DimensionError("complex multiplier family requested in a real pipeline")
     out = _empty_like_kind(device, (spec.rows, spec.cols))
     m, keep = _multiplier(spec, device)
     _sync_stream_for(device)
@@ -309,6 +311,8 @@ def batched_preprocess_solve_32(a, g, b, want_lu=True, want_summary=True):
 # ---- dense products ------------------------------------------------------------
 def matmul(a, b):
     """matmul (matrix.hpp:115-121): C = A B, FP64 DMMA on the GPU."""
+    if _any_complex(a, b):
+        return _zmatmul(a, b)
     device = _is_device(a, b)
     if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
         raise DimensionError("matmul: inner dimensions differ")
@@ -328,6 +332,8 @@ def matmul(a, b):
 def svd_values(a):
     """svd_values (svd.hpp:76-88): the min(m, n) singular values, non-increasing,
     by the device's one-sided Jacobi (small matrices: one CTA)."""
+    if _any_complex(a):
+        return _zsvd_values(a)
     device = _is_device(a)
     a = _dev(a) if device else _host(a)
     m, n = a.shape
@@ -668,6 +674,8 @@ def preprocess_solve(a, b, pre_spec=None, post_spec=None, refine_steps=0, want_l
     product F (A H) (dense sides by the DMMA GEMM, circulant sides through the
     FFT kernel), GENP, x = H (LU)^-1 (F b), refinement steps. Raises
     ZeroPivotError like the reference; retry with preprocess_solve_with_retry."""
+    if _any_complex(a, b):
+        return _zpreprocess_solve(a, b, pre_spec, post_spec, refine_steps, want_lu)
     device = _is_device(a, b)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise DimensionError("preprocess_solve: square input required")
@@ -778,6 +786,12 @@ class CirculantMatrix:
 
     def dense(self):
         n = self.size()
+        if _any_complex(self._c):  # entry (i, j) = c[(i - j) mod n] (circulant.hpp:27-36): a gather
+            idx = (np.arange(n)[:, None] - np.arange(n)[None, :]) % n
+            if isinstance(self._c, np.ndarray):
+                return self._c[idx]
+            import torch
+            return self._c[torch.from_numpy(idx).to(self._c.device)]
         spec = MultiplierSpec(MultiplierKind.REAL_CIRCULANT, 0, n, n, column=self._c)
         return materialize(spec, device=_is_device(self._c))
 
@@ -830,6 +844,8 @@ def _column_of(c):
 def circulant_apply(c, x):
     """circulant_apply(RealCirculant, x) (circulant.hpp:91-96): C x by FFT on the GPU."""
     c = _column_of(c)
+    if _any_complex(c, x):
+        return _zcirculant_apply(c, x)
     device = _is_device(c, x)
     n = c.shape[0]
     if x.shape[0] != n:
@@ -846,6 +862,10 @@ def matmul_by_circulant(a, c):
     """matmul_by_circulant(A, C) (circulant.hpp:171-185): A (m x n) times the
     real circulant C (a RealCirculant or its first column), by FFT on the GPU."""
     c = _column_of(c)
+    if _any_complex(a, c):
+        if c.shape[0] != a.shape[1]:
+            raise DimensionError("matmul_by_circulant: shape mismatch")
+        return _zcirc_right(a, c, c.shape[0])
     device = _is_device(a, c)
     m, n = a.shape
     if c.shape[0] != n:
@@ -867,6 +887,10 @@ def matmul_by_toeplitz_block(a, c, cols=None):
         if a.shape[1] != c.rows():
             raise DimensionError("matmul_by_toeplitz_block: shape mismatch")
         c, cols = c.parent.first_column(), c.cols()
+    if _any_complex(a, c):
+        if a.shape[1] > c.shape[0] or cols > c.shape[0] or cols < 1:
+            raise DimensionError("toeplitz block exceeds parent dimensions")
+        return _zcirc_right(a, c, cols)
     device = _is_device(a, c)
     m, k = a.shape
     np_ = c.shape[0]
@@ -922,6 +946,8 @@ def range_find(a, r, p, spec, power_steps=0, with_residual=True):
     GEMM), power_steps alternating products Y <- A (A^T Y) (lowrank.hpp:51-57),
     Q = orthonormal_basis(Y). With with_residual (one call, A resident once)
     the result also carries ||A - Q Q^T A||_F and _2 of this A in `info`."""
+    if _any_complex(a):
+        return _zrange_find(a, r, p, spec, power_steps)
     device = _is_device(a)
     m, n = a.shape
     l = r + p
@@ -949,6 +975,10 @@ def basis_residual(result, truth_left):
     """basis_residual (lowrank.hpp:88-93): ||Q (Q^H S_r) - S_r||_2 for the
     leading left singular basis S_r, products and norm on the GPU."""
     q = result.q
+    if _any_complex(q, truth_left):
+        qh = np.ascontiguousarray(np.asarray(q).conj().T) if isinstance(q, np.ndarray) else q.conj().T.contiguous()
+        d = matmul(q, matmul(qh, truth_left)) - truth_left
+        return spectral_norm(d)
     y = matmul(np.ascontiguousarray(np.asarray(q).T) if isinstance(q, np.ndarray) else q.T.contiguous(), truth_left)
     d = matmul(q, y) - truth_left
     return spectral_norm(d)
@@ -958,6 +988,8 @@ def residual_norms(a, result):
     """||A - Q (Q^T A)||_F and ||.||_2 (power iteration, norms.hpp:52-77 on
     the implicit operator) of `a` against result.q, on the GPU."""
     q = result.q
+    if _any_complex(a, q):
+        return _zresidual_norms(a, q)
     device = _is_device(a, q)
     m, n = a.shape
     l = q.shape[1]
@@ -977,3 +1009,273 @@ def approximation_residual(a, result):
     """approximation_residual(a, result) (lowrank.hpp:99-102):
     ||A - Q (Q^H A)||_2 of the given A, evaluated on the GPU."""
     return residual_norms(a, result)["residual_spectral"]
+
+
+# ---- the complex field (Matrix<Complex>; SURVEY §8(f) rank 4) -------------------
+# Complex arrays are numpy complex128 (host) or torch complex128 CUDA tensors
+# (device); the library computes on the GPU (complex.cu).
+Complex = complex
+
+
+class SketchVariant(enum.IntEnum):
+    """SketchVariant (lowrank.hpp:199)"""
+    SRFT = 0
+    CIRCULANT_PERMUTATION = 1
+    Srft = 0
+    CirculantPermutation = 1
+
+
+def _any_complex(*arrays):
+    for a in arrays:
+        if a is None:
+            continue
+        if isinstance(a, np.ndarray):
+            if np.iscomplexobj(a):
+                return True
+        elif hasattr(a, "is_complex"):
+            if a.is_complex():
+                return True
+        elif isinstance(a, (list, tuple)) and any(isinstance(v, complex) for v in a):
+            return True
+    return False
+
+
+def _zhost(a):
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def _zdev(a):
+    import torch
+    if not a.is_cuda:
+        raise DimensionError("device arrays must be CUDA tensors")
+    return a.to(torch.complex128).contiguous()
+
+
+def _zempty(device, shape, ref=None):
+    if device:
+        import torch
+        return torch.empty(shape, dtype=torch.complex128, device=ref.device if ref is not None else "cuda")
+    return np.empty(shape, np.complex128)
+
+
+def _zprep(device, *arrays):
+    return [None if a is None else (_zdev(a) if device else _zhost(a)) for a in arrays]
+
+
+def to_complex(a):
+    """to_complex (matrix.hpp): the same entries with zero imaginary parts."""
+    if isinstance(a, np.ndarray):
+        return a.astype(np.complex128)
+    import torch
+    return a.to(torch.complex128)
+
+
+def unit_roots(n):
+    """polar(1, 2 pi k / n), k < n, rounded as the reference (glibc via std::polar)."""
+    out = np.empty(n, np.complex128)
+    _raise(capi.lib().rl_unit_roots(n, out.ctypes.data))
+    return out
+
+
+def dft_dense(n):
+    """dft_dense (fft.hpp:21-30): Omega = (root[(i j) mod n]), bit-identical."""
+    if n < 1:
+        raise DimensionError("dft_dense: n must be positive")
+    root = unit_roots(n)
+    i = np.arange(n, dtype=np.int64)
+    return root[np.outer(i, i) % n]
+
+
+def gen_dft_input(n):
+    """gen_dft_input (testbed/inputs.hpp:49-55): the transform matrix itself."""
+    if n < 64 or n & (n - 1):
+        raise DimensionError("gen_dft_input: need a power of two >= 64")
+    return dft_dense(n)
+
+
+def gen_unitary_circulant(n, seed):
+    """gen_unitary_circulant (multipliers.hpp:75-82): spectrum on the unit
+    circle from the reference's stream, first column inverse_fft(u) on the GPU."""
+    out = np.empty(n, np.complex128)
+    _raise(capi.lib().rl_gen_unitary_circulant(_ctx(), capi.RL_HOST, n, seed, out.ctypes.data))
+    return CirculantMatrix(out)
+
+
+def gen_unitary_toeplitz_block(n, l, seed):
+    """gen_unitary_toeplitz_block (multipliers.hpp:88-90)"""
+    return ToeplitzBlock(gen_unitary_circulant(n, seed), n, l)
+
+
+def srft_columns(n, l, seed):
+    """srft_columns (multipliers.hpp:132-138): the sorted sampled column indices."""
+    out = np.empty(l, np.int64)
+    _raise(capi.lib().rl_srft_columns(n, l, seed, out.ctypes.data))
+    return out
+
+
+def materialize_complex(spec, device=False):
+    """materialize<Complex>(spec) (multipliers.hpp:174-218): every family, the
+    complex ones (unitary circulant / Toeplitz, SRFT) included, on the GPU."""
+    if spec.rows <= 0 or spec.cols <= 0:
+        raise DimensionError("materialize: spec.rows and spec.cols must be set")
+    out = _zempty(device, (spec.rows, spec.cols))
+    m, keep = _multiplier(spec, device)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_zmaterialize(_ctx(), _mem(device), ctypes.byref(m), spec.rows, spec.cols, capi.addr(out)))
+    del keep
+    return out
+
+
+def gen_srft(n, l, seed):
+    """gen_srft (multipliers.hpp:123-130): sqrt(n/l) D Omega R, bit-identical."""
+    if l < 1 or l > n:
+        raise DimensionError("gen_srft: need 1 <= l <= n")
+    return materialize_complex(MultiplierSpec(MultiplierKind.SRFT, seed, n, l))
+
+
+def _zmatmul(a, b):
+    device = _is_device(a, b)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise DimensionError("matmul: inner dimensions differ")
+    a, b = _zprep(device, a, b)
+    m, k = a.shape
+    n = b.shape[1]
+    c = _zempty(device, (m, n), a)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_zgemm(_ctx(), _mem(device), m, n, k, capi.addr(a), capi.addr(b), capi.addr(c)))
+    return c
+
+
+def _zsvd_values(a):
+    device = _is_device(a)
+    (a,) = _zprep(device, a)
+    m, n = a.shape
+    out = np.empty(min(m, n))
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_zsingular_values(_ctx(), _mem(device), m, n, capi.addr(a),
+                                          capi.addr(out) if not device else capi.addr(_out_dev(out))))
+    return out if not device else _out_dev.last.cpu().numpy()
+
+
+def _out_dev(out):
+    import torch
+    _out_dev.last = torch.empty(out.shape, dtype=torch.float64, device="cuda")
+    return _out_dev.last
+
+
+def _zcirculant_apply(c, x):
+    device = _is_device(c, x)
+    n = c.shape[0]
+    if x.shape[0] != n:
+        raise DimensionError("circulant_apply: length mismatch")
+    c, x = _zprep(device, c, x)
+    y = _zempty(device, (n,), x)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_zcirculant_apply(_ctx(), _mem(device), n, capi.addr(c), capi.addr(x), capi.addr(y)))
+    return y
+
+
+def _zcirc_right(a, c, cols):
+    device = _is_device(a, c)
+    m, k = a.shape
+    np_ = c.shape[0]
+    a, c = _zprep(device, a, c)
+    out = _zempty(device, (m, cols), a)
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_zcirculant_right_multiply(_ctx(), _mem(device), m, k, capi.addr(a), np_, capi.addr(c), cols,
+                                                   capi.addr(out)))
+    return out
+
+
+def _zpreprocess_solve(a, b, pre_spec, post_spec, refine_steps, want_lu):
+    """preprocess_solve<Complex> (preprocess.hpp:156-180) on the GPU."""
+    device = _is_device(a, b)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionError("preprocess_solve: square input required")
+    n = a.shape[0]
+    if b.shape[0] != n:
+        raise DimensionError("preprocess_solve: length mismatch")
+    _check_side(pre_spec, n)
+    _check_side(post_spec, n)
+    if refine_steps < 0:
+        raise DimensionError("preprocess_solve: negative refine_steps")
+    a, b = _zprep(device, a, b)
+    x = _zempty(device, (n,), b)
+    lu = _zempty(device, (n, n), a) if want_lu else None
+    m, keep = _multiplier(post_spec, device)
+    fm, fkeep = _multiplier(pre_spec, device)
+    info = capi.rl_solve_info()
+    hist = (ctypes.c_double * (refine_steps + 1))()
+    info.history = ctypes.cast(hist, ctypes.POINTER(ctypes.c_double))
+    info.history_capacity = refine_steps + 1
+    _sync_stream_for(device)
+    rc = capi.lib().rl_zpreprocessed_genp_solve(_ctx(), _mem(device), n, capi.addr(a), capi.addr(b),
+                                                ctypes.byref(fm), ctypes.byref(m), refine_steps, capi.addr(x),
+                                                capi.addr(lu), ctypes.byref(info))
+    del keep, fkeep
+    _raise(rc, info.zero_pivot_step)
+    d = info.as_dict()
+    return SolveOutcome(x, d["residual_history"], bool(info.diverged), d, lu)
+
+
+def _zrange_find(a, r, p, spec, power_steps):
+    """range_find<Complex> (lowrank.hpp:62-83) with the residual of this A."""
+    device = _is_device(a)
+    m, n = a.shape
+    l = r + p
+    if r < 1 or l > min(m, n):
+        raise DimensionError("range_find: rank plus oversampling exceeds matrix size")
+    if power_steps < 0:
+        raise DimensionError("range_find: negative power_steps")
+    (a,) = _zprep(device, a)
+    q = _zempty(device, (m, l), a)
+    mlt, keep = _multiplier(spec, device)
+    info = capi.rl_lowrank_info()
+    _sync_stream_for(device)
+    rc = capi.lib().rl_zrange_find_residual(_ctx(), _mem(device), m, n, capi.addr(a), l, ctypes.byref(mlt),
+                                            power_steps, capi.addr(q), ctypes.byref(info))
+    del keep
+    _raise(rc, info.rank_deficient_column)
+    d = {k: getattr(info, k) for k, _ in info._fields_ if k != "reserved"}
+    return LowRankResult(q, r, p, power_steps, d)
+
+
+def _zresidual_norms(a, q):
+    device = _is_device(a, q)
+    m, n = a.shape
+    l = q.shape[1]
+    if q.shape[0] != m:
+        raise DimensionError("approximation_residual: shape mismatch")
+    a, q = _zprep(device, a, q)
+    info = capi.rl_lowrank_info()
+    _sync_stream_for(device)
+    _raise(capi.lib().rl_zapproximation_residual(_ctx(), _mem(device), m, n, capi.addr(a), l, capi.addr(q),
+                                                 ctypes.byref(info)))
+    return {"residual_frobenius": info.residual_frobenius, "residual_spectral": info.residual_spectral,
+            "power_iterations": info.power_iterations}
+
+
+@dataclass
+class SrftCheckResult:
+    """SrftCheckResult (lowrank.hpp:200-205)"""
+    residual: float
+    bound: float
+    sketch_width: int
+    clamped: bool
+
+
+def srft_sketch_check(a, r, seed, variant=SketchVariant.SRFT, known_sigma_r1=None):
+    """srft_sketch_check (lowrank.hpp:216-261): the sampled-transform sketch at
+    its prescribed width (clamped to n), basis, ||(I - P_Y) A|| and the bound
+    sqrt(1 + 7 n / l) sigma_{r+1}, on the GPU."""
+    device = _is_device(a)
+    a = _dev(a) if device else _host(a)
+    m, n = a.shape
+    if r < 1 or r > n:
+        raise DimensionError("srft_sketch_check: rank out of range")
+    out = capi.rl_srft_check()
+    _sync_stream_for(device)
+    sigma = -1.0 if known_sigma_r1 is None else float(known_sigma_r1)
+    _raise(capi.lib().rl_srft_sketch_check(_ctx(), _mem(device), m, n, capi.addr(a), r, seed, int(variant), sigma,
+                                           ctypes.byref(out)))
+    return SrftCheckResult(out.residual, out.bound, int(out.sketch_width), bool(out.clamped))
