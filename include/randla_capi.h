@@ -384,6 +384,9 @@ RL_API rl_status rl_zcirculant_apply(rl_context* ctx, rl_mem mem, int64_t n, con
 /* matmul<Complex> (matrix.hpp:115-121): c (m x n) = a (m x k) b (k x n) */
 RL_API rl_status rl_zgemm(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, int64_t k, const double* a,
                           const double* b, double* c);
+/* `count` next_gaussian draws of RngStream(seed).derived(key) (rng.hpp:20-24),
+ * the probe vectors of posterior_estimate (lowrank.hpp:177-196) (host) */
+RL_API rl_status rl_gen_gaussian_derived(uint64_t seed, uint64_t key, int64_t count, double* out);
 /* the unit roots polar(1, 2 pi k / n), k < n (fft.hpp:21-30, multipliers.hpp:98-100),
  * rounded as the reference's host code: n complex (host) */
 RL_API rl_status rl_unit_roots(int64_t n, double* out);

@@ -254,6 +254,7 @@ class _Ref:
         self._srftm = s("ref_srft_matrix", ctypes.c_int, [i64, i64, u64, ctypes.c_int, _dp])
         self._znormest = s("ref_zspectral_norm_estimate", ctypes.c_double, [i64, i64, _dp])
         self._dft = s("ref_dft_dense", ctypes.c_int, [i64, _dp])
+        self._gder = s("ref_gaussian_derived", None, [u64, u64, i64, _dp])
 
     # status codes of the ref_* entry points (ref_capi.cpp)
     DIM, ZERO_PIVOT, SINGULAR_BLOCK, SINGULAR = 1, 2, 3, 6
@@ -475,6 +476,11 @@ class _Ref:
     def zspectral_norm_estimate(self, a):
         a = self._z(a)
         return float(self._znormest(a.shape[0], a.shape[1], ptr(a.view(np.float64))))
+
+    def gaussian_derived(self, seed, key, count):
+        out = np.empty(count)
+        self._gder(seed, key, count, ptr(out))
+        return out
 
     def dft_dense(self, n):
         out = np.empty((n, n), np.complex128)

@@ -522,6 +522,12 @@ int ref_srft_matrix(int64_t n, int64_t l, uint64_t seed, int variant, double* ou
     });
 }
 
+// RngStream(seed).derived(key).next_gaussian() x count (rng.hpp:20-24, :56-71)
+void ref_gaussian_derived(uint64_t seed, uint64_t key, int64_t count, double* out) {
+    RngStream s = RngStream(seed).derived(key);
+    for (int64_t i = 0; i < count; ++i) out[i] = s.next_gaussian();
+}
+
 double ref_zspectral_norm_estimate(int64_t m, int64_t n, const double* a) {
     return spectral_norm_estimate(wrapz(m, n, a));
 }

@@ -157,6 +157,7 @@ SIGNATURES = {
     "rl_srft_sketch_check": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, u64, i32, ctypes.c_double,
                                             ctypes.POINTER(rl_srft_check)]),
     "rl_unit_roots": (ctypes.c_int, [i64, _vp]),
+    "rl_gen_gaussian_derived": (ctypes.c_int, [u64, u64, i64, _vp]),
     "rl_zcirculant_right_multiply": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, _vp, i64, _vp]),
     "rl_zcirculant_apply": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
     "rl_zgemm": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, i64, _vp, _vp, _vp]),

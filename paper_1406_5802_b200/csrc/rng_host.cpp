@@ -168,9 +168,9 @@ void parallel_for(int64_t count, F&& fn) {
     Pool::get().run(workers - 1, count, f);
 }
 
-// Sequential generator (small matrices): exactly RngStream::next_gaussian.
-void gaussian_sequential(uint64_t seed, int64_t count, double* out) {
-    const uint64_t s0 = stream_state(seed);
+// Sequential generator (small matrices): exactly RngStream::next_gaussian,
+// from a stream state (stream_state(seed), or a derived stream's)
+void gaussian_from_state(uint64_t s0, int64_t count, double* out) {
     uint64_t a = 0;
     int64_t k = 0;
     while (k < count) {
@@ -181,6 +181,8 @@ void gaussian_sequential(uint64_t seed, int64_t count, double* out) {
         if (k < count) out[k++] = v * f;
     }
 }
+
+void gaussian_sequential(uint64_t seed, int64_t count, double* out) { gaussian_from_state(stream_state(seed), count, out); }
 
 constexpr int64_t kChunk = 1 << 16;  // polar attempts per chunk
 
@@ -346,6 +348,14 @@ RL_API uint64_t rl_hash_label(const char* s) {
         h *= 1099511628211ull;
     }
     return h;
+}
+
+// `count` next_gaussian draws of RngStream(seed).derived(key) (rng.hpp:20-24),
+// the probe vectors of posterior_estimate (lowrank.hpp:177-196)
+RL_API rl_status rl_gen_gaussian_derived(uint64_t seed, uint64_t key, int64_t count, double* out) {
+    if (count <= 0 || !out) return RL_ERR_DIMENSION;
+    gaussian_from_state(mix_key(stream_state(seed), key), count, out);
+    return RL_OK;
 }
 
 // polar(1, 2 pi k / n) for k < n (fft.hpp:21-30, multipliers.hpp:98-100)

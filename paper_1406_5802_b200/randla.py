@@ -12,6 +12,7 @@ path in this module.
 """
 import ctypes
 import enum
+import math
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -1279,3 +1280,30 @@ def srft_sketch_check(a, r, seed, variant=SketchVariant.SRFT, known_sigma_r1=Non
     _raise(capi.lib().rl_srft_sketch_check(_ctx(), _mem(device), m, n, capi.addr(a), r, seed, int(variant), sigma,
                                            ctypes.byref(out)))
     return SrftCheckResult(out.residual, out.bound, int(out.sketch_width), bool(out.clamped))
+
+
+def posterior_estimate(a, result, r_probes, seed):
+    """posterior_estimate (lowrank.hpp:177-196): 10 sqrt(2/pi) max_j
+    ||(A - Q Q^H A) g_j|| over r_probes Gaussian probes g_j drawn from
+    RngStream(seed).derived(j + 1); the products on the GPU."""
+    if r_probes < 1:
+        raise DimensionError("posterior_estimate: need at least one probe")
+    n = a.shape[1]
+    g = np.empty((r_probes, n))
+    for j in range(r_probes):
+        _raise(capi.lib().rl_gen_gaussian_derived(seed, j + 1, n, g[j].ctypes.data))
+    cplx = _any_complex(a, result.q)
+    gt = np.ascontiguousarray(g.T).astype(np.complex128 if cplx else np.float64)
+    q = result.q
+    ag = matmul(a, gt if isinstance(a, np.ndarray) else _to_device_like(gt, a))
+    qh = (np.ascontiguousarray(np.asarray(q).conj().T) if isinstance(q, np.ndarray) else q.conj().T.contiguous())
+    proj = matmul(q, matmul(qh, ag))
+    d = ag - proj
+    d = d if isinstance(d, np.ndarray) else d.cpu().numpy()
+    worst = float(np.sqrt((np.abs(d) ** 2).sum(axis=0)).max())
+    return 10.0 * math.sqrt(2.0 / math.pi) * worst
+
+
+def _to_device_like(x, ref):
+    import torch
+    return torch.from_numpy(x).to(ref.device)

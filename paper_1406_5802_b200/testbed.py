@@ -17,15 +17,17 @@ Monte-Carlo tables run their solves and sketches on the GPU.
     error_bounds_from_parts   lowrank.hpp:132-170 (the bound columns)
     run_hardblock_preprocessed  presets.hpp:90-119
     run_lowrank_preset        presets.hpp:121-179
-    PRESETS                   table2 (GEPP baseline), table3 (Gaussian),
-                              table4 (real circulant), table6 / table7
-                              (Gaussian sketch: rn1 / rn2), table8 / table10
-                              (real Toeplitz sketch: rn2 / rn1), table13
-                              (inverse-norm ratio), with the reference's checks
-                              (presets.hpp:194-420)
-
-Out of this path: the complex families (table5, table5a, table9, table11,
-table14) and the a-posteriori estimator (table12).
+    PRESETS                   every preset of presets.hpp:194-459 with the
+                              reference's checks: table2 (GEPP baseline),
+                              table3 (Gaussian), table4 (real circulant),
+                              table5 (unitary circulant, complex pipeline),
+                              table5a (DFT input, Gaussian rescue), table6 /
+                              table7 (Gaussian sketch: rn1 / rn2), table8 /
+                              table10 (real Toeplitz: rn2 / rn1), table9 /
+                              table11 (unitary Toeplitz, complex: rn2 / rn1),
+                              table12 (a-posteriori estimator), table13
+                              (inverse-norm ratio), table14 (SRFT and
+                              circulant-permutation sketch checks)
 """
 from __future__ import annotations
 
@@ -172,22 +174,92 @@ _TOKENS = {rl.MultiplierKind.GAUSSIAN: "gaussian", rl.MultiplierKind.REAL_CIRCUL
 
 
 def run_hardblock_preprocessed(label: str, post_kind: rl.MultiplierKind, seed: int, trials: int, full: bool,
-                               refine: int, dims: Optional[List[int]] = None) -> List[ExperimentReport]:
+                               refine: int, dims: Optional[List[int]] = None,
+                               variant: rl.ToeplitzVariant = rl.ToeplitzVariant.REAL) -> List[ExperimentReport]:
     """presets.hpp:90-119: fresh hard-block input per trial, preprocess_solve with
-    the multiplier seeded from the trial, one column per refinement stage."""
+    the multiplier seeded from the trial, one column per refinement stage; a
+    complex family runs the complex pipeline on to_complex(a), to_complex(b)."""
+    base = rl.MultiplierSpec(post_kind, 0, variant=variant)
+    complex_path = rl.multiplier_is_complex(base)
     out = []
     for n in (dims if dims is not None else solve_dims(full)):
         def trial(ts, _t, n=n):
             a = gen_hard_block(n, rl.derive_seed(ts, 1))
             b = rl.gen_gaussian_vector(n, rl.derive_seed(ts, 2))
-            post = rl.MultiplierSpec(post_kind, rl.derive_seed(ts, 3))
+            post = rl.MultiplierSpec(post_kind, rl.derive_seed(ts, 3), variant=variant)
+            if complex_path:
+                a, b = rl.to_complex(a), rl.to_complex(b)
             hist = list(rl.preprocess_solve(a, b, None, post, refine).residual_history)
             while len(hist) < refine + 1:
                 hist.append(hist[-1])
             return hist
 
         out.append(run_experiment(f"{label}/n={n}", trials, seed, [f"residual_iter{s}" for s in range(refine + 1)],
-                                  trial, _TOKENS.get(post_kind, "none"), refine, n))
+                                  trial, _TOKENS.get(post_kind, format_multiplier_token(base)), refine, n))
+    return out
+
+
+def run_dft_gaussian(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
+    """presets.hpp:254-284 (table5a): unpivoted elimination on the DFT matrix
+    with a Gaussian rescue, one refinement step"""
+    out = []
+    for n in (dims if dims is not None else solve_dims(full)):
+        a = rl.gen_dft_input(n)
+
+        def trial(ts, _t, n=n, a=a):
+            b = rl.to_complex(rl.gen_gaussian_vector(n, rl.derive_seed(ts, 2)))
+            post = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, rl.derive_seed(ts, 3))
+            hist = list(rl.preprocess_solve(a, b, None, post, 1).residual_history)
+            while len(hist) < 2:
+                hist.append(hist[-1])
+            return hist
+
+        out.append(run_experiment(f"table5a/n={n}", trials, seed, ["residual_iter0", "residual_iter1"], trial,
+                                  "gaussian", 1, n))
+    return out
+
+
+def run_posterior(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
+    """presets.hpp:344-378 (table12): the a-posteriori estimator (5 probes)
+    against the true residual of the Gaussian zero-oversampling sketch"""
+    out = []
+    for n in (dims if dims is not None else lowrank_dims(full)):
+        def trial(ts, _t, n=n):
+            r = 8
+            inst = gen_lownumrank(n, r, rl.derive_seed(ts, 1))
+            spec = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, rl.derive_seed(ts, 2))
+            result = rl.range_find(inst.a, r, 0, spec, 0, with_residual=False)
+            truth = rl.approximation_residual(inst.a, result)
+            est = rl.posterior_estimate(inst.a, result, 5, rl.derive_seed(ts, 3))
+            return [est, truth, 1.0 if est >= truth else 0.0]
+
+        out.append(run_experiment(f"table12/n={n}", trials, seed, ["estimate", "true_rn2", "covered"], trial,
+                                  "gaussian", 0, n))
+    return out
+
+
+def _check_table12(rs):
+    c = CheckResult("estimate covers the true residual in >= 99% of trials at n=64")
+    r = _report_at(rs, 64)
+    if r is not None and r.column("covered").values:
+        c.passed = r.column("covered").stats.mean >= 0.99
+    return [c]
+
+
+def run_srft_check(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
+    """presets.hpp:408-457 (table14): the sampled-transform sketch at its
+    prescribed width against its guarantee, both variants"""
+    out = []
+    for n in (dims if dims is not None else ([64, 128, 256, 1024] if full else [64, 128])):
+        for variant, vname in ((rl.SketchVariant.SRFT, "srft"), (rl.SketchVariant.CIRCULANT_PERMUTATION, "circperm")):
+            def trial(ts, _t, n=n, variant=variant):
+                r = 8
+                inst = gen_lownumrank(n, r, rl.derive_seed(ts, 1))
+                res = rl.srft_sketch_check(inst.a, r, rl.derive_seed(ts, 2), variant, inst.singulars[r])
+                return [res.residual, res.bound, 1.0 if res.residual <= res.bound else 0.0]
+
+            out.append(run_experiment(f"table14/{vname}/n={n}", trials, seed, ["residual", "bound", "within"], trial,
+                                      vname, 0, n))
     return out
 
 
@@ -248,7 +320,7 @@ def error_bounds_from_parts(t_r, singulars, h, r) -> BoundReport:
         raise rl.DimensionError("error_bounds: rank out of range")
     rep = BoundReport(sigma_r=float(singulars[r - 1]), sigma_r1=float(singulars[r]) if r < len(singulars) else 0.0,
                       h_frobenius=float(np.linalg.norm(h)))
-    gsv = rl.svd_values(rl.matmul(np.ascontiguousarray(t_r.T), h))
+    gsv = rl.svd_values(rl.matmul(np.ascontiguousarray(t_r.conj().T), h))  # T_r^H H
     if not gsv[-1] > 0.0:
         raise rl.SingularMatrixError("unlucky multiplier: T_r^H H is singular, the bound is undefined")
     rep.t_h_inv_norm = 1.0 / gsv[-1]
@@ -269,6 +341,15 @@ def run_lowrank_preset(label: str, spec_base, basis_metric: bool, seed: int, tri
             spec = copy.copy(spec_base)
             spec.seed = rl.derive_seed(ts, 2)
             spec.rows, spec.cols = n, r
+            if rl.multiplier_is_complex(spec):  # the complex pipeline on to_complex(a) (presets.hpp:150-160)
+                ac = rl.to_complex(inst.a)
+                result = rl.range_find(ac, r, 0, spec, 0)
+                rep = error_bounds_from_parts(rl.to_complex(inst.right), inst.singulars, rl.materialize_complex(spec), r)
+                if basis_metric:
+                    rn, bound = rl.basis_residual(result, rl.to_complex(inst.left)), rep.delta_plus
+                else:
+                    rn, bound = rl.approximation_residual(ac, result), rep.delta_plus_prime
+                return [rn, rn / bound]
             result = rl.range_find(inst.a, r, 0, spec, 0, with_residual=False)
             rep = error_bounds_from_parts(inst.right, inst.singulars, rl.materialize(spec), r)
             if basis_metric:
@@ -284,7 +365,7 @@ def run_lowrank_preset(label: str, spec_base, basis_metric: bool, seed: int, tri
 
 
 def run_gepp_baseline(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
-    """presets.hpp:201-217 (table2): pivoted elimination on the hard-block inputs"""
+    """presets.hpp:195-219 (table2): pivoted elimination on the hard-block inputs"""
     out = []
     for n in (dims if dims is not None else solve_dims(full)):
         def trial(ts, _t, n=n):
@@ -297,7 +378,7 @@ def run_gepp_baseline(seed: int, trials: int, full: bool, dims: Optional[List[in
 
 
 def run_inverse_norm_ratio(seed: int, trials: int, full: bool, dims: Optional[List[int]] = None):
-    """presets.hpp:379-406 (table13): ||(T_r^T H)^+|| against ||(H_rr)^+||"""
+    """presets.hpp:380-406 (table13): ||(T_r^T H)^+|| against ||(H_rr)^+||"""
     out = []
     for n in (dims if dims is not None else lowrank_dims(full)):
         def trial(ts, _t, n=n):
@@ -351,40 +432,71 @@ def check_fraction(reports, dim, column, threshold, quota) -> CheckResult:
 
 _G = rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN)
 _TR = rl.MultiplierSpec(rl.MultiplierKind.TOEPLITZ_BLOCK, variant=rl.ToeplitzVariant.REAL)
+_TU = rl.MultiplierSpec(rl.MultiplierKind.TOEPLITZ_BLOCK, variant=rl.ToeplitzVariant.UNITARY)
+
+
+def _check_table14(rs):
+    """presets.hpp:447-457: residual under the guarantee in >= 99% of trials, per report"""
+    out = []
+    for r in rs:
+        col = r.column("within")
+        out.append(CheckResult(f"{r.label}: residual under the guarantee in >= 99% of trials",
+                               bool(col.values) and col.stats.mean >= 0.99))
+    return out
 
 PRESETS = {
-    # presets.hpp:201-217
+    # presets.hpp:195-219
     "table2": (lambda seed, trials, full, dims=None: run_gepp_baseline(seed, trials, full, dims),
                lambda rs: [check_stat(rs, 64, "residual", False, 1e-11)]),
-    # presets.hpp:219-233
+    # presets.hpp:221-232
     "table3": (lambda seed, trials, full, dims=None: run_hardblock_preprocessed(
                    "table3", rl.MultiplierKind.GAUSSIAN, seed, trials, full, 1, dims),
                lambda rs: [check_stat(rs, 64, "residual_iter0", True, 1e-4),
                            check_stat(rs, 64, "residual_iter0", False, 1e-6),
                            check_stat(rs, 64, "residual_iter1", False, 1e-11),
                            check_stat(rs, 128, "residual_iter1", False, 1e-11)]),
-    # presets.hpp:235-243
+    # presets.hpp:234-242
     "table4": (lambda seed, trials, full, dims=None: run_hardblock_preprocessed(
                    "table4", rl.MultiplierKind.REAL_CIRCULANT, seed, trials, full, 1, dims),
                lambda rs: [check_stat(rs, 64, "residual_iter0", False, 1e-8)]),
-    # presets.hpp:293-300
+    # presets.hpp:244-252: unitary circulant multipliers, the complex pipeline
+    "table5": (lambda seed, trials, full, dims=None: run_hardblock_preprocessed(
+                   "table5", rl.MultiplierKind.UNITARY_CIRCULANT, seed, trials, full, 1, dims),
+               lambda rs: [check_stat(rs, 64, "residual_iter0", False, 1e-8)]),
+    # presets.hpp:254-284: the DFT matrix with a Gaussian rescue
+    "table5a": (lambda seed, trials, full, dims=None: run_dft_gaussian(seed, trials, full, dims),
+                lambda rs: [check_fraction(rs, 256, "residual_iter0", 1e-4, 0.95)]),
+    # presets.hpp:286-293
     "table6": (lambda seed, trials, full, dims=None: run_lowrank_preset("table6", _G, True, seed, trials, full,
                                                                          dims=dims),
                lambda rs: [check_fraction(rs, 64, "ratio_rn1", 1.01, 0.99)]),
-    # presets.hpp:302-311
+    # presets.hpp:295-304
     "table7": (lambda seed, trials, full, dims=None: run_lowrank_preset("table7", _G, False, seed, trials, full,
                                                                          dims=dims),
                lambda rs: [check_stat(rs, 64, "rn2", False, 1e-6), check_stat(rs, 64, "ratio_rn2", False, 0.1),
                            check_fraction(rs, 64, "ratio_rn2", 1.0, 0.99)]),
-    # presets.hpp:313-320
+    # presets.hpp:306-314
     "table8": (lambda seed, trials, full, dims=None: run_lowrank_preset("table8", _TR, False, seed, trials, full,
                                                                          dims=dims),
                lambda rs: [check_stat(rs, 64, "rn2", False, 1e-6), check_fraction(rs, 64, "ratio_rn2", 1.0, 0.99)]),
-    # presets.hpp:324-333
+    # presets.hpp:316-324: unitary Toeplitz sketch (complex pipeline)
+    "table9": (lambda seed, trials, full, dims=None: run_lowrank_preset("table9", _TU, False, seed, trials, full,
+                                                                         dims=dims),
+               lambda rs: [check_stat(rs, 64, "rn2", False, 1e-6), check_fraction(rs, 64, "ratio_rn2", 1.0, 0.99)]),
+    # presets.hpp:326-333
     "table10": (lambda seed, trials, full, dims=None: run_lowrank_preset("table10", _TR, True, seed, trials, full,
                                                                           dims=dims),
                 lambda rs: [check_fraction(rs, 64, "ratio_rn1", 1.01, 0.99)]),
-    # presets.hpp:379-406 (no checks in the reference)
+    # presets.hpp:335-342: unitary Toeplitz sketch, basis residual
+    "table11": (lambda seed, trials, full, dims=None: run_lowrank_preset("table11", _TU, True, seed, trials, full,
+                                                                          dims=dims),
+                lambda rs: [check_fraction(rs, 64, "ratio_rn1", 1.01, 0.99)]),
+    # presets.hpp:408-457: the sampled-transform sketch against its guarantee
+    "table14": (lambda seed, trials, full, dims=None: run_srft_check(seed, trials, full, dims),
+                _check_table14),
+    # presets.hpp:344-378: the a-posteriori estimator
+    "table12": (lambda seed, trials, full, dims=None: run_posterior(seed, trials, full, dims), _check_table12),
+    # presets.hpp:380-406 (no checks in the reference)
     "table13": (lambda seed, trials, full, dims=None: run_inverse_norm_ratio(seed, trials, full, dims),
                 lambda rs: []),
 }

@@ -95,3 +95,25 @@ def test_lowrank_bounds_vs_reference_formula(cuda, orc):
     # the instance: sigma_j = 1/(j+1) up to r, 1e-10 beyond, between orthonormal factors
     s = np.linalg.svd(inst.a, compute_uv=False)
     assert np.allclose(s[:8], 1.0 / np.arange(1, 9), rtol=1e-12) and np.allclose(s[8:], 1e-10, rtol=1e-4)
+
+
+def test_complex_presets_pass_reference_checks(cuda):
+    """the complex-field presets (presets.hpp:244-342, 408-457): table5 (unitary
+    circulant multipliers on to_complex of the hard-block inputs), table5a (the
+    DFT matrix with a Gaussian rescue), table9 / table11 (unitary Toeplitz
+    sketch), table14 (SRFT / circulant-permutation sketch checks), and table12
+    (the a-posteriori estimator), with the reference's checks"""
+    for name, trials, dims in (("table5", 8, [64]), ("table5a", 16, [256]), ("table9", 100, [64]),
+                               ("table11", 100, [64]), ("table12", 100, [64]), ("table14", 8, [64])):
+        reports, checks = testbed.run_preset(name, 11, trials, dims=dims)
+        assert checks and all(c.passed for c in checks), (name, [(c.description, c.passed) for c in checks])
+        assert all(r.failures == 0 for r in reports), name
+
+
+def test_posterior_probes_match_reference_stream(orc):
+    """posterior_estimate's probes: RngStream(seed).derived(j + 1).next_gaussian (lowrank.hpp:183-186)"""
+    if orc.REF is None:
+        pytest.skip("oracle/_ref not built")
+    g = np.empty(33)
+    rl.capi.lib().rl_gen_gaussian_derived(12345, 3, 33, g.ctypes.data)
+    np.testing.assert_array_equal(g, orc.REF.gaussian_derived(12345, 3, 33))
