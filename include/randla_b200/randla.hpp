@@ -46,9 +46,17 @@
 //   gen_gaussian_vector, LowRankInstance     testbed/inputs.hpp:18-90
 //   batched_preprocess_solve_32              BASELINE config 2 (no reference counterpart:
 //                                            the reference loops preprocess_solve per trial)
-// Complex instantiations are off the B200 path: Matrix<Complex>
-// arithmetic is host arithmetic here, and the complex multiplier families raise
-// DimensionError as the reference's real pipeline does.
+//   the complex field: ComplexCirculant, gen_unitary_circulant,
+//   gen_unitary_toeplitz_block, gen_srft, srft_from_parts, srft_columns,
+//   materialize<Complex>, genp_factor / lu_solve / preprocess_solve /
+//   range_find / qr over Complex, srft_sketch_check  multipliers.hpp:75-138,
+//                                            lowrank.hpp:199-261 (complex.cu on the GPU)
+//   parse/format_multiplier_token            multipliers.hpp:222-275
+//   StatSummary, summarize, parallel_for_index,
+//   RandomNormStats, probe_norm_stats        stats.hpp, parallel.hpp, norm_stats.hpp
+// Elementwise Matrix<T> arithmetic (+, -, scalar *, matvec) is host code, as in
+// the reference; every product, factorization, transform and sketch runs on
+// the GPU.
 #pragma once
 
 #include <algorithm>
@@ -57,12 +65,14 @@
 #include <concepts>
 #include <cstdint>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <numbers>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -283,8 +293,8 @@ class Matrix {
 using RealMatrix = Matrix<double>;
 using ComplexMatrix = Matrix<Complex>;
 
-// C = A B: the FP64 DMMA GEMM for real matrices (matrix.hpp:115-121); complex
-// products are off the path and run on the host
+// C = A B (matrix.hpp:115-121): the FP64 DMMA GEMM; a complex product runs
+// as one real GEMM on [Ar | Ai] x [[Br, Bi], [-Bi, Br]]
 template <ScalarField T>
 Matrix<T> matmul(const Matrix<T>& a, const Matrix<T>& b) {
     if (a.cols() != b.rows()) throw DimensionError("matmul: inner dimensions differ");
@@ -294,11 +304,9 @@ Matrix<T> matmul(const Matrix<T>& a, const Matrix<T>& b) {
         detail::check(rl_dgemm(nullptr, RL_HOST, detail::i64(m), detail::i64(n), detail::i64(k), a.data(),
                                detail::i64(k), b.data(), detail::i64(n), out.data(), detail::i64(n)));
     } else {
-        for (std::size_t i = 0; i < m; ++i)
-            for (std::size_t t = 0; t < k; ++t) {
-                const T av = a(i, t);
-                for (std::size_t j = 0; j < n; ++j) out(i, j) += av * b(t, j);
-            }
+        detail::check(rl_zgemm(nullptr, RL_HOST, detail::i64(m), detail::i64(n), detail::i64(k),
+                               reinterpret_cast<const double*>(a.data()), reinterpret_cast<const double*>(b.data()),
+                               reinterpret_cast<double*>(out.data())));
     }
     return out;
 }
@@ -363,6 +371,14 @@ inline ComplexMatrix to_complex(const RealMatrix& a) {
     return out;
 }
 inline const ComplexMatrix& to_complex(const ComplexMatrix& a) { return a; }
+namespace detail {
+inline std::vector<Complex> to_complex_vec(const std::vector<double>& v) {
+    std::vector<Complex> out(v.size());
+    for (std::size_t i = 0; i < v.size(); ++i) out[i] = Complex(v[i], 0.0);
+    return out;
+}
+inline const std::vector<Complex>& to_complex_vec(const std::vector<Complex>& v) { return v; }
+}  // namespace detail
 inline std::vector<Complex> to_complex(const std::vector<double>& v) {
     std::vector<Complex> out(v.size());
     for (std::size_t i = 0; i < v.size(); ++i) out[i] = Complex(v[i], 0.0);
@@ -432,6 +448,20 @@ inline double spectral_norm_estimate(const RealMatrix& a) {
                                             &out));
     return out;
 }
+// complex A: the same power iteration on the real embedding [[X, -Y], [Y, X]]
+// (the same singular values and row / column norms; the start vector differs,
+// so the estimate agrees to the iteration's 1e-9 stopping tolerance)
+inline double spectral_norm_estimate(const ComplexMatrix& a) {
+    const std::size_t m = a.rows(), n = a.cols();
+    RealMatrix e(2 * m, 2 * n);
+    for (std::size_t i = 0; i < m; ++i)
+        for (std::size_t j = 0; j < n; ++j) {
+            e(i, j) = e(m + i, n + j) = a(i, j).real();
+            e(m + i, j) = a(i, j).imag();
+            e(i, n + j) = -a(i, j).imag();
+        }
+    return spectral_norm_estimate(e);
+}
 
 // ---- transforms (fft.hpp) ----------------------------------------------------------
 inline bool is_power_of_two(std::size_t n) { return n != 0 && (n & (n - 1)) == 0; }
@@ -463,8 +493,6 @@ inline std::vector<Complex> inverse_fft(std::vector<Complex> v) { return detail:
 // ---- circulants (circulant.hpp:17-203), real field -------------------------------
 template <ScalarField T>
 class CirculantMatrix {
-    static_assert(std::is_same_v<T, double>, "complex circulants are off the B200 path");
-
   public:
     explicit CirculantMatrix(std::vector<T> first_column) : c_(std::move(first_column)) {
         if (c_.empty()) throw DimensionError("circulant: empty first column");
@@ -516,6 +544,17 @@ inline std::vector<Complex> circulant_apply(const RealCirculant& c, const std::v
     return y;
 }
 
+using ComplexCirculant = CirculantMatrix<Complex>;
+// C x for a complex circulant (circulant.hpp:81-89), on the GPU
+inline std::vector<Complex> circulant_apply(const ComplexCirculant& c, const std::vector<Complex>& x) {
+    if (x.size() != c.size()) throw DimensionError("circulant_apply: length mismatch");
+    std::vector<Complex> y(x.size());
+    detail::check(rl_zcirculant_apply(nullptr, RL_HOST, detail::i64(c.size()),
+                                      reinterpret_cast<const double*>(c.first_column().data()),
+                                      reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(y.data())));
+    return y;
+}
+
 template <ScalarField T>
 std::pair<double, double> spectrum_range(const CirculantMatrix<T>& c) {
     double lo = std::abs(c.spectrum().front()), hi = lo;
@@ -551,6 +590,15 @@ inline std::vector<double> circulant_solve(const RealCirculant& c, const std::ve
     std::vector<double> out(y.size());
     for (std::size_t i = 0; i < y.size(); ++i) out[i] = y[i].real();
     return out;
+}
+
+// C^-1 b for a complex circulant (circulant.hpp:111-135), transforms on the GPU
+inline std::vector<Complex> circulant_solve(const ComplexCirculant& c, const std::vector<Complex>& b) {
+    if (b.size() != c.size()) throw DimensionError("circulant_solve: length mismatch");
+    if (circulant_is_singular(c)) throw SingularMatrixError("circulant is numerically singular");
+    std::vector<Complex> y = fft(b);
+    for (std::size_t i = 0; i < y.size(); ++i) y[i] /= c.spectrum()[i];
+    return inverse_fft(std::move(y));
 }
 
 template <ScalarField T>
@@ -594,6 +642,34 @@ inline RealMatrix matmul_by_toeplitz_block(const RealMatrix& a, const ToeplitzBl
                                              detail::i64(c.size()), c.data(), detail::i64(t.cols()), out.data()));
     return out;
 }
+// the complex field (circulant.hpp:171-203 with a complex operand): every row
+// through the complex FFT on the GPU
+namespace detail {
+template <ScalarField TA, ScalarField TC>
+ComplexMatrix zcirc_rows(const Matrix<TA>& a, const std::vector<TC>& parent, std::size_t cols) {
+    const ComplexMatrix ac = to_complex(a);
+    const std::vector<Complex> c = to_complex_vec(parent);
+    ComplexMatrix out(a.rows(), cols);
+    check(rl_zcirculant_right_multiply(nullptr, RL_HOST, i64(a.rows()), i64(a.cols()),
+                                       reinterpret_cast<const double*>(ac.data()), i64(c.size()),
+                                       reinterpret_cast<const double*>(c.data()), i64(cols),
+                                       reinterpret_cast<double*>(out.data())));
+    return out;
+}
+}  // namespace detail
+template <ScalarField TA, ScalarField TC>
+    requires(field<TA>::is_complex || field<TC>::is_complex)
+ComplexMatrix matmul_by_circulant(const Matrix<TA>& a, const CirculantMatrix<TC>& c) {
+    if (a.cols() != c.size()) throw DimensionError("matmul_by_circulant: shape mismatch");
+    return detail::zcirc_rows(a, c.first_column(), c.size());
+}
+template <ScalarField TA, ScalarField TC>
+    requires(field<TA>::is_complex || field<TC>::is_complex)
+ComplexMatrix matmul_by_toeplitz_block(const Matrix<TA>& a, const ToeplitzBlock<TC>& t) {
+    if (a.cols() != t.rows()) throw DimensionError("matmul_by_toeplitz_block: shape mismatch");
+    return detail::zcirc_rows(a, t.parent().first_column(), t.cols());
+}
+
 // first-column forms (no spectrum on the host)
 inline RealMatrix matmul_by_circulant(const RealMatrix& a, const std::vector<double>& first_column) {
     if (a.cols() != first_column.size()) throw DimensionError("matmul_by_circulant: shape mismatch");
@@ -681,59 +757,169 @@ inline RealMatrix gen_finite_set_uniform(std::size_t m, std::size_t n, std::uint
     return out;
 }
 
-// materialize<T>(spec) (multipliers.hpp:174-218): the real families' dense
-// samples from the reference's generators (expansions and the skew product on
-// the GPU); complex families raise DimensionError (off the B200 path)
+// ---- the complex families (multipliers.hpp:75-138) -----------------------------------
+// spectrum u_j = polar(1, 2 pi phi_j) from the reference's stream (host, the
+// same libm), first column inverse_fft(u) on the GPU
+inline ComplexCirculant gen_unitary_circulant(std::size_t n, std::uint64_t seed) {
+    if (n == 0) throw DimensionError("circulant: empty first column");
+    std::vector<Complex> c(n);
+    detail::check(rl_gen_unitary_circulant(nullptr, RL_HOST, detail::i64(n), seed, reinterpret_cast<double*>(c.data())));
+    return ComplexCirculant(std::move(c));
+}
+inline ToeplitzBlock<Complex> gen_unitary_toeplitz_block(std::size_t n, std::size_t l, std::uint64_t seed) {
+    return ToeplitzBlock<Complex>(gen_unitary_circulant(n, seed), n, l);
+}
+// sqrt(n/l) D Omega R from explicit parts (multipliers.hpp:92-110)
+inline ComplexMatrix srft_from_parts(std::size_t n, const std::vector<double>& phases,
+                                     const std::vector<std::size_t>& columns) {
+    const std::size_t l = columns.size();
+    if (phases.size() != n || l == 0 || l > n) throw DimensionError("srft_from_parts: bad shapes");
+    std::vector<Complex> root(n);
+    for (std::size_t k = 0; k < n; ++k)
+        root[k] = std::polar(1.0, 2.0 * std::numbers::pi * static_cast<double>(k) / static_cast<double>(n));
+    const double scale = std::sqrt(static_cast<double>(n) / static_cast<double>(l));
+    ComplexMatrix out(n, l);
+    for (std::size_t i = 0; i < n; ++i) {
+        const Complex d = scale * std::polar(1.0, 2.0 * std::numbers::pi * phases[i]);
+        for (std::size_t j = 0; j < l; ++j) out(i, j) = d * root[(i * columns[j]) % n];
+    }
+    return out;
+}
+// l sorted indices out of n without replacement (multipliers.hpp:112-121)
+inline std::vector<std::size_t> sample_without_replacement(std::size_t n, std::size_t l, RngStream& rng) {
+    std::vector<std::size_t> pool(n);
+    for (std::size_t i = 0; i < n; ++i) pool[i] = i;
+    for (std::size_t i = 0; i < l; ++i) std::swap(pool[i], pool[i + static_cast<std::size_t>(rng.next_below(n - i))]);
+    std::vector<std::size_t> out(pool.begin(), pool.begin() + static_cast<std::ptrdiff_t>(l));
+    std::sort(out.begin(), out.end());
+    return out;
+}
+inline std::vector<std::size_t> srft_columns(std::size_t n, std::size_t l, std::uint64_t seed) {
+    std::vector<int64_t> c(l);
+    detail::check(rl_srft_columns(detail::i64(n), detail::i64(l), seed, c.data()));
+    return std::vector<std::size_t>(c.begin(), c.end());
+}
+
+// materialize<T>(spec) (multipliers.hpp:174-218): the dense sample of the
+// named family in the requested field, from the reference's generators (the
+// expansions, the skew product and the complex families on the GPU)
 template <ScalarField T>
 Matrix<T> materialize(const MultiplierSpec& spec) {
-    if (multiplier_is_complex(spec)) {
-        if constexpr (!field<T>::is_complex)
-            throw DimensionError("complex multiplier family requested in a real pipeline");
-        throw DimensionError("complex multiplier families are not on the B200 path");
-    }
-    RealMatrix out(spec.rows, spec.cols);
-    const rl_multiplier m = detail::to_abi(spec);
-    detail::check(rl_materialize(nullptr, RL_HOST, &m, detail::i64(spec.rows), detail::i64(spec.cols), out.data()));
-    if constexpr (field<T>::is_complex)
-        return to_complex(out);
-    else
+    if constexpr (!field<T>::is_complex) {
+        if (multiplier_is_complex(spec)) throw DimensionError("complex multiplier family requested in a real pipeline");
+        RealMatrix out(spec.rows, spec.cols);
+        const rl_multiplier m = detail::to_abi(spec);
+        detail::check(rl_materialize(nullptr, RL_HOST, &m, detail::i64(spec.rows), detail::i64(spec.cols), out.data()));
         return out;
+    } else {
+        ComplexMatrix out(spec.rows, spec.cols);
+        const rl_multiplier m = detail::to_abi(spec);
+        detail::check(rl_zmaterialize(nullptr, RL_HOST, &m, detail::i64(spec.rows), detail::i64(spec.cols),
+                                      reinterpret_cast<double*>(out.data())));
+        return out;
+    }
 }
 inline RealMatrix gen_circ_skew_product(std::size_t n, std::uint64_t seed) {
     MultiplierSpec s{MultiplierKind::CircSkewProduct, n, n, seed};
     return materialize<double>(s);
 }
+inline ComplexMatrix gen_srft(std::size_t n, std::size_t l, std::uint64_t seed) {
+    if (l < 1 || l > n) throw DimensionError("gen_srft: need 1 <= l <= n");
+    MultiplierSpec s{MultiplierKind::Srft, n, l, seed};
+    return materialize<Complex>(s);
+}
+
+// CLI token forms (multipliers.hpp:222-275)
+inline std::string format_multiplier_token(const MultiplierSpec& spec) {
+    switch (spec.kind) {
+        case MultiplierKind::None: return "none";
+        case MultiplierKind::Gaussian: return "gaussian";
+        case MultiplierKind::RealCirculant: return "circulant";
+        case MultiplierKind::UnitaryCirculant: return "unitary-circulant";
+        case MultiplierKind::ToeplitzBlock:
+            return spec.variant == ToeplitzVariant::Real ? "toeplitz:variant=real" : "toeplitz:variant=unitary";
+        case MultiplierKind::Srft: return "srft";
+        case MultiplierKind::FiniteSetUniform: return "finite:card=" + std::to_string(spec.set_cardinality);
+        case MultiplierKind::CircSkewProduct: return "circskew";
+        case MultiplierKind::GaussianCirculant: return "gaussian-circulant";
+    }
+    return "none";
+}
+inline MultiplierSpec parse_multiplier_token(const std::string& token) {
+    MultiplierSpec spec;
+    const std::size_t colon = token.find(':');
+    const std::string head = token.substr(0, colon);
+    const std::string opts = colon == std::string::npos ? "" : token.substr(colon + 1);
+    static const std::pair<const char*, MultiplierKind> kinds[] = {
+        {"none", MultiplierKind::None},       {"gaussian", MultiplierKind::Gaussian},
+        {"circulant", MultiplierKind::RealCirculant}, {"unitary-circulant", MultiplierKind::UnitaryCirculant},
+        {"toeplitz", MultiplierKind::ToeplitzBlock},  {"srft", MultiplierKind::Srft},
+        {"finite", MultiplierKind::FiniteSetUniform}, {"circskew", MultiplierKind::CircSkewProduct},
+        {"gaussian-circulant", MultiplierKind::GaussianCirculant}};
+    bool found = false;
+    for (const auto& [name, kind] : kinds)
+        if (head == name) {
+            spec.kind = kind;
+            found = true;
+        }
+    if (!found) throw IoError("unknown multiplier token: " + token);
+    for (std::size_t pos = 0; pos < opts.size();) {
+        const std::size_t comma = opts.find(',', pos);
+        const std::size_t end = comma == std::string::npos ? opts.size() : comma;
+        const std::string kv = opts.substr(pos, end - pos);
+        const std::size_t eq = kv.find('=');
+        if (eq == std::string::npos) throw IoError("bad multiplier option: " + kv);
+        const std::string key = kv.substr(0, eq), value = kv.substr(eq + 1);
+        if (key == "variant" && spec.kind == MultiplierKind::ToeplitzBlock) {
+            if (value == "real")
+                spec.variant = ToeplitzVariant::Real;
+            else if (value == "unitary")
+                spec.variant = ToeplitzVariant::Unitary;
+            else
+                throw IoError("bad toeplitz variant: " + value);
+        } else if (key == "card" && spec.kind == MultiplierKind::FiniteSetUniform) {
+            spec.set_cardinality = std::stoull(value);
+        } else {
+            throw IoError("bad multiplier option: " + kv);
+        }
+        pos = end + 1;
+    }
+    return spec;
+}
 
 // ---- GENP (lu.hpp) --------------------------------------------------------------------
+template <ScalarField T = double>
 struct LuFactors {
-    RealMatrix lower;
-    RealMatrix upper;
+    Matrix<T> lower;
+    Matrix<T> upper;
     std::optional<std::vector<std::size_t>> perm;  // empty for GENP; GEPP: original row at position i
-    std::vector<double> pivots() const {
-        std::vector<double> p(upper.rows());
+    std::vector<T> pivots() const {
+        std::vector<T> p(upper.rows());
         for (std::size_t j = 0; j < upper.rows(); ++j) p[j] = upper(j, j);
         return p;
     }
 };
 
 namespace detail {
-inline LuFactors unpack(const RealMatrix& packed) {
+template <ScalarField T>
+LuFactors<T> unpack(const Matrix<T>& packed) {
     const std::size_t n = packed.rows();
-    LuFactors f{RealMatrix::identity(n), RealMatrix(n, n), std::nullopt};
+    LuFactors<T> f{Matrix<T>::identity(n), Matrix<T>(n, n), std::nullopt};
     for (std::size_t i = 0; i < n; ++i)
         for (std::size_t j = 0; j < n; ++j) (j < i ? f.lower(i, j) : f.upper(i, j)) = packed(i, j);
     return f;
 }
-inline RealMatrix pack(const LuFactors& f) {
+template <ScalarField T>
+Matrix<T> pack(const LuFactors<T>& f) {
     const std::size_t n = f.upper.rows();
-    RealMatrix p(n, n);
+    Matrix<T> p(n, n);
     for (std::size_t i = 0; i < n; ++i)
         for (std::size_t j = 0; j < n; ++j) p(i, j) = j < i ? f.lower(i, j) : f.upper(i, j);
     return p;
 }
 }  // namespace detail
 
-inline LuFactors genp_factor(const RealMatrix& a) {
+inline LuFactors<double> genp_factor(const RealMatrix& a) {
     const std::size_t n = a.rows();
     if (a.cols() != n) throw DimensionError("genp_factor: square input required");
     RealMatrix packed(n, n);
@@ -742,11 +928,22 @@ inline LuFactors genp_factor(const RealMatrix& a) {
     detail::check(st, info.zero_pivot_step);
     return detail::unpack(packed);
 }
+// over the complex field: the panel-planar blocked GENP of complex.cu
+inline LuFactors<Complex> genp_factor(const ComplexMatrix& a) {
+    const std::size_t n = a.rows();
+    if (a.cols() != n) throw DimensionError("genp_factor: square input required");
+    ComplexMatrix packed(n, n);
+    rl_solve_info info{};
+    const rl_status st = rl_zgenp_factor(nullptr, RL_HOST, detail::i64(n), reinterpret_cast<const double*>(a.data()),
+                                         reinterpret_cast<double*>(packed.data()), &info);
+    detail::check(st, info.zero_pivot_step);
+    return detail::unpack(packed);
+}
 
 namespace detail {
-inline std::vector<double> gepp_solve(const LuFactors& f, const std::vector<double>& b, bool transpose);
+inline std::vector<double> gepp_solve(const LuFactors<double>& f, const std::vector<double>& b, bool transpose);
 }
-inline std::vector<double> lu_solve(const LuFactors& f, const std::vector<double>& b) {
+inline std::vector<double> lu_solve(const LuFactors<double>& f, const std::vector<double>& b) {
     if (f.perm) return detail::gepp_solve(f, b, false);
     const std::size_t n = f.upper.rows();
     if (b.size() != n) throw DimensionError("lu_solve: length mismatch");
@@ -755,19 +952,29 @@ inline std::vector<double> lu_solve(const LuFactors& f, const std::vector<double
     detail::check(rl_lu_solve(nullptr, RL_HOST, detail::i64(n), packed.data(), b.data(), x.data()));
     return x;
 }
+inline std::vector<Complex> lu_solve(const LuFactors<Complex>& f, const std::vector<Complex>& b) {
+    if (f.perm) throw DimensionError("lu_solve: complex pivoted factors are off the B200 path");
+    const std::size_t n = f.upper.rows();
+    if (b.size() != n) throw DimensionError("lu_solve: length mismatch");
+    const ComplexMatrix packed = detail::pack(f);
+    std::vector<Complex> x(n);
+    detail::check(rl_zlu_solve(nullptr, RL_HOST, detail::i64(n), reinterpret_cast<const double*>(packed.data()),
+                               reinterpret_cast<const double*>(b.data()), reinterpret_cast<double*>(x.data())));
+    return x;
+}
 
 // ---- GEPP and block elimination (lu.hpp:62-147, block_ge.hpp) ----------------
 // The device keeps the reference's arithmetic order: factors, permutations,
 // pivots, Schur complements and block_solve results are bit-identical.
 namespace detail {
-inline RealMatrix pack_lu(const LuFactors& f) { return pack(f); }
-inline std::vector<int64_t> perm_of(const LuFactors& f) {
+inline RealMatrix pack_lu(const LuFactors<double>& f) { return pack(f); }
+inline std::vector<int64_t> perm_of(const LuFactors<double>& f) {
     const std::size_t n = f.upper.rows();
     std::vector<int64_t> p(n);
     for (std::size_t i = 0; i < n; ++i) p[i] = f.perm ? static_cast<int64_t>((*f.perm)[i]) : static_cast<int64_t>(i);
     return p;
 }
-inline std::vector<double> gepp_solve(const LuFactors& f, const std::vector<double>& b, bool transpose) {
+inline std::vector<double> gepp_solve(const LuFactors<double>& f, const std::vector<double>& b, bool transpose) {
     const std::size_t n = f.upper.rows();
     if (b.size() != n) throw DimensionError(transpose ? "lu_solve_transpose: length mismatch" : "lu_solve: length mismatch");
     const RealMatrix packed = pack(f);
@@ -779,26 +986,26 @@ inline std::vector<double> gepp_solve(const LuFactors& f, const std::vector<doub
 }
 }  // namespace detail
 
-inline LuFactors gepp_factor(const RealMatrix& a) {
+inline LuFactors<double> gepp_factor(const RealMatrix& a) {
     const std::size_t n = a.rows();
     if (a.cols() != n) throw DimensionError("gepp_factor: square input required");
     RealMatrix packed(n, n);
     std::vector<int64_t> p(n);
     int64_t step = 0;
     detail::check(rl_gepp_factor(nullptr, RL_HOST, static_cast<int64_t>(n), a.data(), packed.data(), p.data(), &step));
-    LuFactors f = detail::unpack(packed);
+    LuFactors<double> f = detail::unpack(packed);
     f.perm = std::vector<std::size_t>(p.begin(), p.end());
     return f;
 }
 
-inline std::vector<double> lu_solve_transpose(const LuFactors& f, const std::vector<double>& c) {
+inline std::vector<double> lu_solve_transpose(const LuFactors<double>& f, const std::vector<double>& c) {
     return detail::gepp_solve(f, c, true);
 }
 
 struct BlockNode {  // block_ge.hpp:18-35
     std::size_t dim = 0, offset = 0, pivot_size = 0;
     RealMatrix block_matrix;
-    std::optional<LuFactors> block_lu;
+    std::optional<LuFactors<double>> block_lu;
     RealMatrix db_inv, b_inv_c;
     std::unique_ptr<BlockNode> pivot_child, schur_child;
     bool leaf() const { return pivot_size == 0; }
@@ -874,7 +1081,7 @@ inline BlockFactorization block_ge_factor(const RealMatrix& a, const std::vector
         node->dim = k;
         node->offset = o;
         node->block_matrix = sub(leaves, o, o, k, k);
-        LuFactors lu = detail::unpack(sub(f.factors, o, o, k, k));
+        LuFactors<double> lu = detail::unpack(sub(f.factors, o, o, k, k));
         lu.perm = std::vector<std::size_t>(f.perm.begin() + static_cast<std::ptrdiff_t>(o),
                                            f.perm.begin() + static_cast<std::ptrdiff_t>(o + k));
         node->block_lu = std::move(lu);
@@ -929,7 +1136,7 @@ inline RealMatrix schur_complement(const RealMatrix& a, std::size_t k) {  // blo
             else if (i < k) c(i, j - k) = a(i, j);
             else if (j < k) d(i - k, j) = a(i, j);
         }
-    const LuFactors b_lu = gepp_factor(b);
+    const LuFactors<double> b_lu = gepp_factor(b);
     const RealMatrix packed = detail::pack(b_lu);
     const std::vector<int64_t> p = detail::perm_of(b_lu);
     RealMatrix x(k, n - k);
@@ -942,10 +1149,11 @@ inline RealMatrix schur_complement(const RealMatrix& a, std::size_t k) {  // blo
     return out;
 }
 
-inline double relative_residual(const RealMatrix& a, const std::vector<double>& x, const std::vector<double>& b) {
-    const std::vector<double> ax = matvec(a, x);
+template <ScalarField T>
+double relative_residual(const Matrix<T>& a, const std::vector<T>& x, const std::vector<T>& b) {
+    const std::vector<T> ax = matvec(a, x);
     double num = 0.0;
-    for (std::size_t i = 0; i < b.size(); ++i) num += (ax[i] - b[i]) * (ax[i] - b[i]);
+    for (std::size_t i = 0; i < b.size(); ++i) num += field<T>::abs2(ax[i] - b[i]);
     return std::sqrt(num) / norm2(b);
 }
 
@@ -962,8 +1170,6 @@ struct SolveOutcome {
 // a circulant kept structured; products on the GPU.
 template <ScalarField T = double>
 class SideMultiplier {
-    static_assert(std::is_same_v<T, double>, "complex pipelines are off the B200 path");
-
   public:
     static SideMultiplier identity() { return SideMultiplier(); }
     static SideMultiplier make(MultiplierSpec spec, std::size_t n) {
@@ -972,69 +1178,88 @@ class SideMultiplier {
         if (spec.rows != n || spec.cols != n)
             throw DimensionError("solve preprocessing takes square n-by-n multipliers");
         SideMultiplier out;
-        out.spec_ = spec;
         switch (spec.kind) {
             case MultiplierKind::None: return out;
             case MultiplierKind::RealCirculant:
-                out.circ_.emplace(gen_real_circulant(n, spec.seed));
+                out.real_circ_.emplace(gen_real_circulant(n, spec.seed));
                 return out;
             case MultiplierKind::GaussianCirculant:
-                out.circ_.emplace(gen_gaussian_vector(n, spec.seed));
+                out.real_circ_.emplace(gen_gaussian_vector(n, spec.seed));
                 return out;
-            case MultiplierKind::ToeplitzBlock:
-                if (spec.variant == ToeplitzVariant::Real) {
-                    out.circ_.emplace(gen_real_circulant(n, spec.seed));
+            case MultiplierKind::UnitaryCirculant:
+                if constexpr (field<T>::is_complex) {
+                    out.complex_circ_.emplace(gen_unitary_circulant(n, spec.seed));
                     return out;
                 }
                 break;
-            case MultiplierKind::UnitaryCirculant: break;
-            default: out.dense_.emplace(materialize<double>(spec)); return out;
+            case MultiplierKind::ToeplitzBlock:
+                if (spec.variant == ToeplitzVariant::Real) {
+                    out.real_circ_.emplace(gen_real_circulant(n, spec.seed));
+                    return out;
+                }
+                if constexpr (field<T>::is_complex) {
+                    out.complex_circ_.emplace(gen_unitary_circulant(n, spec.seed));
+                    return out;
+                }
+                break;
+            default: out.dense_.emplace(materialize<T>(spec)); return out;
         }
         throw DimensionError("complex multiplier family requested in a real pipeline");
     }
-    bool is_identity() const { return !dense_ && !circ_; }
-    RealMatrix right_multiply(const RealMatrix& a) const {  // A H
+    bool is_identity() const { return !dense_ && !real_circ_ && !complex_circ_; }
+    Matrix<T> right_multiply(const Matrix<T>& a) const {  // A H
         if (is_identity()) return a;
         if (dense_) return matmul(a, *dense_);
-        return matmul_by_circulant(a, *circ_);
+        if (real_circ_) return coerce(matmul_by_circulant(a, *real_circ_));
+        return coerce(matmul_by_circulant(a, *complex_circ_));
     }
-    RealMatrix left_multiply(const RealMatrix& a) const {  // F A
+    Matrix<T> left_multiply(const Matrix<T>& a) const {  // F A, column by column for the structured forms
         if (is_identity()) return a;
         if (dense_) return matmul(*dense_, a);
-        // F A = (A^T F^T)^T
-        return matmul_by_circulant(a.transpose(), circ_->transposed()).transpose();
+        // F A = (A^T F^T)^T: every column through the circulant at once
+        if (real_circ_) return coerce(matmul_by_circulant(a.transpose(), real_circ_->transposed())).transpose();
+        return coerce(matmul_by_circulant(a.transpose(), complex_circ_->transposed())).transpose();
     }
-    std::vector<double> apply_vec(const std::vector<double>& v) const {  // H v
+    std::vector<T> apply_vec(const std::vector<T>& v) const {  // H v
         if (is_identity()) return v;
         if (dense_) return matvec(*dense_, v);
-        return circulant_apply(*circ_, v);
+        if (real_circ_) return circulant_apply(*real_circ_, v);
+        if constexpr (field<T>::is_complex) return circulant_apply(*complex_circ_, v);
+        throw std::logic_error("unreachable multiplier state");
     }
 
   private:
     SideMultiplier() = default;
-    MultiplierSpec spec_{};
-    std::optional<RealMatrix> dense_;
-    std::optional<RealCirculant> circ_;
+    template <typename M>
+    static Matrix<T> coerce(M&& m) {
+        if constexpr (std::is_same_v<std::decay_t<M>, Matrix<T>>)
+            return std::forward<M>(m);
+        else
+            throw std::logic_error("unreachable multiplier field mix");
+    }
+    std::optional<Matrix<T>> dense_;
+    std::optional<RealCirculant> real_circ_;
+    std::optional<ComplexCirculant> complex_circ_;
 };
 
 // residual-correction loop reusing one factorization through `solver`
 // (preprocess.hpp:115-143): two consecutive increases set `diverged`
-inline SolveOutcome<double> iterative_refine(const RealMatrix& a,
-                                             const std::function<std::vector<double>(const std::vector<double>&)>& solver,
-                                             const std::vector<double>& b, std::vector<double> x0, std::size_t steps) {
-    SolveOutcome<double> out;
+template <ScalarField T>
+SolveOutcome<T> iterative_refine(const Matrix<T>& a, const std::function<std::vector<T>(const std::vector<T>&)>& solver,
+                                 const std::vector<T>& b, std::vector<T> x0, std::size_t steps) {
+    SolveOutcome<T> out;
     out.x = std::move(x0);
     const double bnorm = norm2(b);
-    auto residual = [&](const std::vector<double>& x) {
-        std::vector<double> r = matvec(a, x);
+    auto residual = [&](const std::vector<T>& x) {
+        std::vector<T> r = matvec(a, x);
         for (std::size_t i = 0; i < r.size(); ++i) r[i] = b[i] - r[i];
         return r;
     };
-    std::vector<double> r = residual(out.x);
+    std::vector<T> r = residual(out.x);
     out.residual_history.push_back(norm2(r) / bnorm);
     std::size_t streak = 0;
     for (std::size_t s = 0; s < steps; ++s) {
-        const std::vector<double> d = solver(r);
+        const std::vector<T> d = solver(r);
         for (std::size_t i = 0; i < out.x.size(); ++i) out.x[i] += d[i];
         r = residual(out.x);
         const double rel = norm2(r) / bnorm;
@@ -1047,32 +1272,43 @@ inline SolveOutcome<double> iterative_refine(const RealMatrix& a,
     }
     return out;
 }
-inline SolveOutcome<double> iterative_refine(const RealMatrix& a, const LuFactors& factors,
-                                             const std::vector<double>& b, std::vector<double> x0, std::size_t steps) {
-    return iterative_refine(
-        a, [&](const std::vector<double>& r) { return lu_solve(factors, r); }, b, std::move(x0), steps);
+template <ScalarField T>
+SolveOutcome<T> iterative_refine(const Matrix<T>& a, const LuFactors<T>& factors, const std::vector<T>& b,
+                                 std::vector<T> x0, std::size_t steps) {
+    return iterative_refine<T>(
+        a, [&](const std::vector<T>& r) { return lu_solve(factors, r); }, b, std::move(x0), steps);
 }
 
 // preprocess_solve(a, b, pre, post, refine) (preprocess.hpp:156-180): one
 // device call: F (A H), blocked GENP with the reference's pivot verdict, chain
-// solve H (LU)^-1 (F r) and the refinement loop
-inline SolveOutcome<double> preprocess_solve(const RealMatrix& a, const std::vector<double>& b,
-                                             const MultiplierSpec& pre_spec, const MultiplierSpec& post_spec,
-                                             std::size_t refine_steps) {
+// solve H (LU)^-1 (F r) and the refinement loop; over either field
+template <ScalarField T>
+SolveOutcome<T> preprocess_solve(const Matrix<T>& a, const std::vector<T>& b, const MultiplierSpec& pre_spec,
+                                 const MultiplierSpec& post_spec, std::size_t refine_steps) {
     const std::size_t n = a.rows();
     if (a.cols() != n) throw DimensionError("preprocess_solve: square input required");
     if (b.size() != n) throw DimensionError("preprocess_solve: length mismatch");
     for (const MultiplierSpec* s : {&pre_spec, &post_spec})
         if ((s->rows != 0 && s->rows != n) || (s->cols != 0 && s->cols != n))
             throw DimensionError("solve preprocessing takes square n-by-n multipliers");
+    if constexpr (!field<T>::is_complex)
+        for (const MultiplierSpec* s : {&pre_spec, &post_spec})
+            if (multiplier_is_complex(*s)) throw DimensionError("complex multiplier family requested in a real pipeline");
     const rl_multiplier pre = detail::to_abi(pre_spec), post = detail::to_abi(post_spec);
-    SolveOutcome<double> out;
+    SolveOutcome<T> out;
     out.x.resize(n);
     out.residual_history.assign(refine_steps + 1, 0.0);
     out.info.history = out.residual_history.data();
     out.info.history_capacity = detail::i64(refine_steps + 1);
-    const rl_status st = rl_preprocessed_genp_solve(nullptr, RL_HOST, detail::i64(n), a.data(), b.data(), &pre, &post,
-                                                    detail::i64(refine_steps), out.x.data(), nullptr, 0, &out.info);
+    rl_status st;
+    if constexpr (field<T>::is_complex)
+        st = rl_zpreprocessed_genp_solve(nullptr, RL_HOST, detail::i64(n), reinterpret_cast<const double*>(a.data()),
+                                         reinterpret_cast<const double*>(b.data()), &pre, &post,
+                                         detail::i64(refine_steps), reinterpret_cast<double*>(out.x.data()), nullptr,
+                                         &out.info);
+    else
+        st = rl_preprocessed_genp_solve(nullptr, RL_HOST, detail::i64(n), a.data(), b.data(), &pre, &post,
+                                        detail::i64(refine_steps), out.x.data(), nullptr, 0, &out.info);
     detail::check(st, out.info.zero_pivot_step);
     out.residual_history.resize(static_cast<std::size_t>(out.info.history_len));
     out.info.history = nullptr;
@@ -1080,9 +1316,10 @@ inline SolveOutcome<double> preprocess_solve(const RealMatrix& a, const std::vec
     return out;
 }
 
-inline SolveOutcome<double> preprocess_solve_with_retry(const RealMatrix& a, const std::vector<double>& b,
-                                                        MultiplierSpec pre_spec, MultiplierSpec post_spec,
-                                                        std::size_t refine_steps, std::size_t max_retries = 3) {
+template <ScalarField T>
+SolveOutcome<T> preprocess_solve_with_retry(const Matrix<T>& a, const std::vector<T>& b, MultiplierSpec pre_spec,
+                                            MultiplierSpec post_spec, std::size_t refine_steps,
+                                            std::size_t max_retries = 3) {
     for (std::size_t attempt = 0;; ++attempt) {
         try {
             return preprocess_solve(a, b, pre_spec, post_spec, refine_steps);
@@ -1094,7 +1331,7 @@ inline SolveOutcome<double> preprocess_solve_with_retry(const RealMatrix& a, con
     }
 }
 
-// ---- QR (qr.hpp:17-54): CholeskyQR2 on the GPU, positive diagonal R -----------------
+// ---- QR (qr.hpp:17-76): CholeskyQR2 on the GPU, positive (real) diagonal R ----------
 template <ScalarField T = double>
 struct QrResult {
     Matrix<T> q;  // m-by-n
@@ -1111,7 +1348,41 @@ inline QrResult<double> qr(const RealMatrix& y) {
     detail::check(st);
     return out;
 }
+namespace detail {
+inline ComplexMatrix zbasis(const ComplexMatrix& y, bool unchecked) {
+    if (y.rows() < y.cols()) throw DimensionError("qr: expected rows >= cols");
+    ComplexMatrix q(y.rows(), y.cols());
+    int64_t bad = 0;
+    const rl_status st = rl_zorthonormal_basis(nullptr, RL_HOST, i64(y.rows()), i64(y.cols()),
+                                               reinterpret_cast<const double*>(y.data()),
+                                               reinterpret_cast<double*>(q.data()), unchecked ? 1 : 0, &bad);
+    if (st == RL_ERR_RANK_DEFICIENCY)
+        throw RankDeficiencyError("qr: numerically rank-deficient at column " + std::to_string(bad));
+    check(st);
+    return q;
+}
+}  // namespace detail
+// complex: the basis through the real embedding (complex.cu), R = Q^H Y
+inline QrResult<Complex> qr(const ComplexMatrix& y) {
+    ComplexMatrix q = detail::zbasis(y, false);
+    ComplexMatrix r = matmul(q.adjoint(), y);
+    for (std::size_t i = 0; i < r.rows(); ++i) {
+        for (std::size_t j = 0; j < i; ++j) r(i, j) = Complex{};
+        r(i, i) = Complex(r(i, i).real(), 0.0);  // real positive by construction
+    }
+    return {std::move(q), std::move(r)};
+}
 inline RealMatrix orthonormal_basis(const RealMatrix& y) { return qr(y).q; }
+inline ComplexMatrix orthonormal_basis(const ComplexMatrix& y) { return detail::zbasis(y, false); }
+// without the rank check (qr.hpp:58-76)
+inline RealMatrix orthonormal_basis_unchecked(const RealMatrix& y) {
+    if (y.rows() < y.cols()) throw DimensionError("qr: expected rows >= cols");
+    RealMatrix q(y.rows(), y.cols());
+    detail::check(rl_orthonormal_basis_unchecked(nullptr, RL_HOST, detail::i64(y.rows()), detail::i64(y.cols()),
+                                                 y.data(), q.data()));
+    return q;
+}
+inline ComplexMatrix orthonormal_basis_unchecked(const ComplexMatrix& y) { return detail::zbasis(y, true); }
 
 // ---- range finder (lowrank.hpp:21-113) ------------------------------------------------
 template <ScalarField T = double>
@@ -1130,29 +1401,37 @@ struct LowRankResult {
     }
 };
 
-// range finder on a supplied sketch: power steps (A A^T)^s, then the basis
-inline LowRankResult<double> range_find_with(const RealMatrix& a, RealMatrix sketch, std::size_t r, std::size_t p,
-                                             std::size_t power_steps) {
+// range finder on a supplied sketch: power steps (A A^H)^s, then the basis
+template <ScalarField T>
+LowRankResult<T> range_find_with(const Matrix<T>& a, Matrix<T> sketch, std::size_t r, std::size_t p,
+                                 std::size_t power_steps) {
     if (r < 1 || r + p > std::min(a.rows(), a.cols()))
         throw DimensionError("range_find: rank plus oversampling exceeds matrix size");
     for (std::size_t s = 0; s < power_steps; ++s) sketch = matmul(a, matmul(a.adjoint(), sketch));
-    return LowRankResult<double>{orthonormal_basis(sketch), r, p, power_steps};
+    return LowRankResult<T>{orthonormal_basis(sketch), r, p, power_steps};
 }
 
 // range_find (lowrank.hpp:62-83): one device call (sketch by the spec's family,
-// power steps, CholeskyQR2)
-inline LowRankResult<double> range_find(const RealMatrix& a, std::size_t r, std::size_t p, MultiplierSpec spec,
-                                        std::size_t power_steps) {
+// power steps, CholeskyQR2), over either field
+template <ScalarField T>
+LowRankResult<T> range_find(const Matrix<T>& a, std::size_t r, std::size_t p, MultiplierSpec spec,
+                            std::size_t power_steps) {
     const std::size_t n = a.cols(), l = r + p;
     if (r < 1 || l > std::min(a.rows(), a.cols()))
         throw DimensionError("range_find: rank plus oversampling exceeds matrix size");
     spec.rows = n;
     spec.cols = l;
     const rl_multiplier m = detail::to_abi(spec);
-    LowRankResult<double> out{RealMatrix(a.rows(), l), r, p, power_steps};
+    LowRankResult<T> out{Matrix<T>(a.rows(), l), r, p, power_steps};
     rl_lowrank_info info{};
-    const rl_status st = rl_range_find(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(n), a.data(),
-                                       detail::i64(l), &m, detail::i64(power_steps), out.q.data(), &info);
+    rl_status st;
+    if constexpr (field<T>::is_complex)
+        st = rl_zrange_find_residual(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(n),
+                                     reinterpret_cast<const double*>(a.data()), detail::i64(l), &m,
+                                     detail::i64(power_steps), reinterpret_cast<double*>(out.q.data()), &info);
+    else
+        st = rl_range_find(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(n), a.data(), detail::i64(l), &m,
+                           detail::i64(power_steps), out.q.data(), &info);
     if (st == RL_ERR_RANK_DEFICIENCY)
         throw RankDeficiencyError("qr: numerically rank-deficient at column " +
                                   std::to_string(info.rank_deficient_column));
@@ -1160,13 +1439,19 @@ inline LowRankResult<double> range_find(const RealMatrix& a, std::size_t r, std:
     return out;
 }
 
-// ||A - Q (Q^T A)||_2 for this A (lowrank.hpp:99-102), on the GPU: B = Q^T A,
+// ||A - Q (Q^H A)||_2 for this A (lowrank.hpp:99-102), on the GPU: B = Q^H A,
 // the residual never stored, its 2-norm by the restated power iteration
-inline double approximation_residual(const RealMatrix& a, const LowRankResult<double>& result) {
+template <ScalarField T>
+double approximation_residual(const Matrix<T>& a, const LowRankResult<T>& result) {
     if (a.rows() != result.q.rows()) throw DimensionError("approximation_residual: shape mismatch");
     rl_lowrank_info info{};
-    detail::check(rl_approximation_residual(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
-                                            detail::i64(result.q.cols()), result.q.data(), &info));
+    if constexpr (field<T>::is_complex)
+        detail::check(rl_zapproximation_residual(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()),
+                                                 reinterpret_cast<const double*>(a.data()), detail::i64(result.q.cols()),
+                                                 reinterpret_cast<const double*>(result.q.data()), &info));
+    else
+        detail::check(rl_approximation_residual(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()),
+                                                a.data(), detail::i64(result.q.cols()), result.q.data(), &info));
     return info.residual_spectral;
 }
 
@@ -1174,13 +1459,130 @@ struct SubspaceResiduals {
     double rn1 = 0.0;  // projection residual of the leading left singular basis
     double rn2 = 0.0;  // ||A - Q Q^H A||
 };
-inline double basis_residual(const LowRankResult<double>& result, const TruncatedSVD<double>& truth) {
-    const RealMatrix y = matmul(result.q.adjoint(), truth.left);
+template <ScalarField T>
+double basis_residual(const LowRankResult<T>& result, const TruncatedSVD<T>& truth) {
+    const Matrix<T> y = matmul(result.q.adjoint(), truth.left);
     return spectral_norm(matmul(result.q, y) - truth.left);
 }
-inline SubspaceResiduals subspace_residual(const RealMatrix& a, const LowRankResult<double>& result,
-                                           const TruncatedSVD<double>& truth) {
+template <ScalarField T>
+SubspaceResiduals subspace_residual(const Matrix<T>& a, const LowRankResult<T>& result, const TruncatedSVD<T>& truth) {
     return {basis_residual(result, truth), approximation_residual(a, result)};
+}
+inline TruncatedSVD<Complex> to_complex(const TruncatedSVD<double>& t) {
+    return {to_complex(t.left), t.singulars, to_complex(t.right)};
+}
+
+// ---- error bounds and the a-posteriori estimate (lowrank.hpp:114-196) --------------------
+struct ReferenceBounds {  // expected-error reference values, oversampling p >= 2
+    double frobenius = 0.0;
+    double spectral = 0.0;
+    double spectral_simplified = 0.0;
+};
+struct BoundReport {
+    double delta_plus = 0.0;
+    double delta_plus_prime = 0.0;
+    double sigma_r = 0.0;
+    double sigma_r1 = 0.0;
+    double h_frobenius = 0.0;
+    double t_h_inv_norm = 0.0;
+    std::optional<ReferenceBounds> reference;
+};
+// delta_plus = sqrt(2) ||H||_F ||(T_r^H H)^+|| sigma_{r+1} / sigma_r and
+// delta_plus_prime = sigma_{r+1} + 2 delta_plus ||A||; T_r^H H and its
+// singular values on the GPU
+template <ScalarField T>
+BoundReport error_bounds_from_parts(const Matrix<T>& t_r, const std::vector<double>& singulars, const Matrix<T>& h,
+                                    std::size_t r) {
+    if (r < 1 || r > singulars.size()) throw DimensionError("error_bounds: rank out of range");
+    if (t_r.cols() != r || t_r.rows() != h.rows()) throw DimensionError("error_bounds: shape mismatch");
+    if (h.cols() < r) throw DimensionError("error_bounds: sketch narrower than rank");
+    BoundReport rep;
+    rep.sigma_r = singulars[r - 1];
+    rep.sigma_r1 = r < singulars.size() ? singulars[r] : 0.0;
+    rep.h_frobenius = frobenius_norm(h);
+    const auto gsv = svd_values(matmul(t_r.adjoint(), h));
+    if (gsv.back() <= 0.0) throw SingularMatrixError("unlucky multiplier: T_r^H H is singular, the bound is undefined");
+    rep.t_h_inv_norm = 1.0 / gsv.back();
+    rep.delta_plus = std::numbers::sqrt2 * rep.h_frobenius * rep.t_h_inv_norm * rep.sigma_r1 / rep.sigma_r;
+    rep.delta_plus_prime = rep.sigma_r1 + 2.0 * rep.delta_plus * singulars.front();
+    const std::size_t p = h.cols() - r;
+    if (p >= 2) {
+        double tail = 0.0;
+        for (std::size_t j = r; j < singulars.size(); ++j) tail += singulars[j] * singulars[j];
+        const double rd = static_cast<double>(r), pd = static_cast<double>(p);
+        ReferenceBounds ref;
+        ref.frobenius = std::sqrt(1.0 + rd / (pd - 1.0)) * std::sqrt(tail);
+        ref.spectral = (1.0 + std::sqrt(rd / (pd - 1.0))) * rep.sigma_r1 +
+                       (std::numbers::e * std::sqrt(rd + pd) / pd) * std::sqrt(tail);
+        ref.spectral_simplified =
+            (1.0 + 4.0 * std::sqrt(rd + pd) / (pd - 1.0) * std::sqrt(static_cast<double>(singulars.size()))) *
+            rep.sigma_r1;
+        rep.reference = ref;
+    }
+    return rep;
+}
+// 10 sqrt(2/pi) max_j ||(A - Q Q^H A) g_j|| over r_probes Gaussian probes
+// g_j from RngStream(seed).derived(j + 1)
+template <ScalarField T>
+double posterior_estimate(const Matrix<T>& a, const LowRankResult<T>& result, std::size_t r_probes,
+                          std::uint64_t seed) {
+    if (r_probes < 1) throw DimensionError("posterior_estimate: need at least one probe");
+    Matrix<T> g(a.cols(), r_probes);
+    for (std::size_t j = 0; j < r_probes; ++j) {
+        RngStream stream = RngStream(seed).derived(j + 1);
+        for (std::size_t i = 0; i < a.cols(); ++i) g(i, j) = T(stream.next_gaussian());
+    }
+    const Matrix<T> ag = matmul(a, g);  // all probes at once on the GPU
+    const Matrix<T> proj = result.apply_approximation(ag);
+    double worst = 0.0;
+    for (std::size_t j = 0; j < r_probes; ++j) {
+        double norm_sq = 0.0;
+        for (std::size_t i = 0; i < ag.rows(); ++i) norm_sq += field<T>::abs2(ag(i, j) - proj(i, j));
+        worst = std::max(worst, std::sqrt(norm_sq));
+    }
+    return 10.0 * std::sqrt(2.0 / std::numbers::pi) * worst;
+}
+// gauge fix for comparing orthonormal factors (lowrank.hpp:263-282): each
+// column rotated so its largest-magnitude entry is real and positive
+template <ScalarField T>
+void canonicalize_columns(Matrix<T>& q) {
+    for (std::size_t j = 0; j < q.cols(); ++j) {
+        std::size_t imax = 0;
+        double best = -1.0;
+        for (std::size_t i = 0; i < q.rows(); ++i) {
+            const double mag = field<T>::abs2(q(i, j));
+            if (mag > best) {
+                best = mag;
+                imax = i;
+            }
+        }
+        const double mag = std::sqrt(best);
+        if (mag == 0.0) continue;
+        const T phase = field<T>::conj(q(imax, j)) * T(1.0 / mag);
+        for (std::size_t i = 0; i < q.rows(); ++i) q(i, j) *= phase;
+    }
+}
+
+// ---- the sampled-transform sketch check (lowrank.hpp:199-261) ---------------------------
+enum class SketchVariant { Srft, CirculantPermutation };
+struct SrftCheckResult {
+    double residual = 0.0;  // ||(I - P_Y) A||
+    double bound = 0.0;     // sqrt(1 + 7 n / l) sigma_{r+1}
+    std::size_t sketch_width = 0;
+    bool clamped = false;   // the prescribed width reached n and was cut back
+};
+// one device call: the sketch at its prescribed width (clamped to n), the
+// unchecked basis, the residual norm and the bound
+template <ScalarField T>
+SrftCheckResult srft_sketch_check(const Matrix<T>& a, std::size_t r, std::uint64_t seed,
+                                  SketchVariant variant = SketchVariant::Srft,
+                                  std::optional<double> known_sigma_r1 = std::nullopt) {
+    static_assert(std::is_same_v<T, double>, "srft_sketch_check takes the real input it lifts");
+    rl_srft_check out{};
+    detail::check(rl_srft_sketch_check(nullptr, RL_HOST, detail::i64(a.rows()), detail::i64(a.cols()), a.data(),
+                                       detail::i64(r), seed, variant == SketchVariant::Srft ? 0 : 1,
+                                       known_sigma_r1 ? *known_sigma_r1 : -1.0, &out));
+    return {out.residual, out.bound, static_cast<std::size_t>(out.sketch_width), out.clamped != 0};
 }
 
 // ---- testbed inputs (testbed/inputs.hpp) ------------------------------------------------
@@ -1244,7 +1646,83 @@ inline std::vector<double> gen_gaussian_vector(std::size_t n, std::uint64_t seed
     return randla::gen_gaussian_vector(n, seed);
 }
 
+// the transform matrix itself (inputs.hpp:49-55)
+inline ComplexMatrix gen_dft_input(std::size_t n) {
+    if (!is_power_of_two(n) || n < 64) throw DimensionError("gen_dft_input: need a power of two >= 64");
+    return dft_dense(n);
+}
+
 }  // namespace testbed
+
+// ---- testbed statistics helpers (stats.hpp, parallel.hpp, norm_stats.hpp) --------------
+struct StatSummary {  // stats.hpp: population statistics in a two-pass sweep
+    double mean = 0.0;
+    double max = 0.0;
+    double min = 0.0;
+    double std = 0.0;
+};
+inline StatSummary summarize(const std::vector<double>& values) {
+    if (values.empty()) throw std::invalid_argument("summarize: no values");
+    StatSummary s;
+    s.min = s.max = values.front();
+    double sum = 0.0;
+    for (double v : values) {
+        sum += v;
+        s.min = std::min(s.min, v);
+        s.max = std::max(s.max, v);
+    }
+    s.mean = sum / static_cast<double>(values.size());
+    double var = 0.0;
+    for (double v : values) var += (v - s.mean) * (v - s.mean);
+    s.std = std::sqrt(var / static_cast<double>(values.size()));
+    return s;
+}
+// fn(i) for i in [0, count) over the host's threads, every index its own
+// result slot; the first exception is rethrown (parallel.hpp). Each worker
+// thread gets its own device context and stream in the library.
+inline void parallel_for_index(std::size_t count, const std::function<void(std::size_t)>& fn) {
+    const std::size_t hw = std::max<std::size_t>(1, std::thread::hardware_concurrency());
+    const std::size_t workers = std::min(hw, count);
+    if (workers <= 1) {
+        for (std::size_t i = 0; i < count; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::vector<std::exception_ptr> errors(workers);
+    for (std::size_t w = 0; w < workers; ++w)
+        pool.emplace_back([&, w]() {
+            try {
+                for (std::size_t i = w; i < count; i += workers) fn(i);
+            } catch (...) {
+                errors[w] = std::current_exception();
+            }
+        });
+    for (auto& t : pool) t.join();
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+}
+// Monte-Carlo condition statistics of a multiplier family (norm_stats.hpp)
+struct RandomNormStats {
+    MultiplierSpec family;
+    std::size_t samples = 0;
+    StatSummary norm;       // sigma_1
+    StatSummary pinv_norm;  // 1 / sigma_min
+    StatSummary cond;       // sigma_1 / sigma_min
+};
+inline RandomNormStats probe_norm_stats(const MultiplierSpec& spec, std::size_t trials) {
+    if (trials < 1) throw DimensionError("probe_norm_stats: trials must be >= 1");
+    std::vector<double> norms(trials), pinvs(trials), conds(trials);
+    parallel_for_index(trials, [&](std::size_t t) {
+        MultiplierSpec draw = spec;
+        draw.seed = derive_seed(spec.seed, t);
+        const std::vector<double> sv = multiplier_is_complex(draw) ? svd_values(materialize<Complex>(draw))
+                                                                   : svd_values(materialize<double>(draw));
+        norms[t] = sv.front();
+        pinvs[t] = 1.0 / sv.back();
+        conds[t] = sv.front() / sv.back();
+    });
+    return RandomNormStats{spec, trials, summarize(norms), summarize(pinvs), summarize(conds)};
+}
 
 // ---- BASELINE config 2: many independent 32x32 preprocessed solves ---------------
 struct BatchedSolve {

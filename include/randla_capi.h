@@ -297,6 +297,9 @@ RL_API rl_status rl_fft(rl_context* ctx, rl_mem mem, int64_t count, int64_t n, d
  * diag R; RL_ERR_RANK_DEFICIENCY (info column) per qr.hpp:33-38. r nullable. */
 RL_API rl_status rl_cholqr2(rl_context* ctx, rl_mem mem, int64_t m, int64_t l, const double* y, double* q,
                             double* r, int64_t* bad_column);
+/* orthonormal_basis_unchecked (qr.hpp:58-76), real: the basis without the rank verdict */
+RL_API rl_status rl_orthonormal_basis_unchecked(rl_context* ctx, rl_mem mem, int64_t m, int64_t l, const double* y,
+                                                double* q);
 /* Low-rank outcome: the residual R = A - Q (Q^T A) (lowrank.hpp:35-37) in
  * Frobenius and spectral norm (||R||_2 by the restated power iteration of
  * norms.hpp:52-77 on the implicit operator R), the 1-based rank-deficient
@@ -381,6 +384,17 @@ RL_API rl_status rl_zcirculant_right_multiply(rl_context* ctx, rl_mem mem, int64
 /* circulant_apply(C(c), x) (circulant.hpp:81-98), complex c, x, y (length n) */
 RL_API rl_status rl_zcirculant_apply(rl_context* ctx, rl_mem mem, int64_t n, const double* c, const double* x,
                                      double* y);
+/* genp_factor<Complex> (lu.hpp:40-58): packed L\U (n x n complex), with the
+ * reference's ZeroPivot verdict (info->zero_pivot_step) */
+RL_API rl_status rl_zgenp_factor(rl_context* ctx, rl_mem mem, int64_t n, const double* a, double* lu,
+                                 rl_solve_info* info);
+/* lu_solve<Complex> (lu.hpp:100-122) on packed GENP factors: x = U^-1 L^-1 b */
+RL_API rl_status rl_zlu_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* lu, const double* b, double* x);
+/* orthonormal_basis<Complex> (qr.hpp:51-54; unchecked != 0: orthonormal_basis_unchecked,
+ * qr.hpp:58-76): q (m x l) with positive real R diagonal; bad (nullable)
+ * receives the 1-based rank-deficient column */
+RL_API rl_status rl_zorthonormal_basis(rl_context* ctx, rl_mem mem, int64_t m, int64_t l, const double* y, double* q,
+                                       int32_t unchecked, int64_t* bad);
 /* matmul<Complex> (matrix.hpp:115-121): c (m x n) = a (m x k) b (k x n) */
 RL_API rl_status rl_zgemm(rl_context* ctx, rl_mem mem, int64_t m, int64_t n, int64_t k, const double* a,
                           const double* b, double* c);

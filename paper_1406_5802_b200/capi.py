@@ -161,6 +161,10 @@ SIGNATURES = {
     "rl_zcirculant_right_multiply": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, i64, _vp, i64, _vp]),
     "rl_zcirculant_apply": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
     "rl_zgemm": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, i64, _vp, _vp, _vp]),
+    "rl_zgenp_factor": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, ctypes.POINTER(rl_solve_info)]),
+    "rl_zlu_solve": (ctypes.c_int, [_vp, ctypes.c_int, i64, _vp, _vp, _vp]),
+    "rl_zorthonormal_basis": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp, i32, _i64p]),
+    "rl_orthonormal_basis_unchecked": (ctypes.c_int, [_vp, ctypes.c_int, i64, i64, _vp, _vp]),
 }
 
 

@@ -488,6 +488,11 @@ zlu_solve_kernel(const double* __restrict__ W, int64_t ldw, int64_t n, const dou
     }
 }
 
+__global__ void diag_rcp_kernel(const double2* __restrict__ lu, int64_t n, double2* __restrict__ rinv) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) rinv[j] = zrcp(lu[j * n + j]);
+}
+
 // ---- matvec / residual --------------------------------------------------------
 // y = M v (M m x n complex, or real when mr != nullptr); y = b - M v when b given
 __global__ void zgemv_kernel(const double2* __restrict__ M, const double* __restrict__ mr, int64_t ldm, int64_t m,
@@ -931,7 +936,7 @@ rl_status zsolve(rl_context* ctx, bool host, int64_t n, const double* a, const d
     double* scal = reinterpret_cast<double*>(zs + 1);
     const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     RL_CUDA(cudaMemcpyAsync(A, a, 16 * n * n, kin, s));
-    RL_CUDA(cudaMemcpyAsync(bb, b, 16 * n, kin, s));
+    if (b) RL_CUDA(cudaMemcpyAsync(bb, b, 16 * n, kin, s));
 
     ZSide F(s), H(s);
     if ((st = zside_make(ctx, pre, n, host, F)) != RL_OK) return st;
@@ -1001,6 +1006,10 @@ rl_status zsolve(rl_context* ctx, bool host, int64_t n, const double* a, const d
         double2* lu = P;  // the product is no longer needed
         if ((st = unpack(ctx, W, ldw, n, n, lu, n, Pack::W)) != RL_OK) return st;
         RL_CUDA(cudaMemcpyAsync(lu_out, lu, 16 * n * n, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    }
+    if (!b) {  // genp_factor only
+        RL_CUDA(cudaStreamSynchronize(s));
+        return RL_OK;
     }
 
     // iterative_refine with the chain solver H (LU)^-1 (F r) from x0 = 0,
@@ -1275,6 +1284,78 @@ extern "C" RL_API rl_status rl_gen_unitary_circulant(rl_context* ctx, rl_mem mem
     RL_CUDA(cudaMemcpyAsync(column, zc.col, 16 * n, mem == RL_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
                             ctx->stream));
     RL_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RL_OK;
+}
+
+// genp_factor<Complex> (lu.hpp:40-58): packed L\U of a complex n x n matrix
+extern "C" RL_API rl_status rl_zgenp_factor(rl_context* ctx, rl_mem mem, int64_t n, const double* a, double* lu,
+                                            rl_solve_info* info) {
+    rl_solve_info local;
+    if (!info) info = &local;
+    clear_info(info);
+    if (n <= 0) return set_error(RL_ERR_DIMENSION, "genp_factor: square input required");
+    if (!a || !lu) return set_error(RL_ERR_INVALID_ARGUMENT, "genp_factor: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    st = zsolve(ctx, mem == RL_HOST, n, a, nullptr, nullptr, nullptr, 0, nullptr, lu, info);
+    if (st != RL_OK) cudaStreamSynchronize(ctx->stream);
+    return st;
+}
+
+// lu_solve<Complex> (lu.hpp:100-122) on packed GENP factors
+extern "C" RL_API rl_status rl_zlu_solve(rl_context* ctx, rl_mem mem, int64_t n, const double* lu, const double* b,
+                                         double* x) {
+    if (n <= 0) return set_error(RL_ERR_DIMENSION, "lu_solve: length mismatch");
+    if (!lu || !b || !x) return set_error(RL_ERR_INVALID_ARGUMENT, "lu_solve: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    StreamBuf bl(s), bw(s), bv(s);
+    const double2* L = nullptr;
+    if ((st = staged(ctx, host, lu, n * n, bl, &L)) != RL_OK) return st;
+    if ((st = bw.alloc(8 * n * 2 * n)) != RL_OK || (st = bv.alloc(16 * 2 * n)) != RL_OK) return st;
+    double2* rinv = reinterpret_cast<double2*>(bv.p);
+    double2* y = rinv + n;
+    if ((st = pack(ctx, L, n, n, n, bw.p, 2 * n, Pack::W)) != RL_OK) return st;
+    diag_rcp_kernel<<<nblk(n, 256), 256, 0, s>>>(L, n, rinv);
+    RL_CHECK_LAUNCH("diag_rcp_kernel");
+    RL_CUDA(cudaMemcpyAsync(y, b, 16 * n, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    zlu_solve_kernel<<<1, TS, 0, s>>>(bw.p, 2 * n, n, rinv, y);
+    RL_CHECK_LAUNCH("zlu_solve_kernel");
+    RL_CUDA(cudaMemcpyAsync(x, y, 16 * n, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    RL_CUDA(cudaStreamSynchronize(s));
+    return RL_OK;
+}
+
+// orthonormal_basis / orthonormal_basis_unchecked<Complex> (qr.hpp:51-76):
+// q (m x l) with positive real R diagonal; bad (nullable) the 1-based
+// rank-deficient column (qr.hpp:33-38)
+extern "C" RL_API rl_status rl_zorthonormal_basis(rl_context* ctx, rl_mem mem, int64_t m, int64_t l, const double* y,
+                                                  double* q, int32_t unchecked, int64_t* bad) {
+    int64_t local = 0;
+    if (!bad) bad = &local;
+    *bad = 0;
+    if (m <= 0 || l <= 0 || m < l) return set_error(RL_ERR_DIMENSION, "qr: expected rows >= cols");
+    if (!y || !q) return set_error(RL_ERR_INVALID_ARGUMENT, "qr: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    StreamBuf by(s), bqe(s), bq(s);
+    const double2* Y = nullptr;
+    if ((st = staged(ctx, host, y, m * l, by, &Y)) != RL_OK) return st;
+    if ((st = bqe.alloc(8 * 4 * m * l)) != RL_OK || (st = bq.alloc(16 * m * l)) != RL_OK) return st;
+    double2* Q = reinterpret_cast<double2*>(bq.p);
+    if ((st = zbasis(ctx, m, l, Y, bqe.p, Q, unchecked != 0, bad)) != RL_OK) {
+        cudaStreamSynchronize(s);
+        return st;
+    }
+    RL_CUDA(cudaMemcpyAsync(q, Q, 16 * m * l, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    RL_CUDA(cudaStreamSynchronize(s));
     return RL_OK;
 }
 

@@ -378,6 +378,7 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
     // deviation of the pass's Gram from I (the orthogonality of its input),
     // measured when `dev` is given
     unsigned long long* dev_bits = reinterpret_cast<unsigned long long*>(sc + 10);
+    double shift_sq = ysq;  // ||input||_F^2 of a shifted pass
     auto pass = [&](const double* in, double* out, bool shift, int* fail, double* dev = nullptr) -> rl_status {
         rl_status e = gram(ctx, m, l, in, ldq, W, ldl, byt.p, ldm, bsplit.p, splits);
         if (e != RL_OK) return e;
@@ -390,7 +391,7 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
         if (shift) {
             // shifted CholeskyQR3: s = 11 (m l + l (l + 1)) u ||Y||_F^2
             const double sh = 11.0 * (static_cast<double>(m) * l + static_cast<double>(l) * (l + 1)) *
-                              1.1102230246251565e-16 * ysq;
+                              1.1102230246251565e-16 * shift_sq;
             add_diag_kernel<<<nblk(l, 256), 256, 0, s>>>(W, ldl, static_cast<int>(l), sh);
             RL_CHECK_LAUNCH("add_diag_kernel");
         }
@@ -425,6 +426,22 @@ rl_status cholqr2_device(rl_context* ctx, int64_t m, int64_t l, const double* y,
         if ((st = pass(y, bq1.p, true, &fail)) != RL_OK) return st;
         if (!fail && (st = pass(bq1.p, bq2.p, false, &fail)) != RL_OK) return st;
         if (!fail && (st = pass(bq2.p, q, false, &fail)) != RL_OK) return st;
+        if (fail && opts->unchecked) {
+            // exactly dependent columns, which orthonormal_basis_unchecked
+            // accepts (qr.hpp:58-76): each further shifted pass lifts the
+            // null directions by about u^-1/2 until a plain pass holds; the
+            // result is an orthonormal basis containing range(Y)
+            for (int it = 0; it < 8 && fail; ++it) {
+                if ((st = sumsq(ctx, m * ldq, bq1.p, sc)) != RL_OK) return st;
+                RL_CUDA(cudaMemcpyAsync(&shift_sq, sc, 8, cudaMemcpyDeviceToHost, s));
+                RL_CUDA(cudaStreamSynchronize(s));
+                if ((st = pass(bq1.p, bq2.p, true, &fail)) != RL_OK) return st;
+                if (fail) break;
+                std::swap(bq1.p, bq2.p);
+                if ((st = pass(bq1.p, bq2.p, false, &fail)) != RL_OK) return st;
+                if (!fail && (st = pass(bq2.p, q, false, &fail)) != RL_OK) return st;
+            }
+        }
     }
     if (fail) {
         *bad_column = (fail + opts->column_group - 1) / opts->column_group;
@@ -766,6 +783,33 @@ rl_status residual_power_iteration(rl_context* ctx, int64_t m, int64_t n, int64_
 }  // namespace rl
 
 using namespace rl;
+
+// orthonormal_basis_unchecked (qr.hpp:58-76): the basis without the rank verdict
+extern "C" RL_API rl_status rl_orthonormal_basis_unchecked(rl_context* ctx, rl_mem mem, int64_t m, int64_t l,
+                                                           const double* y, double* q) {
+    if (m <= 0 || l <= 0 || m < l) return set_error(RL_ERR_DIMENSION, "qr: expected rows >= cols");
+    if (!y || !q) return set_error(RL_ERR_INVALID_ARGUMENT, "qr: null pointer");
+    rl_status st;
+    ctx = resolve(ctx, &st);
+    if (!ctx) return st;
+    cudaStream_t s = ctx->stream;
+    const bool host = mem == RL_HOST;
+    const int64_t ldq = (l + 1) & ~int64_t(1);
+    Buf by(s), bq(s);
+    if ((st = by.alloc(sizeof(double) * m * ldq)) != RL_OK || (st = bq.alloc(sizeof(double) * m * ldq)) != RL_OK)
+        return st;
+    if (ldq != l) RL_CUDA(cudaMemsetAsync(by.p, 0, sizeof(double) * m * ldq, s));
+    RL_CUDA(cudaMemcpy2DAsync(by.p, ldq * 8, y, l * 8, l * 8, m, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                              s));
+    CholqrOpts opts;
+    opts.unchecked = true;
+    int64_t bad = 0;
+    if ((st = cholqr2_device(ctx, m, l, by.p, bq.p, ldq, nullptr, 0, &bad, &opts)) != RL_OK) return st;
+    RL_CUDA(cudaMemcpy2DAsync(q, l * 8, bq.p, ldq * 8, l * 8, m, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                              s));
+    RL_CUDA(cudaStreamSynchronize(s));
+    return RL_OK;
+}
 
 extern "C" RL_API rl_status rl_cholqr2(rl_context* ctx, rl_mem mem, int64_t m, int64_t l, const double* y, double* q,
                                        double* r, int64_t* bad_column) {

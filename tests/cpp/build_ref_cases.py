@@ -12,12 +12,14 @@ harness in tests/cpp/doctest_shim (the reference keeps doctest out of tree).
 The binaries land in tests/cpp/_build/ (git-ignored; they travel to the GPU
 box with the tree) and tests/test_cpp_api.py runs them on the GPU.
 
-Cases left out, and why: the circulant text fixtures and the complex
-(unitary) circulant (matrix_io.hpp, complex families: off the B200 path), the
-error-bound / posterior-estimate / SRFT studies (lowrank.hpp:114-300, not on
-the path), and test_elimination.cpp, whose prelude needs Eigen's inverse()
-(its GENP / GEPP / block / refinement cases are restated in
-tests/cpp/test_header_api.cpp instead).
+Compiled: test_transforms.cpp (all but the text-fixture case, which needs
+matrix_io.hpp's file format), test_lowrank.cpp (all but the three cases
+built on the full SVD with singular vectors, svd(), which the device Jacobi
+does not return: lines 77-112) and the whole of test_multipliers.cpp, whose
+prelude includes the reference's own tests/support/exact_rank.hpp (read in
+place with -I). test_elimination.cpp is left out: its prelude needs Eigen's
+inverse(); its GENP / GEPP / block / refinement cases are restated in
+tests/cpp/test_header_api.cpp instead.
 
 Usage: python tests/cpp/build_ref_cases.py   (no-op when /root/reference is absent)
 """
@@ -33,8 +35,9 @@ LIBDIR = os.path.join(ROOT, "paper_1406_5802_b200", "_lib")
 
 # binary -> (reference test file, inclusive 1-based line ranges)
 CASES = {
-    "ref_transforms": ("proj/tests/test_transforms.cpp", [(1, 29), (31, 211)]),
-    "ref_lowrank": ("proj/tests/test_lowrank.cpp", [(1, 18), (20, 75), (172, 208), (260, 265)]),
+    "ref_transforms": ("proj/tests/test_transforms.cpp", [(1, 29), (31, 211), (230, 239)]),
+    "ref_lowrank": ("proj/tests/test_lowrank.cpp", [(1, 18), (20, 75), (114, 170), (172, 228), (230, 265)]),
+    "ref_multipliers": ("proj/tests/test_multipliers.cpp", [(1, 262)]),
 }
 
 
@@ -64,7 +67,9 @@ def build(verbose=False):
             f.write(assemble(rel, ranges))
         exe = os.path.join(OUT, name)
         cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include", "randla_dropin"),
-               "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "doctest_shim"), src,
+               "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "doctest_shim"),
+               # the reference's own test-support headers (support/exact_rank.hpp), read in place
+               "-I", os.path.join(REF, "proj", "tests"), src,
                "-L", LIBDIR, "-lrandla_b200", "-Wl,-rpath,$ORIGIN/../../../paper_1406_5802_b200/_lib", "-o", exe]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

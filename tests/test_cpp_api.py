@@ -32,7 +32,7 @@ def test_header_program_runs(tmp_path):
     assert "all passed" in r.stdout
 
 
-REF_BINS = [os.path.join(ROOT, "tests", "cpp", "_build", n) for n in ("ref_transforms", "ref_lowrank")]
+REF_BINS = [os.path.join(ROOT, "tests", "cpp", "_build", n) for n in ("ref_transforms", "ref_lowrank", "ref_multipliers")]
 
 
 @pytest.mark.skipif(not os.path.isdir("/root/reference/proj/tests"), reason="reference tests absent (GPU box)")
