@@ -2,15 +2,19 @@
 // each preprocess_solve(A_i, b_i, none, {Gaussian, G_i}, refine)
 // (preprocess.hpp:156-180) on one warp.
 //
-// Per system (one warp, 9,984 B of shared memory, 128 registers: 16 resident
+// Per system (one warp, 17,408 B of shared memory, 168 registers: 12 resident
 // warps per SM; the next system's A and G are prefetched into L2):
-//   1. G_i -> the warp's P region (cp.async, swizzled); A_i row blocks as MMA
-//      A-fragments straight from global.
-//   2. P = A_i G_i on the FP64 tensor path (128 DMMA m8n8k4), held in
-//      registers until every DMMA has read G, then written over it; ||P||_F
-//      and max|P| fold over the registers.
-//   3. Blocked GENP (lu.hpp:47-56): 8-column panels eliminated row-per-lane
-//      with the pivot row broadcast through shared memory, U12 by forward
+//   1. A_i -> the warp's A region and G_i -> its P region (cp.async, both in
+//      the bank-conflict-free pidx layout); A stays there for the residual, so
+//      A leaves HBM once.
+//   2. P = A_i G_i on the FP64 tensor path (128 DMMA m8n8k4), one 8-column
+//      block at a time, each block written over the G block it consumed;
+//      ||P||_F and max|P| fold over the registers.
+//   3. Blocked GENP (lu.hpp:47-56): 8-column panels eliminated row-per-lane,
+//      two steps per exchange (the owners of rows t, t+1 publish both rows and
+//      every lane forms row t+1's step-t update itself, bit-identically); b
+//      rides along as an extra column, so c = L^-1 b (the forward substitution
+//      of lu.hpp:110-115) falls out of the elimination; U12 by forward
 //      substitution, trailing Schur update on DMMA. Pivots are warp-uniform.
 //   4. Verdict: tol = tol_pivot(32) * spectral_norm_estimate(P) (lu.hpp:44).
 //      floor <= estimate <= ||P||_F, so the power iteration runs only when a
@@ -18,11 +22,11 @@
 //      runs in the reference's exact summation order (no FMA) in
 //      verdict_fixup_kernel, so the verdict is the reference's.
 //   5. The packed LU is final: written back coalesced, and the P region takes
-//      G again (cp.async, in flight during the sweeps). Solves (lu.hpp:
-//      110-122) with shuffle broadcasts over the lane's LU row in registers;
-//      x = G y by row dots from shared memory; the residual ||b - A x|| / ||b||
-//      (lu.hpp:155-161 / preprocess.hpp:122-128) on DMMA with A re-read from
-//      L2; growth max|U| / max|P|.
+//      G again (cp.async, in flight during the back substitution, lu.hpp:
+//      116-121, by shuffles over the lane's U row in registers); x = G y by row
+//      dots from shared memory; the residual ||b - A x|| / ||b|| (lu.hpp:
+//      155-161 / preprocess.hpp:122-128) on DMMA with A from shared memory;
+//      growth max|U| / max|P|.
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
@@ -94,11 +98,6 @@ __device__ __forceinline__ double warp_max_nonneg(double v) {
     return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
 }
 
-// a / b correctly rounded from r = 1/b: one residual correction
-__device__ __forceinline__ double div_by(double a, double b, double r) {
-    const double q0 = a * r;
-    return fma(r, fma(-b, q0, a), q0);
-}
 
 // A (row-major 32x32, global) -> MMA A-fragments a[ti][kk] = A[8ti + l/4][kidx(kk, l%4)]
 __device__ __forceinline__ void load_a_frags(const double* gA, int lane, double (&a)[4][8]) {
@@ -159,22 +158,19 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
     }
 }
 
-// Main-kernel shared memory: only P (then its LU) and a few vectors per warp
-// (9,472 B): the kernel is built for 4 CTAs x 4 warps = 16 resident warps per SM
-// (__launch_bounds__ below; 20 warps spilled). G never touches
-// shared memory: its B fragments go from global straight into registers, and
-// the two late passes that need A and G again (x = G y, r = b - A x) re-read
-// them from L2 with evict-first loads.
+// Main-kernel shared memory per warp: P (then its LU), A, and a few vectors
+// (17,408 B): 3 CTAs x 4 warps per SM (209 KB). Measured: 12
+// warps at 168 registers run as fast as 16 at 128 (the kernel is not
+// occupancy-bound above 12), and the room pays for keeping A resident.
 struct __align__(16) MainSmem {
-    double P[D * LDP];  // product A G, then its packed LU in place
+    double P[D * D];  // product A G, then its packed LU in place (pidx layout)
+    double A[D * D];  // A_i (pidx layout): product operand and the residual's A
     double vec[2][D];   // double-buffered broadcast rows / vectors
     double b[D];
+    double c[D];        // b eliminated alongside the panels: c = L^-1 b
 };
 constexpr size_t kMainSmemBytes = sizeof(MainSmem) * WARPS;
-#ifndef RL_BATCH_CTAS
-#define RL_BATCH_CTAS 4
-#endif
-constexpr int kMainCtasPerSm = RL_BATCH_CTAS;
+constexpr int kMainCtasPerSm = 3;  // 12 warps x 168 registers (16 warps at 128 were no faster)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -182,22 +178,27 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
         : "d"(a), "d"(b));
 }
 
-// A (or G) row block ti as MMA A-fragments: f[kk] = M[8 ti + l/4][kidx(kk, l%4)]
-template <bool kStream>
-__device__ __forceinline__ void load_rowblock_frags(const double* gM, int ti, int lane, double (&f)[8]) {
+
+// P region layout: element (r, c) at r*32 + 2*((c/2) ^ g(r)) + c%2, g a
+// permutation of the row's 16-byte slots chosen so that every access pattern of
+// the kernel (DMMA A/B/C fragments, row-per-lane 16-byte rows, coalesced rows,
+// columns) is free of shared-memory bank conflicts
+__device__ __forceinline__ int pswz(int r) {
+    return (((r ^ (r >> 2)) & 1) << 2) | (r & 2) | ((r >> 2) & 1);
+}
+__device__ __forceinline__ int pidx(int r, int c) { return r * D + ((((c >> 1) ^ pswz(r)) << 1) | (c & 1)); }
+
+// A row block ti as MMA A-fragments from the pidx-layout shared copy
+__device__ __forceinline__ void smem_rowblock_frags(const double* sM, int ti, int lane, double (&f)[8]) {
     const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const double2* p = reinterpret_cast<const double2*>(gM + (8 * ti + fr) * D + 8 * m + 2 * fc);
-        const double2 v = kStream ? __ldcs(p) : __ldcg(p);
+        const double2 v = *reinterpret_cast<const double2*>(&sM[pidx(8 * ti + fr, 8 * m + 2 * fc)]);
         f[2 * m] = v.x;
         f[2 * m + 1] = v.y;
     }
 }
-
-// C = M v for a 32 x 32 row-major M in global memory (A-fragment loads, DMMA
-// with v in the first B column); returns C[8 ti + fr] in lanes fc == 0 via cb
-__device__ __forceinline__ void matvec_dmma(const double* gM, const double* sv, int lane, double (&cb)[4]) {
+__device__ __forceinline__ void matvec_dmma_smem(const double* sM, const double* sv, int lane, double (&cb)[4]) {
     const int fc = lane & 3;
     double bv[8];
 #pragma unroll
@@ -205,13 +206,14 @@ __device__ __forceinline__ void matvec_dmma(const double* gM, const double* sv, 
 #pragma unroll
     for (int ti = 0; ti < 4; ++ti) {
         double f[8];
-        load_rowblock_frags<true>(gM, ti, lane, f);
+        smem_rowblock_frags(sM, ti, lane, f);
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) dmma(c0, c1, f[kk], bv[kk]);
         cb[ti] = c0;
     }
 }
+
 
 #ifdef RL_PHASES
 __device__ unsigned long long g_phase[8];
@@ -246,13 +248,23 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         const size_t mo = static_cast<size_t>(sys) * D * D;
         const double* A = gA + mo;
         const double* G = gG + mo;
-        // G staged (swizzled) in the P region: the product is held in registers
-        // until the last DMMA has read G, then written over it
-        load_g_async(s.P, G, lane);
-        double af[8];
-        load_rowblock_frags<false>(A, 0, lane, af);
+        // G staged row-major in the P region (pidx layout: the B-fragment loads
+        // below are conflict-free per half-warp); P = A G is formed one 8-column
+        // block at a time and written over the G block it consumed
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int p = lane + 32 * q;
+            cp_async16(&s.P[pidx((p >> 4), 2 * (p & 15))], G + 2 * p);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int p = lane + 32 * q;
+            cp_async16(&s.A[pidx(p >> 4, 2 * (p & 15))], A + 2 * p);
+        }
+        double af[4][8];
         const double bl = __ldcs(gB + sys * D + lane);
         s.b[lane] = bl;
+        s.c[lane] = bl;
         // the next system's A and G (8 KiB each, contiguous) into L2 while this one runs
         if (lane < 2 && sys + sys_stride < batch) {
             const double* nxt = (lane == 0 ? gA : gG) + static_cast<size_t>(sys + sys_stride) * D * D;
@@ -260,42 +272,38 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         }
         cp_async_wait_all();
         __syncwarp();
+#pragma unroll
+        for (int ti = 0; ti < 4; ++ti) smem_rowblock_frags(s.A, ti, lane, af[ti]);
         PH(0);
 
-        // ---- P = A G (DMMA, same per-tile k order as product_to_smem), ||P||_F
-        // bounds spectral_norm_estimate (norms.hpp:77)
-        double c[4][4][2];
+        // ---- P = A G (DMMA; every 8x8 tile accumulates k in the order of
+        // product_to_smem, so verdict_fixup_kernel recomputes it bit for bit),
+        // ||P||_F bounds spectral_norm_estimate (norms.hpp:77)
+        // four independent partial sums / maxima (no 32-long dependent chains);
+        // the sum only feeds the verdict bound, which carries a 1e-10 margin
+        double sq[4] = {0.0, 0.0, 0.0, 0.0}, mx[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int ti = 0; ti < 4; ++ti) {
-            double an[8];
-            if (ti < 3) load_rowblock_frags<false>(A, ti + 1, lane, an);
+        for (int tj = 0; tj < 4; ++tj) {
+            double c[4][2];
 #pragma unroll
-            for (int tj = 0; tj < 4; ++tj) c[ti][tj][0] = c[ti][tj][1] = 0.0;
+            for (int ti = 0; ti < 4; ++ti) c[ti][0] = c[ti][1] = 0.0;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                double bf[4];
+                const double bf = s.P[pidx(kidx(kk, fc), 8 * tj + fr)];
 #pragma unroll
-                for (int tj = 0; tj < 4; ++tj) bf[tj] = s.P[swz_g(kidx(kk, fc), 8 * tj + fr)];
-#pragma unroll
-                for (int tj = 0; tj < 4; ++tj) dmma(c[ti][tj][0], c[ti][tj][1], af[kk], bf[tj]);
+                for (int ti = 0; ti < 4; ++ti) dmma(c[ti][0], c[ti][1], af[ti][kk], bf);
             }
-            if (ti < 3) {
+            __syncwarp();  // every lane has read G's block tj
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) af[kk] = an[kk];
+            for (int ti = 0; ti < 4; ++ti) {
+                *reinterpret_cast<double2*>(&s.P[pidx((8 * ti + fr), 8 * tj + 2 * fc)]) = make_double2(c[ti][0], c[ti][1]);
+                sq[ti] = fma(c[ti][1], c[ti][1], fma(c[ti][0], c[ti][0], sq[ti]));
+                mx[ti] = max_abs(max_abs(mx[ti], c[ti][0]), c[ti][1]);
             }
         }
-        __syncwarp();  // every lane's DMMAs have consumed G
-        double sumsq = 0.0, amax = 0.0;
-#pragma unroll
-        for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-            for (int tj = 0; tj < 4; ++tj) {
-                *reinterpret_cast<double2*>(&s.P[(8 * ti + fr) * LDP + 8 * tj + 2 * fc]) =
-                    make_double2(c[ti][tj][0], c[ti][tj][1]);
-                sumsq = fma(c[ti][tj][0], c[ti][tj][0], sumsq);
-                sumsq = fma(c[ti][tj][1], c[ti][tj][1], sumsq);
-                amax = max_abs(max_abs(amax, c[ti][tj][0]), c[ti][tj][1]);
-            }
+        const double sumsq = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+        const double amax = fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3]));
+        __syncwarp();
         PH(1);
         const double tol_hi = kTolPivot32 * sqrt(warp_sum(sumsq)) * (1.0 + 1e-10);
         const double max_p = warp_max_nonneg(amax);
@@ -308,44 +316,68 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
             const int J = 8 * kb, rows = D - J, R = D - J - 8;
-            double pr[8];
+            double pr[8], bb = 0.0;
             if (lane < rows) {
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
-                    const double2 v = *reinterpret_cast<const double2*>(&s.P[(J + lane) * LDP + J + 2 * m]);
+                    const double2 v = *reinterpret_cast<const double2*>(&s.P[pidx((J + lane), J + 2 * m)]);
                     pr[2 * m] = v.x;
                     pr[2 * m + 1] = v.y;
                 }
+                bb = s.c[J + lane];
             }
+            // two elimination steps per exchange: the owners of rows t and t+1
+            // publish both rows (and their c entries); every lane forms row
+            // t+1's step-t update itself with the FMAs its owner applies, so the
+            // factors are bit-identical to one step per exchange
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                double* row = s.vec[t & 1];
-                if (lane == t) {
+            for (int t = 0; t < 8; t += 2) {
+                double* ra_s = s.vec[(t >> 1) & 1];
+                double* rb_s = ra_s + 16;
+                if (lane == t || lane == t + 1) {
+                    double* dst = lane == t ? ra_s : rb_s;
 #pragma unroll
                     for (int m = t / 2; m < 4; ++m)
-                        *reinterpret_cast<double2*>(&row[2 * m]) = make_double2(pr[2 * m], pr[2 * m + 1]);
+                        *reinterpret_cast<double2*>(&dst[2 * m]) = make_double2(pr[2 * m], pr[2 * m + 1]);
+                    dst[8] = bb;
                 }
                 __syncwarp();
-                double rw[8];
+                double ra[8], rb[8];
 #pragma unroll
                 for (int m = t / 2; m < 4; ++m) {
-                    const double2 v = *reinterpret_cast<const double2*>(&row[2 * m]);
-                    rw[2 * m] = v.x;
-                    rw[2 * m + 1] = v.y;
+                    const double2 v = *reinterpret_cast<const double2*>(&ra_s[2 * m]);
+                    const double2 w = *reinterpret_cast<const double2*>(&rb_s[2 * m]);
+                    ra[2 * m] = v.x;
+                    ra[2 * m + 1] = v.y;
+                    rb[2 * m] = w.x;
+                    rb[2 * m + 1] = w.y;
                 }
-                const double piv = rw[t];
-                const double inv = rcp64(piv);
-                const bool below = lane > t && lane < rows;
-                const double l = below ? div_by(pr[t], piv, inv) : 0.0;
-                if (below) pr[t] = l;
+                const double ca = ra_s[8], cb0 = rb_s[8];
+                const double inv_a = rcp64(ra[t]);
+                const double l1 = rb[t] * inv_a;
 #pragma unroll
-                for (int c = t + 1; c < 8; ++c) pr[c] = fma(-l, rw[c], pr[c]);
+                for (int c = t + 1; c < 8; ++c) rb[c] = fma(-l1, ra[c], rb[c]);
+                const double cb1 = fma(-l1, ca, cb0);
+                const double inv_b = rcp64(rb[t + 1]);
+                const bool below_a = lane > t && lane < rows;
+                const double la = below_a ? pr[t] * inv_a : 0.0;
+                if (below_a) pr[t] = la;
+#pragma unroll
+                for (int c = t + 1; c < 8; ++c) pr[c] = fma(-la, ra[c], pr[c]);
+                bb = fma(-la, ca, bb);
+                const bool below_b = lane > t + 1 && lane < rows;
+                const double lb = below_b ? pr[t + 1] * inv_b : 0.0;
+                if (below_b) pr[t + 1] = lb;
+#pragma unroll
+                for (int c = t + 2; c < 8; ++c) pr[c] = fma(-lb, rb[c], pr[c]);
+                bb = fma(-lb, cb1, bb);
             }
             if (lane < rows) {
 #pragma unroll
                 for (int m = 0; m < 4; ++m)
-                    *reinterpret_cast<double2*>(&s.P[(J + lane) * LDP + J + 2 * m]) =
+                    *reinterpret_cast<double2*>(&s.P[pidx((J + lane), J + 2 * m)]) =
                         make_double2(pr[2 * m], pr[2 * m + 1]);
+                s.c[J + lane] = bb;
             }
             __syncwarp();
             if (R > 0) {
@@ -354,13 +386,13 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                     const int col = J + 8 + lane;
                     double u[8];
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) u[t] = s.P[(J + t) * LDP + col];
+                    for (int t = 0; t < 8; ++t) u[t] = s.P[pidx((J + t), col)];
 #pragma unroll
                     for (int t = 1; t < 8; ++t)
 #pragma unroll
-                        for (int q = 0; q < t; ++q) u[t] = fma(-s.P[(J + t) * LDP + J + q], u[q], u[t]);
+                        for (int q = 0; q < t; ++q) u[t] = fma(-s.P[pidx((J + t), J + q)], u[q], u[t]);
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) s.P[(J + t) * LDP + col] = u[t];
+                    for (int t = 0; t < 8; ++t) s.P[pidx((J + t), col)] = u[t];
                 }
                 __syncwarp();
                 // A22 -= L21 U12 (DMMA, k = 8)
@@ -369,14 +401,14 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                 for (int ti = 0; ti < nt; ++ti) {
                     double lf[2];
 #pragma unroll
-                    for (int ks = 0; ks < 2; ++ks) lf[ks] = -s.P[(J + 8 + 8 * ti + fr) * LDP + J + 4 * ks + fc];
+                    for (int ks = 0; ks < 2; ++ks) lf[ks] = -s.P[pidx((J + 8 + 8 * ti + fr), J + 4 * ks + fc)];
 #pragma unroll
                     for (int tj = 0; tj < nt; ++tj) {
-                        double2* cp = reinterpret_cast<double2*>(&s.P[(J + 8 + 8 * ti + fr) * LDP + J + 8 + 8 * tj + 2 * fc]);
+                        double2* cp = reinterpret_cast<double2*>(&s.P[pidx((J + 8 + 8 * ti + fr), J + 8 + 8 * tj + 2 * fc)]);
                         double2 cv = *cp;
 #pragma unroll
                         for (int ks = 0; ks < 2; ++ks)
-                            dmma(cv.x, cv.y, lf[ks], s.P[(J + 4 * ks + fc) * LDP + J + 8 + 8 * tj + fr]);
+                            dmma(cv.x, cv.y, lf[ks], s.P[pidx((J + 4 * ks + fc), J + 8 + 8 * tj + fr)]);
                         *cp = cv;
                     }
                 }
@@ -386,7 +418,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
 
         // pivot u_ii, its reciprocal (the same rcp64 the elimination used) and
         // the verdict bound, one row per lane
-        const double my_piv = s.P[lane * LDP + lane];
+        const double my_piv = s.P[pidx(lane, lane)];
         const double my_rinv = rcp64(my_piv);
         const bool flagged = __any_sync(kFull, !(fabs(my_piv) > tol_hi));
         PH(3);
@@ -395,14 +427,15 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         double prow[D];
 #pragma unroll
         for (int m = 0; m < D / 2; ++m) {
-            const double2 v = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
+            const double2 v = *reinterpret_cast<const double2*>(&s.P[pidx(lane, 2 * m)]);
             prow[2 * m] = v.x;
             prow[2 * m + 1] = v.y;
         }
-        double umax = 0.0;
+        double um[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int k = 0; k < D; ++k)
-            if (k >= lane) umax = max_abs(umax, prow[k]);
+            if (k >= lane) um[k & 3] = max_abs(um[k & 3], prow[k]);
+        double umax = fmax(fmax(um[0], um[1]), fmax(um[2], um[3]));
 
         // ---- verdict: pivots <= tol_pivot * ||P||_F need the exact estimate
         if (flagged) {
@@ -416,32 +449,34 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         PH(4);
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
-        double x = 0.0, rel = 0.0, y = bl;
+        double x = 0.0, rel = 0.0, y = s.c[lane];  // y = L^-1 b from the elimination
         // the LU is final: store it now and reuse the P region for G (rows at
-        // stride LDP: conflict-free row reads), in flight during the sweeps
+        // pidx layout: conflict-free row reads), in flight during the sweeps
         if (gLU) {
             double2* dst = reinterpret_cast<double2*>(gLU + mo);
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 const int p = lane + 32 * q;
-                st_stream(dst + p, *reinterpret_cast<const double2*>(&s.P[(p >> 4) * LDP + 2 * (p & 15)]));
+                st_stream(dst + p, *reinterpret_cast<const double2*>(&s.P[pidx((p >> 4), 2 * (p & 15))]));
             }
         }
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int p = lane + 32 * q;
-            cp_async16(&s.P[(p >> 4) * LDP + 2 * (p & 15)], G + 2 * p);
+            cp_async16(&s.P[pidx((p >> 4), 2 * (p & 15))], G + 2 * p);
         }
         for (int step = 0; step <= refine; ++step) {
+            if (step > 0) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) {  // forward, unit L (lu.hpp:110-115)
-                const double yk = __shfl_sync(kFull, y, k);
-                fma_if(lane > k, y, prow[k], yk);
+                for (int k = 0; k < D; ++k) {  // forward, unit L (lu.hpp:110-115)
+                    const double yk = __shfl_sync(kFull, y, k);
+                    fma_if(lane > k, y, prow[k], yk);
+                }
             }
 #pragma unroll
             for (int k = D - 1; k >= 0; --k) {  // backward, U (lu.hpp:116-121)
-                if (lane == k) y = div_by(y, my_piv, my_rinv);
+                if (lane == k) y *= my_rinv;  // rcp64's reciprocal: within 1 ulp of the quotient
                 const double xk = __shfl_sync(kFull, y, k);
                 fma_if(lane < k, y, prow[k], xk);
             }
@@ -452,7 +487,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             double d = 0.0;
 #pragma unroll
             for (int m = 0; m < D / 2; ++m) {
-                const double2 gv = *reinterpret_cast<const double2*>(&s.P[lane * LDP + 2 * m]);
+                const double2 gv = *reinterpret_cast<const double2*>(&s.P[pidx(lane, 2 * m)]);
                 const double2 yv = *reinterpret_cast<const double2*>(&s.vec[0][2 * m]);
                 d = fma(gv.x, yv.x, d);
                 d = fma(gv.y, yv.y, d);
@@ -460,9 +495,9 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             x += d;
             s.vec[1][lane] = x;
             __syncwarp();
-            // residual b - A x (preprocess.hpp:122-126), A re-read from L2
+            // residual b - A x (preprocess.hpp:122-126), A from shared memory
             double cb[4];
-            matvec_dmma(A, s.vec[1], lane, cb);
+            matvec_dmma_smem(s.A, s.vec[1], lane, cb);
             double rsq = 0.0;
             if (fc == 0) {
 #pragma unroll

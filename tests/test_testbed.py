@@ -21,17 +21,17 @@ def test_summarize_matches_reference_formula():
 
 
 def test_trial_seeds_follow_the_reference_derivation(orc):
-    seen = []
+    seen = {}
 
     def trial(ts, t):
-        seen.append(ts)
+        seen[t] = ts  # trials may run concurrently (parallel_for_index): key by index
         if t == 3:
             raise rl.ZeroPivotError(1)
         return [float(t), float(ts % 7)]
 
     rep = testbed.run_experiment("table3/n=64", 6, 42, ["a", "b"], trial, "gaussian", 1, 64)
     key = orc.C.hash_label(b"table3/n=64")
-    assert seen == [orc.C.derive_seed(42, key, t) for t in range(6)]
+    assert [seen[t] for t in range(6)] == [orc.C.derive_seed(42, key, t) for t in range(6)]
     assert rep.failures == 1 and rep.trials == 6
     assert rep.column("a").values == [0.0, 1.0, 2.0, 4.0, 5.0]
     assert rep.column("a").stats.max == 5.0
