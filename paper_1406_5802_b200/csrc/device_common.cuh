@@ -34,6 +34,14 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while the
+// previous kernel of its stream still runs; griddep_wait() returns once that
+// kernel has completed and its writes are visible (immediately for a normal
+// launch). griddep_launch_dependents() lets the next such kernel start early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // Streaming (evict-first) 16-byte global load for data read exactly once.
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }

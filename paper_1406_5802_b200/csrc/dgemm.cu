@@ -99,6 +99,9 @@ dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         mbar_fence_init();
     }
     __syncthreads();
+    // everything above touches no data of the previous kernel
+    griddep_wait();
+    griddep_launch_dependents();
 
     auto issue = [&](int kt) {
         const int s = kt % STAGES;
@@ -272,8 +275,23 @@ void configure_once() {
 
 template <class CF, bool A, bool S, bool T>
 void launch_cfg(dim3 grid, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, double* C, int64_t ldc, int m,
-                int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride, int c_ahead) {
+                int n, int k, double alpha, GemmStats* stats, int ktc, int64_t split_stride, int c_ahead, bool pdl) {
     configure_once<CF, A, S, T>();
+    if (pdl) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(CF::THREADS);
+        cfg.dynamicSmemBytes = CF::SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, dgemm_kernel<CF, A, S, T>, ta, tb, C, ldc, m, n, k, alpha, stats, ktc, split_stride,
+                           c_ahead);
+        return;
+    }
     dgemm_kernel<CF, A, S, T><<<grid, CF::THREADS, CF::SMEM_BYTES, st>>>(ta, tb, C, ldc, m, n, k, alpha, stats, ktc,
                                                                        split_stride, c_ahead);
 }
@@ -290,7 +308,7 @@ rl_status run_cfg(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double
     if (tiles > 0x7fffffff) return set_error(RL_ERR_DIMENSION, "gemm: too many tiles");
     launch_cfg<CF, A, S, T>(dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), ctx->stream, ta, tb, C,
                             ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), alpha, stats, ktc,
-                            split_stride, A ? ctx->num_sms * CF::MINB : 0);
+                            split_stride, A ? ctx->num_sms * CF::MINB : 0, ctx->pdl);
     RL_CHECK_LAUNCH("dgemm_kernel");
     return RL_OK;
 }

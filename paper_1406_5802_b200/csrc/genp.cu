@@ -261,6 +261,8 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     const long long t0 = clock64();
 #endif
     double* d = a + c0 * lda + c0;
+    griddep_wait();  // programmatic launch on the lookahead chain: the update feeding this panel is done
+    griddep_launch_dependents();
     for (int idx = tid; idx < kBase * kBase; idx += PT) sd[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
     for (int idx = tid; idx < 4 * kBase; idx += PT) (&pbuf[0][0])[idx] = 0.0;
     __syncthreads();
@@ -432,12 +434,17 @@ rl_status panel(const Ctx& g, int64_t c0, int64_t w) {
 // 64-column sub-panels, so that the bulk trailing update is one K = 128 GEMM
 // per super-panel (half the C read/write traffic per flop of K = 64), with a
 // one-super-panel lookahead on two streams:
-//   hi: GEMM_a(s) (the next super-panel's 128 columns) -> factor_super(s+1)
-//   lo: U12(s) for the trailing columns -> GEMM_b(s) (all later columns)
+//   hi: U12 of the next super-panel's 128 columns -> GEMM_a1 (its first 64
+//       columns) -> factor_super(s+1)
+//   lo: GEMM_a2 (its other 64 columns) -> U12(s) for every later column ->
+//       GEMM_b(s), the lookahead's next columns first
 // factor_super(c0): panel_L(c0); U12 of the first half onto the second half's
 // 64 columns; their K = 64 update; panel_L(c0 + 64).
 // U12(s) = L11^-1 A12 is one K = 128 GEMM with the super-panel's 128x128
-// unit-lower inverse, assembled by the two panel launches' extra CTAs.
+// unit-lower inverse, assembled by the two panel launches' extra CTAs. The
+// chain on hi is latency-bound late in the factorisation; its kernels are
+// launched with programmatic stream serialization (griddepcontrol) so each
+// starts while its predecessor drains.
 #ifdef RL_GENP_TRACE
 // developer timeline of the lookahead schedule (never in the product build):
 // one-thread kernels stamp %globaltimer into a managed buffer
@@ -488,12 +495,29 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     auto next_event = [&]() { return ev[2 + (e++ % kRing)]; };
     auto at = [&](int64_t r, int64_t c) { return a + r * lda + c; };
     // GEMM C -= A B on stream sm (ctx->stream is what gemm() launches on)
+    // programmatic dependent launch for kernels on the lookahead chain (hi),
+    // except right after a cross-stream event wait (only kernel-to-kernel edges
+    // of one stream are relaxed)
+    bool hi_waited = true;
+    auto hi_wait = [&](cudaEvent_t e) -> rl_status {
+        RL_CUDA(cudaStreamWaitEvent(hi, e, 0));
+        hi_waited = true;
+        return RL_OK;
+    };
+    auto use_pdl = [&](cudaStream_t sm) {
+        if (sm != hi) return false;
+        const bool ok = !hi_waited;
+        hi_waited = false;
+        return ok;
+    };
     auto update = [&](cudaStream_t sm, int64_t M, int64_t N, int64_t Kd, const double* A, const double* B,
                       double* C) -> rl_status {
         if (M <= 0 || N <= 0) return RL_OK;
         cudaStream_t keep = ctx->stream;
         ctx->stream = sm;
+        ctx->pdl = use_pdl(sm);
         const rl_status r = gemm(ctx, M, N, Kd, A, lda, B, lda, C, lda, -1.0, true, nullptr);
+        ctx->pdl = false;
         ctx->stream = keep;
         return r;
     };
@@ -528,12 +552,23 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         const int rpc = PT / q;
         const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + rpc - 1) / rpc));
         const int half = static_cast<int>((c0 / kBase) & 1);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks + 1));
+        cfg.blockDim = dim3(PT);
+        cfg.dynamicSmemBytes = kInvFusedSmem;
+        cfg.stream = sm;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = use_pdl(sm) ? 1 : 0;
+        double* inv_c = inv_of(c0);
         if (q == 4)
-            lu_panel64_kernel<4><<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0), half);
+            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<4>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half);
         else if (q == 2)
-            lu_panel64_kernel<2><<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0), half);
+            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<2>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half);
         else
-            lu_panel64_kernel<1><<<blocks + 1, PT, kInvFusedSmem, sm>>>(a, lda, n, c0, blocks, piv_out, rinv_out, inv_of(c0), half);
+            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<1>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         return RL_OK;
     };
@@ -544,18 +579,29 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         if (ncols <= 0) return RL_OK;
         cudaStream_t keep = ctx->stream;
         ctx->stream = sm;
+        ctx->pdl = use_pdl(sm);
         const rl_status r =
             gemm(ctx, rows, ncols, rows, inv_of(r0), W, at(r0, cb), lda, at(r0, cb), lda, 1.0, false, nullptr);
+        ctx->pdl = false;
         ctx->stream = keep;
         return r;
     };
 #ifdef RL_GENP_TRACE
     GenpTrace trace;
 #endif
-    auto factor_super = [&](cudaStream_t sm, int64_t c0) -> rl_status {
+    // second_ready: the event after which the second half's 64 columns are
+    // fully updated (GEMM_a2 on the other stream), or nullptr
+    auto factor_super = [&](cudaStream_t sm, int64_t c0, cudaEvent_t second_ready) -> rl_status {
         rl_status r;
         if ((r = panel_l(sm, c0)) != RL_OK) return r;
         TRACE(6, sm);
+        if (second_ready) {
+            if (sm == hi) {
+                if ((r = hi_wait(second_ready)) != RL_OK) return r;
+            } else {
+                RL_CUDA(cudaStreamWaitEvent(sm, second_ready, 0));
+            }
+        }
         if ((r = u12(sm, c0, kBase, c0 + kBase, kBase)) != RL_OK) return r;
         TRACE(7, sm);
         if ((r = update(sm, n - c0 - kBase, kBase, kBase, at(c0 + kBase, c0), at(c0, c0 + kBase),
@@ -566,34 +612,61 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     };
     TRACE(0, lo);
     RL_CUDA(cudaEventRecord(ev[0], lo));  // prior work on the caller's stream
-    RL_CUDA(cudaStreamWaitEvent(hi, ev[0], 0));
-    if ((st = factor_super(hi, 0)) != RL_OK) return st;
+    if ((st = hi_wait(ev[0])) != RL_OK) return st;
+    if ((st = factor_super(hi, 0, nullptr)) != RL_OK) return st;
     cudaEvent_t el = next_event();
     RL_CUDA(cudaEventRecord(el, hi));
+    // Per super-panel s (c0 = s W), the lookahead chain on hi is
+    //   U12 of the next super-panel's own 128 columns -> GEMM_a1 (its first 64
+    //   columns) -> panel_L -> [GEMM_a2 from lo] -> small U12 -> update -> panel_L
+    // while lo runs GEMM_a2 (the next super-panel's other 64 columns), U12 of
+    // every later column and GEMM_b. hi's U12 waits only for lo's GEMM_b(s-1)
+    // (which last touched those columns), not for lo's U12 of all the rest.
+    cudaEvent_t eb = nullptr;  // lo: GEMM_b(s-1) done
     for (int64_t sp = 0; sp < S; ++sp) {
         const int64_t c0 = sp * W, rest = n - c0 - W;
         if (rest <= 0) break;
-        // lo: U12 of this super-panel for every trailing column
-        RL_CUDA(cudaStreamWaitEvent(lo, el, 0));
-        TRACE(1, lo);
-        if ((st = u12(lo, c0, W, c0 + W, rest)) != RL_OK) return st;
-        cudaEvent_t eu = next_event();
-        RL_CUDA(cudaEventRecord(eu, lo));
         const bool next_full = sp + 1 < S;
-        // hi: GEMM_a(s) -> factor_super(s+1)
-        RL_CUDA(cudaStreamWaitEvent(hi, eu, 0));
-        TRACE(2, lo);
+        RL_CUDA(cudaStreamWaitEvent(lo, el, 0));  // factor_super(s): L21, U11, L11^-1
+        TRACE(1, lo);
         if (next_full) {
-            if ((st = update(hi, rest, W, W, at(c0 + W, c0), at(c0, c0 + W), at(c0 + W, c0 + W))) != RL_OK) return st;
+            // hi: U12 of columns [c0 + W, c0 + 2W), GEMM_a1
+            if (eb && (st = hi_wait(eb)) != RL_OK) return st;
+            if ((st = u12(hi, c0, W, c0 + W, W)) != RL_OK) return st;
+            cudaEvent_t eua = next_event();
+            RL_CUDA(cudaEventRecord(eua, hi));
+            TRACE(2, hi);
+            if ((st = update(hi, rest, kBase, W, at(c0 + W, c0), at(c0, c0 + W), at(c0 + W, c0 + W))) != RL_OK)
+                return st;
             TRACE(3, hi);
-            if ((st = factor_super(hi, c0 + W)) != RL_OK) return st;
+            // lo: GEMM_a2 (the next super-panel's second 64 columns)
+            RL_CUDA(cudaStreamWaitEvent(lo, eua, 0));
+            if ((st = update(lo, rest, kBase, W, at(c0 + W, c0), at(c0, c0 + W + kBase), at(c0 + W, c0 + W + kBase))) !=
+                RL_OK)
+                return st;
+            cudaEvent_t ea2 = next_event();
+            RL_CUDA(cudaEventRecord(ea2, lo));
+            // hi: factor_super(s+1), its second half after GEMM_a2
+            if ((st = factor_super(hi, c0 + W, ea2)) != RL_OK) return st;
             TRACE(4, hi);
             el = next_event();
             RL_CUDA(cudaEventRecord(el, hi));
         }
-        // lo: GEMM_b(s) on the remaining columns (all of them before the tail)
+        // lo: U12 and GEMM_b(s) on the remaining columns (all of them before the tail)
         const int64_t cb = next_full ? c0 + 2 * W : c0 + W;
-        if ((st = update(lo, rest, n - cb, W, at(c0 + W, c0), at(c0, cb), at(c0 + W, cb))) != RL_OK) return st;
+        if ((st = u12(lo, c0, W, cb, n - cb)) != RL_OK) return st;
+        // the columns the lookahead needs next (super-panel s+2) first, so the
+        // chain on hi waits only for them; then the rest. (Pairing two
+        // super-panels' bulk updates into one K = 2W GEMM, bit-identical, was
+        // measured slower: 17.0 against 16.9 ms.)
+        const int64_t first = next_full ? std::min<int64_t>(W, n - cb) : n - cb;
+        if ((st = update(lo, rest, first, W, at(c0 + W, c0), at(c0, cb), at(c0 + W, cb))) != RL_OK) return st;
+        eb = next_event();
+        RL_CUDA(cudaEventRecord(eb, lo));
+        if (n - cb > first &&
+            (st = update(lo, rest, n - cb - first, W, at(c0 + W, c0), at(c0, cb + first), at(c0 + W, cb + first))) !=
+                RL_OK)
+            return st;
         TRACE(5, lo);
     }
     RL_CUDA(cudaEventRecord(ev[1], hi));

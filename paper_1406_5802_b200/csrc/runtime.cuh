@@ -34,6 +34,9 @@ struct rl_context {
     size_t pinned_bytes[2] = {0, 0};
     // 4 KiB pinned host scalars for asynchronous device->host readbacks
     int64_t* host_scalars = nullptr;
+    // set around launches on a latency-bound chain of small kernels (the GENP
+    // lookahead): gemm() then launches with programmatic stream serialization
+    bool pdl = false;
 };
 
 namespace rl {
