@@ -215,8 +215,97 @@ __device__ __forceinline__ void inv_unit_lower64(const double (*sd)[kBase + 1], 
     }
 }
 
+// GENP of the 64x64 block in sd in place (lu.hpp:47-56 up to rounding),
+// blocked by 16: per 16-column step, warp 0 factors the 16x16 diagonal block
+// alone (two lanes per row, pivot rows through shared memory, warp barriers
+// only), then every thread forms L21 rows (x U_D = a) or U12 columns
+// (L_D y = a) by substitution, then the trailing block takes -L21 U12 on DMMA.
+// 21.7k cycles per panel launch against 28.7k for the all-threads elimination
+// above (clock64, RL_PANEL_PHASES); factorisation 16.86 -> 16.70 ms.
+__device__ __forceinline__ void factor64_blocked(double (*sd)[kBase + 1], double (*pbuf)[2 * kBase], int tid) {
+    const int warp = tid >> 5, lane = tid & 31;
+    double* rinv16 = pbuf[0] + 64;  // reciprocals of the current block's pivots
+#pragma unroll 1
+    for (int kb = 0; kb < 4; ++kb) {
+        const int J = 16 * kb, m = kBase - J - 16;
+        if (warp == 0) {
+            const int r = lane >> 1, h = lane & 1;
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = sd[J + r][J + 8 * h + c];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                double* pv = pbuf[1] + 16 * (t & 1);
+                if (r == t) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) pv[8 * h + c] = x[c];
+                }
+                __syncwarp();
+                const double piv = pv[t];
+                double ph[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) ph[c] = pv[8 * h + c];
+                const double inv = rcp64(piv);
+                if (lane == 0) rinv16[t] = inv;
+                const double a_rt = __shfl_sync(kFull, x[t & 7], 2 * r + (t >> 3));
+                const bool below = r > t;
+                const double l = below ? div_by(a_rt, piv, inv) : 0.0;
+                if (below && h == (t >> 3)) x[t & 7] = l;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (8 * h + c > t) x[c] = fma(-l, ph[c], x[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) sd[J + r][J + 8 * h + c] = x[c];
+        }
+        __syncthreads();
+        if (m == 0) break;
+        if (tid < m) {
+            // L21 row i: x U_D = a, x_j = (a_j - sum_{q<j} x_q u_qj) / u_jj
+            const int i = J + 16 + tid;
+            double x[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) x[c] = sd[i][J + c];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+#pragma unroll
+                for (int q = 0; q < j; ++q) x[j] = fma(-x[q], sd[J + q][J + j], x[j]);
+                x[j] = div_by(x[j], sd[J + j][J + j], rinv16[j]);
+            }
+#pragma unroll
+            for (int c = 0; c < 16; ++c) sd[i][J + c] = x[c];
+        } else if (tid >= 64 && tid < 64 + m) {
+            // U12 column c: L_D y = a (unit lower)
+            const int c = J + 16 + tid - 64;
+            double y[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) y[q] = sd[J + q][c];
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+#pragma unroll
+                for (int q = 0; q < i; ++q) y[i] = fma(-sd[J + i][J + q], y[q], y[i]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) sd[J + q][c] = y[q];
+        }
+        __syncthreads();
+        {
+            // A22 -= L21 U12 (K = 16) on DMMA, one 8x8 tile per warp at a time
+            const int tn = m / 8, fr = lane >> 2, fc = lane & 3;
+            for (int t = warp; t < tn * tn; t += PT / 32) {
+                const int r0 = J + 16 + 8 * (t / tn), c0 = J + 16 + 8 * (t % tn);
+                double v0 = sd[r0 + fr][c0 + 2 * fc], v1 = sd[r0 + fr][c0 + 2 * fc + 1];
+#pragma unroll
+                for (int k = 0; k < 16; k += 4) dmma_884(v0, v1, -sd[r0 + fr][J + k + fc], sd[J + k + fc][c0 + fr]);
+                sd[r0 + fr][c0 + 2 * fc] = v0;
+                sd[r0 + fr][c0 + 2 * fc + 1] = v1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 #ifdef RL_PANEL_PHASES
-__device__ unsigned long long g_panel_phase[4];
+__device__ unsigned long long g_panel_phase[6];
 #endif
 // 8x8 tiles (ti0 + {0,1}, 0..7) of S = M N for 64x64 operands in shared
 // memory (M row-major with stride ldm, N with stride ldn), one warp
@@ -269,7 +358,11 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
 #ifdef RL_PANEL_PHASES
     const long long t1 = clock64();
 #endif
+#ifdef RL_FACTOR64_SHIFT
     factor64_shift(sd, pbuf, tid);
+#else
+    factor64_blocked(sd, pbuf, tid);
+#endif
     if (tid < kBase) {
         sp[tid] = sd[tid][tid];
         sr[tid] = 1.0 / sd[tid][tid];
@@ -293,6 +386,9 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
         for (int idx = tid; idx < kBase * kBase; idx += PT) dst[(idx >> 6) * 128 + (idx & 63)] = X[(idx >> 6) * LDX + (idx & 63)];
         if (half == 0) {
             for (int idx = tid; idx < kBase * kBase; idx += PT) inv128[(idx >> 6) * 128 + kBase + (idx & 63)] = 0.0;
+#ifdef RL_PANEL_PHASES
+            if (tid == 0) atomicExch(&g_panel_phase[4], static_cast<unsigned long long>(clock64() - t2));
+#endif
             return;
         }
         // off-diagonal block -Lb^-1 (L_ba La^-1)
@@ -324,6 +420,9 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
                 o[0] = -acc[i][j][0];
                 o[1] = -acc[i][j][1];
             }
+#ifdef RL_PANEL_PHASES
+        if (tid == 0) atomicExch(&g_panel_phase[5], static_cast<unsigned long long>(clock64() - t2));
+#endif
         return;
     }
     if (b == 0) {
@@ -465,10 +564,10 @@ struct GenpTrace {
     ~GenpTrace() {
         cudaDeviceSynchronize();
 #ifdef RL_PANEL_PHASES
-        unsigned long long ph[4];
+        unsigned long long ph[6];
         cudaMemcpyFromSymbol(ph, g_panel_phase, sizeof(ph));
-        std::fprintf(stderr, "P load %.0f factor %.0f rows %.0f cycles per launch (%llu)\n", double(ph[0]) / ph[3],
-                     double(ph[1]) / ph[3], double(ph[2]) / ph[3], ph[3]);
+        std::fprintf(stderr, "P load %.0f factor %.0f rows %.0f inv0 %.0f inv1 %.0f cycles (last launch)\n",
+                     double(ph[0]), double(ph[1]), double(ph[2]), double(ph[4]), double(ph[5]));
 #endif
         for (size_t i = 0; i < tags.size(); ++i)
             std::fprintf(stderr, "T %d %.1f\n", tags[i], (buf[i] - buf[0]) * 1e-3);
