@@ -341,7 +341,8 @@ __device__ __forceinline__ void mm64_rows2(const double* M, int ldm, const doubl
 template <int Q>
 __global__ void __launch_bounds__(PT)
 lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, int row_ctas,
-                  double* __restrict__ piv_out, double* __restrict__ rinv_out, double* __restrict__ inv128, int half) {
+                  double* __restrict__ piv_out, double* __restrict__ rinv_out, double* __restrict__ inv128, int half,
+                  unsigned* __restrict__ tflag) {
     __shared__ double sd[kBase][kBase + 1];
     __shared__ __align__(16) double pbuf[2][2 * kBase];
     __shared__ double sp[kBase], sr[kBase];
@@ -352,6 +353,35 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     double* d = a + c0 * lda + c0;
     griddep_wait();  // programmatic launch on the lookahead chain: the update feeding this panel is done
     griddep_launch_dependents();
+    if (inv128 && half == 1 && blockIdx.x == gridDim.x - 2) {
+        // T = L_ba La^-1 needs nothing of this panel's factorisation: this CTA
+        // forms it while the others factor, parks it in the (zero) top-right
+        // block of the 128x128 inverse and raises tflag for the inverse CTA
+        extern __shared__ double inv_smem[];
+        double* Y = inv_smem;
+        const double* lba = a + c0 * lda + (c0 - kBase);
+        for (int idx = tid; idx < kBase * kBase; idx += PT) {
+            const int i = idx >> 6, k = idx & 63;
+            sd[i][k] = lba[i * lda + k];
+            Y[i * LDX + k] = inv128[i * 128 + k];
+        }
+        __syncthreads();
+        const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
+        double acc[2][8][2];
+        mm64_rows2(&sd[0][0], kBase + 1, Y, LDX, 2 * warp, lane, acc);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                double* o = inv128 + (8 * (2 * warp + i) + fr) * 128 + kBase + 8 * j + 2 * fc;
+                o[0] = acc[i][j][0];
+                o[1] = acc[i][j][1];
+            }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) atomicExch(tflag, static_cast<unsigned>(c0 + 1));
+        return;
+    }
     for (int idx = tid; idx < kBase * kBase; idx += PT) sd[idx >> 6][idx & 63] = d[(idx >> 6) * lda + (idx & 63)];
     for (int idx = tid; idx < 4 * kBase; idx += PT) (&pbuf[0][0])[idx] = 0.0;
     __syncthreads();
@@ -391,26 +421,20 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
 #endif
             return;
         }
-        // off-diagonal block -Lb^-1 (L_ba La^-1)
-        const double* lba = a + c0 * lda + (c0 - kBase);
+        // off-diagonal block -Lb^-1 T, T = L_ba La^-1 from the CTA before this
+        // one (all CTAs of a panel launch are co-resident: row_ctas + 2 <= 66)
+        if (tid == 0)
+            while (*reinterpret_cast<volatile unsigned*>(tflag) != static_cast<unsigned>(c0 + 1)) __nanosleep(64);
+        __syncthreads();
+        __threadfence();
         for (int idx = tid; idx < kBase * kBase; idx += PT) {
             const int i = idx >> 6, k = idx & 63;
-            sd[i][k] = lba[i * lda + k];
-            Y[i * LDX + k] = inv128[i * 128 + k];
+            sd[i][k] = __ldcg(inv128 + i * 128 + kBase + k);
         }
         __syncthreads();
+        for (int idx = tid; idx < kBase * kBase; idx += PT) inv128[(idx >> 6) * 128 + kBase + (idx & 63)] = 0.0;
         const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fc = lane & 3;
         double acc[2][8][2];
-        mm64_rows2(&sd[0][0], kBase + 1, Y, LDX, 2 * warp, lane, acc);  // T = L_ba La^-1
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                sd[8 * (2 * warp + i) + fr][8 * j + 2 * fc] = acc[i][j][0];
-                sd[8 * (2 * warp + i) + fr][8 * j + 2 * fc + 1] = acc[i][j][1];
-            }
-        __syncthreads();
         mm64_rows2(X, LDX, &sd[0][0], kBase + 1, 2 * warp, lane, acc);  // Lb^-1 T
 #pragma unroll
         for (int i = 0; i < 2; ++i)
@@ -634,7 +658,10 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     // ragged tail's 64-column step uses the top-left block of one more),
     // stream-ordered scratch
     double* inv = nullptr;
-    RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&inv), sizeof(double) * W * W * (S + 1), lo));
+    RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&inv), sizeof(double) * W * W * (S + 1) + 256, lo));
+    // the T-ready flag of the second-half panel launches (values c0 + 1, never reused)
+    unsigned* tflag = reinterpret_cast<unsigned*>(inv + W * W * (S + 1));
+    RL_CUDA(cudaMemsetAsync(tflag, 0, 256, lo));
     struct Free {
         double* p;
         cudaStream_t s;
@@ -652,7 +679,7 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + rpc - 1) / rpc));
         const int half = static_cast<int>((c0 / kBase) & 1);
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(static_cast<unsigned>(blocks + 1));
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks + 1 + half));
         cfg.blockDim = dim3(PT);
         cfg.dynamicSmemBytes = kInvFusedSmem;
         cfg.stream = sm;
@@ -663,11 +690,11 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         cfg.numAttrs = use_pdl(sm) ? 1 : 0;
         double* inv_c = inv_of(c0);
         if (q == 4)
-            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<4>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half);
+            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<4>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half, tflag);
         else if (q == 2)
-            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<2>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half);
+            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<2>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half, tflag);
         else
-            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<1>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half);
+            cudaLaunchKernelEx(&cfg, lu_panel64_kernel<1>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half, tflag);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         return RL_OK;
     };
@@ -808,7 +835,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         auto panel_l = [&](int64_t c0) -> rl_status {
             const int64_t rest = n - c0 - kBase;
             const int blocks = static_cast<int>(std::max<int64_t>(1, (rest + PT - 1) / PT));
-            lu_panel64_kernel<1><<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr, 0);
+            lu_panel64_kernel<1><<<blocks, PT, 0, hi>>>(a, lda, n, c0, blocks, piv_out, rinv_out, nullptr, 0, nullptr);
             RL_CHECK_LAUNCH("lu_panel64_kernel");
             return RL_OK;
         };
@@ -861,7 +888,7 @@ rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, doubl
         const int64_t rest = n - c0 - kBase;
         const int blocks = static_cast<int>((rest + PT - 1) / PT);
         lu_panel64_kernel<1><<<std::max(1, 2 * blocks), PT, 0, ctx->stream>>>(a, lda, n, c0, blocks, piv_out, rinv_out,
-                                                                        nullptr, 0);
+                                                                        nullptr, 0, nullptr);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
         if (rest > 0) {
             st = gemm(ctx, rest, rest, kBase, a + (c0 + kBase) * lda + c0, lda, a + c0 * lda + c0 + kBase, lda,
