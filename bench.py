@@ -47,6 +47,25 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 METRIC = "preprocessed-GENP FP64 TFLOP/s at n=8192, % of FP64 peak; batched solves/s"
 FP64_PEAK_TFLOPS = 35.46   # cuBLAS DGEMM 8192^3 measured on this pool's B200 (profiles/r01_fp64_peak.txt)
+
+
+def profiled_traffic(name, systems=None):
+    """dram__bytes_read + dram__bytes_write per launch of a kernel, from the
+    newest committed ncu --set full capture (profiles/rNN_<name>_traffic.json,
+    written by tools/write_profiles.py); scaled to `systems` for the batched
+    kernel. None when no capture is committed."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]_{name}_traffic.json")))
+    if not paths:
+        return None
+    try:
+        d = json.load(open(paths[-1]))
+        t = d.get("dram_bytes_per_launch")
+        if t is not None and systems is not None and d.get("systems"):
+            t = t * systems / d["systems"]
+        return t
+    except Exception:
+        return None
 FP64_DMMA_PEAK = 37.06     # DMMA issue-rate microbenchmark (tools/fp64_peak.cu)
 BATCH_BYTES_PER_SYSTEM = 25104  # SURVEY §8(d) config 2
 WORKLOAD = "Gaussian-preprocessed GENP solve, n=8192 (BASELINE headline; config 1 recipe at n=8192)"
@@ -480,13 +499,7 @@ def run_b200(args):
     # roofline of the dominant kernel: the A*G DMMA GEMM (2 n^3 flops per launch)
     gemm_ms = statistics.mean(prod_ms)
     gemm_tf = 2.0 * n ** 3 / (gemm_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_dgemm_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic = profiled_traffic("dgemm")
     roofline = {"bound": "tensor", "kernel": "dgemm_kernel (A*G, FP64 DMMA)", "achieved": gemm_tf,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": gemm_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "measured on this pool: cuBLAS DGEMM 8192^3 burst (profiles/r01_fp64_peak.txt); "
@@ -545,7 +558,7 @@ def run_b200(args):
                      "zero_pivots": summ["zero_pivots"], "max_residual": summ["max_residual"],
                      "max_growth": summ["max_growth"], "mean_residual": summ["mean_residual"],
                      "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                                  "traffic": None, "algorithmic_bytes_per_system": BATCH_BYTES_PER_SYSTEM}}
+                                  "traffic": profiled_traffic("batched", nb), "algorithmic_bytes_per_system": BATCH_BYTES_PER_SYSTEM}}
         del ba, bg, bb, blu, bx
 
     configs = None

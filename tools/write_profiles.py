@@ -8,7 +8,7 @@ def run(*a):
 os.makedirs("profiles", exist_ok=True)
 open(f"profiles/{tag}_launches_bench_summary.txt", "w").write(run("tools/launch_profile.py", f"{src}/launches_bench.csv"))
 subprocess.run(["cp", f"{src}/launches_bench.csv", f"profiles/{tag}_launches_bench.csv"])
-for name in ("dgemm", "batched", "fft_rows", "gen"):
+for name in ("dgemm", "batched", "fft_rows", "gen", "panel", "ola_rows"):
     rep = f"{src}/{name}.ncu-rep"
     if os.path.exists(rep):
         txt = run("tools/ncu_summary.py", rep) + "\n-- top source lines by stall samples --\n" + run("tools/ncu_lines.py", rep, "25")
@@ -28,4 +28,15 @@ json.dump({"kernel": d.get("Kernel Name", "")[:120], "dram_bytes_per_launch": tr
            "gpu_time_ns": num("gpu__time_duration.sum"),
            "source": f"ncu --set full capture ({src}/dgemm.ncu-rep)"},
           open(f"profiles/{tag}_dgemm_traffic.json", "w"), indent=1)
+# the batched kernel's per-launch DRAM traffic (bench.py's secondary roofline.traffic)
+if os.path.exists(f"{src}/batched.ncu-rep"):
+    raw = subprocess.run(["ncu", "-i", f"{src}/batched.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, v = rows[0], rows[2]
+    d = dict(zip(h, v))
+    traffic = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+    json.dump({"kernel": d.get("Kernel Name", "")[:120], "dram_bytes_per_launch": traffic,
+               "gpu_time_ns": num("gpu__time_duration.sum"), "systems": 65536,
+               "source": f"ncu --set full capture ({src}/batched.ncu-rep)"},
+              open(f"profiles/{tag}_batched_traffic.json", "w"), indent=1)
 print("ok")
