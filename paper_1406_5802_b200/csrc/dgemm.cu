@@ -48,6 +48,13 @@ using SmallCfg = Cfg<128, 64, 4, 2, 4, 2>;
 // updates): 64x32 tiles, 4 warps of 32x16, four CTAs per SM, so a problem of a
 // few 128x64 tiles still spreads over the SMs
 using TinyCfg = Cfg<64, 32, 2, 2, 4, 4>;
+// one tile row of up to 128 rows, 32-column tiles: for products computed in
+// place over their B operand (U12 = L11^-1 A12 overwriting A12), where every
+// CTA must read all rows of its column block before any CTA stores into them
+#ifndef RL_COLCFG
+#define RL_COLCFG 128, 16, 8, 1, 4, 2
+#endif
+using ColCfg = Cfg<RL_COLCFG>;
 
 // element (r, k) of a 128-byte-swizzled tile with 16 doubles per row
 __device__ __forceinline__ int swz128(int r, int k) { return r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3); }
@@ -372,6 +379,18 @@ rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A
     if (stats) RL_GEMM_DISPATCH(false, true);
     RL_GEMM_DISPATCH(false, false);
 #undef RL_GEMM_DISPATCH
+}
+
+rl_status gemm_inplace_b(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, double* BC,
+                         int64_t ldb) {
+    if (M <= 0 || N <= 0) return RL_OK;
+    if (M > 128 || K != M)
+        return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_inplace_b: one tile row of at most 128 rows (K = M)");
+    if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(BC) & 15))
+        return set_error(RL_ERR_INVALID_ARGUMENT, "gemm_inplace_b: TMA needs 16-byte aligned operands with even leading dimensions");
+    const bool tiny = (N + 63) / 64 < ctx->num_sms;  // ColCfg.BM = 128 too
+    return tiny ? run_cfg<ColCfg, false, false, true>(ctx, M, N, K, A, lda, BC, ldb, BC, ldb, 1.0, nullptr, 1, 0, 0)
+                : run_cfg<SmallCfg, false, false, true>(ctx, M, N, K, A, lda, BC, ldb, BC, ldb, 1.0, nullptr, 1, 0, 0);
 }
 
 rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,

@@ -501,6 +501,54 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
     }
 }
 
+// Forward substitution (lu.hpp:110-115) by column blocks, right-looking,
+// following the factorisation: once the panel of columns [c0, c0 + w) is
+// factored, y_k = L_kk^-1 y_k (every CTA solves the w x w unit-lower diagonal
+// block with a warp sweep; CTA 0 stores it to ys, never back into the
+// working vector y that the other CTAs read it from), then each row below
+// takes y_i -= L[i, c0:c0+w] y_k (one warp per row, coalesced).
+#ifndef RL_FWD_ROWS
+#define RL_FWD_ROWS 256
+#endif
+constexpr int FWD_ROWS = RL_FWD_ROWS;  // rows below the block per CTA
+__global__ void __launch_bounds__(256) fwd_panel_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
+                                                        int64_t c0, int w, double* __restrict__ y,
+                                                        double* __restrict__ ys) {
+    __shared__ double sl[kBase][kBase + 1];
+    __shared__ double sy[kBase];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const double* d = a + c0 * lda + c0;
+    for (int idx = tid; idx < kBase * kBase; idx += 256) {
+        const int i = idx >> 6, k = idx & 63;
+        sl[i][k] = (i < w && k < i) ? d[i * lda + k] : 0.0;
+    }
+    if (tid < kBase) sy[tid] = tid < w ? y[c0 + tid] : 0.0;
+    __syncthreads();
+    if (warp == 0) {
+        double v0 = sy[lane], v1 = sy[lane + 32];
+#pragma unroll
+        for (int k = 0; k < kBase; ++k) {  // zero multipliers past w leave the values unchanged
+            const double yk = __shfl_sync(kFull, k < 32 ? v0 : v1, k & 31);
+            if (lane > k) v0 = fma(-sl[lane][k], yk, v0);
+            if (lane + 32 > k) v1 = fma(-sl[lane + 32][k], yk, v1);
+        }
+        sy[lane] = v0;
+        sy[lane + 32] = v1;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && tid < w) ys[c0 + tid] = sy[tid];
+    const int64_t rbase = c0 + w + static_cast<int64_t>(blockIdx.x) * FWD_ROWS;
+    for (int rr = warp; rr < FWD_ROWS; rr += 8) {
+        const int64_t r = rbase + rr;
+        if (r >= n) break;
+        const double* lr = a + r * lda + c0;
+        double acc = 0.0;
+        for (int j = lane; j < w; j += 32) acc = fma(lr[j], sy[j], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) y[r] -= acc;
+    }
+}
+
 // ---- U12 = L11^-1 A12 for the trailing columns of a 64-row panel ---------
 // (the column half of the fused step, split out so it can run after the
 // trailing update of the previous step while the next panel factors on the
@@ -605,18 +653,32 @@ struct GenpTrace {
     } while (0)
 #endif
 static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out,
-                               double* rinv_out) {
+                               double* rinv_out, const double* fwd_b, double* fwd_y) {
     constexpr int64_t W = 2 * kBase;
     const int64_t S = n / W;  // full super-panels
     Ctx g{ctx, a, n, lda, piv_out, rinv_out};
     rl_status st;
-    constexpr int kRing = 8;
-    if ((st = side_resources(ctx, kRing + 2)) != RL_OK) return st;
-    cudaStream_t lo = ctx->stream, hi = ctx->hi_stream;
+    constexpr int kRing = 8, kFsRing = 8;
+    if ((st = side_resources(ctx, kRing + 2 + kFsRing)) != RL_OK) return st;
+    cudaStream_t lo = ctx->stream, hi = ctx->hi_stream, fs = ctx->fs_stream;
     cudaEvent_t* ev = ctx->events;
-    int e = 0;
+    int e = 0, f = 0;
     auto next_event = [&]() { return ev[2 + (e++ % kRing)]; };
     auto at = [&](int64_t r, int64_t c) { return a + r * lda + c; };
+    double* fwd_work = nullptr;  // the working right-hand side (fs-stream-ordered scratch)
+    // the forward substitution of columns [c0, c0 + w) on fs, once their panel
+    // (enqueued on sm) is done
+    auto fwd_after = [&](cudaStream_t sm, int64_t c0, int64_t w) -> rl_status {
+        if (!fwd_y) return RL_OK;
+        cudaEvent_t ef = ev[2 + kRing + (f++ % kFsRing)];
+        RL_CUDA(cudaEventRecord(ef, sm));
+        RL_CUDA(cudaStreamWaitEvent(fs, ef, 0));
+        const int64_t below = n - c0 - w;
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, (below + FWD_ROWS - 1) / FWD_ROWS));
+        fwd_panel_kernel<<<grid, 256, 0, fs>>>(a, lda, n, c0, static_cast<int>(w), fwd_work, fwd_y);
+        RL_CHECK_LAUNCH("fwd_panel_kernel");
+        return RL_OK;
+    };
     // GEMM C -= A B on stream sm (ctx->stream is what gemm() launches on)
     // programmatic dependent launch for kernels on the lookahead chain (hi),
     // except right after a cross-stream event wait (only kernel-to-kernel edges
@@ -628,6 +690,9 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         return RL_OK;
     };
     auto use_pdl = [&](cudaStream_t sm) {
+#ifdef RL_NO_PDL
+        return false;
+#endif
         if (sm != hi) return false;
         const bool ok = !hi_waited;
         hi_waited = false;
@@ -696,18 +761,19 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         else
             cudaLaunchKernelEx(&cfg, lu_panel64_kernel<1>, a, lda, n, c0, blocks, piv_out, rinv_out, inv_c, half, tflag);
         RL_CHECK_LAUNCH("lu_panel64_kernel");
-        return RL_OK;
+        return fwd_after(sm, c0, kBase);
     };
     // U12 = L11^-1 A12 in place for rows [r0, r0 + rows), rows = 64 (the
-    // top-left block) or 128 (the whole super-panel inverse): one CTA tile row,
-    // so each output column block reads all of its own input before any store
+    // top-left block) or 128 (the whole super-panel inverse): gemm_inplace_b
+    // keeps one CTA tile row, so each output column block reads all of its
+    // own input before any store (a 64-row tile configuration here once let a
+    // late-scheduled second tile row read rows the first had overwritten)
     auto u12 = [&](cudaStream_t sm, int64_t r0, int64_t rows, int64_t cb, int64_t ncols) -> rl_status {
         if (ncols <= 0) return RL_OK;
         cudaStream_t keep = ctx->stream;
         ctx->stream = sm;
         ctx->pdl = use_pdl(sm);
-        const rl_status r =
-            gemm(ctx, rows, ncols, rows, inv_of(r0), W, at(r0, cb), lda, at(r0, cb), lda, 1.0, false, nullptr);
+        const rl_status r = gemm_inplace_b(ctx, rows, ncols, rows, inv_of(r0), W, at(r0, cb), lda);
         ctx->pdl = false;
         ctx->stream = keep;
         return r;
@@ -738,6 +804,18 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     };
     TRACE(0, lo);
     RL_CUDA(cudaEventRecord(ev[0], lo));  // prior work on the caller's stream
+    if (fwd_y) {
+        RL_CUDA(cudaStreamWaitEvent(fs, ev[0], 0));
+        RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&fwd_work), sizeof(double) * n, fs));
+        RL_CUDA(cudaMemcpyAsync(fwd_work, fwd_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, fs));
+    }
+    struct FreeFs {
+        double* p;
+        cudaStream_t s;
+        ~FreeFs() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } fwd_guard{fwd_work, fs};
     if ((st = hi_wait(ev[0])) != RL_OK) return st;
     if ((st = factor_super(hi, 0, nullptr)) != RL_OK) return st;
     cudaEvent_t el = next_event();
@@ -808,16 +886,31 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
             return st;
         c0 += kBase;
     }
-    if (c0 < n) return panel(g, c0, n - c0);
+    if (c0 < n) {
+        if ((st = panel(g, c0, n - c0)) != RL_OK) return st;
+        if ((st = fwd_after(lo, c0, n - c0)) != RL_OK) return st;
+    }
+    if (fwd_y) {  // the caller's stream sees y
+        cudaEvent_t ef = ev[2 + kRing + (f++ % kFsRing)];
+        RL_CUDA(cudaEventRecord(ef, fs));
+        RL_CUDA(cudaStreamWaitEvent(lo, ef, 0));
+    }
     return RL_OK;
 }
 
-rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out) {
+rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out,
+                       const double* fwd_b, double* fwd_y, bool* fwd_done) {
+    if (fwd_done) *fwd_done = false;
     if (n <= 0) return RL_OK;
     Ctx g{ctx, a, n, lda, piv_out, rinv_out};
     const int64_t K = n / kBase;  // full 64-column panels
     rl_status st;
-    if (K >= 4) return genp_super128(ctx, n, a, lda, piv_out, rinv_out);
+    if (K >= 4) {
+        const bool fwd = fwd_b && fwd_y && fwd_done;
+        st = genp_super128(ctx, n, a, lda, piv_out, rinv_out, fwd ? fwd_b : nullptr, fwd ? fwd_y : nullptr);
+        if (st == RL_OK && fwd) *fwd_done = true;
+        return st;
+    }
     if (K >= 3) {
         // right-looking GENP with a one-panel lookahead on two streams:
         //   hi: GEMM_a(k) (next panel's 64 columns) -> panel_L(k+1)

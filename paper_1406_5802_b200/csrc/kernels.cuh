@@ -24,6 +24,10 @@ struct GemmStats {
 // accumulates over the written C.
 rl_status gemm(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                int64_t ldb, double* C, int64_t ldc, double alpha, bool accumulate, GemmStats* stats);
+// B <- A B in place (B: M x N, ld ldb; A: M x M, M <= 128), e.g. U12 = L11^-1
+// A12: a single tile row, so no CTA overwrites rows another still reads
+rl_status gemm_inplace_b(rl_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, double* BC,
+                         int64_t ldb);
 
 // Split-K variant for small M x N with long K (Gram matrices, Q^T A): partial
 // products per K-slice into `work` (>= gemm_splitk_work_bytes), then an
@@ -39,12 +43,20 @@ rl_status gemm_residual_stats(rl_context* ctx, int64_t M, int64_t N, int64_t K, 
 // In-place blocked GENP of the n x n row-major matrix `a` (ld = lda, even,
 // 16-byte aligned) into its packed LU. piv_out / rinv_out (device, n) receive
 // u_jj and 1/u_jj. No pivoting, no verdict (the caller decides it).
-rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out);
+// fwd_b / fwd_y (device, n, optional): when the super-panel path runs, the
+// forward substitution y = L^-1 b (lu.hpp:110-115) follows the panels on a side
+// stream, hidden under the factorisation, and *fwd_done is set; the caller then
+// needs only lu_solve_upper_device.
+rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out,
+                       const double* fwd_b = nullptr, double* fwd_y = nullptr, bool* fwd_done = nullptr);
 
 // Triangular solves on packed LU (device): x = U^-1 L^-1 b (x may alias b).
 // `rinv` (nullable) = 1/u_jj from genp_inplace; `work` >= lu_solve_work_bytes(n).
 rl_status lu_solve_device(rl_context* ctx, int64_t n, const double* lu, int64_t ld, const double* rinv,
                           const double* b, double* x, void* work);
+// x = U^-1 y only (the upper half of lu_solve_device; in place allowed)
+rl_status lu_solve_upper_device(rl_context* ctx, int64_t n, const double* lu, int64_t ld, const double* rinv,
+                                const double* y, double* x, void* work);
 size_t lu_solve_work_bytes(int64_t n);
 
 // y = A x (row-major m x n); y = b - A x when `residual` (b given).

@@ -147,6 +147,8 @@ struct Dense {
     double *A = nullptr, *G = nullptr, *P = nullptr;
     double *b = nullptr, *x = nullptr, *r = nullptr, *y = nullptr, *d = nullptr, *piv = nullptr, *rinv = nullptr;
     void* solve_work = nullptr;
+    // y = L^-1 b already formed under the factorisation (genp_inplace's side stream)
+    bool fwd_done = false;
     Scalars* sc = nullptr;
     // host-mode pipelining: A arrives in a_chunks row blocks of a_chunk_rows,
     // block c resident once a_ready[c] has fired (0 chunks: A fully resident)
@@ -263,7 +265,10 @@ rl_status factor_and_verdict(rl_context* ctx, Dense& D, rl_solve_info* info, Sta
     if (tm) tm->mark();
     if ((st = form_product(ctx, D, D.P, &D.sc->prod)) != RL_OK) return st;
     if (tm) tm->mark();
-    st = genp_inplace(ctx, n, D.P, D.ld, D.piv, D.rinv);
+    // with no left multiplier the first chain solve's right-hand side is b, so
+    // its forward substitution can follow the panels
+    D.fwd_done = false;
+    st = genp_inplace(ctx, n, D.P, D.ld, D.piv, D.rinv, D.pre == POST_NONE ? D.b : nullptr, D.y, &D.fwd_done);
     if (st != RL_OK) return st;
     matrix_stats_kernel<<<static_cast<unsigned>(n), 256, 0, s>>>(D.P, D.ld, n, true, &D.sc->upper);
     RL_CHECK_LAUNCH("matrix_stats_kernel(upper)");
@@ -338,7 +343,10 @@ rl_status chain_solve(rl_context* ctx, Dense& D, int64_t refine, rl_solve_info* 
             if ((st = circulant_rows(ctx, 1, n, D.r, n, n, D.fct, n, D.fr, n, D.fspec)) != RL_OK) return st;
             rhs = D.fr;
         }
-        st = lu_solve_device(ctx, n, D.P, D.ld, D.rinv, rhs, D.y, D.solve_work);
+        if (k == 0 && D.fwd_done)
+            st = lu_solve_upper_device(ctx, n, D.P, D.ld, D.rinv, D.y, D.y, D.solve_work);
+        else
+            st = lu_solve_device(ctx, n, D.P, D.ld, D.rinv, rhs, D.y, D.solve_work);
         if (st != RL_OK) return st;
         if (D.post == POST_DENSE) {  // H y = matvec (preprocess.hpp:88-94)
             st = gemv(ctx, n, n, D.G, D.ld, D.y, D.d, nullptr);

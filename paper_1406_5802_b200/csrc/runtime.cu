@@ -66,6 +66,7 @@ static void destroy_context(rl_context* c) {
     if (c->host_scalars) cudaFreeHost(c->host_scalars);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->hi_stream) cudaStreamDestroy(c->hi_stream);
+    if (c->fs_stream) cudaStreamDestroy(c->fs_stream);
     for (int i = 0; i < c->num_events; ++i) cudaEventDestroy(c->events[i]);
     delete[] c->events;
     delete c;
@@ -149,6 +150,7 @@ rl_status side_resources(rl_context* ctx, int count) {
         int lo = 0, hi = 0;
         RL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         RL_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream, cudaStreamNonBlocking, hi));
+        RL_CUDA(cudaStreamCreateWithPriority(&ctx->fs_stream, cudaStreamNonBlocking, hi));
     }
     if (ctx->num_events < count) {
         cudaEvent_t* ev = new cudaEvent_t[count];
@@ -165,6 +167,7 @@ void* pinned_staging(rl_context* ctx, size_t bytes, int slot) {
     if (bytes <= ctx->pinned_bytes[slot]) return ctx->pinned[slot];
     cudaStreamSynchronize(ctx->stream);
     if (ctx->hi_stream) cudaStreamSynchronize(ctx->hi_stream);
+    if (ctx->fs_stream) cudaStreamSynchronize(ctx->fs_stream);
     if (ctx->pinned[slot]) cudaFreeHost(ctx->pinned[slot]);
     ctx->pinned[slot] = nullptr;
     ctx->pinned_bytes[slot] = 0;

@@ -26,6 +26,8 @@ struct rl_context {
     // lookahead stream (high priority) and an event pool for intra-call
     // dependencies between it and `stream` (created on first use)
     cudaStream_t hi_stream = nullptr;
+    // forward-substitution stream: y = L^-1 b follows the GENP panels (genp.cu)
+    cudaStream_t fs_stream = nullptr;
     cudaEvent_t* events = nullptr;
     int num_events = 0;
     // grow-only pinned host staging: slot 0 the exact generator's hard cases,

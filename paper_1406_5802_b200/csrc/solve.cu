@@ -292,6 +292,18 @@ rl_status lu_solve_device(rl_context* ctx, int64_t n, const double* lu, int64_t 
     return RL_OK;
 }
 
+rl_status lu_solve_upper_device(rl_context* ctx, int64_t n, const double* lu, int64_t ld, const double* rinv,
+                                const double* y, double* x, void* work) {
+    if (n <= 0) return RL_OK;
+    const int64_t nblk = (n + TB - 1) / TB;
+    int* flags2 = static_cast<int*>(work);
+    int* ticket2 = flags2 + nblk;
+    RL_CUDA(cudaMemsetAsync(work, 0, sizeof(int) * (nblk + 1), ctx->stream));
+    trsv_kernel<true><<<static_cast<unsigned>(nblk), 256, 0, ctx->stream>>>(lu, ld, n, rinv, y, x, flags2, ticket2);
+    RL_CHECK_LAUNCH("trsv_kernel<upper>");
+    return RL_OK;
+}
+
 rl_status gemv(rl_context* ctx, int64_t m, int64_t n, const double* a, int64_t lda, const double* x, double* y,
                const double* b) {
     if (m <= 0) return RL_OK;

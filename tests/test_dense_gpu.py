@@ -31,6 +31,36 @@ def test_genp_kats(cuda):
     assert f.lower[0, 1] == 0.0
 
 
+def test_genp_bit_identical_under_contention(cuda):
+    """The blocked factorisation's streams (lookahead chain, in-place U12
+    GEMMs, the second-half panel's T handoff, the forward-substitution stream)
+    must not race: repeated factorisations and solves of the same matrix,
+    each while other kernels load the SMs from another stream, are
+    bit-identical. (A 64-row tile configuration of the in-place U12 once let a
+    late-scheduled second tile row read rows the first had already
+    overwritten, only under contention.)"""
+    torch = cuda
+    n = 2048  # every super-panel's U12 is a small product here
+    a = rl.gen_gaussian(n, n, 11)
+    g = rl.gen_gaussian(n, n, 12)
+    b = rl.gen_gaussian_vector(n, 13)
+    da, dg, db = (torch.from_numpy(v).cuda() for v in (a, g, b))
+    hog = torch.randn(4096, 4096, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    outs = []
+    for rep in range(6):
+        with torch.cuda.stream(side):
+            for _ in range(rep % 3):
+                hog = (hog @ hog) * (1.0 / 4096)
+        out = rl.preprocess_solve(da, db, None, rl.MultiplierSpec(rl.MultiplierKind.GAUSSIAN, 0, dense=dg), 0,
+                                  want_lu=True)
+        torch.cuda.synchronize()
+        outs.append((out.x.cpu().numpy().copy(), out.lu.cpu().numpy().copy()))
+    for x, lu in outs[1:]:
+        assert np.array_equal(x, outs[0][0])
+        assert np.array_equal(lu, outs[0][1])
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 64, 65, 127, 128, 129, 200, 511, 1024])
 def test_genp_factor_vs_oracle(cuda, orc, n):
     a = orc.C.gen_gaussian(n, n, 100 + n)

@@ -3,6 +3,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1406_5802_b200 as rl
 from paper_1406_5802_b200 import capi
+if os.environ.get('RANDLA_VARIANT_LIB'):
+    capi.LIB_PATH = os.environ['RANDLA_VARIANT_LIB']
+    capi._lib = None
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 t0 = time.time()
 a = torch.from_numpy(rl.gen_gaussian(n, n, 1)).cuda()
