@@ -506,11 +506,8 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
 // factored, y_k = L_kk^-1 y_k (every CTA solves the w x w unit-lower diagonal
 // block with a warp sweep; CTA 0 stores it to ys, never back into the
 // working vector y that the other CTAs read it from), then each row below
-// takes y_i -= L[i, c0:c0+w] y_k (one warp per row, coalesced).
-#ifndef RL_FWD_ROWS
-#define RL_FWD_ROWS 256
-#endif
-constexpr int FWD_ROWS = RL_FWD_ROWS;  // rows below the block per CTA
+// takes y_i -= L[i, c0:c0+w] y_k (one thread per row, its 64 loads in flight).
+constexpr int FWD_ROWS = 256;  // rows below the block per CTA (one per thread)
 __global__ void __launch_bounds__(256) fwd_panel_kernel(const double* __restrict__ a, int64_t lda, int64_t n,
                                                         int64_t c0, int w, double* __restrict__ y,
                                                         double* __restrict__ ys) {
@@ -537,15 +534,22 @@ __global__ void __launch_bounds__(256) fwd_panel_kernel(const double* __restrict
     }
     __syncthreads();
     if (blockIdx.x == 0 && tid < w) ys[c0 + tid] = sy[tid];
-    const int64_t rbase = c0 + w + static_cast<int64_t>(blockIdx.x) * FWD_ROWS;
-    for (int rr = warp; rr < FWD_ROWS; rr += 8) {
-        const int64_t r = rbase + rr;
-        if (r >= n) break;
+    // rows below: one thread per row, every load of the row in flight at once
+    const int64_t r = c0 + w + static_cast<int64_t>(blockIdx.x) * FWD_ROWS + tid;
+    if (tid < FWD_ROWS && r < n) {
         const double* lr = a + r * lda + c0;
-        double acc = 0.0;
-        for (int j = lane; j < w; j += 32) acc = fma(lr[j], sy[j], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) y[r] -= acc;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (w == kBase) {
+#pragma unroll
+            for (int j = 0; j < kBase; j += 2) {
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(lr + j));
+                acc[j & 3] = fma(v.x, sy[j], acc[j & 3]);
+                acc[(j + 1) & 3] = fma(v.y, sy[j + 1], acc[(j + 1) & 3]);
+            }
+        } else {
+            for (int j = 0; j < w; ++j) acc[j & 3] = fma(lr[j], sy[j], acc[j & 3]);
+        }
+        y[r] -= (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
 }
 
