@@ -674,7 +674,7 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
     // (enqueued on sm) is done
     auto fwd_after = [&](cudaStream_t sm, int64_t c0, int64_t w) -> rl_status {
         if (!fwd_y) return RL_OK;
-        cudaEvent_t ef = ev[2 + kRing + (f++ % kFsRing)];
+        cudaEvent_t ef = ev[2 + kRing + (f++ % (kFsRing - 1))];  // the last one is fwd_guard's
         RL_CUDA(cudaEventRecord(ef, sm));
         RL_CUDA(cudaStreamWaitEvent(fs, ef, 0));
         const int64_t below = n - c0 - w;
@@ -813,13 +813,19 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         RL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&fwd_work), sizeof(double) * n, fs));
         RL_CUDA(cudaMemcpyAsync(fwd_work, fwd_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, fs));
     }
-    struct FreeFs {
+    // on every exit (errors included) the caller's stream orders after the
+    // forward-substitution stream, which writes fwd_y, and its scratch is freed
+    struct FsJoin {
         double* p;
-        cudaStream_t s;
-        ~FreeFs() {
-            if (p) cudaFreeAsync(p, s);
+        cudaStream_t fs, lo;
+        cudaEvent_t ev;
+        ~FsJoin() {
+            if (!p) return;
+            cudaEventRecord(ev, fs);
+            cudaStreamWaitEvent(lo, ev, 0);
+            cudaFreeAsync(p, fs);
         }
-    } fwd_guard{fwd_work, fs};
+    } fwd_guard{fwd_work, fs, lo, ev[2 + kRing + kFsRing - 1]};
     if ((st = hi_wait(ev[0])) != RL_OK) return st;
     if ((st = factor_super(hi, 0, nullptr)) != RL_OK) return st;
     cudaEvent_t el = next_event();
@@ -894,12 +900,7 @@ static rl_status genp_super128(rl_context* ctx, int64_t n, double* a, int64_t ld
         if ((st = panel(g, c0, n - c0)) != RL_OK) return st;
         if ((st = fwd_after(lo, c0, n - c0)) != RL_OK) return st;
     }
-    if (fwd_y) {  // the caller's stream sees y
-        cudaEvent_t ef = ev[2 + kRing + (f++ % kFsRing)];
-        RL_CUDA(cudaEventRecord(ef, fs));
-        RL_CUDA(cudaStreamWaitEvent(lo, ef, 0));
-    }
-    return RL_OK;
+    return RL_OK;  // fwd_guard: the caller's stream sees y
 }
 
 rl_status genp_inplace(rl_context* ctx, int64_t n, double* a, int64_t lda, double* piv_out, double* rinv_out,
