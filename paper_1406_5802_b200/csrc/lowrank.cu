@@ -309,9 +309,7 @@ rl_status chol_inv_blocked(rl_context* ctx, double* W, int64_t ldl, int64_t l, d
         const int64_t rest = l - J - bw;
         if (rest > 0) {
             // panel: R[J:J+bw, J+bw:] = (R_JJ^-1)^T W[J:J+bw, J+bw:]  (in place)
-            if ((e = gemm(ctx, bw, rest, bw, xt, CB, W + J * ldl + J + bw, ldl, W + J * ldl + J + bw, ldl, 1.0, false,
-                          nullptr)) != RL_OK)
-                return e;
+            if ((e = gemm_inplace_b(ctx, bw, rest, bw, xt, CB, W + J * ldl + J + bw, ldl)) != RL_OK) return e;
             // trailing: W[J+bw:, J+bw:] -= panel^T panel
             transpose_kernel<<<dim3(nblk(rest, 32), nblk(bw, 32)), dim3(32, 8), 0, s>>>(W + J * ldl + J + bw, ldl, bw,
                                                                                         rest, pt, ldl);
