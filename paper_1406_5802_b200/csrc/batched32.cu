@@ -25,8 +25,9 @@
 //      G again (cp.async, in flight during the back substitution, lu.hpp:
 //      116-121, by shuffles over the lane's U row in registers); x = G y by row
 //      dots from shared memory; the residual ||b - A x|| / ||b|| (lu.hpp:
-//      155-161 / preprocess.hpp:122-128) on DMMA with A from shared memory;
-//      growth max|U| / max|P|.
+//      155-161 / preprocess.hpp:122-128) by row dots with A from shared memory
+//      (DFMA: a DMMA matvec wastes 3/4 of its products and queues the other
+//      warps' Schur DMMAs behind it); growth max|U| / max|P|.
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
@@ -196,21 +197,6 @@ __device__ __forceinline__ void smem_rowblock_frags(const double* sM, int ti, in
         const double2 v = *reinterpret_cast<const double2*>(&sM[pidx(8 * ti + fr, 8 * m + 2 * fc)]);
         f[2 * m] = v.x;
         f[2 * m + 1] = v.y;
-    }
-}
-__device__ __forceinline__ void matvec_dmma_smem(const double* sM, const double* sv, int lane, double (&cb)[4]) {
-    const int fc = lane & 3;
-    double bv[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) bv[kk] = lane < 4 ? sv[kidx(kk, fc)] : 0.0;
-#pragma unroll
-    for (int ti = 0; ti < 4; ++ti) {
-        double f[8];
-        smem_rowblock_frags(sM, ti, lane, f);
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) dmma(c0, c1, f[kk], bv[kk]);
-        cb[ti] = c0;
     }
 }
 
@@ -496,18 +482,19 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             s.vec[1][lane] = x;
             __syncwarp();
             // residual b - A x (preprocess.hpp:122-126), A from shared memory
-            double cb[4];
-            matvec_dmma_smem(s.A, s.vec[1], lane, cb);
-            double rsq = 0.0;
-            if (fc == 0) {
+            // (row dots: lane i reads its row of A, conflict-free in the pidx
+            // layout, and x broadcast; keeps the DMMA pipe for the other warps)
+            double ax[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int ti = 0; ti < 4; ++ti) {
-                    const double r = s.b[8 * ti + fr] - cb[ti];
-                    rsq = fma(r, r, rsq);
-                    s.vec[0][8 * ti + fr] = r;
-                }
+            for (int m = 0; m < D / 2; ++m) {
+                const double2 av = *reinterpret_cast<const double2*>(&s.A[pidx(lane, 2 * m)]);
+                const double2 xv = *reinterpret_cast<const double2*>(&s.vec[1][2 * m]);
+                ax[(2 * m) & 3] = fma(av.x, xv.x, ax[(2 * m) & 3]);
+                ax[(2 * m + 1) & 3] = fma(av.y, xv.y, ax[(2 * m + 1) & 3]);
             }
-            rel = sqrt(warp_sum(rsq)) / bnorm;
+            const double r = bl - ((ax[0] + ax[1]) + (ax[2] + ax[3]));
+            s.vec[0][lane] = r;
+            rel = sqrt(warp_sum(r * r)) / bnorm;
             __syncwarp();
             y = s.vec[0][lane];
             __syncwarp();
