@@ -86,81 +86,19 @@ panel_rows_kernel_dyn(double* __restrict__ rows, int64_t lda, int64_t nrows, int
 
 // ---- fused right-looking step for a 64-column panel at c0 ------------------
 // Every CTA factors the 64x64 diagonal block redundantly in shared memory
-// (two threads per row, one barrier per elimination step), then does its
-// share of the panel: row CTAs form L21 = A21 U11^-1 (x U11 = a, column sweep
-// per row, one row per thread), column CTAs form U12 = L11^-1 A12 (column
-// sweep per column, one column per thread, coalesced). CTA 0 writes the
-// factored diagonal block and the pivots. One launch per elimination step;
-// the trailing update A22 -= L21 U12 is one DMMA GEMM (K = 64).
+// (factor64_blocked: blocked by 16, warp-synchronous diagonal blocks, DMMA
+// Schur updates), then does its share of the panel: row CTAs form
+// L21 = A21 U11^-1 (x U11 = a, column sweep per row, Q threads per row),
+// column CTAs (small matrices only) form U12 = L11^-1 A12 (column sweep per
+// column, one column per thread, coalesced). CTA 0 writes the factored
+// diagonal block and the pivots. The trailing update A22 -= L21 U12 is a DMMA
+// GEMM.
 constexpr int PT = 128;  // threads per CTA
 #ifndef RL_PANEL_Q4_ROWS
 #define RL_PANEL_Q4_ROWS 2048
 #endif
 constexpr int64_t kPanelQ4Rows = RL_PANEL_Q4_ROWS;
 
-// GENP of the 64x64 block in sd (lu.hpp:47-56 order) with a rolled loop: a
-// panel kernel runs this code once per CTA, so a fully unrolled version is
-// instruction-fetch bound (~1.2k cycles per step). Thread t owns row t>>1,
-// columns of parity t&1, in a window that shifts by one pair of columns per
-// pair of steps, so the current columns always sit in slot 0 (static register
-// indices only). Two steps per barrier: the owners of rows j0 = 2sp and
-// j1 = 2sp+1 publish both rows, and every thread forms row j1's step-j0 update
-// for its parity half itself (the same FMAs the owner performs), so the
-// factors are bit-identical to one step per barrier.
-__device__ __forceinline__ void factor64_shift(double (*sd)[kBase + 1], double (*pbuf)[2 * kBase], int tid) {
-    const int row = tid >> 1, h = tid & 1;
-    double r[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) r[q] = sd[row][2 * q + h];
-#pragma unroll 1
-    for (int sp = 0; sp < kBase / 2; ++sp) {
-        const int j0 = 2 * sp, j1 = j0 + 1;
-        // [0, 64): row j0, [64, 128): row j1, each as window-relative parity
-        // halves ([32 h + q] = column 2 (sp + q) + h). Buffer sp & 1 is
-        // rewritten two pairs later, after every reader passed a barrier.
-        double* pb = pbuf[sp & 1];
-        if (row == j0 || row == j1) {
-            double2* dst = reinterpret_cast<double2*>(pb + (row == j1 ? 64 : 0) + 32 * h);
-#pragma unroll
-            for (int m = 0; m < 16; ++m) dst[m] = make_double2(r[2 * m], r[2 * m + 1]);
-        }
-        __syncthreads();
-        const double pv0 = pb[0];                    // u(j0, j0): parity 0, slot 0
-        const double rinv0 = rcp64(pv0);
-        const double l10 = div_by(pb[64], pv0, rinv0);  // row j1's multiplier at step j0 (lu.hpp:51)
-        const double pv1 = fma(-l10, pb[32], pb[96]);   // u(j1, j1) after step j0 (lu.hpp:53)
-        const double rinv1 = rcp64(pv1);
-        const bool below0 = row > j0, below1 = row > j1;
-        const double other0 = __shfl_xor_sync(kFull, r[0], 1);
-        const double l0 = below0 ? div_by(h == 0 ? r[0] : other0, pv0, rinv0) : 0.0;
-        if (below0 && h == 0) r[0] = l0;
-        const double2* A = reinterpret_cast<const double2*>(pb + 32 * h);
-        const double2* B = reinterpret_cast<const double2*>(pb + 64 + 32 * h);
-        double bp[32];  // row j1 after step j0, this parity
-#pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const double2 av = A[m], bv = B[m];
-            if (m > 0 || h > 0) {  // columns > j0: all but slot 0 of parity 0
-                r[2 * m] = fma(-l0, av.x, r[2 * m]);
-                bp[2 * m] = fma(-l10, av.x, bv.x);
-            } else {
-                bp[0] = bv.x;
-            }
-            r[2 * m + 1] = fma(-l0, av.y, r[2 * m + 1]);
-            bp[2 * m + 1] = fma(-l10, av.y, bv.y);
-        }
-        const double other1 = __shfl_xor_sync(kFull, r[0], 1);
-        const double l1 = below1 ? div_by(h == 1 ? r[0] : other1, pv1, rinv1) : 0.0;
-        if (below1 && h == 1) r[0] = l1;
-#pragma unroll
-        for (int q = 1; q < 32; ++q) r[q] = fma(-l1, bp[q], r[q]);  // slot 0 holds columns j0, j1 only
-        sd[row][2 * sp + h] = r[0];  // column 2 sp + h is final
-#pragma unroll
-        for (int q = 0; q < 31; ++q) r[q] = r[q + 1];
-        r[31] = 0.0;
-    }
-    __syncthreads();
-}
 
 // X = L^-1 for the unit-lower part of a factored 64x64 block (strictly lower
 // entries of sd, implicit unit diagonal) by recursive doubling: the eight 8x8
@@ -220,8 +158,9 @@ __device__ __forceinline__ void inv_unit_lower64(const double (*sd)[kBase + 1], 
 // alone (two lanes per row, pivot rows through shared memory, warp barriers
 // only), then every thread forms L21 rows (x U_D = a) or U12 columns
 // (L_D y = a) by substitution, then the trailing block takes -L21 U12 on DMMA.
-// 21.7k cycles per panel launch against 28.7k for the all-threads elimination
-// above (clock64, RL_PANEL_PHASES); factorisation 16.86 -> 16.70 ms.
+// 21.7k cycles per panel launch against 28.7k for the all-threads,
+// two-steps-per-barrier elimination it replaced (clock64, RL_PANEL_PHASES);
+// factorisation 16.86 -> 16.70 ms.
 __device__ __forceinline__ void factor64_blocked(double (*sd)[kBase + 1], double (*pbuf)[2 * kBase], int tid) {
     const int warp = tid >> 5, lane = tid & 31;
     double* rinv16 = pbuf[0] + 64;  // reciprocals of the current block's pivots
@@ -388,11 +327,7 @@ lu_panel64_kernel(double* __restrict__ a, int64_t lda, int64_t n, int64_t c0, in
 #ifdef RL_PANEL_PHASES
     const long long t1 = clock64();
 #endif
-#ifdef RL_FACTOR64_SHIFT
-    factor64_shift(sd, pbuf, tid);
-#else
     factor64_blocked(sd, pbuf, tid);
-#endif
     if (tid < kBase) {
         sp[tid] = sd[tid][tid];
         sr[tid] = 1.0 / sd[tid][tid];
