@@ -422,8 +422,21 @@ rl_status gemm_splitk(rl_context* ctx, int64_t M, int64_t N, int64_t K, const do
     const int64_t ldp = (N + 1) & ~int64_t(1);
     const int64_t slab = M * ldp;
     double* part = static_cast<double*>(work);
-    rl_status st = run_cfg<BigCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, part, ldp, 1.0, nullptr, splits,
-                                                       ktc, slab);
+    // skinny products (the range finder's A H with r <= 64 columns, Q^T A with
+    // r <= 64 rows): a tile that does not overhang the short side
+#ifndef RL_SPLITK_SKINNY
+#define RL_SPLITK_SKINNY 1
+#endif
+    rl_status st;
+    if (RL_SPLITK_SKINNY && N <= 64 && M > 64)
+        st = run_cfg<SmallCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, part, ldp, 1.0, nullptr, splits, ktc,
+                                                   slab);
+    else if (RL_SPLITK_SKINNY && M <= 64)
+        st = run_cfg<TinyCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, part, ldp, 1.0, nullptr, splits, ktc,
+                                                  slab);
+    else
+        st = run_cfg<BigCfg, false, false, true>(ctx, M, N, K, A, lda, B, ldb, part, ldp, 1.0, nullptr, splits, ktc,
+                                                 slab);
     if (st != RL_OK) return st;
     reduce_splits_kernel<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, ctx->stream>>>(
         part, splits, slab, M, N, ldp, C, ldc, accumulate, alpha);
