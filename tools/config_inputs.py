@@ -151,4 +151,5 @@ if __name__ == "__main__":
         for k, v in PIN_ENV.items():
             if os.environ.get(k) != v:
                 raise SystemExit(f"{k} must be {v}: run through build() (pinned environment)")
-        print(json.dumps(_build_here(sys.argv[1], sys.argv[2])))
+        # stderr: the caller (bench.py) owns stdout for its one JSON line
+        print(json.dumps(_build_here(sys.argv[1], sys.argv[2])), file=sys.stderr)
