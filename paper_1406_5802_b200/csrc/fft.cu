@@ -36,6 +36,7 @@
 
 #include "device_common.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -326,7 +327,13 @@ __global__ void __launch_bounds__(OLA_T) ola_spectra_kernel(const double* __rest
     }
     __syncthreads();
     forward_fft(z, OLA_NF, tw, OLA_NF);
-    for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) spec[static_cast<int64_t>(s) * OLA_NF + u] = z[u];
+    // stored in the rows kernel's pass-3 order: slot 8 g + r (g = t + 128 gg,
+    // the last-pass group of thread t) at (8 gg + r) 128 + t, so one bulk copy
+    // gives every thread its 16 slots at consecutive 16-byte positions
+    for (int u = threadIdx.x; u < OLA_NF; u += blockDim.x) {
+        const int g = u >> 3, r = u & 7;
+        spec[static_cast<int64_t>(s) * OLA_NF + (8 * (g >> 7) + r) * OLA_T + (g & (OLA_T - 1))] = z[u];
+    }
 }
 
 // smem slot of position p: XOR of the 16-byte slot's low three bits with bits
@@ -338,39 +345,81 @@ __device__ __forceinline__ int ola_sw(int p) { return p ^ ((p >> 3) & 7); }
 // row pair per CTA, 128 threads, three passes (radix 16, 16, 8) held in
 // registers between shared-memory exchanges, the accumulated spectrum in
 // registers (each thread owns the 16 frequency slots of its last-pass groups),
-// base twiddles cached per CTA.
+// base twiddles cached per CTA. Latency hiding across chunks:
+// - the segment spectrum of the next chunk is copied into shared memory by
+//   one bulk copy (cp.async.bulk + mbarrier) as soon as the current one has
+//   been consumed (barrier 3), so its L2 round trip runs under passes 1 and 2
+//   instead of stalling pass 3 (the spectra are stored in pass-3 order: a
+//   warp's 16-byte reads are consecutive): 3.63 -> 2.62 ms on config 5 with
+//   per-thread cp.async;
+// - the next chunk's two row segments are prefetched into L2 (one bulk
+//   prefetch per row) at the start of the current chunk, so pass 1's loads
+//   hit L2: 2.62 -> 2.54 ms. Loading them into registers under pass 3
+//   instead spills at the 168-register cap of three CTAs per SM (3.56 ms).
+constexpr int OLA_SMEM = static_cast<int>(sizeof(cplx)) * (OLA_NF + 16 * OLA_T + 4 * 128 + 4 * 8) + 16;
 __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __restrict__ a, int64_t lda, int64_t m,
                                                             int k, int lc, int chunks, const cplx* __restrict__ spec,
                                                             const cplx* __restrict__ tw, double* __restrict__ out,
                                                             int64_t ldo, int l) {
-    __shared__ __align__(16) cplx z[OLA_NF];
-    __shared__ __align__(16) cplx tw1[4][128];  // w_2048^{t 2^j}
-    __shared__ __align__(16) cplx tw2[4][8];    // w_128^{n0 2^j}
+    extern __shared__ __align__(16) unsigned char ola_smem[];
+    cplx* z = reinterpret_cast<cplx*>(ola_smem);                      // OLA_NF
+    cplx* hsm = z + OLA_NF;                                           // 16 * OLA_T thread-private spectrum slots
+    cplx(*tw1)[128] = reinterpret_cast<cplx(*)[128]>(hsm + 16 * OLA_T);  // [4][128]: w_2048^{t 2^j}
+    cplx(*tw2)[8] = reinterpret_cast<cplx(*)[8]>(tw1 + 4);              // [4][8]: w_128^{n0 2^j}
+    uint64_t* hbar = reinterpret_cast<uint64_t*>(tw2 + 4);
     const int t = threadIdx.x;
     for (int i = t; i < 4 * 128; i += OLA_T) tw1[i >> 7][i & 127] = tw[((i & 127) << (i >> 7)) & (OLA_NF - 1)];
     if (t < 32) tw2[t >> 3][t & 7] = tw[(((t & 7) << (t >> 3)) * 16) & (OLA_NF - 1)];
-    __syncthreads();
     const int n2 = t & 7, o2 = (t >> 3) * 128;  // pass-2 group of this thread
+    uint32_t hphase = 0;  // completed spectrum copies
+    auto stage_spec = [&](int s) {  // thread 0, after every reader of hsm passed a barrier
+        mbar_expect_tx(hbar, OLA_NF * sizeof(cplx));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_u32(hsm)),
+            "l"(spec + static_cast<int64_t>(s) * OLA_NF), "r"(static_cast<unsigned>(OLA_NF * sizeof(cplx))),
+            "r"(smem_u32(hbar))
+            : "memory");
+    };
+    if (t == 0) {
+        mbar_init(hbar, 1);
+        mbar_fence_init();
+        if (2 * static_cast<int64_t>(blockIdx.x) < m) stage_spec(0);
+    }
+    __syncthreads();
     for (int64_t pair = blockIdx.x; 2 * pair < m; pair += gridDim.x) {
         const int64_t r0 = 2 * pair;
         const bool two = r0 + 1 < m;
         const double* a0 = a + r0 * lda;
         const double* a1 = two ? a + (r0 + 1) * lda : a0;
-        cplx acc[2][8];
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[g][q] = {0.0, 0.0};
-        for (int s = 0; s < chunks; ++s) {
+        auto load_chunk = [&](cplx (&v)[16], int s) {
             const int t0 = s * lc;
-            cplx v[16];
-            // pass 1 (N = 2048, M = 128), inputs straight from global memory
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int u = t + 128 * j, idx = t0 + u;
                 const bool in = u < lc && idx < k;
                 v[j] = {in ? __ldcs(a0 + idx) : 0.0, (in && two) ? __ldcs(a1 + idx) : 0.0};
             }
+        };
+        cplx acc[2][8];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[g][q] = {0.0, 0.0};
+        cplx v[16];
+        for (int s = 0; s < chunks; ++s) {
+            load_chunk(v, s);
+            // the next chunk's two row segments into L2 (one thread per row)
+            if (t < 2 && s + 1 < chunks && (t == 0 || two)) {
+                const int t0n = (s + 1) * lc;
+                const int len = min(lc, k - t0n);
+                const uintptr_t p0 = reinterpret_cast<uintptr_t>((t == 0 ? a0 : a1) + t0n);
+                const uintptr_t b0 = p0 & ~static_cast<uintptr_t>(15);
+                // the end rounds down: the last row's tail must not reach past A
+                const unsigned bytes = static_cast<unsigned>(((p0 + 8u * len) & ~static_cast<uintptr_t>(15)) - b0);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(b0), "r"(bytes));
+            }
+            // pass 1 (N = 2048, M = 128)
             dft_reg<16, false>(v);
             {
                 cplx w[16];
@@ -405,14 +454,8 @@ __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __rest
             }
             __syncthreads();
             // pass 3 (N = 8, M = 1): positions 8g + r; accumulate conj(Z) H_s
-            const cplx* hs = spec + static_cast<int64_t>(s) * OLA_NF;
-            // the segment spectrum's slots of both groups first: their L2
-            // latency runs under the shared-memory reads and the DFTs
-            cplx hq[2][8];
-#pragma unroll
-            for (int gg = 0; gg < 2; ++gg)
-#pragma unroll
-                for (int r = 0; r < 8; ++r) hq[gg][r] = hs[8 * (t + OLA_T * gg) + r];
+            mbar_wait(hbar, hphase & 1);
+            ++hphase;
 #pragma unroll
             for (int gg = 0; gg < 2; ++gg) {
                 const int g = t + OLA_T * gg;
@@ -422,12 +465,18 @@ __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __rest
                 dft_reg<8, false>(u8);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    const cplx zz = u8[brev<8>(r)], hh = hq[gg][r];
+                    const cplx zz = u8[brev<8>(r)], hh = hsm[(8 * gg + r) * OLA_T + t];
                     acc[gg][r].x = fma(zz.x, hh.x, fma(zz.y, hh.y, acc[gg][r].x));
                     acc[gg][r].y = fma(zz.x, hh.y, fma(-zz.y, hh.x, acc[gg][r].y));
                 }
             }
-            __syncthreads();  // z is rewritten by the next chunk's pass 1
+            __syncthreads();  // z is rewritten by the next chunk's pass 1; hsm by the next copy
+            if (t == 0) {
+                if (s + 1 < chunks)
+                    stage_spec(s + 1);
+                else if (2 * (pair + gridDim.x) < m)
+                    stage_spec(0);  // the next row pair's first chunk, under the inverse
+            }
         }
         // inverse: DIT passes in reverse, the first from the registers
 #pragma unroll
@@ -439,7 +488,7 @@ __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __rest
         }
         __syncthreads();
         {
-            cplx v[16], w[16];
+            cplx w[16];
             w[1] = tw2[0][n2];
             w[2] = tw2[1][n2];
             w[4] = tw2[2][n2];
@@ -457,7 +506,7 @@ __global__ void __launch_bounds__(OLA_T, 3) ola_rows_kernel(const double* __rest
         __syncthreads();
         {
             // last pass (N = 2048, M = 128): outputs t + 128 j; only lags < l are kept
-            cplx v[16], w[16];
+            cplx w[16];
             w[1] = tw1[0][t];
             w[2] = tw1[1][t];
             w[4] = tw1[2][t];
@@ -1069,7 +1118,13 @@ rl_status circulant_rows(rl_context* ctx, int64_t m, int64_t k, const double* a,
         RL_CHECK_LAUNCH("ola_spectra_kernel");
         const int64_t pairs = (m + 1) / 2;
         const int64_t grid = std::min<int64_t>(pairs, static_cast<int64_t>(ctx->num_sms) * 3);
-        ola_rows_kernel<<<static_cast<unsigned>(grid), OLA_T, 0, ctx->stream>>>(
+        static PerDeviceOnce ola_once;
+        const rl_status ost = once_per_device(ola_once, [&]() -> rl_status {
+            RL_CUDA(cudaFuncSetAttribute(ola_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OLA_SMEM));
+            return RL_OK;
+        });
+        if (ost != RL_OK) return ost;
+        ola_rows_kernel<<<static_cast<unsigned>(grid), OLA_T, OLA_SMEM, ctx->stream>>>(
             a, lda, m, static_cast<int>(k), lc, chunks, ospec, tw_f, out, ldo, static_cast<int>(l));
         RL_CHECK_LAUNCH("ola_rows_kernel");
         RL_CUDA(cudaFreeAsync(ospec, ctx->stream));
