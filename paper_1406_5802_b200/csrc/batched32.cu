@@ -7,27 +7,33 @@
 //   1. A_i -> the warp's A region and G_i -> its P region (cp.async, both in
 //      the bank-conflict-free pidx layout); A stays there for the residual, so
 //      A leaves HBM once.
-//   2. P = A_i G_i on the FP64 tensor path (128 DMMA m8n8k4), one 8-column
-//      block at a time, each block written over the G block it consumed;
-//      ||P||_F and max|P| fold over the registers.
+//   2. P = A_i G_i on the FP64 tensor path (128 DMMA m8n8k4). The 16 tiles of P
+//      stay in the DMMA accumulators through the LU: a tile goes to shared
+//      memory once, when its panel needs it. max|P| folds over the registers as
+//      an integer maximum of bit patterns.
 //   3. Blocked GENP (lu.hpp:47-56): 8-column panels eliminated row-per-lane,
 //      two steps per exchange (the owners of rows t, t+1 publish both rows and
 //      every lane forms row t+1's step-t update itself, bit-identically); b
 //      rides along as an extra column, so c = L^-1 b (the forward substitution
 //      of lu.hpp:110-115) falls out of the elimination; U12 by forward
-//      substitution, trailing Schur update on DMMA. Pivots are warp-uniform.
+//      substitution, trailing Schur update by DMMA on the accumulators (no C
+//      traffic). Pivots are warp-uniform. max|U| is taken from the U12
+//      fragments the Schur update loads and from the diagonal tiles.
 //   4. Verdict: tol = tol_pivot(32) * spectral_norm_estimate(P) (lu.hpp:44).
-//      floor <= estimate <= ||P||_F, so the power iteration runs only when a
-//      pivot lies in the band (tol_pivot*floor, tol_pivot*||P||_F]; it then
-//      runs in the reference's exact summation order (no FMA) in
-//      verdict_fixup_kernel, so the verdict is the reference's.
+//      estimate <= ||P||_F <= 32 max|P|, so the power iteration runs only when a
+//      pivot is <= tol_pivot * 32 max|P|; it then runs in the reference's exact
+//      summation order (no FMA) in verdict_fixup_kernel, so the verdict is the
+//      reference's.
 //   5. The packed LU is final: written back coalesced, and the P region takes
 //      G again (cp.async, in flight during the back substitution, lu.hpp:
-//      116-121, by shuffles over the lane's U row in registers); x = G y by row
-//      dots from shared memory; the residual ||b - A x|| / ||b|| (lu.hpp:
-//      155-161 / preprocess.hpp:122-128) by row dots with A from shared memory
-//      (DFMA: a DMMA matvec wastes 3/4 of its products and queues the other
-//      warps' Schur DMMAs behind it); growth max|U| / max|P|.
+//      116-121: x_k reaches every lane by shuffle, lanes >= k keep updating a y
+//      nobody reads, so the sweep has no selects); x = G y by row dots from
+//      shared memory; the residual ||b - A x|| / ||b|| (lu.hpp:155-161 /
+//      preprocess.hpp:122-128) by row dots with A from shared memory (DFMA: a
+//      DMMA matvec wastes 3/4 of its products and queues the other warps' Schur
+//      DMMAs behind it); growth max|U| / max|P|.
+// The kernel is bound by its instruction count: every change
+// above removes instructions, not latency.
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
@@ -65,22 +71,31 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// fast reciprocal: MUFU seed + two Newton steps (pivots are normal numbers;
-// a zero pivot gives inf and the verdict flags the system)
+// fast reciprocal: MUFU seed (relative error e <= 2^-20) and one cubic step
+// r (1 + e + e^2), truncation e^3 <= 2^-60: within 1 ulp of the quotient, one
+// DFMA and one link of the dependent chain fewer than two Newton steps (pivots
+// are normal numbers; a zero pivot gives inf and the verdict flags the system)
 __device__ __forceinline__ double rcp64(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-x, r, 1.0);
+    const double t = fma(e, e, e);
+    return fma(r, t, r);
 }
-// max of a non-negative running maximum and |x| without fmax's NaN handling
-// (DSETP + 2 FSEL instead of ~7 instructions)
-__device__ __forceinline__ double max_abs(double m, double x) {
-    const double a = fabs(x);
+// Running maximum of |x| kept as the bit pattern of a non-negative double
+// (patterns order like the values): one LOP3, two ISETP and two SEL on the
+// integer pipe -- fabs/fmax cost a DADD and a DSETP on the FP64 pipe per entry
+typedef unsigned long long absmax_t;
+__device__ __forceinline__ absmax_t max_abs(absmax_t m, double x) {
+    const absmax_t a = static_cast<absmax_t>(__double_as_longlong(x)) & 0x7fffffffffffffffULL;
     return a > m ? a : m;
 }
+__device__ __forceinline__ absmax_t max_abs_if(bool pred, absmax_t m, double x) {
+    const absmax_t a = static_cast<absmax_t>(__double_as_longlong(x)) & 0x7fffffffffffffffULL;
+    return (pred && a > m) ? a : m;
+}
+__device__ __forceinline__ absmax_t max_u64(absmax_t a, absmax_t b) { return a > b ? a : b; }
+__device__ __forceinline__ double absmax_value(absmax_t m) { return __longlong_as_double(static_cast<long long>(m)); }
 
 // y -= l * v on lanes where `pred` holds: a predicated DFMA, no select/moves
 __device__ __forceinline__ void fma_if(bool pred, double& y, double l, double v) {
@@ -128,7 +143,7 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
                                                 double& sumsq, double& amax) {
     const int fr = lane >> 2, fc = lane & 3;
     sumsq = 0.0;
-    amax = 0.0;
+    absmax_t amax_bits = 0;
 #pragma unroll
     for (int tp = 0; tp < 2; ++tp) {
         double c[2][4][2];
@@ -154,9 +169,10 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
                     make_double2(c[h][tj][0], c[h][tj][1]);
                 sumsq = fma(c[h][tj][0], c[h][tj][0], sumsq);
                 sumsq = fma(c[h][tj][1], c[h][tj][1], sumsq);
-                amax = max_abs(max_abs(amax, c[h][tj][0]), c[h][tj][1]);
+                amax_bits = max_abs(max_abs(amax_bits, c[h][tj][0]), c[h][tj][1]);
             }
     }
+    amax = absmax_value(amax_bits);
 }
 
 // Main-kernel shared memory per warp: P (then its LU), A, and a few vectors
@@ -167,7 +183,7 @@ struct __align__(16) MainSmem {
     double P[D * D];  // product A G, then its packed LU in place (pidx layout)
     double A[D * D];  // A_i (pidx layout): product operand and the residual's A
     double vec[2][D];   // double-buffered broadcast rows / vectors
-    double b[D];
+    double b[D];        // reciprocals of the pivots (back substitution)
     double c[D];        // b eliminated alongside the panels: c = L^-1 b
 };
 constexpr size_t kMainSmemBytes = sizeof(MainSmem) * WARPS;
@@ -188,18 +204,6 @@ __device__ __forceinline__ int pswz(int r) {
     return (((r ^ (r >> 2)) & 1) << 2) | (r & 2) | ((r >> 2) & 1);
 }
 __device__ __forceinline__ int pidx(int r, int c) { return r * D + ((((c >> 1) ^ pswz(r)) << 1) | (c & 1)); }
-
-// A row block ti as MMA A-fragments from the pidx-layout shared copy
-__device__ __forceinline__ void smem_rowblock_frags(const double* sM, int ti, int lane, double (&f)[8]) {
-    const int fr = lane >> 2, fc = lane & 3;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const double2 v = *reinterpret_cast<const double2*>(&sM[pidx(8 * ti + fr, 8 * m + 2 * fc)]);
-        f[2 * m] = v.x;
-        f[2 * m + 1] = v.y;
-    }
-}
-
 
 #ifdef RL_PHASES
 __device__ unsigned long long g_phase[8];
@@ -224,6 +228,14 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fr = lane >> 2, fc = lane & 3;
     MainSmem& s = reinterpret_cast<MainSmem*>(smem_raw)[warp];
+    // C-fragment (double2) address of tile (ti, tj) in the pidx layout: row
+    // 8 ti + fr, slot (4 tj + fc) ^ pswz(fr) = 4 (tj ^ gh) + (fc ^ gl) -- two
+    // per-lane bases and compile-time offsets
+    char* const pt_lo = reinterpret_cast<char*>(s.P) + fr * 256 + 16 * (fc ^ (pswz(fr) & 3));
+    char* const pt0 = pt_lo + 64 * (pswz(fr) >> 2);
+    char* const pt1 = pt_lo + 64 * ((pswz(fr) >> 2) ^ 1);
+#define P_TILE(ti, tj) reinterpret_cast<double2*>((((tj) & 1) ? pt1 : pt0) + (ti) * 2048 + ((tj) >> 1) * 128)
+#define A_TILE(ti, tj) reinterpret_cast<double2*>((((tj) & 1) ? pt1 : pt0) + 8192 + (ti) * 2048 + ((tj) >> 1) * 128)
 #ifdef RL_PHASES
     long long t_prev = clock64();
     long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -249,7 +261,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         }
         double af[4][8];
         const double bl = __ldcs(gB + sys * D + lane);
-        s.b[lane] = bl;
+        // (s.b takes the pivots' reciprocals for the back substitution)
         s.c[lane] = bl;
         // the next system's A and G (8 KiB each, contiguous) into L2 while this one runs
         if (lane < 2 && sys + sys_stride < batch) {
@@ -259,7 +271,13 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         cp_async_wait_all();
         __syncwarp();
 #pragma unroll
-        for (int ti = 0; ti < 4; ++ti) smem_rowblock_frags(s.A, ti, lane, af[ti]);
+        for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const double2 v = *A_TILE(ti, m);
+                af[ti][2 * m] = v.x;
+                af[ti][2 * m + 1] = v.y;
+            }
         PH(0);
 
         // ---- P = A G (DMMA; every 8x8 tile accumulates k in the order of
@@ -267,41 +285,52 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         // ||P||_F bounds spectral_norm_estimate (norms.hpp:77)
         // four independent partial sums / maxima (no 32-long dependent chains);
         // the sum only feeds the verdict bound, which carries a 1e-10 margin
-        double sq[4] = {0.0, 0.0, 0.0, 0.0}, mx[4] = {0.0, 0.0, 0.0, 0.0};
+        absmax_t mx[4] = {0, 0, 0, 0};
+        // the 16 tiles of P stay in the DMMA accumulators through the LU: tile
+        // (ti, tj) is written to shared memory once, when its panel needs it
+        double c[4][4][2];
 #pragma unroll
         for (int tj = 0; tj < 4; ++tj) {
-            double c[4][2];
 #pragma unroll
-            for (int ti = 0; ti < 4; ++ti) c[ti][0] = c[ti][1] = 0.0;
+            for (int ti = 0; ti < 4; ++ti) c[ti][tj][0] = c[ti][tj][1] = 0.0;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
                 const double bf = s.P[pidx(kidx(kk, fc), 8 * tj + fr)];
 #pragma unroll
-                for (int ti = 0; ti < 4; ++ti) dmma(c[ti][0], c[ti][1], af[ti][kk], bf);
+                for (int ti = 0; ti < 4; ++ti) dmma(c[ti][tj][0], c[ti][tj][1], af[ti][kk], bf);
             }
-            __syncwarp();  // every lane has read G's block tj
 #pragma unroll
             for (int ti = 0; ti < 4; ++ti) {
-                *reinterpret_cast<double2*>(&s.P[pidx((8 * ti + fr), 8 * tj + 2 * fc)]) = make_double2(c[ti][0], c[ti][1]);
-                sq[ti] = fma(c[ti][1], c[ti][1], fma(c[ti][0], c[ti][0], sq[ti]));
-                mx[ti] = max_abs(max_abs(mx[ti], c[ti][0]), c[ti][1]);
+                mx[ti] = max_abs(max_abs(mx[ti], c[ti][tj][0]), c[ti][tj][1]);
             }
         }
-        const double sumsq = (sq[0] + sq[1]) + (sq[2] + sq[3]);
-        const double amax = fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3]));
+        const double amax = absmax_value(max_u64(max_u64(mx[0], mx[1]), max_u64(mx[2], mx[3])));
         __syncwarp();
         PH(1);
-        const double tol_hi = kTolPivot32 * sqrt(warp_sum(sumsq)) * (1.0 + 1e-10);
         const double max_p = warp_max_nonneg(amax);
+        // spectral_norm_estimate(P) <= ||P||_F <= 32 max|P| (norms.hpp:77): pivots
+        // above tol_pivot times that bound pass whatever the exact estimate is
+        const double tol_hi = kTolPivot32 * (32.0 * max_p) * (1.0 + 1e-10);
         __syncwarp();
         PH(2);
 
         // ---- blocked GENP on P (lu.hpp:47-56 reorganised: 8-column panels
         // eliminated in natural order, U12 by forward substitution, trailing
         // Schur update on the FP64 tensor path). No row exchanges.
+        absmax_t um[2] = {0, 0};  // max |U| over the entries this lane sees
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
             const int J = 8 * kb, rows = D - J, R = D - J - 8;
+            // this panel's column tiles (ti >= kb, tj = kb) and row tiles
+            // (ti = kb, tj > kb) leave the accumulators
+            if (kb == 0) __syncwarp();  // every lane has read G
+#pragma unroll
+            for (int ti = kb; ti < 4; ++ti)
+                *P_TILE(ti, kb) = make_double2(c[ti][kb][0], c[ti][kb][1]);
+#pragma unroll
+            for (int tj = kb + 1; tj < 4; ++tj)
+                *P_TILE(kb, tj) = make_double2(c[kb][tj][0], c[kb][tj][1]);
+            __syncwarp();
             double pr[8], bb = 0.0;
             if (lane < rows) {
 #pragma unroll
@@ -381,24 +410,25 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                     for (int t = 0; t < 8; ++t) s.P[pidx((J + t), col)] = u[t];
                 }
                 __syncwarp();
-                // A22 -= L21 U12 (DMMA, k = 8)
-                const int nt = R / 8;
+                // A22 -= L21 U12 (DMMA, k = 8) on the accumulators
+                double bf2[3][2];
 #pragma unroll
-                for (int ti = 0; ti < nt; ++ti) {
+                for (int tj = kb + 1; tj < 4; ++tj)
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks) {
+                        bf2[tj - 1][ks] = s.P[pidx((J + 4 * ks + fc), 8 * tj + fr)];
+                        um[ks] = max_abs(um[ks], bf2[tj - 1][ks]);  // U12 is final: growth numerator
+                    }
+#pragma unroll
+                for (int ti = kb + 1; ti < 4; ++ti) {
                     double lf[2];
 #pragma unroll
-                    for (int ks = 0; ks < 2; ++ks) lf[ks] = -s.P[pidx((J + 8 + 8 * ti + fr), J + 4 * ks + fc)];
+                    for (int ks = 0; ks < 2; ++ks) lf[ks] = -s.P[pidx((8 * ti + fr), J + 4 * ks + fc)];
 #pragma unroll
-                    for (int tj = 0; tj < nt; ++tj) {
-                        double2* cp = reinterpret_cast<double2*>(&s.P[pidx((J + 8 + 8 * ti + fr), J + 8 + 8 * tj + 2 * fc)]);
-                        double2 cv = *cp;
+                    for (int tj = kb + 1; tj < 4; ++tj)
 #pragma unroll
-                        for (int ks = 0; ks < 2; ++ks)
-                            dmma(cv.x, cv.y, lf[ks], s.P[pidx((J + 4 * ks + fc), J + 8 + 8 * tj + fr)]);
-                        *cp = cv;
-                    }
+                        for (int ks = 0; ks < 2; ++ks) dmma(c[ti][tj][0], c[ti][tj][1], lf[ks], bf2[tj - 1][ks]);
                 }
-                __syncwarp();
             }
         }
 
@@ -417,11 +447,17 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             prow[2 * m] = v.x;
             prow[2 * m + 1] = v.y;
         }
-        double um[4] = {0.0, 0.0, 0.0, 0.0};
+        // the diagonal tiles' upper triangles complete max |U|
+        {
+            const bool in0 = 2 * fc >= fr, in1 = 2 * fc + 1 >= fr;
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-            if (k >= lane) um[k & 3] = max_abs(um[k & 3], prow[k]);
-        double umax = fmax(fmax(um[0], um[1]), fmax(um[2], um[3]));
+            for (int t = 0; t < 4; ++t) {
+                const double2 v = *P_TILE(t, t);
+                um[0] = max_abs_if(in0, um[0], v.x);
+                um[1] = max_abs_if(in1, um[1], v.y);
+            }
+        }
+        double umax = absmax_value(max_u64(um[0], um[1]));
 
         // ---- verdict: pivots <= tol_pivot * ||P||_F need the exact estimate
         if (flagged) {
@@ -435,6 +471,8 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         PH(4);
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
+        s.b[lane] = my_rinv;
+        __syncwarp();
         double x = 0.0, rel = 0.0, y = s.c[lane];  // y = L^-1 b from the elimination
         // the LU is final: store it now and reuse the P region for G (rows at
         // pidx layout: conflict-free row reads), in flight during the sweeps
@@ -461,12 +499,15 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                 }
             }
 #pragma unroll
-            for (int k = D - 1; k >= 0; --k) {  // backward, U (lu.hpp:116-121)
-                if (lane == k) y *= my_rinv;  // rcp64's reciprocal: within 1 ulp of the quotient
-                const double xk = __shfl_sync(kFull, y, k);
-                fma_if(lane < k, y, prow[k], xk);
+            // backward, U (lu.hpp:116-121): x_k = y_k / u_kk reaches every lane; lanes
+            // >= k keep updating a y that is never read again (no selects), and x_k
+            // goes to shared memory as the same value from every lane
+#pragma unroll
+            for (int k = D - 1; k >= 0; --k) {
+                const double xk = __shfl_sync(kFull, y, k) * s.b[k];  // rcp64's reciprocal: within 1 ulp of the quotient
+                y = fma(-prow[k], xk, y);
+                s.vec[0][k] = xk;
             }
-            s.vec[0][lane] = y;
             cp_async_wait_all();
             __syncwarp();
             // d = G y (matvec, matrix.hpp:146-156): lane i dots row i of G
