@@ -354,7 +354,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
 #pragma unroll
                     for (int m = t / 2; m < 4; ++m)
                         *reinterpret_cast<double2*>(&dst[2 * m]) = make_double2(pr[2 * m], pr[2 * m + 1]);
-                    dst[8] = bb;
+                    ra_s[8 + (lane - t)] = bb;  // c entries of rows t, t+1 side by side
                 }
                 __syncwarp();
                 double ra[8], rb[8];
@@ -367,7 +367,8 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                     rb[2 * m] = w.x;
                     rb[2 * m + 1] = w.y;
                 }
-                const double ca = ra_s[8], cb0 = rb_s[8];
+                const double2 cc = *reinterpret_cast<const double2*>(&ra_s[8]);
+                const double ca = cc.x, cb0 = cc.y;
                 const double inv_a = rcp64(ra[t]);
                 const double l1 = rb[t] * inv_a;
 #pragma unroll
@@ -440,10 +441,18 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         PH(3);
         // ---- this lane's LU row into registers (the sweeps' operands) and the
         // growth numerator max|U| over its U part
+        // row `lane`, 16-byte slot m of the P region in the pidx layout: eight
+        // per-lane addresses (slot (m & 7) ^ pswz(lane)) and compile-time offsets;
+        // the A region lies 8192 B above
+        char* rowp[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) rowp[j] = reinterpret_cast<char*>(s.P) + lane * 256 + 16 * (j ^ pswz(lane));
+#define P_ROW(m) reinterpret_cast<const double2*>(rowp[(m) & 7] + 128 * ((m) >> 3))
+#define A_ROW(m) reinterpret_cast<const double2*>(rowp[(m) & 7] + 8192 + 128 * ((m) >> 3))
         double prow[D];
 #pragma unroll
         for (int m = 0; m < D / 2; ++m) {
-            const double2 v = *reinterpret_cast<const double2*>(&s.P[pidx(lane, 2 * m)]);
+            const double2 v = *P_ROW(m);
             prow[2 * m] = v.x;
             prow[2 * m + 1] = v.y;
         }
@@ -514,7 +523,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             double d = 0.0;
 #pragma unroll
             for (int m = 0; m < D / 2; ++m) {
-                const double2 gv = *reinterpret_cast<const double2*>(&s.P[pidx(lane, 2 * m)]);
+                const double2 gv = *P_ROW(m);
                 const double2 yv = *reinterpret_cast<const double2*>(&s.vec[0][2 * m]);
                 d = fma(gv.x, yv.x, d);
                 d = fma(gv.y, yv.y, d);
@@ -528,7 +537,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             double ax[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int m = 0; m < D / 2; ++m) {
-                const double2 av = *reinterpret_cast<const double2*>(&s.A[pidx(lane, 2 * m)]);
+                const double2 av = *A_ROW(m);
                 const double2 xv = *reinterpret_cast<const double2*>(&s.vec[1][2 * m]);
                 ax[(2 * m) & 3] = fma(av.x, xv.x, ax[(2 * m) & 3]);
                 ax[(2 * m + 1) & 3] = fma(av.y, xv.y, ax[(2 * m + 1) & 3]);
