@@ -44,6 +44,33 @@ def test_config2_parity_first_4096(cuda, orc):
     assert abs(out.summary["max_growth"] - out.growth.max()) == 0
 
 
+def test_growth_numerator_covers_every_entry_of_u(cuda, orc):
+    """growth = max|U| / max|P|: the kernel takes max|U| from the U12 fragments of
+    its Schur updates and from the diagonal tiles instead of a pass over the
+    rows. One system per position (r, c), r <= c, of the upper triangle: A = I
+    with 1000 added at (r, c) and G = I, so P = U = A exactly, L = I and the
+    growth factor is exactly 1 -- unless the kernel's maximum misses (r, c)."""
+    pos = [(r, c) for r in range(32) for c in range(r, 32)]
+    n = len(pos)
+    a = np.tile(np.eye(32), (n, 1, 1))
+    for i, (r, c) in enumerate(pos):
+        a[i, r, c] += 1000.0
+    g = np.tile(np.eye(32), (n, 1, 1))
+    b = np.ones((n, 32))
+    out = rl.batched_preprocess_solve_32(a, g, b)
+    assert (out.status == 0).all()
+    assert (out.lu == a).all()
+    bad = [pos[i] for i in range(n) if out.growth[i] != 1.0]
+    assert not bad, bad[:8]
+    # and on config-2 systems the numerator is the maximum of the returned U
+    ref = _config2_inputs(orc, 512)
+    out = rl.batched_preprocess_solve_32(ref["a"], ref["g"], ref["b"])
+    for i in range(512):
+        umax = np.abs(np.triu(out.lu[i])).max()
+        pmax = np.abs(ref["a"][i] @ ref["g"][i]).max()
+        assert abs(out.growth[i] * pmax - umax) <= 1e-12 * umax, (i, out.growth[i] * pmax, umax)
+
+
 def test_config2_full_batch_device_pointers(cuda, orc):
     """65536 systems, device-resident (torch) — spot-check 512 systems against
     the oracle and the whole batch through size-independent properties."""
