@@ -2,7 +2,7 @@
 // each preprocess_solve(A_i, b_i, none, {Gaussian, G_i}, refine)
 // (preprocess.hpp:156-180) on one warp.
 //
-// Per system (one warp, 17,408 B of shared memory, 168 registers: 12 resident
+// Per system (one warp, 17,152 B of shared memory, 168 registers: 12 resident
 // warps per SM; the next system's A and G are prefetched into L2):
 //   1. A_i -> the warp's A region and G_i -> its P region (cp.async, both in
 //      the bank-conflict-free pidx layout); A stays there for the residual, so
@@ -26,7 +26,7 @@
 //      reference's.
 //   5. The packed LU is final: written back coalesced, and the P region takes
 //      G again (cp.async, in flight during the back substitution, lu.hpp:
-//      116-121: x_k reaches every lane by shuffle, lanes >= k keep updating a y
+//      116-121: x_k = y_k (1/u_kk) reaches every lane by shuffle, lanes >= k keep updating a y
 //      nobody reads, so the sweep has no selects); x = G y by row dots from
 //      shared memory; the residual ||b - A x|| / ||b|| (lu.hpp:155-161 /
 //      preprocess.hpp:122-128) by row dots with A from shared memory (DFMA: a
@@ -176,14 +176,13 @@ __device__ __forceinline__ void product_to_smem(const double (&a)[4][8], const d
 }
 
 // Main-kernel shared memory per warp: P (then its LU), A, and a few vectors
-// (17,408 B): 3 CTAs x 4 warps per SM (209 KB). Measured: 12
+// (17,152 B): 3 CTAs x 4 warps per SM (206 KB). Measured: 12
 // warps at 168 registers run as fast as 16 at 128 (the kernel is not
 // occupancy-bound above 12), and the room pays for keeping A resident.
 struct __align__(16) MainSmem {
     double P[D * D];  // product A G, then its packed LU in place (pidx layout)
     double A[D * D];  // A_i (pidx layout): product operand and the residual's A
     double vec[2][D];   // double-buffered broadcast rows / vectors
-    double b[D];        // reciprocals of the pivots (back substitution)
     double c[D];        // b eliminated alongside the panels: c = L^-1 b
 };
 constexpr size_t kMainSmemBytes = sizeof(MainSmem) * WARPS;
@@ -261,7 +260,6 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         }
         double af[4][8];
         const double bl = __ldcs(gB + sys * D + lane);
-        // (s.b takes the pivots' reciprocals for the back substitution)
         s.c[lane] = bl;
         // the next system's A and G (8 KiB each, contiguous) into L2 while this one runs
         if (lane < 2 && sys + sys_stride < batch) {
@@ -480,8 +478,6 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
         PH(4);
         // ---- chain solve x = G (LU)^-1 r, refinement (preprocess.hpp:115-143)
         const double bnorm = sqrt(warp_sum(bl * bl));
-        s.b[lane] = my_rinv;
-        __syncwarp();
         double x = 0.0, rel = 0.0, y = s.c[lane];  // y = L^-1 b from the elimination
         // the LU is final: store it now and reuse the P region for G (rows at
         // pidx layout: conflict-free row reads), in flight during the sweeps
@@ -513,7 +509,7 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
             // goes to shared memory as the same value from every lane
 #pragma unroll
             for (int k = D - 1; k >= 0; --k) {
-                const double xk = __shfl_sync(kFull, y, k) * s.b[k];  // rcp64's reciprocal: within 1 ulp of the quotient
+                const double xk = __shfl_sync(kFull, y * my_rinv, k);  // rcp64's reciprocal: within 1 ulp of the quotient
                 y = fma(-prow[k], xk, y);
                 s.vec[0][k] = xk;
             }
