@@ -83,8 +83,10 @@ __device__ __forceinline__ double rcp64(double x) {
     return fma(r, t, r);
 }
 // Running maximum of |x| kept as the bit pattern of a non-negative double
-// (patterns order like the values): one LOP3, two ISETP and two SEL on the
-// integer pipe -- fabs/fmax cost a DADD and a DSETP on the FP64 pipe per entry
+// (patterns order like the values): the compare and the select are two ISETP
+// and two SEL on the integer pipe instead of fmax's DSETP and FSELs. ptxas turns
+// the sign mask into a DADD (|x|); forcing it onto the integer pipe with an
+// explicit and.b32 was measured slower
 typedef unsigned long long absmax_t;
 __device__ __forceinline__ absmax_t max_abs(absmax_t m, double x) {
     const absmax_t a = static_cast<absmax_t>(__double_as_longlong(x)) & 0x7fffffffffffffffULL;
@@ -97,7 +99,7 @@ __device__ __forceinline__ absmax_t max_abs_if(bool pred, absmax_t m, double x) 
 __device__ __forceinline__ absmax_t max_u64(absmax_t a, absmax_t b) { return a > b ? a : b; }
 __device__ __forceinline__ double absmax_value(absmax_t m) { return __longlong_as_double(static_cast<long long>(m)); }
 
-// y -= l * v on lanes where `pred` holds: a predicated DFMA, no select/moves
+// y -= l * v on lanes where `pred` holds (the refinement's forward sweep)
 __device__ __forceinline__ void fma_if(bool pred, double& y, double l, double v) {
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p fma.rn.f64 %0, %1, %2, %0;\n\t}"
         : "+d"(y) : "d"(-l), "d"(v), "r"(static_cast<unsigned>(pred)));
