@@ -82,6 +82,16 @@ __device__ __forceinline__ double rcp64(double x) {
     const double t = fma(e, e, e);
     return fma(r, t, r);
 }
+// -1/x with the same seed and step (the exact negation of rcp64): the
+// elimination multiplies by it so that its updates are plain FMAs -- with the
+// positive reciprocal ptxas materialises every -l by a DADD on the FP64 pipe
+__device__ __forceinline__ double nrcp64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    const double t = fma(e, e, e);
+    return fma(-r, t, -r);
+}
 // Running maximum of |x| kept as the bit pattern of a non-negative double
 // (patterns order like the values): the compare and the select are two ISETP
 // and two SEL on the integer pipe instead of fmax's DSETP and FSELs. ptxas turns
@@ -369,24 +379,25 @@ batched_genp32_kernel(const double* __restrict__ gA, const double* __restrict__ 
                 }
                 const double2 cc = *reinterpret_cast<const double2*>(&ra_s[8]);
                 const double ca = cc.x, cb0 = cc.y;
-                const double inv_a = rcp64(ra[t]);
-                const double l1 = rb[t] * inv_a;
+                // multipliers are formed negated (nl = -l): a_ij += nl * u_kj
+                const double ninv_a = nrcp64(ra[t]);
+                const double nl1 = rb[t] * ninv_a;
 #pragma unroll
-                for (int c = t + 1; c < 8; ++c) rb[c] = fma(-l1, ra[c], rb[c]);
-                const double cb1 = fma(-l1, ca, cb0);
-                const double inv_b = rcp64(rb[t + 1]);
+                for (int c = t + 1; c < 8; ++c) rb[c] = fma(nl1, ra[c], rb[c]);
+                const double cb1 = fma(nl1, ca, cb0);
+                const double ninv_b = nrcp64(rb[t + 1]);
                 const bool below_a = lane > t && lane < rows;
-                const double la = below_a ? pr[t] * inv_a : 0.0;
-                if (below_a) pr[t] = la;
+                const double nla = below_a ? pr[t] * ninv_a : 0.0;
+                if (below_a) pr[t] = -nla;
 #pragma unroll
-                for (int c = t + 1; c < 8; ++c) pr[c] = fma(-la, ra[c], pr[c]);
-                bb = fma(-la, ca, bb);
+                for (int c = t + 1; c < 8; ++c) pr[c] = fma(nla, ra[c], pr[c]);
+                bb = fma(nla, ca, bb);
                 const bool below_b = lane > t + 1 && lane < rows;
-                const double lb = below_b ? pr[t + 1] * inv_b : 0.0;
-                if (below_b) pr[t + 1] = lb;
+                const double nlb = below_b ? pr[t + 1] * ninv_b : 0.0;
+                if (below_b) pr[t + 1] = -nlb;
 #pragma unroll
-                for (int c = t + 2; c < 8; ++c) pr[c] = fma(-lb, rb[c], pr[c]);
-                bb = fma(-lb, cb1, bb);
+                for (int c = t + 2; c < 8; ++c) pr[c] = fma(nlb, rb[c], pr[c]);
+                bb = fma(nlb, cb1, bb);
             }
             if (lane < rows) {
 #pragma unroll
